@@ -1,0 +1,158 @@
+"""CPU oracle for the Bayesian-MDS hot path (arXiv 1905.04582).
+
+TEST INFRASTRUCTURE ONLY.  Only ``tests/``, ``__graft_entry__.smoke()`` and
+``bench.py``'s ``cpu_baseline`` / ``--impl reference`` legs may import this
+package.  The product package ``paper_1905_04582_b200`` never imports it; the
+two share no code.
+
+The arithmetic lives in ``mds_oracle.c`` (plain serial C, fp64, libm,
+Neumaier sums, ``-O2 -fno-fast-math -ffp-contract=off``); this module only
+builds it with gcc and marshals numpy arrays through ctypes.  See the C file's
+header for the passages each function follows (Eq. 1, 2, 5, 6 and
+App. B).
+
+Pins (tests/test_oracle_pins.py): scipy truncnorm / norm log-densities,
+closed-form 3-4-5 triangle values (tests/golden/closed_forms.json), mpmath
+brute force, central finite differences, invariants, and the closed-form
+leapfrog map of a Gaussian target.  Every function here is pinned; none is
+"parity unpinned".
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "mds_oracle.c")
+_LIB = os.path.join(_HERE, "liboracle.so")
+CFLAGS = ["-O2", "-fno-fast-math", "-ffp-contract=off", "-fPIC", "-shared", "-std=c11"]
+
+_lib = None
+
+
+def build(force: bool = False) -> str:
+    """Compile mds_oracle.c -> liboracle.so with gcc (idempotent)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        tmp = _LIB + ".tmp%d" % os.getpid()
+        subprocess.check_call(["gcc", *CFLAGS, "-o", tmp, _SRC, "-lm"])
+        os.replace(tmp, _LIB)
+    return _LIB
+
+
+def _load():
+    global _lib
+    if _lib is None:
+        build()
+        lib = ctypes.CDLL(_LIB)
+        P = ctypes.POINTER
+        d_p = P(ctypes.c_double)
+        i64 = ctypes.c_int64
+        i32 = ctypes.c_int32
+        lib.oracle_pair_term.argtypes = [ctypes.c_double, ctypes.c_double, ctypes.c_double,
+                                         ctypes.c_int, d_p, d_p]
+        lib.oracle_log_phi.argtypes = [ctypes.c_double]
+        lib.oracle_log_phi.restype = ctypes.c_double
+        lib.oracle_loglik_grad.argtypes = [i64, i32, d_p, d_p, ctypes.c_double, i32,
+                                           d_p, d_p, d_p, P(i64), P(i64)]
+        lib.oracle_grad_rows.argtypes = [i64, i32, i64, P(i64), d_p, d_p, ctypes.c_double, i32,
+                                         d_p, d_p, d_p]
+        lib.oracle_leapfrog.argtypes = [i64, i32, d_p, d_p, d_p, ctypes.c_double, i32,
+                                        ctypes.c_double, ctypes.c_double, i32, d_p, d_p, d_p]
+        _lib = lib
+    return _lib
+
+
+def _dp(a):
+    return a.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+
+
+def _f64(a):
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def pack_lower(y_full: np.ndarray) -> np.ndarray:
+    """Full n x n matrix -> packed strict lower triangle (row i: y_i0..y_i,i-1)."""
+    n = y_full.shape[0]
+    il, jl = np.tril_indices(n, -1)
+    return _f64(y_full[il, jl])
+
+
+def pair_term(y: float, d: float, sigma: float, truncation: int = 1):
+    """(ell, coef) of one pair: Eq. 2 term and Eq. 6 coefficient."""
+    lib = _load()
+    e = ctypes.c_double()
+    c = ctypes.c_double()
+    if lib.oracle_pair_term(float(y), float(d), float(sigma), int(truncation),
+                            ctypes.byref(e), ctypes.byref(c)):
+        raise ValueError("invalid pair_term arguments")
+    return e.value, c.value
+
+
+def log_phi(t: float) -> float:
+    return _load().oracle_log_phi(float(t))
+
+
+def loglik_grad(y_packed: np.ndarray, x: np.ndarray, sigma: float, truncation: int = 1,
+                want_absscale: bool = True):
+    """Serial oracle over the packed lower triangle.
+
+    Returns dict(loglik, grad (n,d), absscale (n,d) or None, n_obs, zero_pairs).
+    """
+    lib = _load()
+    x = _f64(x)
+    n, d = x.shape
+    y_packed = _f64(y_packed)
+    if y_packed.size != n * (n - 1) // 2:
+        raise ValueError("y_packed must hold n(n-1)/2 entries")
+    ll = ctypes.c_double()
+    g = np.zeros((n, d))
+    s = np.zeros((n, d)) if want_absscale else None
+    nobs = ctypes.c_int64()
+    nz = ctypes.c_int64()
+    rc = lib.oracle_loglik_grad(n, d, _dp(y_packed), _dp(x), float(sigma), int(truncation),
+                                ctypes.byref(ll), _dp(g), _dp(s) if s is not None else None,
+                                ctypes.byref(nobs), ctypes.byref(nz))
+    if rc:
+        raise ValueError("invalid oracle arguments")
+    return dict(loglik=ll.value, grad=g, absscale=s, n_obs=nobs.value, zero_pairs=nz.value)
+
+
+def grad_rows(rows, yrows: np.ndarray, x: np.ndarray, sigma: float, truncation: int = 1):
+    """Gradient rows (Eq. 6) for selected i, given y_ij for all j (yrows[r, j])."""
+    lib = _load()
+    x = _f64(x)
+    n, d = x.shape
+    rows = np.ascontiguousarray(rows, dtype=np.int64)
+    yrows = _f64(yrows)
+    m = rows.size
+    if yrows.shape != (m, n):
+        raise ValueError("yrows must be (len(rows), n)")
+    g = np.zeros((m, d))
+    s = np.zeros((m, d))
+    rl = np.zeros(m)
+    rc = lib.oracle_grad_rows(n, d, m, rows.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
+                              _dp(yrows), _dp(x), float(sigma), int(truncation), _dp(g), _dp(s), _dp(rl))
+    if rc:
+        raise ValueError("invalid oracle arguments")
+    return dict(grad=g, absscale=s, rowlik=rl)
+
+
+def leapfrog(y_packed: np.ndarray, x0: np.ndarray, p0: np.ndarray, sigma: float, eps: float,
+             n_steps: int, truncation: int = 1, prior_sd: float = 0.0):
+    """n_steps leapfrog steps (Eq. 5 dynamics, M = I). Returns dict(x, p, H0, H1, loglik)."""
+    lib = _load()
+    x = _f64(x0).copy()
+    p = _f64(p0).copy()
+    n, d = x.shape
+    H0 = ctypes.c_double()
+    H1 = ctypes.c_double()
+    ll = ctypes.c_double()
+    rc = lib.oracle_leapfrog(n, d, _dp(_f64(y_packed)), _dp(x), _dp(p), float(sigma), int(truncation),
+                             float(prior_sd), float(eps), int(n_steps),
+                             ctypes.byref(H0), ctypes.byref(H1), ctypes.byref(ll))
+    if rc:
+        raise ValueError("invalid oracle arguments")
+    return dict(x=x, p=p, H0=H0.value, H1=H1.value, loglik=ll.value)

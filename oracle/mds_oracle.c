@@ -1,0 +1,233 @@
+/*
+ * mds_oracle.c -- CPU ORACLE for the Bayesian-MDS hot path (arXiv 1905.04582).
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and
+ * bench.py's cpu_baseline / --impl reference legs may load this library.
+ * The product path (paper_1905_04582_b200/, libmds.so) never links, imports
+ * or calls anything here, and this file shares no code, header, constant or
+ * helper with the CUDA path.
+ *
+ * What it computes is the plain definition, written out term by term:
+ *
+ *   PAPER.md:78-83  (Sec. 2.1, Eq. 1)   y_ij ~ N(delta_ij, sigma^2) I(y_ij > 0), i > j,
+ *                                       delta_ij = ||x_i - x_j||.
+ *   PAPER.md:84-112 (Eq. 2)             log p(Y|X,sigma^2) = sum_{i>j} [ -1/2 log(2 pi sigma^2)
+ *                                        - (y_ij - delta_ij)^2/(2 sigma^2) - log Phi(delta_ij/sigma) ]
+ *                                       (full normalised density per OBSERVED pair: DESIGN.md reading R2;
+ *                                        sign of log Phi: reading R3).
+ *   PAPER.md:338-348 (Eq. 6)            d/dx_i log p = - sum_{j != i} [ (delta_ij - y_ij)/sigma^2
+ *                                        + phi(delta_ij/sigma)/(sigma Phi(delta_ij/sigma)) ] (x_i - x_j)/delta_ij
+ *   PAPER.md:821-826 (App. B)           truncation flag T: T = 0 drops the log Phi term and its
+ *                                       derivative (reading R12).
+ *   PAPER.md:321-336 (Sec. 2.3, Eq. 5)  leapfrog integrator for HMC (readings R19, R20).
+ *
+ * Numerics: double precision only, libm erfc/log1p/exp/sqrt, i-major order
+ * (i ascending, j ascending < i), Neumaier-compensated sums for log L and the
+ * gradient.  Compile with -O2 -fno-fast-math -ffp-contract=off.
+ *
+ * Readings: NaN y = missing pair (R7);
+ * only the strict lower triangle is read (R4, R9); delta = 0 for an observed
+ * pair contributes its likelihood term but a zero gradient direction and is
+ * counted (R10); log Phi(t) = log1p(-erfc(t/sqrt 2)/2) (R11).
+ *
+ * Every entry point returns 0 on success, -1 on invalid arguments.
+ */
+#include <math.h>
+#include <stddef.h>
+#include <stdint.h>
+#include <string.h>
+#include <stdlib.h>
+
+#define ORACLE_PI 3.14159265358979323846
+
+/* ---- Neumaier (improved Kahan) compensated accumulator ------------------ */
+typedef struct { double s, c; } acc_t;
+
+static void acc_add(acc_t *a, double v)
+{
+    double t = a->s + v;
+    if (fabs(a->s) >= fabs(v)) a->c += (a->s - t) + v;
+    else                       a->c += (v - t) + a->s;
+    a->s = t;
+}
+static double acc_val(const acc_t *a) { return a->s + a->c; }
+
+/* ---- one pair, Eq. 2 term and Eq. 6 coefficient ------------------------- */
+/* ell  = -1/2 log(2 pi sigma^2) - (y-d)^2/(2 sigma^2) - T log Phi(d/sigma)
+ * coef = (d - y)/sigma^2 + T phi(d/sigma) / (sigma Phi(d/sigma))
+ * so that the pair adds  -coef (x_i-x_j)/d  to g_i and  +coef (x_i-x_j)/d to g_j. */
+int oracle_pair_term(double y, double d, double sigma, int truncation,
+                     double *ell, double *coef)
+{
+    if (!(sigma > 0.0) || !isfinite(sigma) || !(d >= 0.0) || !isfinite(y)) return -1;
+    double sigma2 = sigma * sigma;
+    double t = d / sigma;
+    double Q = 0.5 * erfc(t / sqrt(2.0));        /* 1 - Phi(t) */
+    double logPhi = log1p(-Q);                   /* log Phi(t) */
+    double phi = exp(-0.5 * t * t) / sqrt(2.0 * ORACLE_PI);
+    double r = y - d;
+    double e = -0.5 * log(2.0 * ORACLE_PI * sigma2) - (r * r) / (2.0 * sigma2);
+    double c = (d - y) / sigma2;
+    if (truncation) {
+        e -= logPhi;
+        c += phi / (sigma * (1.0 - Q));
+    }
+    if (ell) *ell = e;
+    if (coef) *coef = c;
+    return 0;
+}
+
+/* log Phi(t) for t >= 0 exactly as the oracle forms it (exposed for pins). */
+double oracle_log_phi(double t) { return log1p(-0.5 * erfc(t / sqrt(2.0))); }
+
+/* ---- full evaluation over the packed strict lower triangle -------------- */
+/* y_packed: row i (i = 1..n-1) holds y_i0 .. y_i,i-1 at offset i(i-1)/2.
+ * x: n*d row-major.  Outputs: *loglik, grad[n*d], absscale[n*d] (may be NULL:
+ * S_ik = sum_j |v_ijk|, the conditioning scale of gradient entry ik),
+ * *n_obs, *zero_pairs (observed pairs with delta = 0). */
+int oracle_loglik_grad(int64_t n, int32_t d, const double *y_packed, const double *x,
+                       double sigma, int32_t truncation,
+                       double *loglik, double *grad, double *absscale,
+                       int64_t *n_obs, int64_t *zero_pairs)
+{
+    if (n < 2 || d < 1 || !y_packed || !x || !(sigma > 0.0) || !isfinite(sigma)) return -1;
+    acc_t L = {0.0, 0.0};
+    acc_t *G = (acc_t *)calloc((size_t)n * (size_t)d, sizeof(acc_t));
+    double *diff = (double *)malloc((size_t)d * sizeof(double));
+    if (!G || !diff) { free(G); free(diff); return -1; }
+    if (absscale) memset(absscale, 0, (size_t)n * (size_t)d * sizeof(double));
+    int64_t nobs = 0, nzero = 0;
+
+    for (int64_t i = 1; i < n; ++i) {
+        const double *yrow = y_packed + (i * (i - 1)) / 2;
+        for (int64_t j = 0; j < i; ++j) {
+            double y = yrow[j];
+            if (isnan(y)) continue;                       /* missing (R7) */
+            double s = 0.0;
+            for (int k = 0; k < d; ++k) {
+                diff[k] = x[i * d + k] - x[j * d + k];
+                s += diff[k] * diff[k];
+            }
+            double dist = sqrt(s);
+            double ell, coef;
+            oracle_pair_term(y, dist, sigma, truncation, &ell, &coef);
+            acc_add(&L, ell);
+            ++nobs;
+            if (dist > 0.0) {
+                for (int k = 0; k < d; ++k) {
+                    double v = (coef * diff[k]) / dist;
+                    acc_add(&G[i * d + k], -v);
+                    acc_add(&G[j * d + k], v);
+                    if (absscale) {
+                        absscale[i * d + k] += fabs(v);
+                        absscale[j * d + k] += fabs(v);
+                    }
+                }
+            } else {
+                ++nzero;                                   /* R10 */
+            }
+        }
+    }
+    if (loglik) *loglik = acc_val(&L);
+    if (grad) for (int64_t q = 0; q < n * d; ++q) grad[q] = acc_val(&G[q]);
+    if (n_obs) *n_obs = nobs;
+    if (zero_pairs) *zero_pairs = nzero;
+    free(G);
+    free(diff);
+    return 0;
+}
+
+/* ---- selected rows only (sampled parity at full size) ------------------- */
+/* For each requested row i = rows[r]: yrows[r*n + j] holds y_ij for every
+ * j != i (y_ij = y_ji; entry j == i ignored).  Outputs grad_rows[r*d+k] =
+ * d log L / d x_ik (Eq. 6, all j != i), absscale_rows likewise, and
+ * rowlik[r] = sum over j < i (observed) of the Eq. 2 term -- the row's share
+ * of log L in the lower-triangle partition. */
+int oracle_grad_rows(int64_t n, int32_t d, int64_t nrows, const int64_t *rows,
+                     const double *yrows, const double *x, double sigma, int32_t truncation,
+                     double *grad_rows, double *absscale_rows, double *rowlik)
+{
+    if (n < 2 || d < 1 || nrows < 0 || !(sigma > 0.0) || !isfinite(sigma)) return -1;
+    double *diff = (double *)malloc((size_t)d * sizeof(double));
+    acc_t *G = (acc_t *)malloc((size_t)d * sizeof(acc_t));
+    if (!diff || !G) { free(diff); free(G); return -1; }
+    for (int64_t r = 0; r < nrows; ++r) {
+        int64_t i = rows[r];
+        if (i < 0 || i >= n) { free(diff); free(G); return -1; }
+        acc_t L = {0.0, 0.0};
+        for (int k = 0; k < d; ++k) { G[k].s = 0.0; G[k].c = 0.0; }
+        if (absscale_rows) for (int k = 0; k < d; ++k) absscale_rows[r * d + k] = 0.0;
+        for (int64_t j = 0; j < n; ++j) {
+            if (j == i) continue;
+            double y = yrows[r * n + j];
+            if (isnan(y)) continue;
+            double s = 0.0;
+            for (int k = 0; k < d; ++k) {
+                diff[k] = x[i * d + k] - x[j * d + k];
+                s += diff[k] * diff[k];
+            }
+            double dist = sqrt(s);
+            double ell, coef;
+            oracle_pair_term(y, dist, sigma, truncation, &ell, &coef);
+            if (j < i) acc_add(&L, ell);
+            if (dist > 0.0) {
+                for (int k = 0; k < d; ++k) {
+                    double v = (coef * diff[k]) / dist;
+                    acc_add(&G[k], -v);
+                    if (absscale_rows) absscale_rows[r * d + k] += fabs(v);
+                }
+            }
+        }
+        for (int k = 0; k < d; ++k) grad_rows[r * d + k] = acc_val(&G[k]);
+        if (rowlik) rowlik[r] = acc_val(&L);
+    }
+    free(diff);
+    free(G);
+    return 0;
+}
+
+/* ---- HMC leapfrog (Sec. 2.3, Eq. 5) ------------------------------------- */
+/* Target log pi(x) = log L(x) + log prior(x), prior iid N(0, prior_sd^2) per
+ * coordinate (reading R20; prior_sd <= 0 means no prior), mass M = I (R19).
+ * x (n*d) and p (n*d) are updated in place by n_steps leapfrog steps of size
+ * eps:  p += eps/2 grad;  x += eps p;  p += eps/2 grad.
+ * Outputs: H0 = -log pi(x0) + p0.p0/2 and H1 at the end, and the final
+ * log L.  Returns -1 on bad arguments. */
+static double prior_logpdf(int64_t m, const double *x, double prior_sd)
+{
+    if (!(prior_sd > 0.0)) return 0.0;
+    acc_t a = {0.0, 0.0};
+    for (int64_t q = 0; q < m; ++q) acc_add(&a, -(x[q] * x[q]) / (2.0 * prior_sd * prior_sd));
+    return acc_val(&a);
+}
+static double kinetic(int64_t m, const double *p)
+{
+    acc_t a = {0.0, 0.0};
+    for (int64_t q = 0; q < m; ++q) acc_add(&a, 0.5 * p[q] * p[q]);
+    return acc_val(&a);
+}
+
+int oracle_leapfrog(int64_t n, int32_t d, const double *y_packed, double *x, double *p,
+                    double sigma, int32_t truncation, double prior_sd,
+                    double eps, int32_t n_steps, double *H0, double *H1, double *loglik_end)
+{
+    if (n < 2 || d < 1 || n_steps < 1 || !(eps > 0.0)) return -1;
+    int64_t m = n * (int64_t)d;
+    double *g = (double *)malloc((size_t)m * sizeof(double));
+    if (!g) return -1;
+    double ll;
+    if (oracle_loglik_grad(n, d, y_packed, x, sigma, truncation, &ll, g, NULL, NULL, NULL)) { free(g); return -1; }
+    if (prior_sd > 0.0) for (int64_t q = 0; q < m; ++q) g[q] -= x[q] / (prior_sd * prior_sd);
+    if (H0) *H0 = -(ll + prior_logpdf(m, x, prior_sd)) + kinetic(m, p);
+    for (int32_t s = 0; s < n_steps; ++s) {
+        for (int64_t q = 0; q < m; ++q) p[q] += 0.5 * eps * g[q];
+        for (int64_t q = 0; q < m; ++q) x[q] += eps * p[q];
+        oracle_loglik_grad(n, d, y_packed, x, sigma, truncation, &ll, g, NULL, NULL, NULL);
+        if (prior_sd > 0.0) for (int64_t q = 0; q < m; ++q) g[q] -= x[q] / (prior_sd * prior_sd);
+        for (int64_t q = 0; q < m; ++q) p[q] += 0.5 * eps * g[q];
+    }
+    if (H1) *H1 = -(ll + prior_logpdf(m, x, prior_sd)) + kinetic(m, p);
+    if (loglik_end) *loglik_end = ll;
+    free(g);
+    return 0;
+}
