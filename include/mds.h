@@ -1,0 +1,256 @@
+/*
+ * mds.h -- C-ABI of libmds, the B200 (sm_100a) hot path of Bayesian
+ * multidimensional scaling (Holbrook et al., arXiv 1905.04582).
+ *
+ * What the library computes (PAPER.md = /root/reference/PAPER.md):
+ *
+ *   log L(X) = sum over observed i > j of
+ *                 -1/2 log(2 pi sigma^2) - (y_ij - delta_ij)^2 / (2 sigma^2)
+ *                 - T log Phi(delta_ij / sigma)                     PAPER.md:84-112 (Eq. 2)
+ *   d log L / d x_i = - sum_{j != i} [ (delta_ij - y_ij)/sigma^2
+ *                 + T phi(delta_ij/sigma) / (sigma Phi(delta_ij/sigma)) ] (x_i - x_j)/delta_ij
+ *                                                                    PAPER.md:338-348 (Eq. 6)
+ *   with delta_ij = ||x_i - x_j||, the truncated-normal model
+ *   y_ij ~ N(delta_ij, sigma^2) I(y_ij > 0) of PAPER.md:78-83 (Eq. 1), and T the
+ *   truncation flag of the App. B ablation.  The sum is one
+ *   fused transformation-reduction over the strict lower
+ *   triangle, each unordered pair evaluated once.
+ *
+ * Readings of the paper (full list in DESIGN.md): y is the observed
+ * dissimilarity, delta the latent distance (R1); the normalising constant is
+ * the full density per OBSERVED pair (R2); log L carries -log Phi (R3); NaN in
+ * Y means missing (R7); only the strict lower triangle of Y is read (R4, R9);
+ * y >= 0 accepted, y < 0 or +-inf rejected (R8); an observed pair with
+ * delta = 0 contributes its likelihood term and a zero gradient (R10); sigma
+ * is the standard deviation (R13); precision selects fp64 / fp32 storage and
+ * per-pair arithmetic (R14, R15).
+ *
+ * Conventions for every entry point:
+ *   - Return value: MDS_OK or an error status; mds_last_error() gives text.
+ *   - Argument errors (MDS_E_INVALID_ARG) leave the context usable.  A CUDA
+ *     error poisons the context: every later call returns MDS_E_CUDA.
+ *   - Host arrays are owned by the caller; setters copy them, getters write
+ *     into caller buffers; no caller pointer is retained after a call returns.
+ *   - "_device" variants take device pointers and are stream-ordered on the
+ *     context's stream (mds_set_stream); they do not synchronise the host.
+ *   - One context may be used by one host thread at a time; distinct contexts
+ *     are independent.
+ *   - Arrays are row-major: X is n x d (x_ik at [i*d + k]); the packed lower
+ *     triangle stores row i (i >= 1) as y_i0 .. y_i,i-1 at offset i(i-1)/2.
+ *   - The library needs an sm_100 device; otherwise creation fails with
+ *     MDS_E_UNSUPPORTED.  There is no CPU fallback.
+ */
+#ifndef MDS_H
+#define MDS_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct mds_ctx_s *mds_ctx;
+
+typedef enum { MDS_F64 = 0, MDS_F32 = 1 } mds_precision;
+
+typedef enum {
+    MDS_OK = 0,
+    MDS_E_INVALID_ARG = 1,
+    MDS_E_STATE = 2,       /* evaluation before Y, X and sigma are all set */
+    MDS_E_OOM = 3,
+    MDS_E_CUDA = 4,        /* sticky: the context is poisoned */
+    MDS_E_COMM = 5,
+    MDS_E_UNSUPPORTED = 6  /* no sm_100 device, or an option not built */
+} mds_status;
+
+#define MDS_D_MAX 8
+
+/* ---- lifetime ---------------------------------------------------------- */
+
+/* Create a context for n items in d latent dimensions on the current CUDA
+ * device.  n >= 2; 1 <= d <= MDS_D_MAX; precision MDS_F64 or MDS_F32;
+ * truncation 0 or 1 (T above).  Allocates the tile-packed triangle of Y
+ * (about n^2/2 values of the chosen precision) and O(n d) side buffers.
+ * Errors: MDS_E_INVALID_ARG, MDS_E_OOM, MDS_E_UNSUPPORTED, MDS_E_CUDA. */
+mds_status mds_create(int64_t n, int32_t d, int32_t precision, int32_t truncation, mds_ctx *out);
+
+/* As mds_create, but this rank owns only the tile-rows r with
+ * r mod world == rank of the tiled triangle: it stores and
+ * evaluates only its share of the pairs.  Evaluations then produce this
+ * rank's PARTIAL log L and gradient (mds_evaluate_partial_device); the caller
+ * gathers the world partials (e.g. NCCL all-gather through torch.distributed)
+ * and combines them with mds_combine_partials_device.  world == 1 is the
+ * unsharded case.  Errors as mds_create, plus rank/world out of range. */
+mds_status mds_create_sharded(int64_t n, int32_t d, int32_t precision, int32_t truncation,
+                              int32_t rank, int32_t world, mds_ctx *out);
+
+/* Free every device and host resource of ctx (NULL is ignored). */
+void mds_destroy(mds_ctx ctx);
+
+/* Use the given cudaStream_t (e.g. torch.cuda.current_stream().cuda_stream)
+ * for all later work.  NULL selects the legacy default stream. */
+mds_status mds_set_stream(mds_ctx ctx, void *cuda_stream);
+
+/* ---- inputs ------------------------------------------------------------ */
+
+/* Observed dissimilarities from a host n x n matrix with leading dimension
+ * ld >= n (row-major).  Only the strict lower triangle (i > j) is read.
+ * NaN = missing.  Any y < 0 or +-inf -> MDS_E_INVALID_ARG (then Y counts as
+ * not set).  Under sharding only this rank's tile-rows are stored. */
+mds_status mds_set_dissimilarities(mds_ctx ctx, const double *y, int64_t ld);
+
+/* Rows [i0, i1) of the packed strict lower triangle (row i holds its i
+ * entries y_i0..y_i,i-1 back to back; the first value is y_{i0,0}).  Lets
+ * callers stream Y without an n x n host matrix.  Same validation as above.
+ * Under sharding, rows outside this rank's tile-rows are ignored, so every
+ * rank may be fed the same stream.  Evaluation requires every row to have
+ * been supplied once (else MDS_E_STATE). */
+mds_status mds_set_dissimilarity_rows(mds_ctx ctx, int64_t i0, int64_t i1, const double *y_lower);
+
+/* Device-pointer variant of mds_set_dissimilarity_rows (y_lower_dev is fp64
+ * device memory, read on the ctx stream before the call returns). */
+mds_status mds_set_dissimilarity_rows_device(mds_ctx ctx, int64_t i0, int64_t i1,
+                                             const double *y_lower_dev);
+
+/* Latent locations X (host, n x d row-major).  Non-finite -> INVALID_ARG. */
+mds_status mds_set_locations(mds_ctx ctx, const double *x);
+
+/* Latent locations from device memory (fp64, n x d), stream-ordered.  Not
+ * validated (the caller owns finiteness of device data). */
+mds_status mds_set_locations_device(mds_ctx ctx, const double *x_dev);
+
+/* sigma > 0 and finite (the standard deviation, not sigma^2; R13). */
+mds_status mds_set_sigma(mds_ctx ctx, double sigma);
+
+/* ---- evaluation (one fused pass computes both) ------------------------- */
+
+/* log L into *loglik (host).  Synchronises.  A following mds_gradient with
+ * no setter in between reuses the same pass. */
+mds_status mds_log_likelihood(mds_ctx ctx, double *loglik);
+
+/* d log L / dX into grad (host, n x d).  Synchronises. */
+mds_status mds_gradient(mds_ctx ctx, double *grad);
+
+/* Both from one pass; either pointer may be NULL.  Synchronises. */
+mds_status mds_log_likelihood_and_gradient(mds_ctx ctx, double *loglik, double *grad);
+
+/* Stream-ordered evaluation into device memory: *loglik_dev (1 double) and
+ * grad_dev (n x d doubles); either may be NULL.  Does not synchronise. */
+mds_status mds_evaluate_device(mds_ctx ctx, double *loglik_dev, double *grad_dev);
+
+/* Sharded contexts: this rank's partial result into part_dev, laid out as
+ * n*d gradient values followed by 1 log L value (n*d + 1 doubles). */
+mds_status mds_evaluate_partial_device(mds_ctx ctx, double *part_dev);
+
+/* Exchange used by sharded contexts.  fn must all-gather `count` doubles
+ * from every rank's send_dev into recv_dev[world][count] in rank order,
+ * stream-ordered on cuda_stream (e.g. NCCL all-gather over NVLink through
+ * torch.distributed), and return 0 on success.  Once registered, sharded
+ * contexts run the whole pass themselves: local pair kernel -> fixed-order
+ * local reduction -> fn -> rank-ordered combine, so mds_evaluate_device,
+ * mds_log_likelihood_and_gradient, mds_leapfrog_device and the HMC driver
+ * return the FULL result on every rank (bitwise identical across ranks).
+ * Without fn, sharded evaluations fail with MDS_E_STATE.  A non-zero return
+ * from fn fails the call with MDS_E_COMM. */
+typedef int (*mds_allgather_fn)(void *user, const double *send_dev, double *recv_dev, int64_t count,
+                                void *cuda_stream);
+mds_status mds_set_allgather(mds_ctx ctx, mds_allgather_fn fn, void *user);
+
+/* Combine world partials gathered_dev[world][n*d + 1] (rank order) into the
+ * full result by a fixed rank-ordered sum (bitwise identical on every rank).
+ * Either output may be NULL. */
+mds_status mds_combine_partials_device(mds_ctx ctx, const double *gathered_dev, int32_t world,
+                                       double *loglik_dev, double *grad_dev);
+
+/* ---- diagnostics ------------------------------------------------------- */
+
+/* Number of observed pairs stored by this context (this rank's share). */
+mds_status mds_observed_pairs(mds_ctx ctx, int64_t *count);
+
+/* Number of observed pairs with delta_ij == 0 at the current X (R10). */
+mds_status mds_zero_distance_pairs(mds_ctx ctx, int64_t *count);
+
+/* Timing mode (mds_set_timing(ctx, 1)): every fused pass outside a CUDA graph
+ * records CUDA events on the ctx stream around the pair kernel and around the
+ * reduction (+ exchange when sharded), without any host sync.
+ * mds_last_timing synchronises on the last event and returns the MEAN
+ * per-launch device time, in ms, of the pair kernel and of the reduction over
+ * all passes recorded since the previous mds_last_timing / mds_set_timing
+ * call (0 when none). */
+mds_status mds_set_timing(mds_ctx ctx, int32_t enable);
+mds_status mds_last_timing(mds_ctx ctx, float *pair_kernel_ms, float *reduce_ms);
+
+/* ---- HMC driver (Eq. 5; readings R19, R20) ------------ */
+
+typedef struct {
+    int32_t n_iter;      /* HMC transitions */
+    int32_t n_leapfrog;  /* L, leapfrog steps per transition (>= 1) */
+    double step_size;    /* epsilon > 0 */
+    double prior_sd;     /* tau: iid N(0, tau^2) prior per coordinate; <= 0 -> none */
+    uint64_t seed;       /* momentum / accept-reject stream */
+} mds_hmc_config;
+
+typedef struct {
+    int64_t accepted;
+    int64_t grad_evals;
+    double mean_abs_dH;
+    double seconds;       /* device time of the chain (CUDA events) */
+    double final_loglik;
+} mds_hmc_stats;
+
+/* One leapfrog trajectory from the current X with caller-supplied momentum
+ * p0 (host, n x d): L steps of p += eps/2 grad; x += eps p; p += eps/2 grad
+ * of log pi = log L + log prior.  Writes the end point to x_out / p_out
+ * (host, either may be NULL) and the Hamiltonians H0, H1 (Eq. 5 with M = I).
+ * The context's X is NOT changed (pure proposal). */
+mds_status mds_hmc_trajectory(mds_ctx ctx, const mds_hmc_config *cfg, const double *p0,
+                              double *x_out, double *p_out, double *H0, double *H1);
+
+/* Device-resident leapfrog (the per-step hot path of HMC): enqueue
+ * cfg->n_leapfrog steps that move the context's X in place, stream-ordered,
+ * no host sync.  If p0_dev != NULL the momentum is (re)initialised from it
+ * (device, n x d fp64) and grad log pi is primed at the current X; otherwise
+ * the steps continue from the momentum and gradient the previous call left.
+ * cfg->n_iter and cfg->seed are ignored.  Each step is one fused likelihood+
+ * gradient pass (plus the exchange when sharded). */
+mds_status mds_leapfrog_device(mds_ctx ctx, const mds_hmc_config *cfg, const double *p0_dev);
+
+/* Current X (host, n x d) / momentum of the device-resident leapfrog (host,
+ * n x d; zeros before any leapfrog call).  Synchronise. */
+mds_status mds_get_locations(mds_ctx ctx, double *x);
+mds_status mds_get_momentum(mds_ctx ctx, double *p);
+
+/* Run cfg->n_iter HMC transitions (momentum ~ N(0, I) from a counter-based
+ * generator seeded by cfg->seed; Metropolis accept with min(1, e^{-dH})),
+ * starting from x_inout (host, n x d; NULL = the context's current X) and
+ * writing the final state back to it.  One CUDA graph replays the L fused
+ * leapfrog steps of a transition (unsharded contexts; sharded ones launch
+ * directly since the exchange callback runs on the host); the only
+ * per-transition host sync is the accept/reject.  The context's X is left at
+ * the final state. */
+mds_status mds_hmc_run(mds_ctx ctx, const mds_hmc_config *cfg, double *x_inout, mds_hmc_stats *stats);
+
+/* ---- misc -------------------------------------------------------------- */
+
+/* Text of the last error on ctx (never NULL; "" when none). */
+const char *mds_last_error(mds_ctx ctx);
+
+/* Static text for a status code. */
+const char *mds_status_string(mds_status s);
+
+/* Library version "major.minor.patch". */
+const char *mds_version(void);
+
+/* SM count and compute capability of the current device (MDS_E_UNSUPPORTED
+ * if there is no device). */
+mds_status mds_device_info(int32_t *sm_count, int32_t *cc_major, int32_t *cc_minor);
+
+/* Measure this device's FP64 (dfma) and FP32 (ffma) lane throughput with a
+ * register-resident dependent-chain microbenchmark; results in lane-FMA/s.
+ * Used for the ALU roofline denominator. */
+mds_status mds_measure_fma_peaks(double *fp64_fma_per_s, double *fp32_fma_per_s);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MDS_H */

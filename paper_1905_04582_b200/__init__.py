@@ -1,0 +1,185 @@
+"""B200-native hot path of Bayesian MDS (Holbrook et al., arXiv 1905.04582).
+
+The product is ``libmds.so`` (sm_100a CUDA, C-ABI declared in include/mds.h).
+This package is its thin Python binding: ``_abi`` exposes every C entry point
+under the same name; ``MDS`` below only bundles a context handle with numpy /
+torch argument marshalling.  All arithmetic runs in the CUDA kernels; there
+is no CPU path.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from . import _abi
+from ._abi import *  # noqa: F401,F403  (mds_* same-name wrappers)
+from ._abi import MDS_F32, MDS_F64, HmcConfig, HmcStats, MDSError
+
+__all__ = ["MDS", "MDSError", "HmcConfig", "HmcStats", "MDS_F64", "MDS_F32"] + _abi.EXPORTS
+
+def _wrap_dev(ptr: int, count: int, dev):
+    """A torch float64 view of `count` doubles of device memory at ptr (no copy)."""
+    import torch
+
+    class _CAI:
+        __cuda_array_interface__ = {"shape": (int(count),), "typestr": "<f8", "data": (int(ptr), False),
+                                    "version": 3, "strides": None, "stream": None}
+
+    return torch.as_tensor(_CAI(), device=dev)
+
+
+_PREC = {"f64": MDS_F64, "fp64": MDS_F64, "float64": MDS_F64, MDS_F64: MDS_F64,
+         "f32": MDS_F32, "fp32": MDS_F32, "float32": MDS_F32, MDS_F32: MDS_F32}
+
+
+class MDS:
+    """One libmds context (marshalling only)."""
+
+    def __init__(self, n: int, d: int, precision="f64", truncation: bool = True,
+                 rank: int = 0, world: int = 1, stream=None):
+        self.n, self.d = int(n), int(d)
+        self.precision = _PREC[precision]
+        self.rank, self.world = int(rank), int(world)
+        if world == 1:
+            self.ctx = _abi.mds_create(n, d, self.precision, int(bool(truncation)))
+        else:
+            self.ctx = _abi.mds_create_sharded(n, d, self.precision, int(bool(truncation)), rank, world)
+        if stream is not None:
+            self.set_stream(stream)
+
+    # lifetime
+    def close(self):
+        if getattr(self, "ctx", None):
+            _abi.mds_destroy(self.ctx)
+            self.ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    def set_stream(self, stream):
+        """stream: a torch.cuda.Stream, a raw cudaStream_t int, or None."""
+        h = getattr(stream, "cuda_stream", stream)
+        _abi.mds_set_stream(self.ctx, h)
+
+    # inputs
+    def set_dissimilarities(self, y_full: np.ndarray):
+        y = np.ascontiguousarray(y_full, dtype=np.float64)
+        _abi.mds_set_dissimilarities(self.ctx, y, y.shape[1])
+
+    def set_dissimilarity_rows(self, i0: int, i1: int, y_lower):
+        if hasattr(y_lower, "data_ptr"):
+            _abi.mds_set_dissimilarity_rows_device(self.ctx, i0, i1, y_lower)
+        else:
+            _abi.mds_set_dissimilarity_rows(self.ctx, i0, i1, np.ascontiguousarray(y_lower, dtype=np.float64))
+
+    def set_dissimilarities_packed(self, y_packed):
+        self.set_dissimilarity_rows(0, self.n, y_packed)
+
+    def set_locations(self, x):
+        if hasattr(x, "data_ptr"):
+            _abi.mds_set_locations_device(self.ctx, x)
+        else:
+            _abi.mds_set_locations(self.ctx, np.ascontiguousarray(x, dtype=np.float64))
+
+    def set_sigma(self, sigma: float):
+        _abi.mds_set_sigma(self.ctx, sigma)
+
+    # evaluation
+    def log_likelihood_and_gradient(self):
+        ll = np.zeros(1)
+        g = np.zeros((self.n, self.d))
+        _abi.mds_log_likelihood_and_gradient(self.ctx, ll, g)
+        return float(ll[0]), g
+
+    def log_likelihood(self) -> float:
+        ll = np.zeros(1)
+        _abi.mds_log_likelihood(self.ctx, ll)
+        return float(ll[0])
+
+    def gradient(self) -> np.ndarray:
+        g = np.zeros((self.n, self.d))
+        _abi.mds_gradient(self.ctx, g)
+        return g
+
+    def evaluate_device(self, loglik_dev, grad_dev):
+        _abi.mds_evaluate_device(self.ctx, loglik_dev, grad_dev)
+
+    def evaluate_partial_device(self, part_dev):
+        _abi.mds_evaluate_partial_device(self.ctx, part_dev)
+
+    def combine_partials_device(self, gathered_dev, world, loglik_dev, grad_dev):
+        _abi.mds_combine_partials_device(self.ctx, gathered_dev, world, loglik_dev, grad_dev)
+
+    # diagnostics / timing
+    def observed_pairs(self) -> int:
+        return _abi.mds_observed_pairs(self.ctx)
+
+    def zero_distance_pairs(self) -> int:
+        return _abi.mds_zero_distance_pairs(self.ctx)
+
+    def set_timing(self, on: bool = True):
+        _abi.mds_set_timing(self.ctx, on)
+
+    def last_timing(self):
+        return _abi.mds_last_timing(self.ctx)
+
+    def use_torch_allgather(self, group=None):
+        """Register torch.distributed all_gather_into_tensor (NCCL on GPU) as
+        the exchange of this sharded context (mds_set_allgather)."""
+        import torch
+        import torch.distributed as dist
+
+        dev = torch.device("cuda", torch.cuda.current_device())
+
+        def _ag(user, send, recv, count, stream):
+            try:
+                st = torch.cuda.ExternalStream(stream) if stream else torch.cuda.current_stream()
+                with torch.cuda.stream(st):
+                    s = _wrap_dev(send, count, dev)
+                    r = _wrap_dev(recv, count * self.world, dev)
+                    dist.all_gather_into_tensor(r, s, group=group)
+                return 0
+            except Exception as e:  # reported as MDS_E_COMM
+                self.last_exchange_error = repr(e)
+                return 1
+
+        self._ag_cb = _abi.ALLGATHER_FN(_ag)
+        _abi.mds_set_allgather(self.ctx, self._ag_cb, None)
+
+    def get_locations(self) -> np.ndarray:
+        x = np.zeros((self.n, self.d))
+        _abi.mds_get_locations(self.ctx, x)
+        return x
+
+    def get_momentum(self) -> np.ndarray:
+        p = np.zeros((self.n, self.d))
+        _abi.mds_get_momentum(self.ctx, p)
+        return p
+
+    def leapfrog_device(self, n_steps: int, step_size: float, prior_sd: float = 0.0, p0_dev=None):
+        cfg = HmcConfig(0, int(n_steps), float(step_size), float(prior_sd), 0)
+        _abi.mds_leapfrog_device(self.ctx, cfg, p0_dev)
+
+    # HMC
+    def hmc_trajectory(self, p0: np.ndarray, step_size: float, n_leapfrog: int, prior_sd: float = 0.0):
+        cfg = HmcConfig(0, int(n_leapfrog), float(step_size), float(prior_sd), 0)
+        x = np.zeros((self.n, self.d))
+        p = np.zeros((self.n, self.d))
+        h0, h1 = _abi.mds_hmc_trajectory(self.ctx, cfg, np.ascontiguousarray(p0, dtype=np.float64), x, p)
+        return dict(x=x, p=p, H0=h0, H1=h1)
+
+    def hmc_run(self, n_iter: int, n_leapfrog: int, step_size: float, prior_sd: float, seed: int,
+                x0: np.ndarray | None = None):
+        cfg = HmcConfig(int(n_iter), int(n_leapfrog), float(step_size), float(prior_sd), int(seed))
+        x = None if x0 is None else np.ascontiguousarray(x0, dtype=np.float64).copy()
+        st = _abi.mds_hmc_run(self.ctx, cfg, x)
+        return x, dict(accepted=st.accepted, grad_evals=st.grad_evals, mean_abs_dH=st.mean_abs_dH,
+                       seconds=st.seconds, final_loglik=st.final_loglik)

@@ -1,0 +1,288 @@
+// mds_hmc.inl -- thin HMC driver (Eq. 5; readings R19, R20).
+// Included at the end of mds_api.cu (same translation unit).
+//
+// Target log pi(x) = log L(x) - |x|^2/(2 tau^2) (iid N(0, tau^2) prior, Eq. 3 with
+// V_G = tau I, Sigma = I; R20), mass M = I, leapfrog
+//   p += eps/2 grad log pi;  x += eps p;  p += eps/2 grad log pi     (L times)
+// The L steps of one transition are captured once into a CUDA graph: per step
+// kick_drift -> [X->fp32] -> tile kernel -> reduce+kick (the reduction kernel
+// applies the second half-kick as it produces each gradient entry).  The only
+// per-transition host sync reads H0 and H1 for the accept/reject.
+
+namespace {
+
+inline uint64_t hmc_mix(uint64_t z) {
+    z += 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+inline double hmc_u01(uint64_t h) { return ((double)(h >> 11) + 1.0) * (1.0 / 9007199254740992.0); }
+inline double hmc_normal(uint64_t seed, uint64_t it, uint64_t q) {
+    const uint64_t h1 = hmc_mix(seed ^ hmc_mix(it ^ hmc_mix(2 * q)));
+    const uint64_t h2 = hmc_mix(seed ^ hmc_mix(it ^ hmc_mix(2 * q + 1)));
+    return std::sqrt(-2.0 * std::log(hmc_u01(h1))) * std::cos(6.283185307179586 * hmc_u01(h2));
+}
+
+mds_status hmc_alloc(mds_ctx c) {
+    const size_t m = (size_t)c->npad * c->d;
+    mds_status st = MDS_OK;
+    const bool fresh = !c->d_p;
+    if (!c->d_p) st = dalloc(c, &c->d_p, m);
+    if (!st && !c->d_gl) st = dalloc(c, &c->d_gl, m);
+    if (!st && !c->d_xsave) st = dalloc(c, &c->d_xsave, m);
+    if (!st && !c->d_glsave) st = dalloc(c, &c->d_glsave, m);
+    if (!st && !c->d_liksave) st = dalloc(c, &c->d_liksave, 1);
+    if (!st && !c->d_H) st = dalloc(c, &c->d_H, 3);
+    if (!st && !c->d_H0) st = dalloc(c, &c->d_H0, 3);
+    if (!st && fresh) {
+        cudaError_t e = cudaMemset(c->d_p, 0, m * sizeof(double));
+        if (e) return fail(c, MDS_E_CUDA, cudaGetErrorString(e));
+    }
+    return st;
+}
+
+mds_status check_hmc_cfg(mds_ctx c, const mds_hmc_config* cfg) {
+    if (!cfg || cfg->n_leapfrog < 1 || !(cfg->step_size > 0.0) || !std::isfinite(cfg->step_size) ||
+        cfg->n_iter < 0 || !std::isfinite(cfg->prior_sd))
+        return fail(c, MDS_E_INVALID_ARG, "bad HMC config (need n_leapfrog >= 1, step_size > 0, n_iter >= 0)");
+    return MDS_OK;
+}
+
+inline double inv_tau2_of(const mds_hmc_config* cfg) {
+    return cfg->prior_sd > 0.0 ? 1.0 / (cfg->prior_sd * cfg->prior_sd) : 0.0;
+}
+
+// gl = grad log pi at the current X; d_lik = log L at the current X
+mds_status hmc_prime(mds_ctx c, double inv_tau2, cudaStream_t s) {
+    KickArgs kk{};
+    mds_status st = run_pass<false>(c, c->d_grad, c->d_lik, kk, s, false);
+    if (st) return st;
+    const int64_t m = c->n * c->d;
+    grad_logpi_kernel<<<(unsigned)((m + 255) / 256), 256, 0, s>>>(c->d_grad, c->d_x, c->d_gl, m, inv_tau2);
+    CK(cudaGetLastError());
+    return MDS_OK;
+}
+
+mds_status hmc_enqueue_steps(mds_ctx c, int L, double eps, double inv_tau2, cudaStream_t s, bool timed = false) {
+    const int64_t m = c->n * c->d;
+    KickArgs kk;
+    kk.p = c->d_p;
+    kk.gl = c->d_gl;
+    kk.x = c->d_x;
+    kk.half_eps = 0.5 * eps;
+    kk.inv_tau2 = inv_tau2;
+    for (int step = 0; step < L; ++step) {
+        kick_drift_kernel<<<(unsigned)((m + 255) / 256), 256, 0, s>>>(c->d_x, c->d_p, c->d_gl, m, 0.5 * eps, eps);
+        mds_status st = run_pass<true>(c, c->d_grad, c->d_lik, kk, s, timed);
+        if (st) return st;
+    }
+    CK(cudaGetLastError());
+    return MDS_OK;
+}
+
+mds_status hmc_energy(mds_ctx c, double* out, double inv_tau2, cudaStream_t s) {
+    hamiltonian_kernel<<<1, 1024, 0, s>>>(c->d_x, c->d_p, c->d_lik, c->n * c->d, inv_tau2, out);
+    CK(cudaGetLastError());
+    return MDS_OK;
+}
+
+struct StreamGuard {
+    cudaStream_t s = nullptr;
+    bool owned = false;
+    ~StreamGuard() {
+        if (owned && s) cudaStreamDestroy(s);
+    }
+};
+
+}  // namespace
+
+extern "C" {
+
+mds_status mds_hmc_trajectory(mds_ctx c, const mds_hmc_config* cfg, const double* p0, double* x_out, double* p_out,
+                              double* H0, double* H1) {
+    GUARD(c);
+    mds_status st = check_hmc_cfg(c, cfg);
+    if (st) return st;
+    if (!p0) return fail(c, MDS_E_INVALID_ARG, "NULL momentum");
+    st = ready(c);
+    if (st) return st;
+    st = hmc_alloc(c);
+    if (st) return st;
+    cudaStream_t s = c->stream;
+    const int64_t m = c->n * c->d;
+    const double it2 = inv_tau2_of(cfg);
+    CK(cudaMemcpyAsync(c->d_xsave, c->d_x, (size_t)c->npad * c->d * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    CK(cudaMemcpyAsync(c->d_p, p0, m * sizeof(double), cudaMemcpyHostToDevice, s));
+    st = hmc_prime(c, it2, s);
+    if (st) return st;
+    st = hmc_energy(c, c->d_H0, it2, s);
+    if (st) return st;
+    st = hmc_enqueue_steps(c, cfg->n_leapfrog, cfg->step_size, it2, s);
+    if (st) return st;
+    st = hmc_energy(c, c->d_H, it2, s);
+    if (st) return st;
+    double h0 = 0, h1 = 0;
+    CK(cudaMemcpyAsync(&h0, c->d_H0, sizeof(double), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(&h1, c->d_H, sizeof(double), cudaMemcpyDeviceToHost, s));
+    if (x_out) CK(cudaMemcpyAsync(x_out, c->d_x, m * sizeof(double), cudaMemcpyDeviceToHost, s));
+    if (p_out) CK(cudaMemcpyAsync(p_out, c->d_p, m * sizeof(double), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(c->d_x, c->d_xsave, (size_t)c->npad * c->d * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    CK(cudaStreamSynchronize(s));
+    c->eval_version = 0;   // internal results now belong to the proposal, not X
+    c->lf_version = 0;
+    if (H0) *H0 = h0;
+    if (H1) *H1 = h1;
+    return MDS_OK;
+}
+
+mds_status mds_leapfrog_device(mds_ctx c, const mds_hmc_config* cfg, const double* p0_dev) {
+    GUARD(c);
+    mds_status st = check_hmc_cfg(c, cfg);
+    if (st) return st;
+    st = ready(c);
+    if (st) return st;
+    st = hmc_alloc(c);
+    if (st) return st;
+    cudaStream_t s = c->stream;
+    const int64_t m = c->n * c->d;
+    const double it2 = inv_tau2_of(cfg);
+    if (p0_dev) CK(cudaMemcpyAsync(c->d_p, p0_dev, m * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    // (re)prime grad log pi unless it is the one the previous steps left for this X
+    if (p0_dev || c->lf_version != c->version || c->lf_inv_tau2 != it2) {
+        st = hmc_prime(c, it2, s);
+        if (st) return st;
+    }
+    st = hmc_enqueue_steps(c, cfg->n_leapfrog, cfg->step_size, it2, s, true);
+    if (st) return st;
+    ++c->version;                    // X moved
+    c->lf_version = c->version;
+    c->lf_inv_tau2 = it2;
+    c->eval_version = c->version;    // d_grad / d_lik hold the pass at the new X
+    return MDS_OK;
+}
+
+mds_status mds_hmc_run(mds_ctx c, const mds_hmc_config* cfg, double* x_inout, mds_hmc_stats* stats) {
+    GUARD(c);
+    mds_status st = check_hmc_cfg(c, cfg);
+    if (st) return st;
+    if (x_inout) {
+        st = mds_set_locations(c, x_inout);
+        if (st) return st;
+    }
+    st = ready(c);
+    if (st) return st;
+    st = hmc_alloc(c);
+    if (st) return st;
+    // graph capture needs a non-legacy stream
+    StreamGuard sg;
+    sg.s = c->stream;
+    if (!sg.s) {
+        CK(cudaStreamCreateWithFlags(&sg.s, cudaStreamNonBlocking));
+        sg.owned = true;
+        CK(cudaDeviceSynchronize());
+    }
+    cudaStream_t s = sg.s;
+    const int64_t m = c->n * c->d;
+    const size_t mbytes = (size_t)c->npad * c->d * sizeof(double);
+    const double it2 = inv_tau2_of(cfg);
+    const int L = cfg->n_leapfrog;
+    const double eps = cfg->step_size;
+
+    // capture the L-step trajectory once (unsharded: the exchange callback of a
+    // sharded context runs on the host, so those launch directly)
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    cudaError_t ce = cudaSuccess;
+    if (c->world == 1) {
+        CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+        st = hmc_enqueue_steps(c, L, eps, it2, s);
+        ce = cudaStreamEndCapture(s, &graph);
+        if (st) {
+            if (graph) cudaGraphDestroy(graph);
+            return st;
+        }
+        if (ce) return fail(c, MDS_E_CUDA, std::string("graph capture: ") + cudaGetErrorString(ce));
+        ce = cudaGraphInstantiate(&exec, graph, 0);
+        cudaGraphDestroy(graph);
+        if (ce) return fail(c, MDS_E_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(ce));
+    }
+
+    std::vector<double> ph((size_t)m);
+    double* ph_pinned = nullptr;
+    if (cudaMallocHost(&ph_pinned, m * sizeof(double)) != cudaSuccess) {
+        cudaGetLastError();
+        ph_pinned = nullptr;
+    }
+    double* pbuf = ph_pinned ? ph_pinned : ph.data();
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+
+    int64_t accepted = 0;
+    double sum_abs_dh = 0.0;
+    double hh[2] = {0, 0};
+    st = hmc_prime(c, it2, s);
+    CK(cudaEventRecord(e0, s));
+    for (int it = 0; it < cfg->n_iter && !st; ++it) {
+        for (int64_t q = 0; q < m; ++q) pbuf[q] = hmc_normal(cfg->seed, (uint64_t)it, (uint64_t)q);
+        ce = cudaMemcpyAsync(c->d_p, pbuf, m * sizeof(double), cudaMemcpyHostToDevice, s);
+        if (!ce) ce = cudaMemcpyAsync(c->d_xsave, c->d_x, mbytes, cudaMemcpyDeviceToDevice, s);
+        if (!ce) ce = cudaMemcpyAsync(c->d_glsave, c->d_gl, m * sizeof(double), cudaMemcpyDeviceToDevice, s);
+        if (!ce) ce = cudaMemcpyAsync(c->d_liksave, c->d_lik, sizeof(double), cudaMemcpyDeviceToDevice, s);
+        if (ce) break;
+        st = hmc_energy(c, c->d_H0, it2, s);
+        if (st) break;
+        if (exec) {
+            ce = cudaGraphLaunch(exec, s);
+            if (ce) break;
+        } else {
+            st = hmc_enqueue_steps(c, L, eps, it2, s);
+            if (st) break;
+        }
+        st = hmc_energy(c, c->d_H, it2, s);
+        if (st) break;
+        ce = cudaMemcpyAsync(&hh[0], c->d_H0, sizeof(double), cudaMemcpyDeviceToHost, s);
+        if (!ce) ce = cudaMemcpyAsync(&hh[1], c->d_H, sizeof(double), cudaMemcpyDeviceToHost, s);
+        if (!ce) ce = cudaStreamSynchronize(s);
+        if (ce) break;
+        const double dH = hh[1] - hh[0];
+        const double u = hmc_u01(hmc_mix(cfg->seed ^ hmc_mix(0xACCE97ull ^ hmc_mix((uint64_t)it))));
+        const bool ok = std::isfinite(dH) && std::log(u) < -dH;
+        sum_abs_dh += std::isfinite(dH) ? std::fabs(dH) : 0.0;
+        if (ok) {
+            ++accepted;
+        } else {
+            ce = cudaMemcpyAsync(c->d_x, c->d_xsave, mbytes, cudaMemcpyDeviceToDevice, s);
+            if (!ce) ce = cudaMemcpyAsync(c->d_gl, c->d_glsave, m * sizeof(double), cudaMemcpyDeviceToDevice, s);
+            if (!ce) ce = cudaMemcpyAsync(c->d_lik, c->d_liksave, sizeof(double), cudaMemcpyDeviceToDevice, s);
+            if (ce) break;
+        }
+    }
+    if (!ce && !st) ce = cudaEventRecord(e1, s);
+    double final_ll = 0.0;
+    if (!ce && !st) ce = cudaMemcpyAsync(&final_ll, c->d_lik, sizeof(double), cudaMemcpyDeviceToHost, s);
+    if (!ce && !st && x_inout) ce = cudaMemcpyAsync(x_inout, c->d_x, m * sizeof(double), cudaMemcpyDeviceToHost, s);
+    if (!ce && !st) ce = cudaStreamSynchronize(s);
+    float ms = 0.f;
+    if (!ce && !st) cudaEventElapsedTime(&ms, e0, e1);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    if (exec) cudaGraphExecDestroy(exec);
+    if (ph_pinned) cudaFreeHost(ph_pinned);
+    if (st) return st;
+    if (ce) return fail(c, MDS_E_CUDA, std::string("hmc: ") + cudaGetErrorString(ce));
+    ++c->version;          // X moved
+    c->eval_version = 0;
+    c->lf_version = 0;
+    if (stats) {
+        stats->accepted = accepted;
+        stats->grad_evals = (int64_t)cfg->n_iter * L;
+        stats->mean_abs_dH = cfg->n_iter ? sum_abs_dh / cfg->n_iter : 0.0;
+        stats->seconds = ms * 1e-3;
+        stats->final_loglik = final_ll;
+    }
+    return MDS_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,173 @@
+// mds_math.cuh -- per-pair arithmetic of the fused MDS likelihood+gradient pass.
+//
+// For one unordered pair (i > j) with squared latent distance s = ||x_i-x_j||^2
+// and observation y this computes
+//   ell = -1/2 log(2 pi sigma^2) - (y - d)^2/(2 sigma^2) - T log Phi(t)   (Eq. 2)
+//   u   = [ (d - y)/sigma^2 + T phi(t)/(sigma Phi(t)) ] / d               (Eq. 6)
+// with d = sqrt(s), t = d/sigma, so that the pair adds -u (x_i - x_j) to g_i and
+// +u (x_i - x_j) to g_j.  The pair's v = u (x_i - x_j) is formed by the caller.
+//
+// Device math, t >= 0 always on this path:
+//   E      = exp(-t^2/2) = exp(-s/(2 sigma^2))     -- one exp, argument from s directly
+//   Q      = 1 - Phi(t) = E q(w),  q = erfcx(t/sqrt2)/2 as a minimax polynomial in
+//            w = (t-K)/(t+K) (one reciprocal); absolute error of Q <= 3e-16
+//   1/Phi, 1/(1+Phi) from ONE reciprocal of Phi(1+Phi)
+//   log Phi = log1p(-Q) = -2 atanh(Q/(2-Q))        -- polynomial in z = (Q/(2-Q))^2 <= 1/9
+//   phi/Phi = E / (sqrt(2 pi) Phi)                 -- shares E with Q
+// The reciprocal and rsqrt seeds come from MUFU (rcp/rsqrt.approx) refined by one
+// cubic Newton step.  About 80 FP64 instructions per pair (D = 2) instead of ~160
+// for libdevice erfc/log1p/exp/div.
+#pragma once
+#include <cstdint>
+#include "mds_coeffs.h"
+
+namespace mdsk {
+
+// Per-sigma constants, passed by value as kernel parameters (constant bank).
+struct SigmaParams {
+    double inv_sigma;        // 1/sigma
+    double inv_sigma2;       // 1/sigma^2
+    double half_inv_sigma2;  // 1/(2 sigma^2)
+    double k0;               // -1/2 log(2 pi sigma^2)
+    double cg;               // 1/(sigma sqrt(2 pi))
+    float inv_sigma_f, inv_sigma2_f, half_inv_sigma2_f, k0_f, cg_f;
+};
+
+// Canonical NaN marks every non-pair slot of the tiled triangle (missing y,
+// i <= j in diagonal tiles, padding).  Tested by its high word only.
+constexpr uint32_t CANON_NAN_HI64 = 0x7FF80000u;
+constexpr uint32_t CANON_NAN_F32 = 0x7FC00000u;
+
+__device__ __forceinline__ double rsqrt_seed(double x) {
+    double r;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+    return r;
+}
+__device__ __forceinline__ double rcp_seed(double x) {
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+    return r;
+}
+__device__ __forceinline__ float rsqrt_f(float x) {
+    float r;
+    asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+__device__ __forceinline__ float rcp_f(float x) {
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+__device__ __forceinline__ float ex2_f(float x) {
+    float r;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+__device__ __forceinline__ float lg2_f(float x) {
+    float r;
+    asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+
+// 1/x to ~1 ulp: MUFU seed (~20 bits) + one cubic Newton step (3 DFMA).
+__device__ __forceinline__ double rcp_refined(double x) {
+    double y0 = rcp_seed(x);
+    double e = fma(-x, y0, 1.0);
+    double ee = fma(e, e, e);
+    return fma(ee, y0, y0);
+}
+
+template <int DEG, typename T>
+__device__ __forceinline__ T horner(const T* c, T x) {
+    T p = c[DEG];
+#pragma unroll
+    for (int k = DEG - 1; k >= 0; --k) p = fma(p, x, c[k]);
+    return p;
+}
+
+__device__ __forceinline__ bool is_missing(double y) {
+    return (uint32_t)__double2hiint(y) == CANON_NAN_HI64;
+}
+__device__ __forceinline__ bool is_missing(float y) {
+    return (uint32_t)__float_as_uint(y) == CANON_NAN_F32;
+}
+
+// ---------------------------------------------------------------- fp64 pair
+template <bool TRUNC>
+__device__ __forceinline__ void pair_f64(double s, double y, const SigmaParams& P,
+                                         double& ell, double& u) {
+    // s >= 2^-1007 for the rsqrt seed (integer max on the high word; s >= 0).
+    const double sc = __hiloint2double(max(__double2hiint(s), 0x01000000), __double2loint(s));
+    const double r0 = rsqrt_seed(sc);
+    const double h = sc * r0;
+    const double e = fma(-h, r0, 1.0);               // 1 - s r0^2
+    const double c = fma(e, 0.375, 0.5);
+    const double re = r0 * e;
+    const double rs = fma(re, c, r0);                // 1/d  (cubic step)
+    const double d = s * rs;                         // exactly 0 when s == 0
+    const double res = y - d;
+    double l = fma(-(res * P.half_inv_sigma2), res, P.k0);
+    if (TRUNC) {
+        const double t = d * P.inv_sigma;
+        double a = s * P.half_inv_sigma2;            // t^2/2 >= 0
+        a = __hiloint2double(min(__double2hiint(a), 0x4085E000), __double2loint(a));  // a <= ~700
+        // E = exp(-a): k = rint(-a log2 e), r = -a - k ln2, E = 2^k p(r)
+        const double MAGIC = 6755399441055744.0;     // 1.5 * 2^52
+        const double kd = fma(a, -1.4426950408889634, MAGIC);
+        const int k = __double2loint(kd);
+        const double fk = kd - MAGIC;
+        double r = fma(fk, -0.6931471805599453, -a);
+        r = fma(fk, -2.3190468138462996e-17, r);
+        const double p = horner<EXP64_DEG>(EXP64_C, r);
+        const double E = __hiloint2double(__double2hiint(p) + (int)((unsigned)k << 20), __double2loint(p));
+        // Q = 1 - Phi(t) = E q(w), w = (t - K)/(t + K)
+        const double rden = rcp_refined(t + KAPPA64);
+        const double w = fma(-2.0 * KAPPA64, rden, 1.0);
+        const double q = horner<Q64_DEG>(Q64_C, w);
+        const double Q = E * q;
+        const double Phi = 1.0 - Q;
+        const double opp = 2.0 - Q;                  // 1 + Phi
+        const double rp = rcp_refined(Phi * opp);    // 1/(Phi (1 + Phi))
+        const double invPhi = opp * rp;
+        const double invOpp = Phi * rp;
+        const double G = (E * P.cg) * invPhi;        // phi(t) / (sigma Phi(t))
+        const double sa = Q * invOpp;                // Q/(2 - Q), in [0, 1/3]
+        const double at = horner<ATANH64_DEG>(ATANH64_C, sa * sa);
+        l = fma(sa, at, l);                          // - log Phi = 2 atanh(sa)
+        u = fma(-res, P.inv_sigma2, G) * rs;
+    } else {
+        u = (-res * P.inv_sigma2) * rs;
+    }
+    ell = l;
+}
+
+// ---------------------------------------------------------------- fp32 pair
+// fp32 storage and per-pair math (reading R15); MUFU rsqrt/ex2/rcp/lg2.
+template <bool TRUNC>
+__device__ __forceinline__ void pair_f32(float s, float y, const SigmaParams& P,
+                                         float& ell, float& u) {
+    const float sc = fmaxf(s, 1e-30f);
+    const float rs = rsqrt_f(sc);
+    const float d = s * rs;
+    const float res = y - d;
+    float l = fmaf(-(res * P.half_inv_sigma2_f), res, P.k0_f);
+    if (TRUNC) {
+        const float t = d * P.inv_sigma_f;
+        const float a = s * P.half_inv_sigma2_f;
+        const float E = ex2_f(-a * 1.44269504f);
+        const float rden = rcp_f(t + KAPPA32);
+        const float w = fmaf(-2.0f * KAPPA32, rden, 1.0f);
+        const float q = horner<Q32_DEG>(Q32_C, w);
+        const float Q = E * q;
+        const float Phi = 1.0f - Q;
+        const float invPhi = rcp_f(Phi);
+        const float G = (E * P.cg_f) * invPhi;
+        l = fmaf(-0.693147181f, lg2_f(Phi), l);      // - log Phi
+        u = fmaf(-res, P.inv_sigma2_f, G) * rs;
+    } else {
+        u = (-res * P.inv_sigma2_f) * rs;
+    }
+    ell = l;
+}
+
+}  // namespace mdsk

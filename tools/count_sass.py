@@ -1,0 +1,66 @@
+#!/usr/bin/env python
+"""Static SASS instruction mix of the pair kernel's inner loop -> profiles/sass_counts.json.
+
+For every tile_kernel<T, D, TRUNC> instantiation in libmds.so: find the loop
+(the backward branch of the column-group loop), count its instructions by
+class, and divide by the pairs one loop trip evaluates per lane (4).  The
+FP64 count per pair is the 'algorithmic' FP64 work of the roofline.
+"""
+import json
+import os
+import re
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+LIB = os.path.join(ROOT, "paper_1905_04582_b200", "libmds.so")
+OUT = os.path.join(ROOT, "profiles", "sass_counts.json")
+PAIRS_PER_TRIP = 4
+
+FP64 = {"DFMA", "DMUL", "DADD", "DSETP", "DMNMX"}
+FP32 = {"FFMA", "FMUL", "FADD", "FSETP", "FMNMX", "FSEL"}
+
+
+def main():
+    sass = subprocess.check_output(["cuobjdump", "-sass", LIB], text=True)
+    funcs = re.split(r"\n\s+Function : ", sass)
+    res = {}
+    for f in funcs[1:]:
+        name = f.split("\n", 1)[0].strip()
+        m = re.match(r"_ZN4mdsk11tile_kernelI([fd])Li(\d)ELb([01])EEEvNS_8TileArgsE", name)
+        if not m:
+            continue
+        prec = "f64" if m.group(1) == "d" else "f32"
+        d, t = int(m.group(2)), int(m.group(3))
+        lines = re.findall(r"/\*([0-9a-f]{4,})\*/\s+(.*?);", f)
+        ins = [(int(a, 16), txt.strip()) for a, txt in lines]
+        # backward branch of the group loop
+        loop = None
+        for addr, txt in ins:
+            mm = re.match(r"(?:@!?U?P\w+\s+)?BRA(?:\.\w+)*\s+(?:`?\(?)?(?:U?P\w+,\s*)?(0x[0-9a-f]+)", txt)
+            if mm and int(mm.group(1), 16) < addr:
+                cand = (int(mm.group(1), 16), addr)
+                if loop is None or cand[1] - cand[0] > loop[1] - loop[0]:
+                    loop = cand
+        if loop is None:
+            continue
+        body = [txt for addr, txt in ins if loop[0] <= addr <= loop[1]]
+        ops = [re.sub(r"^@!?U?P\w+\s+", "", b).split()[0].split(".")[0] for b in body]
+        n64 = sum(o in FP64 for o in ops)
+        n32 = sum(o in FP32 for o in ops)
+        nmufu = sum(o == "MUFU" for o in ops)
+        res["%s_d%d_t%d" % (prec, d, t)] = {
+            "kernel": name, "loop_instructions": len(ops),
+            "fp64_per_pair": n64 / PAIRS_PER_TRIP, "fp32_per_pair": n32 / PAIRS_PER_TRIP,
+            "mufu_per_pair": nmufu / PAIRS_PER_TRIP, "issued_per_pair": len(ops) / PAIRS_PER_TRIP,
+        }
+    os.makedirs(os.path.dirname(OUT), exist_ok=True)
+    json.dump(res, open(OUT, "w"), indent=1, sort_keys=True)
+    for k in sorted(res):
+        r = res[k]
+        print("%-10s fp64/pair %6.2f  fp32/pair %6.2f  mufu/pair %4.2f  issued/pair %6.2f" % (
+            k, r["fp64_per_pair"], r["fp32_per_pair"], r["mufu_per_pair"], r["issued_per_pair"]))
+
+
+if __name__ == "__main__":
+    main()
