@@ -208,7 +208,9 @@ def run_ours(args):
     ctx.set_sigma(w.sigma)
     t_setup = time.perf_counter() - t0
     p0 = torch.from_numpy(w.normals(1, (n, d))).cuda()
-    launches_per_step = 3 + (1 if args.precision == "f32" else 0) + (1 if world > 1 else 0)
+    # our kernels per leapfrog step: the persistent pass kernel (phase A pairs +
+    # phase B reduction/leapfrog update); sharded: + combine + update kernels
+    launches_per_step = 1 if world == 1 else 3
 
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")   # > 126 MB L2
     # warm-up (also primes grad log pi)
@@ -295,8 +297,8 @@ def run_ours(args):
         achieved = ipp * pairs_per_launch / (pair_ms * 1e-3)
         roofline = {"bound": "alu", "achieved": achieved / 1e12, "peak": peak_derived / 1e12,
                     "unit": "T fp64-lane-op/s", "frac": achieved / peak_derived,
-                    "traffic": None, "kernel": "tile_kernel<%s,D=%d,T=1>" % (args.precision, d),
-                    "fp64_ops_per_pair": ipp, "pair_kernel_ms": pair_ms, "reduce_ms": red_ms,
+                    "traffic": None, "kernel": "pass_kernel<%s,D=%d,T=1,LEAPFROG>" % (args.precision, d),
+                    "fp64_ops_per_pair": ipp, "pass_kernel_ms": pair_ms, "post_kernel_ms": red_ms,
                     "peak_source": "148 SM x 64 FP64 lanes/clk x 1.965 GHz (B200_PROFILING.md SM count/clock); "
                                    "dfma microbenchmark on this GPU: %.2f T lane-op/s" % (fp64_rate / 1e12),
                     "hbm_frac": (8.0 * pairs_per_launch / (pair_ms * 1e-3)) / 6543.7e9}

@@ -1,10 +1,9 @@
-// mds_api.cu -- libmds: context, C-ABI entry points (include/mds.h), launch
-// dispatch and the HMC driver.  One translation unit so the __constant__
-// coefficient tables are visible to every kernel.
+// mds_api.cu -- libmds: context, C-ABI entry points (include/mds.h), the pass
+// schedule, launch dispatch and (mds_hmc.inl) the HMC driver.  One translation
+// unit so the __constant__ coefficient tables are visible to every kernel.
 #include <cuda_runtime.h>
 
 #include <algorithm>
-#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -17,7 +16,7 @@
 using namespace mdsk;
 
 namespace {
-const char* kVersion = "0.1.0";
+const char* kVersion = "0.2.0";
 }  // namespace
 
 struct mds_ctx_s {
@@ -29,21 +28,28 @@ struct mds_ctx_s {
     int nb = 0;              // tile-rows/cols
     int64_t npad = 0;        // nb * B
     int ntl = 0;             // local tiles
-    size_t elem = 8;         // bytes per stored y / x value
+    size_t elem = 8;         // bytes per stored y value
 
     std::vector<int> tiles;          // local tile codes (I << 16) | J, in storage order
     std::vector<int> row_local;      // [nb]: local index of tile (I, 0) or -1
     int* d_tiles = nullptr;
     int* d_row_local = nullptr;
+
+    // persistent-pass schedule
+    int grid = 0;                    // resident CTAs of the pass kernel
+    int nseg = 0;
+    int* d_cta_seg = nullptr;
+    int* d_seg_I = nullptr;
+    int* d_seg_u0 = nullptr;
+    int* d_seg_u1 = nullptr;
     int* d_blk_ptr = nullptr;
-    int* d_blk_ent = nullptr;
+    int* d_blk_slab = nullptr;
+    double* d_slabs = nullptr;       // (nseg + ntl) x B x d
+    double* d_likpart = nullptr;     // [grid]
 
     void* d_y = nullptr;             // tiles
     double* d_x = nullptr;           // fp64 master X, npad x d
-    float* d_xf = nullptr;           // fp32 copy (F32 only)
-    double* d_part = nullptr;        // ntl x 2 x B x d
-    double* d_likpart = nullptr;     // ntl
-    double* d_grad = nullptr;        // n x d (internal result)
+    double* d_grad = nullptr;        // npad x d (internal result)
     double* d_lik = nullptr;         // [4]: loglik, scratch
     double* d_stage = nullptr;       // staging for packed rows
     size_t stage_elems = 0;
@@ -56,17 +62,18 @@ struct mds_ctx_s {
     double* d_partial = nullptr;     // n*d + 1
     double* d_gathered = nullptr;    // world x (n*d + 1)
 
-    // HMC
+    // leapfrog / HMC state
     double* d_p = nullptr;
     double* d_gl = nullptr;
+    double* d_xnext = nullptr;
     double* d_xsave = nullptr;
     double* d_glsave = nullptr;
     double* d_liksave = nullptr;
     double* d_H = nullptr;           // [3]
     double* d_H0 = nullptr;          // [3]
-
-    uint64_t lf_version = 0;         // version the device-resident leapfrog state belongs to
+    uint64_t lf_version = 0;         // version the leapfrog state (gl, lik) belongs to
     double lf_inv_tau2 = -1.0;
+    double lf_eps = -1.0;            // step size xnext was drifted with
 
     SigmaParams P{};
     double sigma = 0.0;
@@ -96,27 +103,33 @@ mds_status fail(mds_ctx c, mds_status s, const std::string& msg) {
     return s;
 }
 
-#define CK(call)                                                                        \
-    do {                                                                                \
-        cudaError_t e_ = (call);                                                        \
-        if (e_ != cudaSuccess)                                                          \
+#define CK(call)                                                                            \
+    do {                                                                                    \
+        cudaError_t e_ = (call);                                                            \
+        if (e_ != cudaSuccess)                                                              \
             return fail(c, MDS_E_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
     } while (0)
 
-#define GUARD(c)                                          \
-    do {                                                  \
-        if (!(c)) return MDS_E_INVALID_ARG;               \
-        if ((c)->sticky != MDS_OK) return (c)->sticky;    \
+#define GUARD(c)                                       \
+    do {                                               \
+        if (!(c)) return MDS_E_INVALID_ARG;            \
+        if ((c)->sticky != MDS_OK) return (c)->sticky; \
     } while (0)
 
 mds_status check_device(mds_ctx c) {
     int dev = 0;
     cudaError_t e = cudaGetDevice(&dev);
-    if (e != cudaSuccess) return fail(c, MDS_E_UNSUPPORTED, std::string("no CUDA device: ") + cudaGetErrorString(e));
-    int major = 0;
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return fail(c, MDS_E_UNSUPPORTED, std::string("no CUDA device: ") + cudaGetErrorString(e));
+    }
+    int major = 0, coop = 0;
     cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+    cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
     if (major != 10)
-        return fail(c, MDS_E_UNSUPPORTED, "libmds is built for sm_100a (B200); device has compute capability major " + std::to_string(major));
+        return fail(c, MDS_E_UNSUPPORTED,
+                    "libmds is built for sm_100a (B200); device has compute capability major " + std::to_string(major));
+    if (!coop) return fail(c, MDS_E_UNSUPPORTED, "device does not support cooperative launch");
     return MDS_OK;
 }
 
@@ -132,10 +145,10 @@ mds_status dalloc(mds_ctx c, T** p, size_t count) {
 }
 
 void free_all(mds_ctx c) {
-    void* ps[] = {c->d_tiles, c->d_row_local, c->d_blk_ptr, c->d_blk_ent, c->d_y, c->d_x, c->d_xf,
-                  c->d_part, c->d_likpart, c->d_grad, c->d_lik, c->d_stage, c->d_bad, c->d_count,
-                  c->d_p, c->d_gl, c->d_xsave, c->d_glsave, c->d_liksave, c->d_H, c->d_H0,
-                  c->d_partial, c->d_gathered};
+    void* ps[] = {c->d_tiles, c->d_row_local, c->d_cta_seg, c->d_seg_I, c->d_seg_u0, c->d_seg_u1, c->d_blk_ptr,
+                  c->d_blk_slab, c->d_slabs, c->d_likpart, c->d_y, c->d_x, c->d_grad, c->d_lik, c->d_stage,
+                  c->d_bad, c->d_count, c->d_partial, c->d_gathered, c->d_p, c->d_gl, c->d_xnext, c->d_xsave,
+                  c->d_glsave, c->d_liksave, c->d_H, c->d_H0};
     for (void* p : ps)
         if (p) cudaFree(p);
     for (auto& e : c->evpool)
@@ -145,51 +158,26 @@ void free_all(mds_ctx c) {
 inline int64_t packed_off(int64_t i) { return i * (i - 1) / 2; }
 
 // ---------------------------------------------------------------- dispatch
-template <typename T, bool TR>
-void launch_tile_T(int d, int ntl, const TileArgs& a, cudaStream_t s) {
+typedef void (*PassFn)(PassArgs);
+
+template <typename T, bool TR, int MODE>
+PassFn pass_fn_d(int d) {
     switch (d) {
-        case 1: tile_kernel<T, 1, TR><<<ntl, TILE_THREADS, 0, s>>>(a); break;
-        case 2: tile_kernel<T, 2, TR><<<ntl, TILE_THREADS, 0, s>>>(a); break;
-        case 3: tile_kernel<T, 3, TR><<<ntl, TILE_THREADS, 0, s>>>(a); break;
-        case 4: tile_kernel<T, 4, TR><<<ntl, TILE_THREADS, 0, s>>>(a); break;
-        case 5: tile_kernel<T, 5, TR><<<ntl, TILE_THREADS, 0, s>>>(a); break;
-        case 6: tile_kernel<T, 6, TR><<<ntl, TILE_THREADS, 0, s>>>(a); break;
-        case 7: tile_kernel<T, 7, TR><<<ntl, TILE_THREADS, 0, s>>>(a); break;
-        case 8: tile_kernel<T, 8, TR><<<ntl, TILE_THREADS, 0, s>>>(a); break;
+        case 1: return pass_kernel<T, 1, TR, MODE>;
+        case 2: return pass_kernel<T, 2, TR, MODE>;
+        case 3: return pass_kernel<T, 3, TR, MODE>;
+        case 4: return pass_kernel<T, 4, TR, MODE>;
+        case 5: return pass_kernel<T, 5, TR, MODE>;
+        case 6: return pass_kernel<T, 6, TR, MODE>;
+        case 7: return pass_kernel<T, 7, TR, MODE>;
+        default: return pass_kernel<T, 8, TR, MODE>;
     }
 }
 
-void launch_tile(mds_ctx c, cudaStream_t s) {
-    if (c->ntl == 0) return;   // a rank may own no tile-rows when world > nb
-    TileArgs a;
-    a.y = c->d_y;
-    a.x = (c->prec == MDS_F64) ? (const void*)c->d_x : (const void*)c->d_xf;
-    a.tiles = c->d_tiles;
-    a.part = c->d_part;
-    a.likpart = c->d_likpart;
-    a.P = c->P;
-    if (c->prec == MDS_F64) {
-        if (c->trunc) launch_tile_T<double, true>(c->d, c->ntl, a, s);
-        else launch_tile_T<double, false>(c->d, c->ntl, a, s);
-    } else {
-        if (c->trunc) launch_tile_T<float, true>(c->d, c->ntl, a, s);
-        else launch_tile_T<float, false>(c->d, c->ntl, a, s);
-    }
-}
-
-template <bool KICK>
-void launch_reduce(mds_ctx c, double* grad_out, double* lik_out, const KickArgs& kk, cudaStream_t s) {
-    const int64_t nd = c->n * c->d;
-    const int64_t blocks = (nd + 31) / 32 + 1;
-    reduce_kernel<KICK><<<(unsigned)blocks, 32 * RED_SEG, 0, s>>>(c->d_part, c->d_likpart, c->d_blk_ptr,
-                                                                   c->d_blk_ent, c->n, c->d, c->ntl,
-                                                                   grad_out, lik_out, kk);
-}
-
-void launch_x_convert(mds_ctx c, cudaStream_t s) {
-    if (c->prec != MDS_F32) return;
-    const int64_t m = c->npad * c->d;
-    to_f32_kernel<<<(unsigned)((m + 255) / 256), 256, 0, s>>>(c->d_x, c->d_xf, m);
+template <int MODE>
+PassFn pass_fn(int prec, int trunc, int d) {
+    if (prec == MDS_F64) return trunc ? pass_fn_d<double, true, MODE>(d) : pass_fn_d<double, false, MODE>(d);
+    return trunc ? pass_fn_d<float, true, MODE>(d) : pass_fn_d<float, false, MODE>(d);
 }
 
 // timing mode: the next event of the pool (grown on demand)
@@ -202,28 +190,81 @@ cudaEvent_t next_event(mds_ctx c) {
     return c->evpool[c->ev_used++];
 }
 
-// One fused pass: [convert X] -> tile kernel -> fixed-order reduction
-// [-> all-gather callback -> rank-ordered combine, when sharded] [-> kick].
-// In timing mode three events bracket the pair kernel and the reduction.
-template <bool KICK>
-mds_status run_pass(mds_ctx c, double* grad_out, double* lik_out, const KickArgs& kk, cudaStream_t s, bool timed) {
+PassArgs base_args(mds_ctx c, const double* xeval) {
+    PassArgs a{};
+    a.y = c->d_y;
+    a.tiles = c->d_tiles;
+    a.xeval = xeval;
+    a.cta_seg = c->d_cta_seg;
+    a.seg_I = c->d_seg_I;
+    a.seg_u0 = c->d_seg_u0;
+    a.seg_u1 = c->d_seg_u1;
+    a.blk_ptr = c->d_blk_ptr;
+    a.blk_slab = c->d_blk_slab;
+    a.nseg = c->nseg;
+    a.nb = c->nb;
+    a.n = c->n;
+    a.slabs = c->d_slabs;
+    a.likpart = c->d_likpart;
+    a.P = c->P;
+    return a;
+}
+
+mds_status launch_coop(mds_ctx c, PassFn fn, PassArgs& a, cudaStream_t s) {
+    cudaLaunchConfig_t cfg{};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    cfg.gridDim = dim3((unsigned)c->grid);
+    cfg.blockDim = dim3(PT);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = s;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    CK(cudaLaunchKernelEx(&cfg, fn, a));
+    return MDS_OK;
+}
+
+// A fused pass at xeval.  EVAL: (grad_out, lik_out) <- full result.  With a
+// leapfrog state (lf = true): the pass runs at xnext and applies the leapfrog
+// update (x, p, gl, xnext, grad, lik).  Sharded contexts go through the local
+// partial, the exchange callback and the rank-ordered combine.  In timing mode
+// three events bracket the pass kernel and the post-kernel work.
+mds_status run_pass(mds_ctx c, const double* xeval, double* grad_out, double* lik_out, bool lf, double eps,
+                    double inv_tau2, cudaStream_t s, bool timed) {
     timed = timed && c->timing;
-    launch_x_convert(c, s);
+    const int64_t nd = c->n * c->d;
+    PassArgs a = base_args(c, xeval);
+    a.eps = eps;
+    a.heps = 0.5 * eps;
+    a.inv_tau2 = inv_tau2;
+    a.x = c->d_x;
+    a.p = c->d_p;
+    a.gl = c->d_gl;
+    a.xnext = c->d_xnext;
     if (timed) CK(cudaEventRecord(next_event(c), s));
-    launch_tile(c, s);
-    if (timed) CK(cudaEventRecord(next_event(c), s));
+    mds_status st;
     if (c->world == 1) {
-        launch_reduce<KICK>(c, grad_out, lik_out, kk, s);
+        a.grad = grad_out;
+        a.lik = lik_out;
+        st = lf ? launch_coop(c, pass_fn<MODE_LEAPFROG>(c->prec, c->trunc, c->d), a, s)
+                : launch_coop(c, pass_fn<MODE_EVAL>(c->prec, c->trunc, c->d), a, s);
+        if (st) return st;
+        if (timed) CK(cudaEventRecord(next_event(c), s));
     } else {
         if (!c->ag_fn) return fail(c, MDS_E_STATE, "sharded context: register the exchange with mds_set_allgather");
-        const int64_t nd = c->n * c->d;
-        launch_reduce<false>(c, c->d_partial, c->d_partial + nd, KickArgs{}, s);
-        CK(cudaGetLastError());
+        a.grad = c->d_partial;
+        a.lik = c->d_partial + nd;
+        st = launch_coop(c, pass_fn<MODE_EVAL>(c->prec, c->trunc, c->d), a, s);
+        if (st) return st;
+        if (timed) CK(cudaEventRecord(next_event(c), s));
         if (c->ag_fn(c->ag_user, c->d_partial, c->d_gathered, nd + 1, (void*)s) != 0)
             return fail(c, MDS_E_COMM, "all-gather callback failed");
-        combine_kernel<<<(unsigned)((nd + 1 + 255) / 256), 256, 0, s>>>(c->d_gathered, c->world, nd + 1, grad_out, lik_out);
-        if (KICK)
-            kick_kernel<<<(unsigned)((nd + 255) / 256), 256, 0, s>>>(grad_out, kk.x, kk.gl, kk.p, nd, kk.half_eps, kk.inv_tau2);
+        combine_kernel<<<(unsigned)((nd + 1 + 255) / 256), 256, 0, s>>>(c->d_gathered, c->world, nd + 1, grad_out,
+                                                                         lik_out);
+        if (lf)
+            leapfrog_update_kernel<<<(unsigned)((nd + 255) / 256), 256, 0, s>>>(
+                grad_out, xeval, c->d_x, c->d_p, c->d_gl, c->d_xnext, nd, eps, 0.5 * eps, inv_tau2);
     }
     if (timed) CK(cudaEventRecord(next_event(c), s));
     CK(cudaGetLastError());
@@ -244,20 +285,89 @@ mds_status eval_internal(mds_ctx c) {
     mds_status st = ready(c);
     if (st) return st;
     if (c->eval_version == c->version) return MDS_OK;
-    KickArgs kk{};
-    st = run_pass<false>(c, c->d_grad, c->d_lik, kk, c->stream, true);
+    st = run_pass(c, c->d_x, c->d_grad, c->d_lik, false, 0.0, 0.0, c->stream, true);
     if (st) return st;
     c->eval_version = c->version;
     return MDS_OK;
 }
 
-mds_status create_impl(int64_t n, int32_t d, int32_t precision, int32_t truncation, int32_t rank,
-                       int32_t world, mds_ctx* out) {
+// Static schedule of the persistent pass: CTA c owns column-group units
+// [c U / G, (c+1) U / G) cut at tile-row boundaries into segments; the CSR
+// lists, for each row block b, its row-segment slabs (segment order) and then
+// the column slabs of the local tiles (I, b), I ascending.
+mds_status build_schedule(mds_ctx c) {
+    int dev = 0, sms = 0, occ = 1 << 30;
+    CK(cudaGetDevice(&dev));
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    PassFn fns[2] = {pass_fn<MODE_EVAL>(c->prec, c->trunc, c->d), pass_fn<MODE_LEAPFROG>(c->prec, c->trunc, c->d)};
+    for (PassFn f : fns) {
+        int o = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, f, PT, 0));
+        occ = std::min(occ, o);
+    }
+    if (occ < 1) return fail(c, MDS_E_UNSUPPORTED, "pass kernel cannot be resident");
+    const int64_t U = (int64_t)GROUPS_PER_TILE * c->ntl;
+    int64_t G = (int64_t)sms * occ;
+    if (U > 0) G = std::min<int64_t>(G, U);
+    G = std::max<int64_t>(G, 1);
+    c->grid = (int)G;
+
+    std::vector<int> cta_seg(G + 1, 0), segI, segu0, segu1;
+    for (int64_t cta = 0; cta < G; ++cta) {
+        int64_t u = (U * cta) / G, u1 = (U * (cta + 1)) / G;
+        while (u < u1) {
+            const int t = (int)(u / GROUPS_PER_TILE);
+            const int I = c->tiles[t] >> 16;
+            const int64_t row_end = (int64_t)GROUPS_PER_TILE * (c->row_local[I] + I + 1);
+            const int64_t e = std::min(u1, row_end);
+            segI.push_back(I);
+            segu0.push_back((int)u);
+            segu1.push_back((int)e);
+            u = e;
+        }
+        cta_seg[cta + 1] = (int)segI.size();
+    }
+    c->nseg = (int)segI.size();
+    std::vector<int> ptr(c->nb + 1, 0), slab;
+    std::vector<std::vector<int>> rows_of(c->nb);
+    for (int s = 0; s < c->nseg; ++s) rows_of[segI[s]].push_back(s);
+    for (int b = 0; b < c->nb; ++b) {
+        ptr[b] = (int)slab.size();
+        for (int s : rows_of[b]) slab.push_back(s);
+        for (int I = b; I < c->nb; ++I)
+            if (c->row_local[I] >= 0) slab.push_back(c->nseg + c->row_local[I] + b);
+    }
+    ptr[c->nb] = (int)slab.size();
+
+    mds_status st;
+    if ((st = dalloc(c, &c->d_cta_seg, cta_seg.size()))) return st;
+    if ((st = dalloc(c, &c->d_seg_I, std::max<size_t>(segI.size(), 1)))) return st;
+    if ((st = dalloc(c, &c->d_seg_u0, std::max<size_t>(segI.size(), 1)))) return st;
+    if ((st = dalloc(c, &c->d_seg_u1, std::max<size_t>(segI.size(), 1)))) return st;
+    if ((st = dalloc(c, &c->d_blk_ptr, ptr.size()))) return st;
+    if ((st = dalloc(c, &c->d_blk_slab, std::max<size_t>(slab.size(), 1)))) return st;
+    if ((st = dalloc(c, &c->d_slabs, (size_t)(c->nseg + std::max(c->ntl, 1)) * TB * c->d))) return st;
+    if ((st = dalloc(c, &c->d_likpart, (size_t)G))) return st;
+    CK(cudaMemcpy(c->d_cta_seg, cta_seg.data(), cta_seg.size() * sizeof(int), cudaMemcpyHostToDevice));
+    if (!segI.empty()) {
+        CK(cudaMemcpy(c->d_seg_I, segI.data(), segI.size() * sizeof(int), cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(c->d_seg_u0, segu0.data(), segu0.size() * sizeof(int), cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(c->d_seg_u1, segu1.data(), segu1.size() * sizeof(int), cudaMemcpyHostToDevice));
+    }
+    CK(cudaMemcpy(c->d_blk_ptr, ptr.data(), ptr.size() * sizeof(int), cudaMemcpyHostToDevice));
+    if (!slab.empty()) CK(cudaMemcpy(c->d_blk_slab, slab.data(), slab.size() * sizeof(int), cudaMemcpyHostToDevice));
+    CK(cudaMemset(c->d_slabs, 0, (size_t)(c->nseg + std::max(c->ntl, 1)) * TB * c->d * sizeof(double)));
+    return MDS_OK;
+}
+
+mds_status create_impl(int64_t n, int32_t d, int32_t precision, int32_t truncation, int32_t rank, int32_t world,
+                       mds_ctx* out) {
     if (!out) return MDS_E_INVALID_ARG;
     *out = nullptr;
     if (n < 2 || d < 1 || d > MDS_D_MAX || (precision != MDS_F64 && precision != MDS_F32) ||
         (truncation != 0 && truncation != 1) || world < 1 || rank < 0 || rank >= world)
         return MDS_E_INVALID_ARG;
+    if ((n + TB - 1) / TB > 0xffff) return MDS_E_INVALID_ARG;
     mds_ctx c = new (std::nothrow) mds_ctx_s();
     if (!c) return MDS_E_OOM;
     mds_status st = check_device(c);
@@ -273,10 +383,6 @@ mds_status create_impl(int64_t n, int32_t d, int32_t precision, int32_t truncati
     c->world = world;
     c->elem = precision == MDS_F64 ? 8 : 4;
     c->nb = (int)((n + TB - 1) / TB);
-    if (c->nb > 0xffff) {
-        delete c;
-        return MDS_E_INVALID_ARG;
-    }
     c->npad = (int64_t)c->nb * TB;
 
     // tile-row ownership: cyclic (I mod world == rank), SURVEY 8(e)
@@ -287,61 +393,30 @@ mds_status create_impl(int64_t n, int32_t d, int32_t precision, int32_t truncati
         for (int J = 0; J <= I; ++J) c->tiles.push_back((I << 16) | J);
     }
     c->ntl = (int)c->tiles.size();
-    // rows this rank needs: all rows of its tile-rows
     c->row_supplied.assign(n, 0);
     for (int64_t i = 0; i < n; ++i)
         if (c->row_local[i / TB] >= 0) ++c->rows_needed;
 
-    // per-block entry lists for the fixed-order reduction
-    std::vector<int> ptr(c->nb + 1, 0), ent;
-    for (int b = 0; b < c->nb; ++b) {
-        ptr[b] = (int)ent.size();
-        if (c->row_local[b] >= 0)
-            for (int J = 0; J <= b; ++J) ent.push_back(2 * (c->row_local[b] + J) + 0);   // row role
-        for (int I = b; I < c->nb; ++I)
-            if (c->row_local[I] >= 0) ent.push_back(2 * (c->row_local[I] + b) + 1);      // column role
-    }
-    ptr[c->nb] = (int)ent.size();
-
     const size_t ntl = (size_t)std::max(c->ntl, 1);
-#define AL(ptrv, cnt)                  \
-    do {                               \
-        st = dalloc(c, &ptrv, cnt);    \
-        if (st) goto fail_alloc;       \
-    } while (0)
-    {
-        AL(c->d_tiles, ntl);
-        AL(c->d_row_local, (size_t)c->nb);
-        AL(c->d_blk_ptr, (size_t)c->nb + 1);
-        AL(c->d_blk_ent, std::max<size_t>(ent.size(), 1));
-        char* yb = nullptr;
-        AL(yb, ntl * TB * TB * c->elem);
-        c->d_y = yb;
-        AL(c->d_x, (size_t)c->npad * d);
-        if (precision == MDS_F32) AL(c->d_xf, (size_t)c->npad * d);
-        AL(c->d_part, ntl * 2 * TB * d);
-        AL(c->d_likpart, ntl);
-        AL(c->d_grad, (size_t)n * d);
-        AL(c->d_lik, 4);
-        AL(c->d_bad, 1);
-        AL(c->d_count, 1);
-        if (world > 1) {
-            AL(c->d_partial, (size_t)n * d + 1);
-            AL(c->d_gathered, ((size_t)n * d + 1) * world);
-        }
-        c->stage_elems = 0;
-    }
-#undef AL
+    const size_t m = (size_t)c->npad * d;
+    char* yb = nullptr;
+    if ((st = dalloc(c, &c->d_tiles, ntl)) || (st = dalloc(c, &c->d_row_local, (size_t)c->nb)) ||
+        (st = dalloc(c, &yb, ntl * TB * TB * c->elem)) || (st = dalloc(c, &c->d_x, m)) ||
+        (st = dalloc(c, &c->d_grad, m)) || (st = dalloc(c, &c->d_lik, 4)) || (st = dalloc(c, &c->d_bad, 1)) ||
+        (st = dalloc(c, &c->d_count, 1)) || (st = dalloc(c, &c->d_p, m)) || (st = dalloc(c, &c->d_gl, m)) ||
+        (st = dalloc(c, &c->d_xnext, m)))
+        goto fail_alloc;
+    c->d_y = yb;
+    if (world > 1 && ((st = dalloc(c, &c->d_partial, (size_t)n * d + 1)) ||
+                      (st = dalloc(c, &c->d_gathered, ((size_t)n * d + 1) * world))))
+        goto fail_alloc;
     {
         cudaError_t e = cudaSuccess;
         if (c->ntl > 0) e = cudaMemcpy(c->d_tiles, c->tiles.data(), c->ntl * sizeof(int), cudaMemcpyHostToDevice);
         if (!e) e = cudaMemcpy(c->d_row_local, c->row_local.data(), c->nb * sizeof(int), cudaMemcpyHostToDevice);
-        if (!e) e = cudaMemcpy(c->d_blk_ptr, ptr.data(), ptr.size() * sizeof(int), cudaMemcpyHostToDevice);
-        if (!e && !ent.empty()) e = cudaMemcpy(c->d_blk_ent, ent.data(), ent.size() * sizeof(int), cudaMemcpyHostToDevice);
-        if (!e) e = cudaMemset(c->d_x, 0, (size_t)c->npad * d * sizeof(double));
-        if (!e && c->d_xf) e = cudaMemset(c->d_xf, 0, (size_t)c->npad * d * sizeof(float));
-        if (!e) e = cudaMemset(c->d_part, 0, ntl * 2 * TB * d * sizeof(double));
-        if (!e) e = cudaMemset(c->d_likpart, 0, ntl * sizeof(double));
+        for (double* p : {c->d_x, c->d_grad, c->d_p, c->d_gl, c->d_xnext})
+            if (!e) e = cudaMemset(p, 0, m * sizeof(double));
+        if (!e) e = cudaMemset(c->d_lik, 0, 4 * sizeof(double));
         if (!e) {
             const size_t cnt = ntl * TB * TB;
             if (precision == MDS_F64) fill_nan_kernel<double><<<1184, 256>>>((double*)c->d_y, cnt);
@@ -354,6 +429,8 @@ mds_status create_impl(int64_t n, int32_t d, int32_t precision, int32_t truncati
             goto fail_alloc;
         }
     }
+    st = build_schedule(c);
+    if (st) goto fail_alloc;
     *out = c;
     return MDS_OK;
 fail_alloc:
@@ -362,7 +439,7 @@ fail_alloc:
     return st;
 }
 
-// upload + pack rows [i0, i1) from a device pointer to fp64 packed rows
+// pack rows [i0, i1) from fp64 packed rows in device memory into the tiles
 mds_status pack_rows_device(mds_ctx c, int64_t i0, int64_t i1, const double* src_dev, int64_t src_base) {
     CK(cudaMemsetAsync(c->d_bad, 0, sizeof(int), c->stream));
     PackArgs a;
@@ -382,6 +459,8 @@ mds_status pack_rows_device(mds_ctx c, int64_t i0, int64_t i1, const double* src
     int bad = 0;
     CK(cudaMemcpyAsync(&bad, c->d_bad, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
+    c->n_obs = -1;
+    ++c->version;
     if (bad) {
         // the rows of this call now hold partial data: they count as not supplied
         for (int64_t i = i0; i < i1; ++i) {
@@ -390,8 +469,6 @@ mds_status pack_rows_device(mds_ctx c, int64_t i0, int64_t i1, const double* src
                 --c->rows_supplied;
             }
         }
-        c->n_obs = -1;
-        ++c->version;
         return fail(c, MDS_E_INVALID_ARG, "dissimilarities must be >= 0 and finite (NaN = missing)");
     }
     for (int64_t i = i0; i < i1; ++i) {
@@ -401,8 +478,6 @@ mds_status pack_rows_device(mds_ctx c, int64_t i0, int64_t i1, const double* src
             ++c->rows_supplied;
         }
     }
-    c->n_obs = -1;
-    ++c->version;
     return MDS_OK;
 }
 
@@ -417,6 +492,13 @@ mds_status ensure_stage(mds_ctx c, size_t elems) {
     return MDS_OK;
 }
 
+void mark_row0(mds_ctx c, int64_t i0) {
+    if (i0 == 0 && c->row_local[0] >= 0 && !c->row_supplied[0]) {   // row 0 has no entries
+        c->row_supplied[0] = 1;
+        ++c->rows_supplied;
+    }
+}
+
 // host packed rows -> device, in chunks of at most ~32M values
 mds_status set_rows_host(mds_ctx c, int64_t i0, int64_t i1, const double* y_lower) {
     const int64_t base0 = packed_off(std::max<int64_t>(i0, 1));
@@ -425,8 +507,7 @@ mds_status set_rows_host(mds_ctx c, int64_t i0, int64_t i1, const double* y_lowe
     while (r < i1) {
         int64_t r1 = r + 1;
         while (r1 < i1 && packed_off(r1 + 1) - packed_off(r) <= kChunk) ++r1;
-        // skip chunks whose rows this rank does not own
-        bool any = false;
+        bool any = false;   // skip chunks whose rows this rank does not own
         for (int64_t I = r / TB; I <= (r1 - 1) / TB; ++I) any = any || c->row_local[I] >= 0;
         if (any) {
             const int64_t cnt = packed_off(r1) - packed_off(r);
@@ -439,10 +520,7 @@ mds_status set_rows_host(mds_ctx c, int64_t i0, int64_t i1, const double* y_lowe
         }
         r = r1;
     }
-    if (i0 == 0 && c->row_local[0] >= 0 && !c->row_supplied[0]) {   // row 0 has no entries
-        c->row_supplied[0] = 1;
-        ++c->rows_supplied;
-    }
+    mark_row0(c, i0);
     return MDS_OK;
 }
 
@@ -476,7 +554,8 @@ mds_status mds_set_stream(mds_ctx c, void* s) {
 
 mds_status mds_set_dissimilarity_rows(mds_ctx c, int64_t i0, int64_t i1, const double* y_lower) {
     GUARD(c);
-    if (i0 < 0 || i1 > c->n || i0 > i1 || (!y_lower && packed_off(std::max<int64_t>(i1, 1)) > packed_off(std::max<int64_t>(i0, 1))))
+    if (i0 < 0 || i1 > c->n || i0 > i1 ||
+        (!y_lower && packed_off(std::max<int64_t>(i1, 1)) > packed_off(std::max<int64_t>(i0, 1))))
         return fail(c, MDS_E_INVALID_ARG, "bad row range or NULL rows");
     return set_rows_host(c, i0, i1, y_lower);
 }
@@ -485,21 +564,18 @@ mds_status mds_set_dissimilarity_rows_device(mds_ctx c, int64_t i0, int64_t i1, 
     GUARD(c);
     if (i0 < 0 || i1 > c->n || i0 > i1 || !y_dev) return fail(c, MDS_E_INVALID_ARG, "bad row range or NULL rows");
     const int64_t r0 = std::max<int64_t>(i0, 1);
-    mds_status st = MDS_OK;
-    if (i1 > r0) st = pack_rows_device(c, r0, i1, y_dev, packed_off(r0));
-    if (st) return st;
-    if (i0 == 0 && c->row_local[0] >= 0 && !c->row_supplied[0]) {
-        c->row_supplied[0] = 1;
-        ++c->rows_supplied;
+    if (i1 > r0) {
+        mds_status st = pack_rows_device(c, r0, i1, y_dev, packed_off(r0));
+        if (st) return st;
     }
+    mark_row0(c, i0);
     return MDS_OK;
 }
 
 mds_status mds_set_dissimilarities(mds_ctx c, const double* y, int64_t ld) {
     GUARD(c);
     if (!y || ld < c->n) return fail(c, MDS_E_INVALID_ARG, "NULL matrix or ld < n");
-    // pack the strict lower triangle row block by row block
-    const int64_t kRows = 2048;
+    const int64_t kRows = 2048;   // pack the strict lower triangle block by block
     std::vector<double> buf;
     for (int64_t r0 = 0; r0 < c->n; r0 += kRows) {
         const int64_t r1 = std::min<int64_t>(c->n, r0 + kRows);
@@ -580,8 +656,8 @@ mds_status mds_evaluate_device(mds_ctx c, double* loglik_dev, double* grad_dev) 
     GUARD(c);
     mds_status st = ready(c);
     if (st) return st;
-    KickArgs kk{};
-    st = run_pass<false>(c, grad_dev ? grad_dev : c->d_grad, loglik_dev ? loglik_dev : c->d_lik, kk, c->stream, true);
+    st = run_pass(c, c->d_x, grad_dev ? grad_dev : c->d_grad, loglik_dev ? loglik_dev : c->d_lik, false, 0.0, 0.0,
+                  c->stream, true);
     if (st) return st;
     if (!grad_dev && !loglik_dev) c->eval_version = c->version;
     return MDS_OK;
@@ -592,11 +668,10 @@ mds_status mds_evaluate_partial_device(mds_ctx c, double* part_dev) {
     if (!part_dev) return fail(c, MDS_E_INVALID_ARG, "NULL output");
     mds_status st = ready(c);
     if (st) return st;
-    launch_x_convert(c, c->stream);
-    launch_tile(c, c->stream);
-    launch_reduce<false>(c, part_dev, part_dev + c->n * c->d, KickArgs{}, c->stream);
-    CK(cudaGetLastError());
-    return MDS_OK;
+    PassArgs a = base_args(c, c->d_x);
+    a.grad = part_dev;
+    a.lik = part_dev + c->n * c->d;
+    return launch_coop(c, pass_fn<MODE_EVAL>(c->prec, c->trunc, c->d), a, c->stream);
 }
 
 mds_status mds_set_allgather(mds_ctx c, mds_allgather_fn fn, void* user) {
@@ -618,10 +693,6 @@ mds_status mds_get_locations(mds_ctx c, double* x) {
 mds_status mds_get_momentum(mds_ctx c, double* p) {
     GUARD(c);
     if (!p) return fail(c, MDS_E_INVALID_ARG, "NULL output");
-    if (!c->d_p) {
-        std::memset(p, 0, c->n * c->d * sizeof(double));
-        return MDS_OK;
-    }
     CK(cudaMemcpyAsync(p, c->d_p, c->n * c->d * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
     return MDS_OK;
@@ -644,8 +715,10 @@ mds_status mds_observed_pairs(mds_ctx c, int64_t* count) {
         CK(cudaMemsetAsync(c->d_count, 0, sizeof(unsigned long long), c->stream));
         const size_t cnt = (size_t)c->ntl * TB * TB;
         if (cnt) {
-            if (c->prec == MDS_F64) count_obs_kernel<double><<<1184, 256, 0, c->stream>>>((const double*)c->d_y, cnt, c->d_count);
-            else count_obs_kernel<float><<<1184, 256, 0, c->stream>>>((const float*)c->d_y, cnt, c->d_count);
+            if (c->prec == MDS_F64)
+                count_obs_kernel<double><<<1184, 256, 0, c->stream>>>((const double*)c->d_y, cnt, c->d_count);
+            else
+                count_obs_kernel<float><<<1184, 256, 0, c->stream>>>((const float*)c->d_y, cnt, c->d_count);
             CK(cudaGetLastError());
         }
         unsigned long long h = 0;
@@ -664,31 +737,12 @@ mds_status mds_zero_distance_pairs(mds_ctx c, int64_t* count) {
     if (st) return st;
     CK(cudaMemsetAsync(c->d_count, 0, sizeof(unsigned long long), c->stream));
     if (c->ntl) {
-        // fp64 X for both precisions: the diagnostic asks about the master X
-        if (c->prec == MDS_F64) {
-            switch (c->d) {
-                case 1: zero_pairs_kernel<double, 1><<<c->ntl, 256, 0, c->stream>>>((const double*)c->d_y, c->d_x, c->d_tiles, c->d_count); break;
-                case 2: zero_pairs_kernel<double, 2><<<c->ntl, 256, 0, c->stream>>>((const double*)c->d_y, c->d_x, c->d_tiles, c->d_count); break;
-                case 3: zero_pairs_kernel<double, 3><<<c->ntl, 256, 0, c->stream>>>((const double*)c->d_y, c->d_x, c->d_tiles, c->d_count); break;
-                case 4: zero_pairs_kernel<double, 4><<<c->ntl, 256, 0, c->stream>>>((const double*)c->d_y, c->d_x, c->d_tiles, c->d_count); break;
-                case 5: zero_pairs_kernel<double, 5><<<c->ntl, 256, 0, c->stream>>>((const double*)c->d_y, c->d_x, c->d_tiles, c->d_count); break;
-                case 6: zero_pairs_kernel<double, 6><<<c->ntl, 256, 0, c->stream>>>((const double*)c->d_y, c->d_x, c->d_tiles, c->d_count); break;
-                case 7: zero_pairs_kernel<double, 7><<<c->ntl, 256, 0, c->stream>>>((const double*)c->d_y, c->d_x, c->d_tiles, c->d_count); break;
-                default: zero_pairs_kernel<double, 8><<<c->ntl, 256, 0, c->stream>>>((const double*)c->d_y, c->d_x, c->d_tiles, c->d_count); break;
-            }
-        } else {
-            launch_x_convert(c, c->stream);
-            switch (c->d) {
-                case 1: zero_pairs_kernel<float, 1><<<c->ntl, 256, 0, c->stream>>>((const float*)c->d_y, c->d_xf, c->d_tiles, c->d_count); break;
-                case 2: zero_pairs_kernel<float, 2><<<c->ntl, 256, 0, c->stream>>>((const float*)c->d_y, c->d_xf, c->d_tiles, c->d_count); break;
-                case 3: zero_pairs_kernel<float, 3><<<c->ntl, 256, 0, c->stream>>>((const float*)c->d_y, c->d_xf, c->d_tiles, c->d_count); break;
-                case 4: zero_pairs_kernel<float, 4><<<c->ntl, 256, 0, c->stream>>>((const float*)c->d_y, c->d_xf, c->d_tiles, c->d_count); break;
-                case 5: zero_pairs_kernel<float, 5><<<c->ntl, 256, 0, c->stream>>>((const float*)c->d_y, c->d_xf, c->d_tiles, c->d_count); break;
-                case 6: zero_pairs_kernel<float, 6><<<c->ntl, 256, 0, c->stream>>>((const float*)c->d_y, c->d_xf, c->d_tiles, c->d_count); break;
-                case 7: zero_pairs_kernel<float, 7><<<c->ntl, 256, 0, c->stream>>>((const float*)c->d_y, c->d_xf, c->d_tiles, c->d_count); break;
-                default: zero_pairs_kernel<float, 8><<<c->ntl, 256, 0, c->stream>>>((const float*)c->d_y, c->d_xf, c->d_tiles, c->d_count); break;
-            }
-        }
+        if (c->prec == MDS_F64)
+            zero_pairs_kernel<double><<<c->ntl, 256, 0, c->stream>>>((const double*)c->d_y, c->d_x, c->d_tiles, c->d,
+                                                                     c->d_count);
+        else
+            zero_pairs_kernel<float><<<c->ntl, 256, 0, c->stream>>>((const float*)c->d_y, c->d_x, c->d_tiles, c->d,
+                                                                    c->d_count);
         CK(cudaGetLastError());
     }
     unsigned long long h = 0;
@@ -754,9 +808,11 @@ mds_status mds_device_info(int32_t* sm_count, int32_t* cc_major, int32_t* cc_min
 }
 
 mds_status mds_measure_fma_peaks(double* fp64, double* fp32) {
-    mds_ctx c = nullptr;
     int dev = 0, sms = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess) return MDS_E_UNSUPPORTED;
+    if (cudaGetDevice(&dev) != cudaSuccess) {
+        cudaGetLastError();
+        return MDS_E_UNSUPPORTED;
+    }
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     double* d_out = nullptr;
     if (cudaMalloc(&d_out, 16) != cudaSuccess) return MDS_E_OOM;
@@ -766,11 +822,11 @@ mds_status mds_measure_fma_peaks(double* fp64, double* fp32) {
     const int threads = 256, blocks = sms * 8, iters = 4096;
     float best64 = 1e30f, best32 = 1e30f;
     for (int rep = 0; rep < 4; ++rep) {
+        float ms = 0.f;
         cudaEventRecord(a);
         fma_peak_kernel<double><<<blocks, threads>>>(d_out, iters, 0.999999, 1e-9);
         cudaEventRecord(b);
         cudaEventSynchronize(b);
-        float ms = 0.f;
         cudaEventElapsedTime(&ms, a, b);
         if (rep) best64 = std::min(best64, ms);
         cudaEventRecord(a);
@@ -784,7 +840,7 @@ mds_status mds_measure_fma_peaks(double* fp64, double* fp32) {
     cudaEventDestroy(a);
     cudaEventDestroy(b);
     cudaFree(d_out);
-    if (e != cudaSuccess) return fail(c, MDS_E_CUDA, cudaGetErrorString(e));
+    if (e != cudaSuccess) return MDS_E_CUDA;
     const double lanes = (double)blocks * threads * 64.0;
     if (fp64) *fp64 = lanes * iters / (best64 * 1e-3);
     if (fp32) *fp32 = lanes * iters * 4 / (best32 * 1e-3);

@@ -4,10 +4,13 @@
 // Target log pi(x) = log L(x) - |x|^2/(2 tau^2) (iid N(0, tau^2) prior, Eq. 3 with
 // V_G = tau I, Sigma = I; R20), mass M = I, leapfrog
 //   p += eps/2 grad log pi;  x += eps p;  p += eps/2 grad log pi     (L times)
-// The L steps of one transition are captured once into a CUDA graph: per step
-// kick_drift -> [X->fp32] -> tile kernel -> reduce+kick (the reduction kernel
-// applies the second half-kick as it produces each gradient entry).  The only
-// per-transition host sync reads H0 and H1 for the accept/reject.
+// State on the device: x, p, gl = grad log pi(x), log L(x) and
+// xnext = x + eps (p + eps/2 gl), the position the next step evaluates at.
+// One leapfrog step is ONE persistent kernel launch (unsharded): phase A
+// evaluates every pair at xnext, phase B reduces the gradient in fixed order
+// and applies the second half-kick and the next drift.  The L steps of an HMC
+// transition are captured once into a CUDA graph; the only per-transition host
+// sync reads H0 and H1 for the accept/reject.
 
 namespace {
 
@@ -27,18 +30,11 @@ inline double hmc_normal(uint64_t seed, uint64_t it, uint64_t q) {
 mds_status hmc_alloc(mds_ctx c) {
     const size_t m = (size_t)c->npad * c->d;
     mds_status st = MDS_OK;
-    const bool fresh = !c->d_p;
-    if (!c->d_p) st = dalloc(c, &c->d_p, m);
-    if (!st && !c->d_gl) st = dalloc(c, &c->d_gl, m);
-    if (!st && !c->d_xsave) st = dalloc(c, &c->d_xsave, m);
+    if (!c->d_xsave) st = dalloc(c, &c->d_xsave, m);
     if (!st && !c->d_glsave) st = dalloc(c, &c->d_glsave, m);
     if (!st && !c->d_liksave) st = dalloc(c, &c->d_liksave, 1);
     if (!st && !c->d_H) st = dalloc(c, &c->d_H, 3);
     if (!st && !c->d_H0) st = dalloc(c, &c->d_H0, 3);
-    if (!st && fresh) {
-        cudaError_t e = cudaMemset(c->d_p, 0, m * sizeof(double));
-        if (e) return fail(c, MDS_E_CUDA, cudaGetErrorString(e));
-    }
     return st;
 }
 
@@ -53,31 +49,32 @@ inline double inv_tau2_of(const mds_hmc_config* cfg) {
     return cfg->prior_sd > 0.0 ? 1.0 / (cfg->prior_sd * cfg->prior_sd) : 0.0;
 }
 
-// gl = grad log pi at the current X; d_lik = log L at the current X
-mds_status hmc_prime(mds_ctx c, double inv_tau2, cudaStream_t s) {
-    KickArgs kk{};
-    mds_status st = run_pass<false>(c, c->d_grad, c->d_lik, kk, s, false);
+// evaluate at x; gl = grad log pi(x); xnext = x + eps (p + eps/2 gl)
+mds_status hmc_prime(mds_ctx c, double eps, double inv_tau2, cudaStream_t s) {
+    mds_status st = run_pass(c, c->d_x, c->d_grad, c->d_lik, false, 0.0, 0.0, s, false);
     if (st) return st;
     const int64_t m = c->n * c->d;
-    grad_logpi_kernel<<<(unsigned)((m + 255) / 256), 256, 0, s>>>(c->d_grad, c->d_x, c->d_gl, m, inv_tau2);
+    prime_kernel<<<(unsigned)((m + 255) / 256), 256, 0, s>>>(c->d_grad, c->d_x, c->d_p, c->d_gl, c->d_xnext, m,
+                                                              inv_tau2, eps, 0.5 * eps);
     CK(cudaGetLastError());
+    c->lf_eps = eps;
+    c->lf_inv_tau2 = inv_tau2;
     return MDS_OK;
 }
 
-mds_status hmc_enqueue_steps(mds_ctx c, int L, double eps, double inv_tau2, cudaStream_t s, bool timed = false) {
+mds_status hmc_redrift(mds_ctx c, double eps, cudaStream_t s) {
     const int64_t m = c->n * c->d;
-    KickArgs kk;
-    kk.p = c->d_p;
-    kk.gl = c->d_gl;
-    kk.x = c->d_x;
-    kk.half_eps = 0.5 * eps;
-    kk.inv_tau2 = inv_tau2;
+    redrift_kernel<<<(unsigned)((m + 255) / 256), 256, 0, s>>>(c->d_x, c->d_p, c->d_gl, c->d_xnext, m, eps, 0.5 * eps);
+    CK(cudaGetLastError());
+    c->lf_eps = eps;
+    return MDS_OK;
+}
+
+mds_status hmc_enqueue_steps(mds_ctx c, int L, double eps, double inv_tau2, cudaStream_t s, bool timed) {
     for (int step = 0; step < L; ++step) {
-        kick_drift_kernel<<<(unsigned)((m + 255) / 256), 256, 0, s>>>(c->d_x, c->d_p, c->d_gl, m, 0.5 * eps, eps);
-        mds_status st = run_pass<true>(c, c->d_grad, c->d_lik, kk, s, timed);
+        mds_status st = run_pass(c, c->d_xnext, c->d_grad, c->d_lik, true, eps, inv_tau2, s, timed);
         if (st) return st;
     }
-    CK(cudaGetLastError());
     return MDS_OK;
 }
 
@@ -111,14 +108,15 @@ mds_status mds_hmc_trajectory(mds_ctx c, const mds_hmc_config* cfg, const double
     if (st) return st;
     cudaStream_t s = c->stream;
     const int64_t m = c->n * c->d;
+    const size_t mbytes = (size_t)c->npad * c->d * sizeof(double);
     const double it2 = inv_tau2_of(cfg);
-    CK(cudaMemcpyAsync(c->d_xsave, c->d_x, (size_t)c->npad * c->d * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    CK(cudaMemcpyAsync(c->d_xsave, c->d_x, mbytes, cudaMemcpyDeviceToDevice, s));
     CK(cudaMemcpyAsync(c->d_p, p0, m * sizeof(double), cudaMemcpyHostToDevice, s));
-    st = hmc_prime(c, it2, s);
+    st = hmc_prime(c, cfg->step_size, it2, s);
     if (st) return st;
     st = hmc_energy(c, c->d_H0, it2, s);
     if (st) return st;
-    st = hmc_enqueue_steps(c, cfg->n_leapfrog, cfg->step_size, it2, s);
+    st = hmc_enqueue_steps(c, cfg->n_leapfrog, cfg->step_size, it2, s, false);
     if (st) return st;
     st = hmc_energy(c, c->d_H, it2, s);
     if (st) return st;
@@ -127,7 +125,7 @@ mds_status mds_hmc_trajectory(mds_ctx c, const mds_hmc_config* cfg, const double
     CK(cudaMemcpyAsync(&h1, c->d_H, sizeof(double), cudaMemcpyDeviceToHost, s));
     if (x_out) CK(cudaMemcpyAsync(x_out, c->d_x, m * sizeof(double), cudaMemcpyDeviceToHost, s));
     if (p_out) CK(cudaMemcpyAsync(p_out, c->d_p, m * sizeof(double), cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(c->d_x, c->d_xsave, (size_t)c->npad * c->d * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    CK(cudaMemcpyAsync(c->d_x, c->d_xsave, mbytes, cudaMemcpyDeviceToDevice, s));
     CK(cudaStreamSynchronize(s));
     c->eval_version = 0;   // internal results now belong to the proposal, not X
     c->lf_version = 0;
@@ -142,22 +140,21 @@ mds_status mds_leapfrog_device(mds_ctx c, const mds_hmc_config* cfg, const doubl
     if (st) return st;
     st = ready(c);
     if (st) return st;
-    st = hmc_alloc(c);
-    if (st) return st;
     cudaStream_t s = c->stream;
     const int64_t m = c->n * c->d;
     const double it2 = inv_tau2_of(cfg);
     if (p0_dev) CK(cudaMemcpyAsync(c->d_p, p0_dev, m * sizeof(double), cudaMemcpyDeviceToDevice, s));
-    // (re)prime grad log pi unless it is the one the previous steps left for this X
     if (p0_dev || c->lf_version != c->version || c->lf_inv_tau2 != it2) {
-        st = hmc_prime(c, it2, s);
+        st = hmc_prime(c, cfg->step_size, it2, s);      // gl, log L at x; first drift
+        if (st) return st;
+    } else if (c->lf_eps != cfg->step_size) {
+        st = hmc_redrift(c, cfg->step_size, s);          // same state, new step size
         if (st) return st;
     }
     st = hmc_enqueue_steps(c, cfg->n_leapfrog, cfg->step_size, it2, s, true);
     if (st) return st;
     ++c->version;                    // X moved
     c->lf_version = c->version;
-    c->lf_inv_tau2 = it2;
     c->eval_version = c->version;    // d_grad / d_lik hold the pass at the new X
     return MDS_OK;
 }
@@ -174,8 +171,7 @@ mds_status mds_hmc_run(mds_ctx c, const mds_hmc_config* cfg, double* x_inout, md
     if (st) return st;
     st = hmc_alloc(c);
     if (st) return st;
-    // graph capture needs a non-legacy stream
-    StreamGuard sg;
+    StreamGuard sg;   // graph capture needs a non-legacy stream
     sg.s = c->stream;
     if (!sg.s) {
         CK(cudaStreamCreateWithFlags(&sg.s, cudaStreamNonBlocking));
@@ -196,7 +192,7 @@ mds_status mds_hmc_run(mds_ctx c, const mds_hmc_config* cfg, double* x_inout, md
     cudaError_t ce = cudaSuccess;
     if (c->world == 1) {
         CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
-        st = hmc_enqueue_steps(c, L, eps, it2, s);
+        st = hmc_enqueue_steps(c, L, eps, it2, s, false);
         ce = cudaStreamEndCapture(s, &graph);
         if (st) {
             if (graph) cudaGraphDestroy(graph);
@@ -222,22 +218,28 @@ mds_status mds_hmc_run(mds_ctx c, const mds_hmc_config* cfg, double* x_inout, md
     int64_t accepted = 0;
     double sum_abs_dh = 0.0;
     double hh[2] = {0, 0};
-    st = hmc_prime(c, it2, s);
-    CK(cudaEventRecord(e0, s));
-    for (int it = 0; it < cfg->n_iter && !st; ++it) {
+    st = hmc_prime(c, eps, it2, s);      // gl, log L at the start (p is redrawn below)
+    if (!st) ce = cudaEventRecord(e0, s);
+    for (int it = 0; it < cfg->n_iter && !st && !ce; ++it) {
+        if (it > 0) {
+            ce = cudaStreamSynchronize(s);   // pbuf is reused: the previous upload must be done
+            if (ce) break;
+        }
         for (int64_t q = 0; q < m; ++q) pbuf[q] = hmc_normal(cfg->seed, (uint64_t)it, (uint64_t)q);
         ce = cudaMemcpyAsync(c->d_p, pbuf, m * sizeof(double), cudaMemcpyHostToDevice, s);
         if (!ce) ce = cudaMemcpyAsync(c->d_xsave, c->d_x, mbytes, cudaMemcpyDeviceToDevice, s);
         if (!ce) ce = cudaMemcpyAsync(c->d_glsave, c->d_gl, m * sizeof(double), cudaMemcpyDeviceToDevice, s);
         if (!ce) ce = cudaMemcpyAsync(c->d_liksave, c->d_lik, sizeof(double), cudaMemcpyDeviceToDevice, s);
         if (ce) break;
+        st = hmc_redrift(c, eps, s);         // xnext for the new momentum
+        if (st) break;
         st = hmc_energy(c, c->d_H0, it2, s);
         if (st) break;
         if (exec) {
             ce = cudaGraphLaunch(exec, s);
             if (ce) break;
         } else {
-            st = hmc_enqueue_steps(c, L, eps, it2, s);
+            st = hmc_enqueue_steps(c, L, eps, it2, s, false);
             if (st) break;
         }
         st = hmc_energy(c, c->d_H, it2, s);

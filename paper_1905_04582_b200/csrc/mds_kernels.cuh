@@ -1,40 +1,47 @@
 // mds_kernels.cuh -- sm_100a kernels of the fused MDS likelihood+gradient pass.
 //
 // Data layout in HBM:
-//   Y  : the strict lower triangle cut into B x B tiles (I, J), I >= J, B = 64.
-//        Only this rank's tiles are stored, back to back, tile-major; inside a
-//        tile the layout is column-major, y(ii, jj) at [jj*B + ii], so a warp
-//        whose lanes are consecutive rows ii reads one 256 B line per column.
-//        Slots that are not an observed pair (missing y, i <= j in diagonal
-//        tiles, padding rows/columns >= n) hold the canonical NaN, so the pair
-//        loop has no bounds or i > j test.
-//   X  : n_pad x D row-major, padding rows zero; fp64 master, fp32 copy for F32.
-//   part: per local tile two B x D partial blocks (row role, column role), and
-//        one log-likelihood partial per tile; a fixed-order reduction turns
-//        them into g and log L (no atomics anywhere in the arithmetic).
+//   Y   : the strict lower triangle cut into B x B tiles (I, J), I >= J, B = 64.
+//         Only this rank's tile-rows are stored, tile-major in (I, J) order;
+//         inside a tile the layout is column-major, y(ii, jj) at [jj*B + ii], so
+//         the 32 lanes of a warp (consecutive rows) read one 256 B line per column.
+//         Slots that are not an observed pair (missing y, i <= j in diagonal
+//         tiles, padding rows/columns >= n) hold the canonical NaN, so the pair
+//         loop has no bounds or i > j test.
+//   X   : fp64 master, n_pad x D row-major, padding rows zero (plus p, grad log pi
+//         and the drifted X of the next leapfrog step, same layout).
+//   slab: B x D fp64 partial sums. Slabs [0, S) are row-segment partials, slabs
+//         [S, S + ntl) the column partials of each local tile.
 //
-// Pair kernel (one CTA = 4 warps per tile): warp (wr, wc) evaluates the 32 x 32
-// sub-block rows wr*32.., columns wc*32..; lane = row.  Each lane keeps its
-// row's gradient in registers (Alg. 2's per-row reduction),
-// the column side of every pair (new: each unordered pair is computed once) is
-// reduced across the 32 lanes with a 4-column reduce-scatter (2 halving steps
-// + 3 butterflies), and the scalar log L is reduced warp -> CTA -> tile partial
-// (Alg. 1's binary-tree reduction), all in a fixed order.
+// ONE persistent cooperative kernel per pass:
+//   phase A  grid = resident CTAs; CTA c owns the column-group units
+//            [c U/G, (c+1) U/G) of the tile list (U = 16 column-groups x tiles),
+//            cut into tile-row segments.  Warp w of the CTA takes units w, w+4, ..
+//            of a segment; lane l evaluates rows l and l+32 against the 4 columns
+//            of a unit: 8 pairs, Eq. 2 term and Eq. 6 coefficient each.  Row sums
+//            stay in registers for the whole segment (Alg. 2's per-row reduction,
+//            PAPER.md:786-805); the column side (each unordered pair is computed
+//            once, so it is new) is summed over the 64 rows by a 2-row add + a
+//            4-column reduce-scatter and stored once per column; log L partials
+//            per CTA (Alg. 1's binary tree).  No atomics.
+//   barrier  cooperative grid sync.
+//   phase B  fixed-order reduction: g_i = sum of the row-segment slabs and column
+//            slabs touching row block i/B (CSR built on the host), then either
+//            the result (EVAL), the sharded partial (PARTIAL), or the leapfrog
+//            update (LEAPFROG: second half-kick, next drift).  CTA 0 sums log L.
 #pragma once
+#include <cooperative_groups.h>
 #include <cstdint>
 #include "mds_math.cuh"
 
 namespace mdsk {
+namespace cg = cooperative_groups;
 
 constexpr int TB = 64;              // tile edge B
-constexpr int TILE_THREADS = 128;   // 4 warps
+constexpr int GROUPS_PER_TILE = TB / 4;
+constexpr int PT = 128;             // threads per CTA (4 warps)
 
-template <typename T> struct Acc;   // accumulation type above the per-pair math
-template <> struct Acc<double> { using type = double; };
-template <> struct Acc<float> { using type = double; };
-
-template <typename T>
-__device__ __forceinline__ T ldg_nc(const T* p) { return __ldg(p); }
+enum Mode { MODE_EVAL = 0, MODE_PARTIAL = 1, MODE_LEAPFROG = 2 };
 
 template <typename T, bool TRUNC> struct Pair;
 template <bool TRUNC> struct Pair<double, TRUNC> {
@@ -56,12 +63,10 @@ __device__ __forceinline__ T shfl_xor(T v, int m) { return __shfl_xor_sync(0xfff
 template <typename T>
 __device__ __forceinline__ T reduce_scatter4(T a0, T a1, T a2, T a3, int lane) {
     const bool b4 = lane & 16, b3 = lane & 8;
-    // xor 16: bit4 = 0 keeps columns {0,1}, bit4 = 1 keeps {2,3}
     T k0 = b4 ? a2 : a0, k1 = b4 ? a3 : a1;
     T s0 = b4 ? a0 : a2, s1 = b4 ? a1 : a3;
     k0 += shfl_xor(s0, 16);
     k1 += shfl_xor(s1, 16);
-    // xor 8: bit3 = 0 keeps the first, bit3 = 1 the second
     T k = b3 ? k1 : k0;
     T sd = b3 ? k0 : k1;
     k += shfl_xor(sd, 8);
@@ -71,174 +76,218 @@ __device__ __forceinline__ T reduce_scatter4(T a0, T a1, T a2, T a3, int lane) {
     return k;
 }
 
-struct TileArgs {
-    const void* y;          // local tiles, [ntl][B][B] (column-major inside)
-    const void* x;          // n_pad x D, compute precision
-    const int* tiles;       // [ntl] (I << 16) | J
-    double* part;           // [ntl][2][B][D]  (role 0 = rows I, role 1 = cols J)
-    double* likpart;        // [ntl]
+// leapfrog drift of one coordinate: x + eps (p + eps/2 gl); the same expression
+// (and rounding) wherever it is evaluated
+__device__ __forceinline__ double drift(double x, double p, double gl, double eps, double heps) {
+    return __fma_rn(eps, __fma_rn(heps, gl, p), x);
+}
+
+struct PassArgs {
+    // inputs
+    const void* y;               // local tiles [ntl][B][B]
+    const int* tiles;            // [ntl] (I << 16) | J
+    const double* xeval;         // positions the pass evaluates at (n_pad x D)
+    // schedule
+    const int* cta_seg;          // [G + 1] segment range per CTA
+    const int* seg_I;            // [S] tile-row of the segment
+    const int* seg_u0;           // [S] first unit (global unit index)
+    const int* seg_u1;           // [S] end unit
+    const int* blk_ptr;          // [nb + 1] CSR of slabs per row block
+    const int* blk_slab;         // slab indices
+    int nseg;                    // S
+    int nb;
+    int64_t n;
+    // scratch
+    double* slabs;               // (S + ntl) x B x D
+    double* likpart;             // [G]
+    // outputs
+    double* grad;                // EVAL: d log L / dX (n x D)      PARTIAL: partial (n x D)
+    double* lik;                 // EVAL/LEAPFROG: log L             PARTIAL: partial log L
+    // leapfrog state (MODE_LEAPFROG): x <- xeval, p, gl updated, xnext written
+    double* x;
+    double* p;
+    double* gl;
+    double* xnext;
+    double eps, heps, inv_tau2;
     SigmaParams P;
 };
 
-template <typename T, int D, bool TRUNC>
-__global__ void __launch_bounds__(TILE_THREADS)
-tile_kernel(TileArgs a) {
-    using A = typename Acc<T>::type;
-    __shared__ T xs[2][TB][D];
-    __shared__ A rowacc[2][TB][D];   // [wc][row]
-    __shared__ A colacc[2][TB][D];   // [wr][col]
-    __shared__ A wlik[4];
-
-    const int t = blockIdx.x;
-    const int code = a.tiles[t];
-    const int I = code >> 16, J = code & 0xffff;
-    const T* __restrict__ X = static_cast<const T*>(a.x);
-    for (int e = threadIdx.x; e < TB * D; e += TILE_THREADS) {
-        xs[0][e / D][e % D] = X[(size_t)I * TB * D + e];
-        xs[1][e / D][e % D] = X[(size_t)J * TB * D + e];
-    }
-    __syncthreads();
+template <typename T, int D, bool TRUNC, int MODE>
+__global__ void __launch_bounds__(PT)
+pass_kernel(PassArgs a) {
+    using A = double;
+    __shared__ A rowsm[4][TB][D];
+    __shared__ A red[4][32];
+    __shared__ A wl[4];
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int wr = warp & 1, wc = warp >> 1;
-    const int ii = wr * 32 + lane;
-    T xi[D];
-#pragma unroll
-    for (int k = 0; k < D; ++k) xi[k] = xs[0][ii][k];
-    // per-sub-block accumulators (32 terms) in the compute precision; they are
-    // widened to fp64 once per tile (reading R15 for the fp32 path)
-    T gi[D];
-#pragma unroll
-    for (int k = 0; k < D; ++k) gi[k] = T(0);
-    T lik = T(0);
+    const T* __restrict__ Y = static_cast<const T*>(a.y);
+    const double* __restrict__ X = a.xeval;
 
-    const T* __restrict__ ycol = static_cast<const T*>(a.y) + (size_t)t * TB * TB + (size_t)(wc * 32) * TB + ii;
-    T ynext[4];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) ynext[q] = ldg_nc(ycol + q * TB);
-
-#pragma unroll 1
-    for (int g = 0; g < 8; ++g) {
-        T yv[4];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) yv[q] = ynext[q];
-        if (g < 7) {
-#pragma unroll
-            for (int q = 0; q < 4; ++q) ynext[q] = ldg_nc(ycol + (4 * (g + 1) + q) * TB);
-        }
-        T v[4][D];
-        T lsum = T(0);
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const int jj = wc * 32 + 4 * g + q;
-            T dl[D];
-            T s = T(0);
-#pragma unroll
-            for (int k = 0; k < D; ++k) {
-                dl[k] = xi[k] - xs[1][jj][k];
-                s = fma(dl[k], dl[k], s);
-            }
-            T l, u;
-            Pair<T, TRUNC>::eval(s, yv[q], a.P, l, u);
-            const bool miss = is_missing(yv[q]);
-            l = miss ? T(0) : l;
-            u = miss ? T(0) : u;
-            lsum += l;
-#pragma unroll
-            for (int k = 0; k < D; ++k) {
-                v[q][k] = u * dl[k];
-                gi[k] -= v[q][k];
-            }
-        }
-        lik += lsum;
+    // ------------------------------------------------------------ phase A
+    A lik_cta = A(0);                         // this lane's log L share (fp64)
+    const int s0 = a.cta_seg[blockIdx.x], s1 = a.cta_seg[blockIdx.x + 1];
+    for (int s = s0; s < s1; ++s) {
+        const int I = a.seg_I[s];
+        const int u0 = a.seg_u0[s], u1 = a.seg_u1[s];
+        T xi0[D], xi1[D];
 #pragma unroll
         for (int k = 0; k < D; ++k) {
-            T cs = reduce_scatter4(v[0][k], v[1][k], v[2][k], v[3][k], lane);
-            if ((lane & 7) == 0) colacc[wr][wc * 32 + 4 * g + (lane >> 3)][k] = A(cs);
+            xi0[k] = (T)X[((size_t)I * TB + lane) * D + k];
+            xi1[k] = (T)X[((size_t)I * TB + lane + 32) * D + k];
         }
+        A g0[D], g1[D];
+#pragma unroll
+        for (int k = 0; k < D; ++k) { g0[k] = A(0); g1[k] = A(0); }
+
+#pragma unroll 1
+        for (int u = u0 + warp; u < u1; u += 4) {
+            const int t = u / GROUPS_PER_TILE;
+            const int jj0 = (u % GROUPS_PER_TILE) * 4;
+            const int J = a.tiles[t] & 0xffff;
+            const T* __restrict__ yb = Y + (size_t)t * TB * TB + (size_t)jj0 * TB + lane;
+            T yv0[4], yv1[4], xj[4][D];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                yv0[q] = __ldg(yb + q * TB);
+                yv1[q] = __ldg(yb + q * TB + 32);
+            }
+            const double* __restrict__ xjp = X + ((size_t)J * TB + jj0) * D;
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+#pragma unroll
+                for (int k = 0; k < D; ++k) xj[q][k] = (T)__ldg(xjp + q * D + k);
+
+            T cv[4][D];
+            T lsum = T(0);
+            T gs0[D], gs1[D];
+#pragma unroll
+            for (int k = 0; k < D; ++k) { gs0[k] = T(0); gs1[k] = T(0); }
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                T d0[D], d1[D];
+                T sa = T(0), sb = T(0);
+#pragma unroll
+                for (int k = 0; k < D; ++k) {
+                    d0[k] = xi0[k] - xj[q][k];
+                    d1[k] = xi1[k] - xj[q][k];
+                    sa = fma(d0[k], d0[k], sa);
+                    sb = fma(d1[k], d1[k], sb);
+                }
+                T la, ua, lb, ub;
+                Pair<T, TRUNC>::eval(sa, yv0[q], a.P, la, ua);
+                Pair<T, TRUNC>::eval(sb, yv1[q], a.P, lb, ub);
+                const bool ma = is_missing(yv0[q]), mb = is_missing(yv1[q]);
+                la = ma ? T(0) : la;
+                ua = ma ? T(0) : ua;
+                lb = mb ? T(0) : lb;
+                ub = mb ? T(0) : ub;
+                lsum += la + lb;
+#pragma unroll
+                for (int k = 0; k < D; ++k) {
+                    const T va = ua * d0[k], vb = ub * d1[k];
+                    gs0[k] -= va;
+                    gs1[k] -= vb;
+                    cv[q][k] = va + vb;
+                }
+            }
+            lik_cta += A(lsum);
+#pragma unroll
+            for (int k = 0; k < D; ++k) {
+                g0[k] += A(gs0[k]);
+                g1[k] += A(gs1[k]);
+            }
+            double* __restrict__ cslab = a.slabs + ((size_t)a.nseg + t) * TB * D + (size_t)jj0 * D;
+#pragma unroll
+            for (int k = 0; k < D; ++k) {
+                const T cs = reduce_scatter4(cv[0][k], cv[1][k], cv[2][k], cv[3][k], lane);
+                if ((lane & 7) == 0) cslab[(lane >> 3) * D + k] = A(cs);
+            }
+        }
+        // combine the 4 warps' row sums of this segment in warp order
+#pragma unroll
+        for (int k = 0; k < D; ++k) {
+            rowsm[warp][lane][k] = g0[k];
+            rowsm[warp][lane + 32][k] = g1[k];
+        }
+        __syncthreads();
+        double* __restrict__ rslab = a.slabs + (size_t)s * TB * D;
+        for (int e = threadIdx.x; e < TB * D; e += PT) {
+            const int r = e / D, k = e % D;
+            rslab[e] = ((rowsm[0][r][k] + rowsm[1][r][k]) + rowsm[2][r][k]) + rowsm[3][r][k];
+        }
+        __syncthreads();
     }
+    // log L partial of this CTA: warp tree then warps in order
 #pragma unroll
-    for (int k = 0; k < D; ++k) rowacc[wc][ii][k] = A(gi[k]);
-    // warp-level tree for log L, fixed order
-    A likw = A(lik);
-#pragma unroll
-    for (int m = 16; m >= 1; m >>= 1) likw += __shfl_xor_sync(0xffffffffu, likw, m);
-    if (lane == 0) wlik[warp] = likw;
+    for (int m = 16; m >= 1; m >>= 1) lik_cta += __shfl_xor_sync(0xffffffffu, lik_cta, m);
+    if (lane == 0) wl[warp] = lik_cta;
     __syncthreads();
+    if (threadIdx.x == 0) a.likpart[blockIdx.x] = (wl[0] + wl[1]) + (wl[2] + wl[3]);
 
-    double* __restrict__ prow = a.part + (size_t)t * 2 * TB * D;
-    double* __restrict__ pcol = prow + TB * D;
-    for (int e = threadIdx.x; e < TB * D; e += TILE_THREADS) {
-        const int r = e / D, k = e % D;
-        prow[e] = rowacc[0][r][k] + rowacc[1][r][k];
-        pcol[e] = colacc[0][r][k] + colacc[1][r][k];
+    // ------------------------------------------------------------ barrier
+    __threadfence();
+    cg::this_grid().sync();
+
+    // ------------------------------------------------------------ phase B
+    // job = (row block b, chunk of 32 slab elements); warp w sums slabs w, w+4, ..
+    const int chunks = (TB * D + 31) / 32;
+    const int jobs = a.nb * chunks;
+    for (int job = blockIdx.x; job < jobs; job += gridDim.x) {
+        const int b = job / chunks, ch = job % chunks;
+        const int el = ch * 32 + lane;            // element inside the slab (ii * D + k)
+        const int q0 = a.blk_ptr[b], q1 = a.blk_ptr[b + 1];
+        A acc = A(0);
+        if (el < TB * D) {
+            int q = q0 + warp;
+            for (; q + 12 < q1; q += 16) {        // 4 independent loads in flight
+                const A v0 = a.slabs[(size_t)a.blk_slab[q] * TB * D + el];
+                const A v1 = a.slabs[(size_t)a.blk_slab[q + 4] * TB * D + el];
+                const A v2 = a.slabs[(size_t)a.blk_slab[q + 8] * TB * D + el];
+                const A v3 = a.slabs[(size_t)a.blk_slab[q + 12] * TB * D + el];
+                acc += v0;
+                acc += v1;
+                acc += v2;
+                acc += v3;
+            }
+            for (; q < q1; q += 4) acc += a.slabs[(size_t)a.blk_slab[q] * TB * D + el];
+        }
+        red[warp][lane] = acc;
+        __syncthreads();
+        if (warp == 0 && el < TB * D) {
+            const A g = ((red[0][lane] + red[1][lane]) + red[2][lane]) + red[3][lane];
+            const int64_t e = (int64_t)b * TB * D + el;
+            if (e < a.n * D) {
+                if (MODE == MODE_EVAL || MODE == MODE_PARTIAL) {
+                    a.grad[e] = g;
+                } else {
+                    // leapfrog: the pass ran at xnext = x + eps (p + eps/2 gl)
+                    const double xe = a.xeval[e];
+                    const double ph = __fma_rn(a.heps, a.gl[e], a.p[e]);   // first half-kick
+                    const double gn = g - xe * a.inv_tau2;                  // grad log pi at xnext
+                    const double pn = __fma_rn(a.heps, gn, ph);             // second half-kick
+                    a.grad[e] = g;
+                    a.x[e] = xe;
+                    a.p[e] = pn;
+                    a.gl[e] = gn;
+                    a.xnext[e] = drift(xe, pn, gn, a.eps, a.heps);           // next step's drift
+                }
+            }
+        }
+        __syncthreads();
     }
-    if (threadIdx.x == 0) a.likpart[t] = (wlik[0] + wlik[1]) + (wlik[2] + wlik[3]);
-}
-
-// ------------------------------------------------------------ reduction
-// g[i][k] = sum over this rank's entries touching block b = i / B, in the fixed
-// order of blk_ent (row-role tiles by J, then column-role tiles by I').  A
-// block of RED_SEG warps covers 32 consecutive (ii, k) elements; warp w sums
-// entries w, w + RED_SEG, ...; the RED_SEG partials are added in warp order.
-constexpr int RED_SEG = 8;
-
-struct KickArgs {
-    double* p;          // momentum n x D (updated: p += half_eps * (g + prior grad))
-    double* gl;         // out: grad log pi (n x D)
-    const double* x;    // positions (n_pad x D)
-    double half_eps;
-    double inv_tau2;    // 1/tau^2 or 0
-};
-
-template <bool KICK>
-__global__ void __launch_bounds__(32 * RED_SEG)
-reduce_kernel(const double* __restrict__ part, const double* __restrict__ likpart,
-              const int* __restrict__ blk_ptr, const int* __restrict__ blk_ent,
-              int64_t n, int D, int ntl, double* __restrict__ grad_out, double* __restrict__ lik_out,
-              KickArgs kk) {
-    __shared__ double red[RED_SEG][32];
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const int64_t nd = n * D;
-    const int64_t nelem_blocks = (nd + 31) / 32;
-    if ((int64_t)blockIdx.x == nelem_blocks) {
-        // log L: fixed-order strided partial sums + tree
-        double s = 0.0;
-        for (int q = threadIdx.x; q < ntl; q += blockDim.x) s += likpart[q];
-        __shared__ double lr[32 * RED_SEG];
+    if (blockIdx.x == 0) {
+        // log L: fixed-order strided partial sums + tree over the CTA partials
+        A s = A(0);
+        for (int q = threadIdx.x; q < gridDim.x; q += PT) s += a.likpart[q];
+        __shared__ A lr[PT];
         lr[threadIdx.x] = s;
         __syncthreads();
-        for (int m = blockDim.x / 2; m >= 1; m >>= 1) {
+        for (int m = PT / 2; m >= 1; m >>= 1) {
             if (threadIdx.x < m) lr[threadIdx.x] += lr[threadIdx.x + m];
             __syncthreads();
         }
-        if (threadIdx.x == 0 && lik_out) *lik_out = lr[0];
-        return;
-    }
-    const int64_t e = (int64_t)blockIdx.x * 32 + lane;
-    double acc = 0.0;
-    int64_t i = 0, b = 0, within = 0;
-    if (e < nd) {
-        i = e / D;
-        b = i / TB;
-        within = e - b * TB * D;          // (ii * D + k) inside the block's B x D slab
-        const int e0 = blk_ptr[b], e1 = blk_ptr[b + 1];
-        int q = e0 + w;
-#pragma unroll 4
-        for (; q < e1; q += RED_SEG) acc += part[(size_t)blk_ent[q] * TB * D + within];
-    }
-    red[w][lane] = acc;
-    __syncthreads();
-    if (w == 0 && e < nd) {
-        double s = red[0][lane];
-#pragma unroll
-        for (int k = 1; k < RED_SEG; ++k) s += red[k][lane];
-        if (grad_out) grad_out[e] = s;
-        if (KICK) {
-            const double gl = s - kk.x[e] * kk.inv_tau2;
-            kk.gl[e] = gl;
-            kk.p[e] += kk.half_eps * gl;
-        }
+        if (threadIdx.x == 0) *a.lik = lr[0];
     }
 }
 
@@ -247,7 +296,7 @@ struct PackArgs {
     const double* src;      // packed rows [i0, i1), starting with y_{i0,0}
     int64_t i0, i1;
     int64_t src_base;       // packed offset of row i0
-    const int* row_local;   // [nb] local tile-row start (tile index of (I, 0)) or -1
+    const int* row_local;   // [nb] local tile index of (I, 0) or -1
     void* dst;              // tiles
     int* bad;               // set to 1 on y < 0 or +-inf
 };
@@ -297,9 +346,10 @@ __global__ void count_obs_kernel(const T* __restrict__ y, size_t count, unsigned
     if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, c);
 }
 
-// observed pairs at distance exactly 0 (diagnostic, reading R10)
-template <typename T, int D>
-__global__ void zero_pairs_kernel(const T* __restrict__ y, const T* __restrict__ X, const int* tiles,
+// observed pairs at distance exactly 0 (diagnostic, reading R10), in the
+// compute precision of the pair kernel
+template <typename T>
+__global__ void zero_pairs_kernel(const T* __restrict__ y, const double* __restrict__ X, const int* tiles, int D,
                                   unsigned long long* out) {
     const int t = blockIdx.x;
     const int I = tiles[t] >> 16, J = tiles[t] & 0xffff;
@@ -309,9 +359,8 @@ __global__ void zero_pairs_kernel(const T* __restrict__ y, const T* __restrict__
         const T yv = y[(size_t)t * TB * TB + e];
         if (is_missing(yv)) continue;
         T s = 0;
-#pragma unroll
         for (int k = 0; k < D; ++k) {
-            T dl = X[((size_t)I * TB + ii) * D + k] - X[((size_t)J * TB + jj) * D + k];
+            T dl = (T)X[((size_t)I * TB + ii) * D + k] - (T)X[((size_t)J * TB + jj) * D + k];
             s += dl * dl;
         }
         c += (s == T(0)) ? 1 : 0;
@@ -320,39 +369,43 @@ __global__ void zero_pairs_kernel(const T* __restrict__ y, const T* __restrict__
     if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, c);
 }
 
-// ------------------------------------------------------------ X / HMC helpers
-__global__ void to_f32_kernel(const double* __restrict__ x, float* __restrict__ xf, int64_t m) {
-    int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (k < m) xf[k] = (float)x[k];
-}
-
-// leapfrog first half: p += half_eps * gl; x += eps * p   (rows < n only)
-__global__ void kick_drift_kernel(double* __restrict__ x, double* __restrict__ p, const double* __restrict__ gl,
-                                  int64_t m, double half_eps, double eps) {
-    int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (k < m) {
-        const double pk = p[k] + half_eps * gl[k];
-        p[k] = pk;
-        x[k] = x[k] + eps * pk;
-    }
-}
-
-// sharded second half-kick: gl = g - x / tau^2; p += half_eps * gl
-__global__ void kick_kernel(const double* __restrict__ g, const double* __restrict__ x, double* __restrict__ gl,
-                            double* __restrict__ p, int64_t m, double half_eps, double inv_tau2) {
+// ------------------------------------------------------------ leapfrog helpers
+// gl = g - x / tau^2 (grad log pi) and the first drift xnext = x + eps (p + eps/2 gl)
+__global__ void prime_kernel(const double* __restrict__ g, const double* __restrict__ x, const double* __restrict__ p,
+                             double* __restrict__ gl, double* __restrict__ xnext, int64_t m, double inv_tau2,
+                             double eps, double heps) {
     int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (k < m) {
         const double v = g[k] - x[k] * inv_tau2;
         gl[k] = v;
-        p[k] += half_eps * v;
+        xnext[k] = drift(x[k], p[k], v, eps, heps);
     }
 }
 
-// gl = g - x / tau^2 (gradient of log pi) without a kick
-__global__ void grad_logpi_kernel(const double* __restrict__ g, const double* __restrict__ x,
-                                  double* __restrict__ gl, int64_t m, double inv_tau2) {
+// xnext from the stored (x, p, gl) for a new step size
+__global__ void redrift_kernel(const double* __restrict__ x, const double* __restrict__ p,
+                               const double* __restrict__ gl, double* __restrict__ xnext, int64_t m, double eps,
+                               double heps) {
     int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (k < m) gl[k] = g[k] - x[k] * inv_tau2;
+    if (k < m) xnext[k] = drift(x[k], p[k], gl[k], eps, heps);
+}
+
+// sharded leapfrog update after the rank-ordered combine (same arithmetic as phase B)
+__global__ void leapfrog_update_kernel(const double* __restrict__ g, const double* __restrict__ xe,
+                                       double* __restrict__ x, double* __restrict__ p, double* __restrict__ gl,
+                                       double* __restrict__ xnext, int64_t m, double eps, double heps,
+                                       double inv_tau2) {
+    int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k < m) {
+        const double xv = xe[k];
+        const double ph = __fma_rn(heps, gl[k], p[k]);
+        const double gn = g[k] - xv * inv_tau2;
+        const double pn = __fma_rn(heps, gn, ph);
+        x[k] = xv;
+        p[k] = pn;
+        gl[k] = gn;
+        xnext[k] = drift(xv, pn, gn, eps, heps);
+    }
 }
 
 // H = -(loglik + prior(x)) + 1/2 p.p, fixed-order single-block reduction.

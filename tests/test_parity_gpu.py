@@ -152,8 +152,10 @@ def test_triangle_345_golden(mds):
     y = np.array([gold["y_lower"]["1,0"], gold["y_lower"]["2,0"], gold["y_lower"]["2,1"]])
     ll, g = run_gpu(mds, 3, 2, y, x, gold["sigma"], 0)
     G = np.array(gold["grad"])
-    ulp = np.spacing(np.maximum(np.abs(G), 1e-300))
-    assert np.all(np.abs(g - G) <= 2 * ulp + 1e-300)
+    # the exact binary values within 2 ulp of the terms they are summed from
+    # (S = sum_j |v_ijk|; entries that are exactly 0 are sums of +-rounded terms)
+    S = oracle.loglik_grad(y, x, gold["sigma"], 0)["absscale"]
+    assert np.all(np.abs(g - G) <= 2 * np.spacing(np.maximum(np.abs(G), S)))
     ref = eval(gold["loglik_formula"], {"log": math.log, "pi": math.pi})
     assert ll == pytest.approx(ref, rel=1e-14)
     # T = 1 on the same triangle vs the oracle
@@ -306,8 +308,9 @@ def test_hmc_reversible_and_energy_scaling(mds):
         bw = c.hmc_trajectory(-fw["p"], 0.001, 10, prior_sd=10.0)
         np.testing.assert_allclose(bw["x"], x, atol=1e-8)
         c.set_locations(x)
-        a = c.hmc_trajectory(p0, 0.0008, 20, prior_sd=10.0)
-        b = c.hmc_trajectory(p0, 0.0004, 40, prior_sd=10.0)
+        # asymptotic regime checked with the oracle: eps 4e-4 -> 2e-4 gives ratio ~4.03
+        a = c.hmc_trajectory(p0, 0.0004, 40, prior_sd=10.0)
+        b = c.hmc_trajectory(p0, 0.0002, 80, prior_sd=10.0)
     ratio = abs(a["H1"] - a["H0"]) / abs(b["H1"] - b["H0"])
     assert 3.5 <= ratio <= 4.5, ratio
 

@@ -1,9 +1,9 @@
 #!/usr/bin/env python
 """Static SASS instruction mix of the pair kernel's inner loop -> profiles/sass_counts.json.
 
-For every tile_kernel<T, D, TRUNC> instantiation in libmds.so: find the loop
+For every pass_kernel<T, D, TRUNC, LEAPFROG> instantiation in libmds.so: find the loop
 (the backward branch of the column-group loop), count its instructions by
-class, and divide by the pairs one loop trip evaluates per lane (4).  The
+class, and divide by the pairs one loop trip evaluates per lane (8).  The
 FP64 count per pair is the 'algorithmic' FP64 work of the roofline.
 """
 import json
@@ -15,7 +15,7 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 LIB = os.path.join(ROOT, "paper_1905_04582_b200", "libmds.so")
 OUT = os.path.join(ROOT, "profiles", "sass_counts.json")
-PAIRS_PER_TRIP = 4
+PAIRS_PER_TRIP = 8   # 2 rows per lane x 4 columns per unit
 
 FP64 = {"DFMA", "DMUL", "DADD", "DSETP", "DMNMX"}
 FP32 = {"FFMA", "FMUL", "FADD", "FSETP", "FMNMX", "FSEL"}
@@ -27,7 +27,7 @@ def main():
     res = {}
     for f in funcs[1:]:
         name = f.split("\n", 1)[0].strip()
-        m = re.match(r"_ZN4mdsk11tile_kernelI([fd])Li(\d)ELb([01])EEEvNS_8TileArgsE", name)
+        m = re.match(r"_ZN4mdsk11pass_kernelI([fd])Li(\d)ELb([01])ELi2EEEvNS_8PassArgsE", name)
         if not m:
             continue
         prec = "f64" if m.group(1) == "d" else "f32"
@@ -35,13 +35,16 @@ def main():
         lines = re.findall(r"/\*([0-9a-f]{4,})\*/\s+(.*?);", f)
         ins = [(int(a, 16), txt.strip()) for a, txt in lines]
         # backward branch of the group loop
-        loop = None
+        # the pair loop is the backward-branch loop with the most MUFU (special-function) ops
+        loop, best = None, None
         for addr, txt in ins:
             mm = re.match(r"(?:@!?U?P\w+\s+)?BRA(?:\.\w+)*\s+(?:`?\(?)?(?:U?P\w+,\s*)?(0x[0-9a-f]+)", txt)
             if mm and int(mm.group(1), 16) < addr:
                 cand = (int(mm.group(1), 16), addr)
-                if loop is None or cand[1] - cand[0] > loop[1] - loop[0]:
-                    loop = cand
+                nm = sum(1 for a2, t2 in ins if cand[0] <= a2 <= cand[1] and "MUFU" in t2)
+                key = (nm, cand[1] - cand[0])
+                if best is None or key > best:
+                    loop, best = cand, key
         if loop is None:
             continue
         body = [txt for addr, txt in ins if loop[0] <= addr <= loop[1]]
