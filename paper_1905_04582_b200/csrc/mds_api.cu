@@ -37,15 +37,14 @@ struct mds_ctx_s {
 
     // persistent-pass schedule
     int grid = 0;                    // resident CTAs of the pass kernel
+    size_t smem = 0;                 // its dynamic shared memory
     int nseg = 0;
-    int* d_cta_seg = nullptr;
-    int* d_seg_I = nullptr;
-    int* d_seg_u0 = nullptr;
-    int* d_seg_u1 = nullptr;
+    int* d_warp_seg = nullptr;
+    int4* d_segs = nullptr;
     int* d_blk_ptr = nullptr;
     int* d_blk_slab = nullptr;
     double* d_slabs = nullptr;       // (nseg + ntl) x B x d
-    double* d_likpart = nullptr;     // [grid]
+    double* d_likpart = nullptr;     // [4 * grid] (one per warp)
 
     void* d_y = nullptr;             // tiles
     double* d_x = nullptr;           // fp64 master X, npad x d
@@ -145,7 +144,7 @@ mds_status dalloc(mds_ctx c, T** p, size_t count) {
 }
 
 void free_all(mds_ctx c) {
-    void* ps[] = {c->d_tiles, c->d_row_local, c->d_cta_seg, c->d_seg_I, c->d_seg_u0, c->d_seg_u1, c->d_blk_ptr,
+    void* ps[] = {c->d_tiles, c->d_row_local, c->d_warp_seg, c->d_segs, c->d_blk_ptr,
                   c->d_blk_slab, c->d_slabs, c->d_likpart, c->d_y, c->d_x, c->d_grad, c->d_lik, c->d_stage,
                   c->d_bad, c->d_count, c->d_partial, c->d_gathered, c->d_p, c->d_gl, c->d_xnext, c->d_xsave,
                   c->d_glsave, c->d_liksave, c->d_H, c->d_H0};
@@ -160,22 +159,32 @@ inline int64_t packed_off(int64_t i) { return i * (i - 1) / 2; }
 // ---------------------------------------------------------------- dispatch
 typedef void (*PassFn)(PassArgs);
 
+struct PassKernel {
+    PassFn fn;
+    size_t smem;
+};
+
+template <typename T, bool TR, int MODE, int D>
+PassKernel pk() {
+    return PassKernel{pass_kernel<T, D, TR, MODE>, pass_smem_bytes<T, D>()};
+}
+
 template <typename T, bool TR, int MODE>
-PassFn pass_fn_d(int d) {
+PassKernel pass_fn_d(int d) {
     switch (d) {
-        case 1: return pass_kernel<T, 1, TR, MODE>;
-        case 2: return pass_kernel<T, 2, TR, MODE>;
-        case 3: return pass_kernel<T, 3, TR, MODE>;
-        case 4: return pass_kernel<T, 4, TR, MODE>;
-        case 5: return pass_kernel<T, 5, TR, MODE>;
-        case 6: return pass_kernel<T, 6, TR, MODE>;
-        case 7: return pass_kernel<T, 7, TR, MODE>;
-        default: return pass_kernel<T, 8, TR, MODE>;
+        case 1: return pk<T, TR, MODE, 1>();
+        case 2: return pk<T, TR, MODE, 2>();
+        case 3: return pk<T, TR, MODE, 3>();
+        case 4: return pk<T, TR, MODE, 4>();
+        case 5: return pk<T, TR, MODE, 5>();
+        case 6: return pk<T, TR, MODE, 6>();
+        case 7: return pk<T, TR, MODE, 7>();
+        default: return pk<T, TR, MODE, 8>();
     }
 }
 
 template <int MODE>
-PassFn pass_fn(int prec, int trunc, int d) {
+PassKernel pass_fn(int prec, int trunc, int d) {
     if (prec == MDS_F64) return trunc ? pass_fn_d<double, true, MODE>(d) : pass_fn_d<double, false, MODE>(d);
     return trunc ? pass_fn_d<float, true, MODE>(d) : pass_fn_d<float, false, MODE>(d);
 }
@@ -193,12 +202,9 @@ cudaEvent_t next_event(mds_ctx c) {
 PassArgs base_args(mds_ctx c, const double* xeval) {
     PassArgs a{};
     a.y = c->d_y;
-    a.tiles = c->d_tiles;
     a.xeval = xeval;
-    a.cta_seg = c->d_cta_seg;
-    a.seg_I = c->d_seg_I;
-    a.seg_u0 = c->d_seg_u0;
-    a.seg_u1 = c->d_seg_u1;
+    a.warp_seg = c->d_warp_seg;
+    a.segs = c->d_segs;
     a.blk_ptr = c->d_blk_ptr;
     a.blk_slab = c->d_blk_slab;
     a.nseg = c->nseg;
@@ -210,18 +216,18 @@ PassArgs base_args(mds_ctx c, const double* xeval) {
     return a;
 }
 
-mds_status launch_coop(mds_ctx c, PassFn fn, PassArgs& a, cudaStream_t s) {
+mds_status launch_coop(mds_ctx c, PassKernel k, PassArgs& a, cudaStream_t s) {
     cudaLaunchConfig_t cfg{};
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeCooperative;
     attr[0].val.cooperative = 1;
     cfg.gridDim = dim3((unsigned)c->grid);
     cfg.blockDim = dim3(PT);
-    cfg.dynamicSmemBytes = 0;
+    cfg.dynamicSmemBytes = k.smem;
     cfg.stream = s;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    CK(cudaLaunchKernelEx(&cfg, fn, a));
+    CK(cudaLaunchKernelEx(&cfg, k.fn, a));
     return MDS_OK;
 }
 
@@ -291,46 +297,52 @@ mds_status eval_internal(mds_ctx c) {
     return MDS_OK;
 }
 
-// Static schedule of the persistent pass: CTA c owns column-group units
-// [c U / G, (c+1) U / G) cut at tile-row boundaries into segments; the CSR
-// lists, for each row block b, its row-segment slabs (segment order) and then
-// the column slabs of the local tiles (I, b), I ascending.
+// Static schedule of the persistent pass.  The local tiles' column-group
+// units (16 per tile, in tile order) are cut into GW = 4 G equal contiguous
+// ranges, one per warp; each range is cut at tile-row boundaries into
+// segments (I, u0, u1, tbase).  The CSR lists, for each row block b, its row
+// slabs (the segments of tile-row b, in order) and then the column slabs of
+// the local tiles (I, b), I ascending: the fixed order of the reduction.
 mds_status build_schedule(mds_ctx c) {
     int dev = 0, sms = 0, occ = 1 << 30;
     CK(cudaGetDevice(&dev));
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    PassFn fns[2] = {pass_fn<MODE_EVAL>(c->prec, c->trunc, c->d), pass_fn<MODE_LEAPFROG>(c->prec, c->trunc, c->d)};
-    for (PassFn f : fns) {
+    PassKernel ks[2] = {pass_fn<MODE_EVAL>(c->prec, c->trunc, c->d), pass_fn<MODE_LEAPFROG>(c->prec, c->trunc, c->d)};
+    for (PassKernel k : ks) {
+        CK(cudaFuncSetAttribute(k.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k.smem));
         int o = 0;
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, f, PT, 0));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k.fn, PT, k.smem));
         occ = std::min(occ, o);
     }
     if (occ < 1) return fail(c, MDS_E_UNSUPPORTED, "pass kernel cannot be resident");
+    c->smem = ks[0].smem;
     const int64_t U = (int64_t)GROUPS_PER_TILE * c->ntl;
     int64_t G = (int64_t)sms * occ;
-    if (U > 0) G = std::min<int64_t>(G, U);
-    G = std::max<int64_t>(G, 1);
+    G = std::max<int64_t>(std::min<int64_t>(G, (U + 3) / 4), 1);
     c->grid = (int)G;
+    const int64_t GW = 4 * G;
 
-    std::vector<int> cta_seg(G + 1, 0), segI, segu0, segu1;
-    for (int64_t cta = 0; cta < G; ++cta) {
-        int64_t u = (U * cta) / G, u1 = (U * (cta + 1)) / G;
+    std::vector<int> warp_seg(GW + 1, 0);
+    std::vector<int4> segs;
+    for (int64_t w = 0; w < GW; ++w) {
+        int64_t u = (U * w) / GW, u1 = (U * (w + 1)) / GW;
+        int nsw = 0;
         while (u < u1) {
             const int t = (int)(u / GROUPS_PER_TILE);
             const int I = c->tiles[t] >> 16;
             const int64_t row_end = (int64_t)GROUPS_PER_TILE * (c->row_local[I] + I + 1);
             const int64_t e = std::min(u1, row_end);
-            segI.push_back(I);
-            segu0.push_back((int)u);
-            segu1.push_back((int)e);
+            segs.push_back(make_int4(I, (int)u, (int)e, c->row_local[I]));
             u = e;
+            ++nsw;
         }
-        cta_seg[cta + 1] = (int)segI.size();
+        if (nsw > MAXSEG_W) return fail(c, MDS_E_UNSUPPORTED, "schedule: too many segments per warp");
+        warp_seg[w + 1] = (int)segs.size();
     }
-    c->nseg = (int)segI.size();
+    c->nseg = (int)segs.size();
     std::vector<int> ptr(c->nb + 1, 0), slab;
     std::vector<std::vector<int>> rows_of(c->nb);
-    for (int s = 0; s < c->nseg; ++s) rows_of[segI[s]].push_back(s);
+    for (int s = 0; s < c->nseg; ++s) rows_of[segs[s].x].push_back(s);
     for (int b = 0; b < c->nb; ++b) {
         ptr[b] = (int)slab.size();
         for (int s : rows_of[b]) slab.push_back(s);
@@ -340,23 +352,18 @@ mds_status build_schedule(mds_ctx c) {
     ptr[c->nb] = (int)slab.size();
 
     mds_status st;
-    if ((st = dalloc(c, &c->d_cta_seg, cta_seg.size()))) return st;
-    if ((st = dalloc(c, &c->d_seg_I, std::max<size_t>(segI.size(), 1)))) return st;
-    if ((st = dalloc(c, &c->d_seg_u0, std::max<size_t>(segI.size(), 1)))) return st;
-    if ((st = dalloc(c, &c->d_seg_u1, std::max<size_t>(segI.size(), 1)))) return st;
+    const size_t nslab = (size_t)(c->nseg + std::max(c->ntl, 1));
+    if ((st = dalloc(c, &c->d_warp_seg, warp_seg.size()))) return st;
+    if ((st = dalloc(c, &c->d_segs, std::max<size_t>(segs.size(), 1)))) return st;
     if ((st = dalloc(c, &c->d_blk_ptr, ptr.size()))) return st;
     if ((st = dalloc(c, &c->d_blk_slab, std::max<size_t>(slab.size(), 1)))) return st;
-    if ((st = dalloc(c, &c->d_slabs, (size_t)(c->nseg + std::max(c->ntl, 1)) * TB * c->d))) return st;
-    if ((st = dalloc(c, &c->d_likpart, (size_t)G))) return st;
-    CK(cudaMemcpy(c->d_cta_seg, cta_seg.data(), cta_seg.size() * sizeof(int), cudaMemcpyHostToDevice));
-    if (!segI.empty()) {
-        CK(cudaMemcpy(c->d_seg_I, segI.data(), segI.size() * sizeof(int), cudaMemcpyHostToDevice));
-        CK(cudaMemcpy(c->d_seg_u0, segu0.data(), segu0.size() * sizeof(int), cudaMemcpyHostToDevice));
-        CK(cudaMemcpy(c->d_seg_u1, segu1.data(), segu1.size() * sizeof(int), cudaMemcpyHostToDevice));
-    }
+    if ((st = dalloc(c, &c->d_slabs, nslab * TB * c->d))) return st;
+    if ((st = dalloc(c, &c->d_likpart, (size_t)GW))) return st;
+    CK(cudaMemcpy(c->d_warp_seg, warp_seg.data(), warp_seg.size() * sizeof(int), cudaMemcpyHostToDevice));
+    if (!segs.empty()) CK(cudaMemcpy(c->d_segs, segs.data(), segs.size() * sizeof(int4), cudaMemcpyHostToDevice));
     CK(cudaMemcpy(c->d_blk_ptr, ptr.data(), ptr.size() * sizeof(int), cudaMemcpyHostToDevice));
     if (!slab.empty()) CK(cudaMemcpy(c->d_blk_slab, slab.data(), slab.size() * sizeof(int), cudaMemcpyHostToDevice));
-    CK(cudaMemset(c->d_slabs, 0, (size_t)(c->nseg + std::max(c->ntl, 1)) * TB * c->d * sizeof(double)));
+    CK(cudaMemset(c->d_slabs, 0, nslab * TB * c->d * sizeof(double)));
     return MDS_OK;
 }
 

@@ -41,7 +41,7 @@ constexpr int TB = 64;              // tile edge B
 constexpr int GROUPS_PER_TILE = TB / 4;
 constexpr int PT = 128;             // threads per CTA (4 warps)
 
-enum Mode { MODE_EVAL = 0, MODE_PARTIAL = 1, MODE_LEAPFROG = 2 };
+enum Mode { MODE_EVAL = 0, MODE_LEAPFROG = 2 };
 
 template <typename T, bool TRUNC> struct Pair;
 template <bool TRUNC> struct Pair<double, TRUNC> {
@@ -85,13 +85,10 @@ __device__ __forceinline__ double drift(double x, double p, double gl, double ep
 struct PassArgs {
     // inputs
     const void* y;               // local tiles [ntl][B][B]
-    const int* tiles;            // [ntl] (I << 16) | J
     const double* xeval;         // positions the pass evaluates at (n_pad x D)
-    // schedule
-    const int* cta_seg;          // [G + 1] segment range per CTA
-    const int* seg_I;            // [S] tile-row of the segment
-    const int* seg_u0;           // [S] first unit (global unit index)
-    const int* seg_u1;           // [S] end unit
+    // schedule (per global warp gw = blockIdx.x * 4 + warp)
+    const int* warp_seg;         // [GW + 1] segment range per warp
+    const int4* segs;            // [S] (I, u0, u1, tbase): tile-row, unit range, local index of tile (I, 0)
     const int* blk_ptr;          // [nb + 1] CSR of slabs per row block
     const int* blk_slab;         // slab indices
     int nseg;                    // S
@@ -99,10 +96,10 @@ struct PassArgs {
     int64_t n;
     // scratch
     double* slabs;               // (S + ntl) x B x D
-    double* likpart;             // [G]
+    double* likpart;             // [GW]
     // outputs
-    double* grad;                // EVAL: d log L / dX (n x D)      PARTIAL: partial (n x D)
-    double* lik;                 // EVAL/LEAPFROG: log L             PARTIAL: partial log L
+    double* grad;                // EVAL: d log L / dX (n x D)      (sharded: this rank's partial)
+    double* lik;                 // log L                           (sharded: partial)
     // leapfrog state (MODE_LEAPFROG): x <- xeval, p, gl updated, xnext written
     double* x;
     double* p;
@@ -112,52 +109,113 @@ struct PassArgs {
     SigmaParams P;
 };
 
+constexpr int MAXSEG_W = 32;    // segments per warp (host checks)
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t cnt) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(cnt) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t* b, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+// TMA bulk copy global -> shared (SASS UBLKCP), completion counted on the mbarrier
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* b) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(b))
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+    asm volatile(
+        "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}" ::"r"(
+            smem_u32(b)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+// per-warp staging area (dynamic shared memory), double buffered
+template <typename T, int D>
+struct WarpStage {
+    uint64_t bar[2];
+    double xrow[2][TB * D];      // x of the 64 rows of the segment (copied with its first unit)
+    double xj[2][4 * D];         // x of the 4 columns of the unit
+    T y[2][4 * TB];              // the unit's 4 tile columns (contiguous in the tile)
+    int4 seg[MAXSEG_W];
+};
+
+template <typename T, int D>
+constexpr size_t pass_smem_bytes() { return 4 * sizeof(WarpStage<T, D>); }
+
 template <typename T, int D, bool TRUNC, int MODE>
 __global__ void __launch_bounds__(PT)
 pass_kernel(PassArgs a) {
     using A = double;
-    __shared__ A rowsm[4][TB][D];
+    extern __shared__ __align__(128) unsigned char dsm[];
     __shared__ A red[4][32];
-    __shared__ A wl[4];
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int gw = blockIdx.x * 4 + warp;
+    WarpStage<T, D>& W = reinterpret_cast<WarpStage<T, D>*>(dsm)[warp];
     const T* __restrict__ Y = static_cast<const T*>(a.y);
     const double* __restrict__ X = a.xeval;
 
-    // ------------------------------------------------------------ phase A
-    A lik_cta = A(0);                         // this lane's log L share (fp64)
-    const int s0 = a.cta_seg[blockIdx.x], s1 = a.cta_seg[blockIdx.x + 1];
-    for (int s = s0; s < s1; ++s) {
-        const int I = a.seg_I[s];
-        const int u0 = a.seg_u0[s], u1 = a.seg_u1[s];
+    // ------------------------------------------------------------ phase A (per warp)
+    const int ws0 = a.warp_seg[gw], ws1 = a.warp_seg[gw + 1];
+    const int nsw = ws1 - ws0;
+    if (lane < nsw) W.seg[lane] = a.segs[ws0 + lane];
+    if (lane == 0) {
+        mbar_init(&W.bar[0], 1);
+        mbar_init(&W.bar[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        fence_async_smem();
+    }
+    __syncwarp();
+
+    A lik_w = A(0);
+    if (nsw > 0) {
+        constexpr uint32_t YB = 4 * TB * sizeof(T), XJB = 4 * D * sizeof(double), XRB = TB * D * sizeof(double);
+        const int ub = W.seg[0].y, ue = W.seg[nsw - 1].z;
+        // issue the staging copies of unit u (segment index si) into stage st
+        auto issue = [&](int u, int si, int st) {
+            if (lane == 0) {
+                const int4 sg = W.seg[si];
+                const int t = u / GROUPS_PER_TILE, jj0 = (u % GROUPS_PER_TILE) * 4;
+                const int J = t - sg.w;
+                const bool first = (u == sg.y);
+                fence_async_smem();
+                mbar_arrive_tx(&W.bar[st], YB + XJB + (first ? XRB : 0));
+                bulk_g2s(W.y[st], Y + (size_t)t * TB * TB + (size_t)jj0 * TB, YB, &W.bar[st]);
+                bulk_g2s(W.xj[st], X + ((size_t)J * TB + jj0) * D, XJB, &W.bar[st]);
+                if (first) bulk_g2s(W.xrow[st], X + (size_t)sg.x * TB * D, XRB, &W.bar[st]);
+            }
+        };
+        int si = 0, si_next = 0;
+        issue(ub, 0, 0);
+        uint32_t ph0 = 0, ph1 = 0;
         T xi0[D], xi1[D];
-#pragma unroll
-        for (int k = 0; k < D; ++k) {
-            xi0[k] = (T)X[((size_t)I * TB + lane) * D + k];
-            xi1[k] = (T)X[((size_t)I * TB + lane + 32) * D + k];
-        }
         A g0[D], g1[D];
 #pragma unroll
-        for (int k = 0; k < D; ++k) { g0[k] = A(0); g1[k] = A(0); }
-
+        for (int k = 0; k < D; ++k) { xi0[k] = xi1[k] = T(0); g0[k] = g1[k] = A(0); }
 #pragma unroll 1
-        for (int u = u0 + warp; u < u1; u += 4) {
-            const int t = u / GROUPS_PER_TILE;
-            const int jj0 = (u % GROUPS_PER_TILE) * 4;
-            const int J = a.tiles[t] & 0xffff;
-            const T* __restrict__ yb = Y + (size_t)t * TB * TB + (size_t)jj0 * TB + lane;
-            T yv0[4], yv1[4], xj[4][D];
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                yv0[q] = __ldg(yb + q * TB);
-                yv1[q] = __ldg(yb + q * TB + 32);
+        for (int u = ub, kk = 0; u < ue; ++u, ++kk) {
+            const int st = kk & 1;
+            if (u + 1 < ue) {
+                if (u + 1 >= W.seg[si_next].z) ++si_next;
+                __syncwarp();                         // every lane is done with stage st ^ 1
+                issue(u + 1, si_next, st ^ 1);
             }
-            const double* __restrict__ xjp = X + ((size_t)J * TB + jj0) * D;
+            if (st == 0) { mbar_wait(&W.bar[0], ph0); ph0 ^= 1; }
+            else         { mbar_wait(&W.bar[1], ph1); ph1 ^= 1; }
+            const int4 sg = W.seg[si];
+            if (u == sg.y) {                          // first unit of a segment: its 64 rows
 #pragma unroll
-            for (int q = 0; q < 4; ++q)
-#pragma unroll
-                for (int k = 0; k < D; ++k) xj[q][k] = (T)__ldg(xjp + q * D + k);
-
+                for (int k = 0; k < D; ++k) {
+                    xi0[k] = (T)W.xrow[st][lane * D + k];
+                    xi1[k] = (T)W.xrow[st][(lane + 32) * D + k];
+                }
+            }
+            const int t = u / GROUPS_PER_TILE, jj0 = (u % GROUPS_PER_TILE) * 4;
             T cv[4][D];
             T lsum = T(0);
             T gs0[D], gs1[D];
@@ -165,33 +223,35 @@ pass_kernel(PassArgs a) {
             for (int k = 0; k < D; ++k) { gs0[k] = T(0); gs1[k] = T(0); }
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
+                const T ya = W.y[st][q * TB + lane], yb = W.y[st][q * TB + lane + 32];
                 T d0[D], d1[D];
                 T sa = T(0), sb = T(0);
 #pragma unroll
                 for (int k = 0; k < D; ++k) {
-                    d0[k] = xi0[k] - xj[q][k];
-                    d1[k] = xi1[k] - xj[q][k];
+                    const T xjk = (T)W.xj[st][q * D + k];
+                    d0[k] = xi0[k] - xjk;
+                    d1[k] = xi1[k] - xjk;
                     sa = fma(d0[k], d0[k], sa);
                     sb = fma(d1[k], d1[k], sb);
                 }
-                T la, ua, lb, ub;
-                Pair<T, TRUNC>::eval(sa, yv0[q], a.P, la, ua);
-                Pair<T, TRUNC>::eval(sb, yv1[q], a.P, lb, ub);
-                const bool ma = is_missing(yv0[q]), mb = is_missing(yv1[q]);
+                T la, ua, lb, ubb;
+                Pair<T, TRUNC>::eval(sa, ya, a.P, la, ua);
+                Pair<T, TRUNC>::eval(sb, yb, a.P, lb, ubb);
+                const bool ma = is_missing(ya), mb = is_missing(yb);
                 la = ma ? T(0) : la;
                 ua = ma ? T(0) : ua;
                 lb = mb ? T(0) : lb;
-                ub = mb ? T(0) : ub;
+                ubb = mb ? T(0) : ubb;
                 lsum += la + lb;
 #pragma unroll
                 for (int k = 0; k < D; ++k) {
-                    const T va = ua * d0[k], vb = ub * d1[k];
+                    const T va = ua * d0[k], vb = ubb * d1[k];
                     gs0[k] -= va;
                     gs1[k] -= vb;
                     cv[q][k] = va + vb;
                 }
             }
-            lik_cta += A(lsum);
+            lik_w += A(lsum);
 #pragma unroll
             for (int k = 0; k < D; ++k) {
                 g0[k] += A(gs0[k]);
@@ -203,27 +263,22 @@ pass_kernel(PassArgs a) {
                 const T cs = reduce_scatter4(cv[0][k], cv[1][k], cv[2][k], cv[3][k], lane);
                 if ((lane & 7) == 0) cslab[(lane >> 3) * D + k] = A(cs);
             }
-        }
-        // combine the 4 warps' row sums of this segment in warp order
+            if (u + 1 == sg.z) {                      // last unit of the segment: its row partial
+                double* __restrict__ rslab = a.slabs + (size_t)(ws0 + si) * TB * D;
 #pragma unroll
-        for (int k = 0; k < D; ++k) {
-            rowsm[warp][lane][k] = g0[k];
-            rowsm[warp][lane + 32][k] = g1[k];
+                for (int k = 0; k < D; ++k) {
+                    rslab[lane * D + k] = g0[k];
+                    rslab[(lane + 32) * D + k] = g1[k];
+                    g0[k] = A(0);
+                    g1[k] = A(0);
+                }
+                ++si;
+            }
         }
-        __syncthreads();
-        double* __restrict__ rslab = a.slabs + (size_t)s * TB * D;
-        for (int e = threadIdx.x; e < TB * D; e += PT) {
-            const int r = e / D, k = e % D;
-            rslab[e] = ((rowsm[0][r][k] + rowsm[1][r][k]) + rowsm[2][r][k]) + rowsm[3][r][k];
-        }
-        __syncthreads();
     }
-    // log L partial of this CTA: warp tree then warps in order
 #pragma unroll
-    for (int m = 16; m >= 1; m >>= 1) lik_cta += __shfl_xor_sync(0xffffffffu, lik_cta, m);
-    if (lane == 0) wl[warp] = lik_cta;
-    __syncthreads();
-    if (threadIdx.x == 0) a.likpart[blockIdx.x] = (wl[0] + wl[1]) + (wl[2] + wl[3]);
+    for (int m = 16; m >= 1; m >>= 1) lik_w += __shfl_xor_sync(0xffffffffu, lik_w, m);
+    if (lane == 0) a.likpart[gw] = lik_w;
 
     // ------------------------------------------------------------ barrier
     __threadfence();
@@ -240,15 +295,12 @@ pass_kernel(PassArgs a) {
         A acc = A(0);
         if (el < TB * D) {
             int q = q0 + warp;
-            for (; q + 12 < q1; q += 16) {        // 4 independent loads in flight
-                const A v0 = a.slabs[(size_t)a.blk_slab[q] * TB * D + el];
-                const A v1 = a.slabs[(size_t)a.blk_slab[q + 4] * TB * D + el];
-                const A v2 = a.slabs[(size_t)a.blk_slab[q + 8] * TB * D + el];
-                const A v3 = a.slabs[(size_t)a.blk_slab[q + 12] * TB * D + el];
-                acc += v0;
-                acc += v1;
-                acc += v2;
-                acc += v3;
+            for (; q + 28 < q1; q += 32) {        // 8 independent loads in flight
+                A v[8];
+#pragma unroll
+                for (int r = 0; r < 8; ++r) v[r] = a.slabs[(size_t)a.blk_slab[q + 4 * r] * TB * D + el];
+#pragma unroll
+                for (int r = 0; r < 8; ++r) acc += v[r];
             }
             for (; q < q1; q += 4) acc += a.slabs[(size_t)a.blk_slab[q] * TB * D + el];
         }
@@ -258,7 +310,7 @@ pass_kernel(PassArgs a) {
             const A g = ((red[0][lane] + red[1][lane]) + red[2][lane]) + red[3][lane];
             const int64_t e = (int64_t)b * TB * D + el;
             if (e < a.n * D) {
-                if (MODE == MODE_EVAL || MODE == MODE_PARTIAL) {
+                if (MODE == MODE_EVAL) {
                     a.grad[e] = g;
                 } else {
                     // leapfrog: the pass ran at xnext = x + eps (p + eps/2 gl)
@@ -277,9 +329,10 @@ pass_kernel(PassArgs a) {
         __syncthreads();
     }
     if (blockIdx.x == 0) {
-        // log L: fixed-order strided partial sums + tree over the CTA partials
+        // log L: fixed-order strided partial sums + tree over the warp partials
+        const int GW = gridDim.x * 4;
         A s = A(0);
-        for (int q = threadIdx.x; q < gridDim.x; q += PT) s += a.likpart[q];
+        for (int q = threadIdx.x; q < GW; q += PT) s += a.likpart[q];
         __shared__ A lr[PT];
         lr[threadIdx.x] = s;
         __syncthreads();
