@@ -38,7 +38,9 @@ def main():
         # the pair loop is the backward-branch loop with the most MUFU (special-function) ops
         loop, best = None, None
         for addr, txt in ins:
-            mm = re.match(r"(?:@!?U?P\w+\s+)?BRA(?:\.\w+)*\s+(?:`?\(?)?(?:U?P\w+,\s*)?(0x[0-9a-f]+)", txt)
+            # a loop's back edge: predicated, not a warp-uniform retry (BRA.U.ANY) or an
+            # out-of-line wait path jumping back
+            mm = re.match(r"@!?P\w+\s+BRA\s+(0x[0-9a-f]+)", txt)
             if mm and int(mm.group(1), 16) < addr:
                 cand = (int(mm.group(1), 16), addr)
                 nm = sum(1 for a2, t2 in ins if cand[0] <= a2 <= cand[1] and "MUFU" in t2)
