@@ -6,6 +6,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -88,6 +89,8 @@ struct mds_ctx_s {
     std::vector<cudaEvent_t> evpool;  // timing mode: 3 events per recorded pass
     size_t ev_used = 0;               // events recorded since the last mds_last_timing
 
+    unsigned long long* d_prof = nullptr;   // MDS_PROFILE_PHASES=1: globaltimer stamps [grid][4]
+
     std::string err;
     mds_status sticky = MDS_OK;
 };
@@ -147,7 +150,7 @@ void free_all(mds_ctx c) {
     void* ps[] = {c->d_tiles, c->d_row_local, c->d_warp_seg, c->d_segs, c->d_blk_ptr,
                   c->d_blk_slab, c->d_slabs, c->d_likpart, c->d_y, c->d_x, c->d_grad, c->d_lik, c->d_stage,
                   c->d_bad, c->d_count, c->d_partial, c->d_gathered, c->d_p, c->d_gl, c->d_xnext, c->d_xsave,
-                  c->d_glsave, c->d_liksave, c->d_H, c->d_H0};
+                  c->d_glsave, c->d_liksave, c->d_H, c->d_H0, c->d_prof};
     for (void* p : ps)
         if (p) cudaFree(p);
     for (auto& e : c->evpool)
@@ -213,6 +216,7 @@ PassArgs base_args(mds_ctx c, const double* xeval) {
     a.slabs = c->d_slabs;
     a.likpart = c->d_likpart;
     a.P = c->P;
+    a.prof = c->d_prof;
     return a;
 }
 
@@ -364,7 +368,35 @@ mds_status build_schedule(mds_ctx c) {
     CK(cudaMemcpy(c->d_blk_ptr, ptr.data(), ptr.size() * sizeof(int), cudaMemcpyHostToDevice));
     if (!slab.empty()) CK(cudaMemcpy(c->d_blk_slab, slab.data(), slab.size() * sizeof(int), cudaMemcpyHostToDevice));
     CK(cudaMemset(c->d_slabs, 0, nslab * TB * c->d * sizeof(double)));
+    const char* pe = std::getenv("MDS_PROFILE_PHASES");
+    if (pe && pe[0] == '1' && (st = dalloc(c, &c->d_prof, (size_t)G * 4))) return st;
     return MDS_OK;
+}
+
+// MDS_PROFILE_PHASES=1: per-CTA phase times of the last pass, printed to stderr
+void report_phases(mds_ctx c) {
+    if (!c->d_prof) return;
+    std::vector<unsigned long long> h((size_t)c->grid * 4);
+    if (cudaMemcpy(h.data(), c->d_prof, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost)) return;
+    unsigned long long t0 = ~0ull, t3 = 0;
+    std::vector<double> a, w, b;
+    for (int g = 0; g < c->grid; ++g) {
+        t0 = std::min(t0, h[4 * g]);
+        t3 = std::max(t3, h[4 * g + 3]);
+    }
+    for (int g = 0; g < c->grid; ++g) {
+        a.push_back((h[4 * g + 1] - t0) * 1e-3);
+        w.push_back((h[4 * g + 2] - h[4 * g + 1]) * 1e-3);
+        b.push_back((h[4 * g + 3] - h[4 * g + 2]) * 1e-3);
+    }
+    auto st = [](std::vector<double> v) {
+        std::sort(v.begin(), v.end());
+        char buf[128];
+        std::snprintf(buf, sizeof buf, "min %.2f med %.2f max %.2f", v.front(), v[v.size() / 2], v.back());
+        return std::string(buf);
+    };
+    std::fprintf(stderr, "[mds phases us] span %.2f | A end: %s | sync wait: %s | B: %s\n", (t3 - t0) * 1e-3,
+                 st(a).c_str(), st(w).c_str(), st(b).c_str());
 }
 
 mds_status create_impl(int64_t n, int32_t d, int32_t precision, int32_t truncation, int32_t rank, int32_t world,
@@ -779,6 +811,7 @@ mds_status mds_last_timing(mds_ctx c, float* pair_ms, float* reduce_ms) {
         sr += b;
     }
     c->ev_used = 0;
+    report_phases(c);
     if (pair_ms) *pair_ms = passes ? (float)(sp / passes) : 0.f;
     if (reduce_ms) *reduce_ms = passes ? (float)(sr / passes) : 0.f;
     return MDS_OK;

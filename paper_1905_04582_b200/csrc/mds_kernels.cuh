@@ -76,6 +76,21 @@ __device__ __forceinline__ T reduce_scatter4(T a0, T a1, T a2, T a3, int lane) {
     return k;
 }
 
+// Sum of 2 per-lane values over the 32 lanes; lane L ends with the total of
+// column (L >> 4) & 1.  Fixed order.
+template <typename T>
+__device__ __forceinline__ T reduce_scatter2(T a0, T a1, int lane) {
+    const bool b4 = lane & 16;
+    T k = b4 ? a1 : a0;
+    const T sd = b4 ? a0 : a1;
+    k += shfl_xor(sd, 16);
+    k += shfl_xor(k, 8);
+    k += shfl_xor(k, 4);
+    k += shfl_xor(k, 2);
+    k += shfl_xor(k, 1);
+    return k;
+}
+
 // leapfrog drift of one coordinate: x + eps (p + eps/2 gl); the same expression
 // (and rounding) wherever it is evaluated
 __device__ __forceinline__ double drift(double x, double p, double gl, double eps, double heps) {
@@ -107,7 +122,14 @@ struct PassArgs {
     double* xnext;
     double eps, heps, inv_tau2;
     SigmaParams P;
+    unsigned long long* prof;    // optional [G][4] globaltimer stamps (start, end A, after sync, end)
 };
+
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
 
 constexpr int MAXSEG_W = 32;    // segments per warp (host checks)
 
@@ -147,8 +169,14 @@ struct WarpStage {
 template <typename T, int D>
 constexpr size_t pass_smem_bytes() { return 4 * sizeof(WarpStage<T, D>); }
 
+// registers per thread bound the resident warps, which hide the FP64 latency
+// chains of the pair math: target 5 CTAs (20 warps) per SM at D <= 2 in fp64
+template <typename T, int D> struct MinBlocks {
+    static constexpr int value = sizeof(T) == 8 ? (D <= 2 ? 5 : (D <= 4 ? 4 : 3)) : (D <= 4 ? 6 : 4);
+};
+
 template <typename T, int D, bool TRUNC, int MODE>
-__global__ void __launch_bounds__(PT)
+__global__ void __launch_bounds__(PT, (MinBlocks<T, D>::value))
 pass_kernel(PassArgs a) {
     using A = double;
     extern __shared__ __align__(128) unsigned char dsm[];
@@ -159,6 +187,7 @@ pass_kernel(PassArgs a) {
     WarpStage<T, D>& W = reinterpret_cast<WarpStage<T, D>*>(dsm)[warp];
     const T* __restrict__ Y = static_cast<const T*>(a.y);
     const double* __restrict__ X = a.xeval;
+    if (a.prof && threadIdx.x == 0) a.prof[blockIdx.x * 4 + 0] = gtimer();
 
     // ------------------------------------------------------------ phase A (per warp)
     const int ws0 = a.warp_seg[gw], ws1 = a.warp_seg[gw + 1];
@@ -216,52 +245,53 @@ pass_kernel(PassArgs a) {
                 }
             }
             const int t = u / GROUPS_PER_TILE, jj0 = (u % GROUPS_PER_TILE) * 4;
-            T cv[4][D];
-            T lsum = T(0);
-            T gs0[D], gs1[D];
-#pragma unroll
-            for (int k = 0; k < D; ++k) { gs0[k] = T(0); gs1[k] = T(0); }
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const T ya = W.y[st][q * TB + lane], yb = W.y[st][q * TB + lane + 32];
-                T d0[D], d1[D];
-                T sa = T(0), sb = T(0);
-#pragma unroll
-                for (int k = 0; k < D; ++k) {
-                    const T xjk = (T)W.xj[st][q * D + k];
-                    d0[k] = xi0[k] - xjk;
-                    d1[k] = xi1[k] - xjk;
-                    sa = fma(d0[k], d0[k], sa);
-                    sb = fma(d1[k], d1[k], sb);
-                }
-                T la, ua, lb, ubb;
-                Pair<T, TRUNC>::eval(sa, ya, a.P, la, ua);
-                Pair<T, TRUNC>::eval(sb, yb, a.P, lb, ubb);
-                const bool ma = is_missing(ya), mb = is_missing(yb);
-                la = ma ? T(0) : la;
-                ua = ma ? T(0) : ua;
-                lb = mb ? T(0) : lb;
-                ubb = mb ? T(0) : ubb;
-                lsum += la + lb;
-#pragma unroll
-                for (int k = 0; k < D; ++k) {
-                    const T va = ua * d0[k], vb = ubb * d1[k];
-                    gs0[k] -= va;
-                    gs1[k] -= vb;
-                    cv[q][k] = va + vb;
-                }
-            }
-            lik_w += A(lsum);
-#pragma unroll
-            for (int k = 0; k < D; ++k) {
-                g0[k] += A(gs0[k]);
-                g1[k] += A(gs1[k]);
-            }
             double* __restrict__ cslab = a.slabs + ((size_t)a.nseg + t) * TB * D + (size_t)jj0 * D;
+#pragma unroll 1
+            for (int h = 0; h < 2; ++h) {             // two column pairs: 4 pairs in flight per lane
+                T cv[2][D];
+                T lsum = T(0);
+                T gs0[D], gs1[D];
 #pragma unroll
-            for (int k = 0; k < D; ++k) {
-                const T cs = reduce_scatter4(cv[0][k], cv[1][k], cv[2][k], cv[3][k], lane);
-                if ((lane & 7) == 0) cslab[(lane >> 3) * D + k] = A(cs);
+                for (int k = 0; k < D; ++k) { gs0[k] = T(0); gs1[k] = T(0); }
+#pragma unroll
+                for (int qq = 0; qq < 2; ++qq) {
+                    const int q = 2 * h + qq;
+                    const T ya = W.y[st][q * TB + lane], yb = W.y[st][q * TB + lane + 32];
+                    T d0[D], d1[D];
+                    T sa = T(0), sb = T(0);
+#pragma unroll
+                    for (int k = 0; k < D; ++k) {
+                        const T xjk = (T)W.xj[st][q * D + k];
+                        d0[k] = xi0[k] - xjk;
+                        d1[k] = xi1[k] - xjk;
+                        sa = fma(d0[k], d0[k], sa);
+                        sb = fma(d1[k], d1[k], sb);
+                    }
+                    T la, ua, lb, ubb;
+                    Pair<T, TRUNC>::eval(sa, ya, a.P, la, ua);
+                    Pair<T, TRUNC>::eval(sb, yb, a.P, lb, ubb);
+                    const bool ma = is_missing(ya), mb = is_missing(yb);
+                    la = ma ? T(0) : la;
+                    ua = ma ? T(0) : ua;
+                    lb = mb ? T(0) : lb;
+                    ubb = mb ? T(0) : ubb;
+                    lsum += la + lb;
+#pragma unroll
+                    for (int k = 0; k < D; ++k) {
+                        const T va = ua * d0[k], vb = ubb * d1[k];
+                        gs0[k] -= va;
+                        gs1[k] -= vb;
+                        cv[qq][k] = va + vb;
+                    }
+                }
+                lik_w += A(lsum);
+#pragma unroll
+                for (int k = 0; k < D; ++k) {
+                    g0[k] += A(gs0[k]);
+                    g1[k] += A(gs1[k]);
+                    const T cs = reduce_scatter2(cv[0][k], cv[1][k], lane);
+                    if ((lane & 15) == 0) cslab[(2 * h + (lane >> 4)) * D + k] = A(cs);
+                }
             }
             if (u + 1 == sg.z) {                      // last unit of the segment: its row partial
                 double* __restrict__ rslab = a.slabs + (size_t)(ws0 + si) * TB * D;
@@ -281,8 +311,13 @@ pass_kernel(PassArgs a) {
     if (lane == 0) a.likpart[gw] = lik_w;
 
     // ------------------------------------------------------------ barrier
+    if (a.prof) {
+        __syncthreads();
+        if (threadIdx.x == 0) a.prof[blockIdx.x * 4 + 1] = gtimer();
+    }
     __threadfence();
     cg::this_grid().sync();
+    if (a.prof && threadIdx.x == 0) a.prof[blockIdx.x * 4 + 2] = gtimer();
 
     // ------------------------------------------------------------ phase B
     // job = (row block b, chunk of 32 slab elements); warp w sums slabs w, w+4, ..
@@ -341,6 +376,10 @@ pass_kernel(PassArgs a) {
             __syncthreads();
         }
         if (threadIdx.x == 0) *a.lik = lr[0];
+    }
+    if (a.prof) {
+        __syncthreads();
+        if (threadIdx.x == 0) a.prof[blockIdx.x * 4 + 3] = gtimer();
     }
 }
 
