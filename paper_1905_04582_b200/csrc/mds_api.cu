@@ -38,6 +38,7 @@ struct mds_ctx_s {
 
     // persistent-pass schedule
     int grid = 0;                    // resident CTAs of the pass kernel
+    int wpc = 0;                     // its warps per CTA
     size_t smem = 0;                 // its dynamic shared memory
     int nseg = 0;
     int* d_warp_seg = nullptr;
@@ -45,7 +46,7 @@ struct mds_ctx_s {
     int* d_blk_ptr = nullptr;
     int* d_blk_slab = nullptr;
     double* d_slabs = nullptr;       // (nseg + ntl) x B x d
-    double* d_likpart = nullptr;     // [4 * grid] (one per warp)
+    double* d_likpart = nullptr;     // [wpc * grid] (one per warp)
 
     void* d_y = nullptr;             // tiles
     double* d_x = nullptr;           // fp64 master X, npad x d
@@ -165,11 +166,12 @@ typedef void (*PassFn)(PassArgs);
 struct PassKernel {
     PassFn fn;
     size_t smem;
+    int wpc;   // warps per CTA
 };
 
 template <typename T, bool TR, int MODE, int D>
 PassKernel pk() {
-    return PassKernel{pass_kernel<T, D, TR, MODE>, pass_smem_bytes<T, D>()};
+    return PassKernel{pass_kernel<T, D, TR, MODE>, pass_smem_bytes<T, D>(), WarpsPerCTA<T, D>::value};
 }
 
 template <typename T, bool TR, int MODE>
@@ -226,7 +228,7 @@ mds_status launch_coop(mds_ctx c, PassKernel k, PassArgs& a, cudaStream_t s) {
     attr[0].id = cudaLaunchAttributeCooperative;
     attr[0].val.cooperative = 1;
     cfg.gridDim = dim3((unsigned)c->grid);
-    cfg.blockDim = dim3(PT);
+    cfg.blockDim = dim3(32 * k.wpc);
     cfg.dynamicSmemBytes = k.smem;
     cfg.stream = s;
     cfg.attrs = attr;
@@ -302,7 +304,7 @@ mds_status eval_internal(mds_ctx c) {
 }
 
 // Static schedule of the persistent pass.  The local tiles' column-group
-// units (16 per tile, in tile order) are cut into GW = 4 G equal contiguous
+// units (16 per tile, in tile order) are cut into GW = wpc G equal contiguous
 // ranges, one per warp; each range is cut at tile-row boundaries into
 // segments (I, u0, u1, tbase).  The CSR lists, for each row block b, its row
 // slabs (the segments of tile-row b, in order) and then the column slabs of
@@ -315,16 +317,17 @@ mds_status build_schedule(mds_ctx c) {
     for (PassKernel k : ks) {
         CK(cudaFuncSetAttribute(k.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k.smem));
         int o = 0;
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k.fn, PT, k.smem));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k.fn, 32 * k.wpc, k.smem));
         occ = std::min(occ, o);
     }
     if (occ < 1) return fail(c, MDS_E_UNSUPPORTED, "pass kernel cannot be resident");
     c->smem = ks[0].smem;
+    c->wpc = ks[0].wpc;
     const int64_t U = (int64_t)GROUPS_PER_TILE * c->ntl;
     int64_t G = (int64_t)sms * occ;
-    G = std::max<int64_t>(std::min<int64_t>(G, (U + 3) / 4), 1);
+    G = std::max<int64_t>(std::min<int64_t>(G, (U + c->wpc - 1) / c->wpc), 1);
     c->grid = (int)G;
-    const int64_t GW = 4 * G;
+    const int64_t GW = (int64_t)c->wpc * G;
 
     std::vector<int> warp_seg(GW + 1, 0);
     std::vector<int4> segs;

@@ -39,7 +39,7 @@ namespace cg = cooperative_groups;
 
 constexpr int TB = 64;              // tile edge B
 constexpr int GROUPS_PER_TILE = TB / 4;
-constexpr int PT = 128;             // threads per CTA (4 warps)
+constexpr int PT = 128;             // threads per CTA of the small helper kernels
 
 enum Mode { MODE_EVAL = 0, MODE_LEAPFROG = 2 };
 
@@ -166,24 +166,27 @@ struct WarpStage {
     int4 seg[MAXSEG_W];
 };
 
-template <typename T, int D>
-constexpr size_t pass_smem_bytes() { return 4 * sizeof(WarpStage<T, D>); }
-
-// registers per thread bound the resident warps, which hide the FP64 latency
-// chains of the pair math: target 5 CTAs (20 warps) per SM at D <= 2 in fp64
-template <typename T, int D> struct MinBlocks {
-    static constexpr int value = sizeof(T) == 8 ? (D <= 2 ? 5 : (D <= 4 ? 4 : 3)) : (D <= 4 ? 6 : 4);
+// ONE CTA per SM with as many warps as the register file holds: warps of one
+// CTA progress evenly, while several CTAs per SM drift apart by up to ~1.6x
+// (issue arbitration; measured with MDS_PROFILE_PHASES), which a grid barrier
+// turns into idle time.  Warps per CTA = floor(64K regs / (32 x regs/thread)).
+template <typename T, int D> struct WarpsPerCTA {
+    static constexpr int value = sizeof(T) == 8 ? (D <= 2 ? 20 : 12) : (D <= 2 ? 24 : 16);
 };
 
+template <typename T, int D>
+constexpr size_t pass_smem_bytes() { return WarpsPerCTA<T, D>::value * sizeof(WarpStage<T, D>); }
+
 template <typename T, int D, bool TRUNC, int MODE>
-__global__ void __launch_bounds__(PT, (MinBlocks<T, D>::value))
+__global__ void __launch_bounds__(WarpsPerCTA<T, D>::value * 32, 1)
 pass_kernel(PassArgs a) {
     using A = double;
+    constexpr int WPC = WarpsPerCTA<T, D>::value;
     extern __shared__ __align__(128) unsigned char dsm[];
-    __shared__ A red[4][32];
+    __shared__ A red[WPC][32];
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int gw = blockIdx.x * 4 + warp;
+    const int gw = blockIdx.x * WPC + warp;
     WarpStage<T, D>& W = reinterpret_cast<WarpStage<T, D>*>(dsm)[warp];
     const T* __restrict__ Y = static_cast<const T*>(a.y);
     const double* __restrict__ X = a.xeval;
@@ -320,7 +323,7 @@ pass_kernel(PassArgs a) {
     if (a.prof && threadIdx.x == 0) a.prof[blockIdx.x * 4 + 2] = gtimer();
 
     // ------------------------------------------------------------ phase B
-    // job = (row block b, chunk of 32 slab elements); warp w sums slabs w, w+4, ..
+    // job = (row block b, chunk of 32 slab elements); warp w sums slabs w, w+WPC, ..
     const int chunks = (TB * D + 31) / 32;
     const int jobs = a.nb * chunks;
     for (int job = blockIdx.x; job < jobs; job += gridDim.x) {
@@ -330,19 +333,21 @@ pass_kernel(PassArgs a) {
         A acc = A(0);
         if (el < TB * D) {
             int q = q0 + warp;
-            for (; q + 28 < q1; q += 32) {        // 8 independent loads in flight
-                A v[8];
+            for (; q + 3 * WPC < q1; q += 4 * WPC) {   // 4 independent loads in flight
+                A v[4];
 #pragma unroll
-                for (int r = 0; r < 8; ++r) v[r] = a.slabs[(size_t)a.blk_slab[q + 4 * r] * TB * D + el];
+                for (int r = 0; r < 4; ++r) v[r] = a.slabs[(size_t)a.blk_slab[q + r * WPC] * TB * D + el];
 #pragma unroll
-                for (int r = 0; r < 8; ++r) acc += v[r];
+                for (int r = 0; r < 4; ++r) acc += v[r];
             }
-            for (; q < q1; q += 4) acc += a.slabs[(size_t)a.blk_slab[q] * TB * D + el];
+            for (; q < q1; q += WPC) acc += a.slabs[(size_t)a.blk_slab[q] * TB * D + el];
         }
         red[warp][lane] = acc;
         __syncthreads();
         if (warp == 0 && el < TB * D) {
-            const A g = ((red[0][lane] + red[1][lane]) + red[2][lane]) + red[3][lane];
+            A g = red[0][lane];
+#pragma unroll
+            for (int w = 1; w < WPC; ++w) g += red[w][lane];
             const int64_t e = (int64_t)b * TB * D + el;
             if (e < a.n * D) {
                 if (MODE == MODE_EVAL) {
@@ -365,17 +370,19 @@ pass_kernel(PassArgs a) {
     }
     if (blockIdx.x == 0) {
         // log L: fixed-order strided partial sums + tree over the warp partials
-        const int GW = gridDim.x * 4;
+        const int GW = gridDim.x * WPC;
         A s = A(0);
-        for (int q = threadIdx.x; q < GW; q += PT) s += a.likpart[q];
-        __shared__ A lr[PT];
+        for (int q = threadIdx.x; q < GW; q += WPC * 32) s += a.likpart[q];
+        __shared__ A lr[WPC * 32];
         lr[threadIdx.x] = s;
         __syncthreads();
-        for (int m = PT / 2; m >= 1; m >>= 1) {
-            if (threadIdx.x < m) lr[threadIdx.x] += lr[threadIdx.x + m];
-            __syncthreads();
+        if (threadIdx.x < 32) {
+            A t = A(0);
+            for (int w = 0; w < WPC; ++w) t += lr[w * 32 + threadIdx.x];
+#pragma unroll
+            for (int m = 16; m >= 1; m >>= 1) t += __shfl_xor_sync(0xffffffffu, t, m);
+            if (threadIdx.x == 0) *a.lik = t;
         }
-        if (threadIdx.x == 0) *a.lik = lr[0];
     }
     if (a.prof) {
         __syncthreads();
