@@ -45,13 +45,23 @@ enum Mode { MODE_EVAL = 0, MODE_LEAPFROG = 2 };
 
 template <typename T, bool TRUNC> struct Pair;
 template <bool TRUNC> struct Pair<double, TRUNC> {
-    __device__ __forceinline__ static void eval(double s, double y, const SigmaParams& P, double& l, double& u) {
-        pair_f64<TRUNC>(s, y, P, l, u);
+    // the two rows of one column, evaluated in lock-step (mds_math.cuh)
+    __device__ __forceinline__ static void eval2(double sa, double sb, double ya, double yb, const SigmaParams& P,
+                                                 double& la, double& ua, double& lb, double& ub) {
+        const double s[2] = {sa, sb}, y[2] = {ya, yb};
+        double l[2], u[2];
+        pair_f64_n<TRUNC, 2>(s, y, P, l, u);
+        la = l[0];
+        ua = u[0];
+        lb = l[1];
+        ub = u[1];
     }
 };
 template <bool TRUNC> struct Pair<float, TRUNC> {
-    __device__ __forceinline__ static void eval(float s, float y, const SigmaParams& P, float& l, float& u) {
-        pair_f32<TRUNC>(s, y, P, l, u);
+    __device__ __forceinline__ static void eval2(float sa, float sb, float ya, float yb, const SigmaParams& P,
+                                                 float& la, float& ua, float& lb, float& ub) {
+        pair_f32<TRUNC>(sa, ya, P, la, ua);
+        pair_f32<TRUNC>(sb, yb, P, lb, ub);
     }
 };
 
@@ -271,8 +281,7 @@ pass_kernel(PassArgs a) {
                         sb = fma(d1[k], d1[k], sb);
                     }
                     T la, ua, lb, ubb;
-                    Pair<T, TRUNC>::eval(sa, ya, a.P, la, ua);
-                    Pair<T, TRUNC>::eval(sb, yb, a.P, lb, ubb);
+                    Pair<T, TRUNC>::eval2(sa, sb, ya, yb, a.P, la, ua, lb, ubb);
                     const bool ma = is_missing(ya), mb = is_missing(yb);
                     la = ma ? T(0) : la;
                     ua = ma ? T(0) : ua;

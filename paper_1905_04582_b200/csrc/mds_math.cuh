@@ -141,6 +141,117 @@ __device__ __forceinline__ void pair_f64(double s, double y, const SigmaParams& 
     ell = l;
 }
 
+// NP independent pairs in lock-step: every step is issued for all NP pairs
+// before the next, so the FP64 dependency chains (Horner steps, Newton steps)
+// of different pairs interleave in the instruction stream and hide the DFMA
+// latency (a single pair is one long dependent chain).  Same arithmetic as
+// pair_f64, operation for operation.
+template <bool TRUNC, int NP>
+__device__ __forceinline__ void pair_f64_n(const double (&s)[NP], const double (&y)[NP], const SigmaParams& P,
+                                           double (&ell)[NP], double (&u)[NP]) {
+    double rs[NP], d[NP], res[NP], l[NP];
+#pragma unroll
+    for (int i = 0; i < NP; ++i) {
+        const double sc = __hiloint2double(max(__double2hiint(s[i]), 0x01000000), __double2loint(s[i]));
+        rs[i] = rsqrt_seed(sc);
+        const double h = sc * rs[i];
+        const double e = fma(-h, rs[i], 1.0);
+        const double c = fma(e, 0.375, 0.5);
+        const double re = rs[i] * e;
+        rs[i] = fma(re, c, rs[i]);
+    }
+#pragma unroll
+    for (int i = 0; i < NP; ++i) {
+        d[i] = s[i] * rs[i];
+        res[i] = y[i] - d[i];
+        l[i] = fma(-(res[i] * P.half_inv_sigma2), res[i], P.k0);
+    }
+    if (TRUNC) {
+        double t[NP], a[NP], r[NP], E[NP], w[NP];
+        int k[NP];
+        const double MAGIC = 6755399441055744.0;
+#pragma unroll
+        for (int i = 0; i < NP; ++i) {
+            t[i] = d[i] * P.inv_sigma;
+            a[i] = s[i] * P.half_inv_sigma2;
+            a[i] = __hiloint2double(min(__double2hiint(a[i]), 0x4085E000), __double2loint(a[i]));
+            const double kd = fma(a[i], -1.4426950408889634, MAGIC);
+            k[i] = __double2loint(kd);
+            const double fk = kd - MAGIC;
+            r[i] = fma(fk, -0.6931471805599453, -a[i]);
+            r[i] = fma(fk, -2.3190468138462996e-17, r[i]);
+        }
+        // rcp seeds for (t + K) issued early: the MUFU latency overlaps the exp polynomial
+        double den[NP], y0[NP];
+#pragma unroll
+        for (int i = 0; i < NP; ++i) {
+            den[i] = t[i] + KAPPA64;
+            y0[i] = rcp_seed(den[i]);
+        }
+        double p[NP];
+#pragma unroll
+        for (int i = 0; i < NP; ++i) p[i] = EXP64_C[EXP64_DEG];
+#pragma unroll
+        for (int j = EXP64_DEG - 1; j >= 0; --j)
+#pragma unroll
+            for (int i = 0; i < NP; ++i) p[i] = fma(p[i], r[i], EXP64_C[j]);
+#pragma unroll
+        for (int i = 0; i < NP; ++i) {
+            E[i] = __hiloint2double(__double2hiint(p[i]) + (int)((unsigned)k[i] << 20), __double2loint(p[i]));
+            const double e1 = fma(-den[i], y0[i], 1.0);
+            const double ee = fma(e1, e1, e1);
+            const double rden = fma(ee, y0[i], y0[i]);
+            w[i] = fma(-2.0 * KAPPA64, rden, 1.0);
+        }
+        double q[NP];
+#pragma unroll
+        for (int i = 0; i < NP; ++i) q[i] = Q64_C[Q64_DEG];
+#pragma unroll
+        for (int j = Q64_DEG - 1; j >= 0; --j)
+#pragma unroll
+            for (int i = 0; i < NP; ++i) q[i] = fma(q[i], w[i], Q64_C[j]);
+        double Q[NP], Phi[NP], opp[NP], prod[NP], z0[NP];
+#pragma unroll
+        for (int i = 0; i < NP; ++i) {
+            Q[i] = E[i] * q[i];
+            Phi[i] = 1.0 - Q[i];
+            opp[i] = 2.0 - Q[i];
+            prod[i] = Phi[i] * opp[i];
+            z0[i] = rcp_seed(prod[i]);
+        }
+        double sa[NP], zz[NP], G[NP];
+#pragma unroll
+        for (int i = 0; i < NP; ++i) {
+            const double f1 = fma(-prod[i], z0[i], 1.0);
+            const double f2 = fma(f1, f1, f1);
+            const double rp = fma(f2, z0[i], z0[i]);
+            const double invPhi = opp[i] * rp;
+            const double invOpp = Phi[i] * rp;
+            G[i] = (E[i] * P.cg) * invPhi;
+            sa[i] = Q[i] * invOpp;
+            zz[i] = sa[i] * sa[i];
+        }
+        double at[NP];
+#pragma unroll
+        for (int i = 0; i < NP; ++i) at[i] = ATANH64_C[ATANH64_DEG];
+#pragma unroll
+        for (int j = ATANH64_DEG - 1; j >= 0; --j)
+#pragma unroll
+            for (int i = 0; i < NP; ++i) at[i] = fma(at[i], zz[i], ATANH64_C[j]);
+#pragma unroll
+        for (int i = 0; i < NP; ++i) {
+            ell[i] = fma(sa[i], at[i], l[i]);
+            u[i] = fma(-res[i], P.inv_sigma2, G[i]) * rs[i];
+        }
+    } else {
+#pragma unroll
+        for (int i = 0; i < NP; ++i) {
+            ell[i] = l[i];
+            u[i] = (-res[i] * P.inv_sigma2) * rs[i];
+        }
+    }
+}
+
 // ---------------------------------------------------------------- fp32 pair
 // fp32 storage and per-pair math (reading R15); MUFU rsqrt/ex2/rcp/lg2.
 template <bool TRUNC>

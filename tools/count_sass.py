@@ -3,7 +3,7 @@
 
 For every pass_kernel<T, D, TRUNC, LEAPFROG> instantiation in libmds.so: find the loop
 (the backward branch of the column-group loop), count its instructions by
-class, and divide by the pairs one loop trip evaluates per lane (8).  The
+class, and divide by the pairs one loop trip evaluates per lane (its MUFU.RSQ count).  The
 FP64 count per pair is the 'algorithmic' FP64 work of the roofline.
 """
 import json
@@ -15,7 +15,6 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 LIB = os.path.join(ROOT, "paper_1905_04582_b200", "libmds.so")
 OUT = os.path.join(ROOT, "profiles", "sass_counts.json")
-PAIRS_PER_TRIP = 8   # 2 rows per lane x 4 columns per unit
 
 FP64 = {"DFMA", "DMUL", "DADD", "DSETP", "DMNMX"}
 FP32 = {"FFMA", "FMUL", "FADD", "FSETP", "FMNMX", "FSEL"}
@@ -51,13 +50,16 @@ def main():
             continue
         body = [txt for addr, txt in ins if loop[0] <= addr <= loop[1]]
         ops = [re.sub(r"^@!?U?P\w+\s+", "", b).split()[0].split(".")[0] for b in body]
+        # one reciprocal-sqrt seed per evaluated pair: the loop's pair count
+        npairs = sum(1 for b in body if re.search(r"MUFU\.RSQ", b))
         n64 = sum(o in FP64 for o in ops)
         n32 = sum(o in FP32 for o in ops)
         nmufu = sum(o == "MUFU" for o in ops)
         res["%s_d%d_t%d" % (prec, d, t)] = {
             "kernel": name, "loop_instructions": len(ops),
-            "fp64_per_pair": n64 / PAIRS_PER_TRIP, "fp32_per_pair": n32 / PAIRS_PER_TRIP,
-            "mufu_per_pair": nmufu / PAIRS_PER_TRIP, "issued_per_pair": len(ops) / PAIRS_PER_TRIP,
+            "pairs_per_trip": npairs,
+            "fp64_per_pair": n64 / npairs, "fp32_per_pair": n32 / npairs,
+            "mufu_per_pair": nmufu / npairs, "issued_per_pair": len(ops) / npairs,
         }
     os.makedirs(os.path.dirname(OUT), exist_ok=True)
     json.dump(res, open(OUT, "w"), indent=1, sort_keys=True)
