@@ -45,6 +45,10 @@ enum Mode { MODE_EVAL = 0, MODE_LEAPFROG = 2 };
 
 template <typename T, bool TRUNC> struct Pair;
 template <bool TRUNC> struct Pair<double, TRUNC> {
+    __device__ __forceinline__ static void eval4(const double (&s)[4], const double (&y)[4], const SigmaParams& P,
+                                                 double (&l)[4], double (&u)[4]) {
+        pair_f64_n<TRUNC, 4>(s, y, P, l, u);
+    }
     // the two rows of one column, evaluated in lock-step (mds_math.cuh)
     __device__ __forceinline__ static void eval2(double sa, double sb, double ya, double yb, const SigmaParams& P,
                                                  double& la, double& ua, double& lb, double& ub) {
@@ -58,6 +62,11 @@ template <bool TRUNC> struct Pair<double, TRUNC> {
     }
 };
 template <bool TRUNC> struct Pair<float, TRUNC> {
+    __device__ __forceinline__ static void eval4(const float (&s)[4], const float (&y)[4], const SigmaParams& P,
+                                                 float (&l)[4], float (&u)[4]) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) pair_f32<TRUNC>(s[i], y[i], P, l[i], u[i]);
+    }
     __device__ __forceinline__ static void eval2(float sa, float sb, float ya, float yb, const SigmaParams& P,
                                                  float& la, float& ua, float& lb, float& ub) {
         pair_f32<TRUNC>(sa, ya, P, la, ua);
@@ -166,13 +175,16 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
 }
 __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
-// per-warp staging area (dynamic shared memory), double buffered
+// per-warp staging area (dynamic shared memory).  One TMA bulk copy per unit
+// brings its 4 tile columns of y (double buffered); x of the tile's 64 columns
+// is copied once per tile (double buffered), x of the segment's 64 rows once
+// per segment (single buffer: it is moved to registers before the next copy).
 template <typename T, int D>
 struct WarpStage {
     uint64_t bar[2];
-    double xrow[2][TB * D];      // x of the 64 rows of the segment (copied with its first unit)
-    double xj[2][4 * D];         // x of the 4 columns of the unit
-    T y[2][4 * TB];              // the unit's 4 tile columns (contiguous in the tile)
+    double xrow[TB * D];
+    double xcol[2][TB * D];
+    T y[2][4 * TB];
     int4 seg[MAXSEG_W];
 };
 
@@ -216,24 +228,24 @@ pass_kernel(PassArgs a) {
 
     A lik_w = A(0);
     if (nsw > 0) {
-        constexpr uint32_t YB = 4 * TB * sizeof(T), XJB = 4 * D * sizeof(double), XRB = TB * D * sizeof(double);
+        constexpr uint32_t YB = 4 * TB * sizeof(T), XB = TB * D * sizeof(double);
         const int ub = W.seg[0].y, ue = W.seg[nsw - 1].z;
-        // issue the staging copies of unit u (segment index si) into stage st
-        auto issue = [&](int u, int si, int st) {
+        // staging copies of unit u (segment si) into y stage st; new_tile -> x of
+        // its column block into xcol[xb]; first unit of a segment -> x of its rows
+        auto issue = [&](int u, int si, int st, bool new_tile, int xb) {
             if (lane == 0) {
                 const int4 sg = W.seg[si];
                 const int t = u / GROUPS_PER_TILE, jj0 = (u % GROUPS_PER_TILE) * 4;
-                const int J = t - sg.w;
                 const bool first = (u == sg.y);
                 fence_async_smem();
-                mbar_arrive_tx(&W.bar[st], YB + XJB + (first ? XRB : 0));
+                mbar_arrive_tx(&W.bar[st], YB + (new_tile ? XB : 0) + (first ? XB : 0));
                 bulk_g2s(W.y[st], Y + (size_t)t * TB * TB + (size_t)jj0 * TB, YB, &W.bar[st]);
-                bulk_g2s(W.xj[st], X + ((size_t)J * TB + jj0) * D, XJB, &W.bar[st]);
-                if (first) bulk_g2s(W.xrow[st], X + (size_t)sg.x * TB * D, XRB, &W.bar[st]);
+                if (new_tile) bulk_g2s(W.xcol[xb], X + (size_t)(t - sg.w) * TB * D, XB, &W.bar[st]);
+                if (first) bulk_g2s(W.xrow, X + (size_t)sg.x * TB * D, XB, &W.bar[st]);
             }
         };
-        int si = 0, si_next = 0;
-        issue(ub, 0, 0);
+        int si = 0, si_next = 0, xb = 0;
+        issue(ub, 0, 0, true, 0);
         uint32_t ph0 = 0, ph1 = 0;
         T xi0[D], xi1[D];
         A g0[D], g1[D];
@@ -242,65 +254,69 @@ pass_kernel(PassArgs a) {
 #pragma unroll 1
         for (int u = ub, kk = 0; u < ue; ++u, ++kk) {
             const int st = kk & 1;
-            if (u + 1 < ue) {
-                if (u + 1 >= W.seg[si_next].z) ++si_next;
-                __syncwarp();                         // every lane is done with stage st ^ 1
-                issue(u + 1, si_next, st ^ 1);
-            }
             if (st == 0) { mbar_wait(&W.bar[0], ph0); ph0 ^= 1; }
             else         { mbar_wait(&W.bar[1], ph1); ph1 ^= 1; }
             const int4 sg = W.seg[si];
             if (u == sg.y) {                          // first unit of a segment: its 64 rows
 #pragma unroll
                 for (int k = 0; k < D; ++k) {
-                    xi0[k] = (T)W.xrow[st][lane * D + k];
-                    xi1[k] = (T)W.xrow[st][(lane + 32) * D + k];
+                    xi0[k] = (T)W.xrow[lane * D + k];
+                    xi1[k] = (T)W.xrow[(lane + 32) * D + k];
                 }
             }
             const int t = u / GROUPS_PER_TILE, jj0 = (u % GROUPS_PER_TILE) * 4;
+            const int xcur = xb;
+            if (u + 1 < ue) {                         // prefetch the next unit
+                if (u + 1 >= W.seg[si_next].z) ++si_next;
+                const bool nt = (u + 1) / GROUPS_PER_TILE != t;
+                if (nt) xb ^= 1;
+                __syncwarp();                         // all lanes are done with y[st^1], xrow, xcol[xb]
+                issue(u + 1, si_next, st ^ 1, nt, xb);
+            }
+            const double* __restrict__ xc = W.xcol[xcur] + jj0 * D;
             double* __restrict__ cslab = a.slabs + ((size_t)a.nseg + t) * TB * D + (size_t)jj0 * D;
 #pragma unroll 1
-            for (int h = 0; h < 2; ++h) {             // two column pairs: 4 pairs in flight per lane
-                T cv[2][D];
-                T lsum = T(0);
-                T gs0[D], gs1[D];
-#pragma unroll
-                for (int k = 0; k < D; ++k) { gs0[k] = T(0); gs1[k] = T(0); }
+            for (int h = 0; h < 2; ++h) {             // two column pairs: 4 pairs per lane in lock-step
+                T ys[4], ss[4], dd[4][D];
 #pragma unroll
                 for (int qq = 0; qq < 2; ++qq) {
                     const int q = 2 * h + qq;
-                    const T ya = W.y[st][q * TB + lane], yb = W.y[st][q * TB + lane + 32];
-                    T d0[D], d1[D];
+                    ys[2 * qq] = W.y[st][q * TB + lane];
+                    ys[2 * qq + 1] = W.y[st][q * TB + lane + 32];
                     T sa = T(0), sb = T(0);
 #pragma unroll
                     for (int k = 0; k < D; ++k) {
-                        const T xjk = (T)W.xj[st][q * D + k];
-                        d0[k] = xi0[k] - xjk;
-                        d1[k] = xi1[k] - xjk;
-                        sa = fma(d0[k], d0[k], sa);
-                        sb = fma(d1[k], d1[k], sb);
+                        const T xjk = (T)xc[q * D + k];
+                        dd[2 * qq][k] = xi0[k] - xjk;
+                        dd[2 * qq + 1][k] = xi1[k] - xjk;
+                        sa = fma(dd[2 * qq][k], dd[2 * qq][k], sa);
+                        sb = fma(dd[2 * qq + 1][k], dd[2 * qq + 1][k], sb);
                     }
-                    T la, ua, lb, ubb;
-                    Pair<T, TRUNC>::eval2(sa, sb, ya, yb, a.P, la, ua, lb, ubb);
-                    const bool ma = is_missing(ya), mb = is_missing(yb);
-                    la = ma ? T(0) : la;
-                    ua = ma ? T(0) : ua;
-                    lb = mb ? T(0) : lb;
-                    ubb = mb ? T(0) : ubb;
-                    lsum += la + lb;
+                    ss[2 * qq] = sa;
+                    ss[2 * qq + 1] = sb;
+                }
+                T ll[4], uu[4];
+                Pair<T, TRUNC>::eval4(ss, ys, a.P, ll, uu);
+                T lsum = T(0);
+                T cv[2][D];
 #pragma unroll
-                    for (int k = 0; k < D; ++k) {
-                        const T va = ua * d0[k], vb = ubb * d1[k];
-                        gs0[k] -= va;
-                        gs1[k] -= vb;
-                        cv[qq][k] = va + vb;
-                    }
+                for (int i = 0; i < 4; ++i) {
+                    const bool m = is_missing(ys[i]);
+                    if (!m) lsum += ll[i];                // predicated, no select
+                    uu[i] = m ? T(0) : uu[i];
+                }
+#pragma unroll
+                for (int k = 0; k < D; ++k) {
+                    const T va0 = uu[0] * dd[0][k], vb0 = uu[1] * dd[1][k];
+                    const T va1 = uu[2] * dd[2][k], vb1 = uu[3] * dd[3][k];
+                    g0[k] -= A(va0 + va1);
+                    g1[k] -= A(vb0 + vb1);
+                    cv[0][k] = va0 + vb0;
+                    cv[1][k] = va1 + vb1;
                 }
                 lik_w += A(lsum);
 #pragma unroll
                 for (int k = 0; k < D; ++k) {
-                    g0[k] += A(gs0[k]);
-                    g1[k] += A(gs1[k]);
                     const T cs = reduce_scatter2(cv[0][k], cv[1][k], lane);
                     if ((lane & 15) == 0) cslab[(2 * h + (lane >> 4)) * D + k] = A(cs);
                 }
