@@ -85,6 +85,22 @@ __device__ __forceinline__ T horner(const T* c, T x) {
     return p;
 }
 
+// p(x) = E(x^2) + x O(x^2): two independent Horner chains of half the depth
+// (one extra multiply and one extra fma); shortens the FP64 dependency chain
+template <int DEG>
+__device__ __forceinline__ double horner_eo(const double* c, double x) {
+    const double x2 = x * x;
+    constexpr int DE = DEG / 2;                 // even part degree (in x^2)
+    constexpr int DO = (DEG - 1) / 2;           // odd part degree (in x^2)
+    double pe = c[2 * DE], po = c[2 * DO + 1];
+#pragma unroll
+    for (int k = DE - 1; k >= 0; --k) {
+        pe = fma(pe, x2, c[2 * k]);
+        if (k <= DO - 1) po = fma(po, x2, c[2 * k + 1]);
+    }
+    return fma(po, x, pe);
+}
+
 __device__ __forceinline__ bool is_missing(double y) {
     return (uint32_t)__double2hiint(y) == CANON_NAN_HI64;
 }
@@ -190,11 +206,7 @@ __device__ __forceinline__ void pair_f64_n(const double (&s)[NP], const double (
         }
         double p[NP];
 #pragma unroll
-        for (int i = 0; i < NP; ++i) p[i] = EXP64_C[EXP64_DEG];
-#pragma unroll
-        for (int j = EXP64_DEG - 1; j >= 0; --j)
-#pragma unroll
-            for (int i = 0; i < NP; ++i) p[i] = fma(p[i], r[i], EXP64_C[j]);
+        for (int i = 0; i < NP; ++i) p[i] = horner_eo<EXP64_DEG>(EXP64_C, r[i]);
 #pragma unroll
         for (int i = 0; i < NP; ++i) {
             E[i] = __hiloint2double(__double2hiint(p[i]) + (int)((unsigned)k[i] << 20), __double2loint(p[i]));
@@ -205,11 +217,7 @@ __device__ __forceinline__ void pair_f64_n(const double (&s)[NP], const double (
         }
         double q[NP];
 #pragma unroll
-        for (int i = 0; i < NP; ++i) q[i] = Q64_C[Q64_DEG];
-#pragma unroll
-        for (int j = Q64_DEG - 1; j >= 0; --j)
-#pragma unroll
-            for (int i = 0; i < NP; ++i) q[i] = fma(q[i], w[i], Q64_C[j]);
+        for (int i = 0; i < NP; ++i) q[i] = horner_eo<Q64_DEG>(Q64_C, w[i]);
         double Q[NP], Phi[NP], opp[NP], prod[NP], z0[NP];
 #pragma unroll
         for (int i = 0; i < NP; ++i) {
@@ -233,11 +241,7 @@ __device__ __forceinline__ void pair_f64_n(const double (&s)[NP], const double (
         }
         double at[NP];
 #pragma unroll
-        for (int i = 0; i < NP; ++i) at[i] = ATANH64_C[ATANH64_DEG];
-#pragma unroll
-        for (int j = ATANH64_DEG - 1; j >= 0; --j)
-#pragma unroll
-            for (int i = 0; i < NP; ++i) at[i] = fma(at[i], zz[i], ATANH64_C[j]);
+        for (int i = 0; i < NP; ++i) at[i] = horner_eo<ATANH64_DEG>(ATANH64_C, zz[i]);
 #pragma unroll
         for (int i = 0; i < NP; ++i) {
             ell[i] = fma(sa[i], at[i], l[i]);
