@@ -101,6 +101,33 @@ __device__ __forceinline__ double horner_eo(const double* c, double x) {
     return fma(po, x, pe);
 }
 
+// p(x) = [A(x^4) + x B(x^4)] + x^2 [C(x^4) + x D(x^4)]: four independent
+// Horner chains of quarter depth.  Measured on B200 (tools/fp64_probe.cu): a
+// warp whose consecutive DFMAs are dependent caps the FP64 pipe at ~65% of
+// peak however many warps are resident; 4 independent chains reach ~91%.
+template <int DEG>
+__device__ __forceinline__ double horner4(const double* c, double x) {
+    const double x2 = x * x;
+    const double x4 = x2 * x2;
+    double ch[4];
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+        const int top = (DEG - m) / 4;            // highest k with 4k + m <= DEG
+        ch[m] = (m <= DEG) ? c[4 * top + m] : 0.0;
+    }
+#pragma unroll
+    for (int k = DEG / 4; k >= 0; --k) {
+#pragma unroll
+        for (int m = 0; m < 4; ++m) {
+            const int top = (DEG - m) / 4;
+            if (m <= DEG && k < top) ch[m] = fma(ch[m], x4, c[4 * k + m]);
+        }
+    }
+    const double lo = fma(ch[1], x, ch[0]);
+    const double hi = fma(ch[3], x, ch[2]);
+    return fma(hi, x2, lo);
+}
+
 __device__ __forceinline__ bool is_missing(double y) {
     return (uint32_t)__double2hiint(y) == CANON_NAN_HI64;
 }
@@ -206,7 +233,7 @@ __device__ __forceinline__ void pair_f64_n(const double (&s)[NP], const double (
         }
         double p[NP];
 #pragma unroll
-        for (int i = 0; i < NP; ++i) p[i] = horner_eo<EXP64_DEG>(EXP64_C, r[i]);
+        for (int i = 0; i < NP; ++i) p[i] = horner4<EXP64_DEG>(EXP64_C, r[i]);
 #pragma unroll
         for (int i = 0; i < NP; ++i) {
             E[i] = __hiloint2double(__double2hiint(p[i]) + (int)((unsigned)k[i] << 20), __double2loint(p[i]));
@@ -217,7 +244,7 @@ __device__ __forceinline__ void pair_f64_n(const double (&s)[NP], const double (
         }
         double q[NP];
 #pragma unroll
-        for (int i = 0; i < NP; ++i) q[i] = horner_eo<Q64_DEG>(Q64_C, w[i]);
+        for (int i = 0; i < NP; ++i) q[i] = horner4<Q64_DEG>(Q64_C, w[i]);
         double Q[NP], Phi[NP], opp[NP], prod[NP], z0[NP];
 #pragma unroll
         for (int i = 0; i < NP; ++i) {
@@ -241,7 +268,7 @@ __device__ __forceinline__ void pair_f64_n(const double (&s)[NP], const double (
         }
         double at[NP];
 #pragma unroll
-        for (int i = 0; i < NP; ++i) at[i] = horner_eo<ATANH64_DEG>(ATANH64_C, zz[i]);
+        for (int i = 0; i < NP; ++i) at[i] = horner4<ATANH64_DEG>(ATANH64_C, zz[i]);
 #pragma unroll
         for (int i = 0; i < NP; ++i) {
             ell[i] = fma(sa[i], at[i], l[i]);
