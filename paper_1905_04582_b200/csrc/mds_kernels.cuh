@@ -193,7 +193,7 @@ struct WarpStage {
 // (issue arbitration; measured with MDS_PROFILE_PHASES), which a grid barrier
 // turns into idle time.  Warps per CTA = floor(64K regs / (32 x regs/thread)).
 template <typename T, int D> struct WarpsPerCTA {
-    static constexpr int value = sizeof(T) == 8 ? (D <= 2 ? 20 : 12) : (D <= 2 ? 24 : 16);
+    static constexpr int value = sizeof(T) == 8 ? (D <= 2 ? 12 : 12) : (D <= 2 ? 24 : 16);
 };
 
 template <typename T, int D>

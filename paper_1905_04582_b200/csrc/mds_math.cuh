@@ -233,7 +233,11 @@ __device__ __forceinline__ void pair_f64_n(const double (&s)[NP], const double (
         }
         double p[NP];
 #pragma unroll
-        for (int i = 0; i < NP; ++i) p[i] = horner4<EXP64_DEG>(EXP64_C, r[i]);
+        for (int i = 0; i < NP; ++i) p[i] = EXP64_C[EXP64_DEG];
+#pragma unroll
+        for (int j = EXP64_DEG - 1; j >= 0; --j)
+#pragma unroll
+            for (int i = 0; i < NP; ++i) p[i] = fma(p[i], r[i], EXP64_C[j]);
 #pragma unroll
         for (int i = 0; i < NP; ++i) {
             E[i] = __hiloint2double(__double2hiint(p[i]) + (int)((unsigned)k[i] << 20), __double2loint(p[i]));
@@ -244,7 +248,11 @@ __device__ __forceinline__ void pair_f64_n(const double (&s)[NP], const double (
         }
         double q[NP];
 #pragma unroll
-        for (int i = 0; i < NP; ++i) q[i] = horner4<Q64_DEG>(Q64_C, w[i]);
+        for (int i = 0; i < NP; ++i) q[i] = Q64_C[Q64_DEG];
+#pragma unroll
+        for (int j = Q64_DEG - 1; j >= 0; --j)
+#pragma unroll
+            for (int i = 0; i < NP; ++i) q[i] = fma(q[i], w[i], Q64_C[j]);
         double Q[NP], Phi[NP], opp[NP], prod[NP], z0[NP];
 #pragma unroll
         for (int i = 0; i < NP; ++i) {
@@ -268,7 +276,11 @@ __device__ __forceinline__ void pair_f64_n(const double (&s)[NP], const double (
         }
         double at[NP];
 #pragma unroll
-        for (int i = 0; i < NP; ++i) at[i] = horner4<ATANH64_DEG>(ATANH64_C, zz[i]);
+        for (int i = 0; i < NP; ++i) at[i] = ATANH64_C[ATANH64_DEG];
+#pragma unroll
+        for (int j = ATANH64_DEG - 1; j >= 0; --j)
+#pragma unroll
+            for (int i = 0; i < NP; ++i) at[i] = fma(at[i], zz[i], ATANH64_C[j]);
 #pragma unroll
         for (int i = 0; i < NP; ++i) {
             ell[i] = fma(sa[i], at[i], l[i]);
