@@ -11,7 +11,8 @@ import ctypes
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libmds.so")
+# MDS_LIB_PATH overrides the in-tree library (A/B builds of the same sources)
+LIB_PATH = os.environ.get("MDS_LIB_PATH") or os.path.join(HERE, "libmds.so")
 
 MDS_F64, MDS_F32 = 0, 1
 STATUS = {0: "MDS_OK", 1: "MDS_E_INVALID_ARG", 2: "MDS_E_STATE", 3: "MDS_E_OOM", 4: "MDS_E_CUDA",

@@ -95,6 +95,21 @@ __device__ __forceinline__ T reduce_scatter4(T a0, T a1, T a2, T a3, int lane) {
     return k;
 }
 
+// Sum over the 32 lanes of 4 per-lane column values stored in the per-lane
+// order v[p] = column p ^ m, m = (L >> 3) & 3 (see the unit loop): every
+// exchange then sends a fixed register, so no selects are needed.  Lane L ends
+// with the total of column m (all 8 lanes with the same m hold it).  Fixed order.
+template <typename T>
+__device__ __forceinline__ T reduce_scatter4_perm(T v0, T v1, T v2, T v3) {
+    T k0 = v0 + shfl_xor(v2, 16);     // partner L^16 holds my columns 0,1 at its positions 2,3
+    T k1 = v1 + shfl_xor(v3, 16);
+    T k = k0 + shfl_xor(k1, 8);       // partner L^8 holds my column 0 at its position 1
+    k += shfl_xor(k, 4);
+    k += shfl_xor(k, 2);
+    k += shfl_xor(k, 1);
+    return k;
+}
+
 // Sum of 2 per-lane values over the 32 lanes; lane L ends with the total of
 // column (L >> 4) & 1.  Fixed order.
 template <typename T>
@@ -178,22 +193,29 @@ __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.a
 // per-warp staging area (dynamic shared memory).  One TMA bulk copy per unit
 // brings its 4 tile columns of y (double buffered); x of the tile's 64 columns
 // is copied once per tile (double buffered), x of the segment's 64 rows once
-// per segment (single buffer: it is moved to registers before the next copy).
+// per segment (single buffer: it is moved to registers before the next copy;
+// with two units in flight the next segment's copy is issued only once the
+// current segment's first unit has read it).
+constexpr int NSTAGE = 3;        // y stages in flight per warp (prefetch two units ahead)
+
 template <typename T, int D>
 struct WarpStage {
-    uint64_t bar[2];
+    uint64_t bar[NSTAGE];
+    uint64_t pad_;
     double xrow[TB * D];
     double xcol[2][TB * D];
-    T y[2][4 * TB];
+    T y[NSTAGE][4 * TB];
     int4 seg[MAXSEG_W];
 };
 
 // ONE CTA per SM with as many warps as the register file holds: warps of one
 // CTA progress evenly, while several CTAs per SM drift apart by up to ~1.6x
 // (issue arbitration; measured with MDS_PROFILE_PHASES), which a grid barrier
-// turns into idle time.  Warps per CTA = floor(64K regs / (32 x regs/thread)).
+// turns into idle time.  Warps per CTA bound the registers per thread (ptxas
+// budgets blocks in 4-warp granules: 12 warps -> 168 regs, 8 -> 255); fp64
+// needs ~150 for 4 interleaved pairs (tools/pair_probe.cu), more at larger D.
 template <typename T, int D> struct WarpsPerCTA {
-    static constexpr int value = sizeof(T) == 8 ? (D <= 2 ? 12 : 12) : (D <= 2 ? 24 : 16);
+    static constexpr int value = sizeof(T) == 8 ? (D <= 3 ? 12 : 8) : (D <= 2 ? 24 : 16);
 };
 
 template <typename T, int D>
@@ -219,8 +241,8 @@ pass_kernel(PassArgs a) {
     const int nsw = ws1 - ws0;
     if (lane < nsw) W.seg[lane] = a.segs[ws0 + lane];
     if (lane == 0) {
-        mbar_init(&W.bar[0], 1);
-        mbar_init(&W.bar[1], 1);
+#pragma unroll
+        for (int b = 0; b < NSTAGE; ++b) mbar_init(&W.bar[b], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         fence_async_smem();
     }
@@ -230,6 +252,7 @@ pass_kernel(PassArgs a) {
     if (nsw > 0) {
         constexpr uint32_t YB = 4 * TB * sizeof(T), XB = TB * D * sizeof(double);
         const int ub = W.seg[0].y, ue = W.seg[nsw - 1].z;
+        const int m = (lane >> 3) & 3;           // this lane's column order: position p <-> column p ^ m
         // staging copies of unit u (segment si) into y stage st; new_tile -> x of
         // its column block into xcol[xb]; first unit of a segment -> x of its rows
         auto issue = [&](int u, int si, int st, bool new_tile, int xb) {
@@ -244,19 +267,38 @@ pass_kernel(PassArgs a) {
                 if (first) bulk_g2s(W.xrow, X + (size_t)sg.x * TB * D, XB, &W.bar[st]);
             }
         };
-        int si = 0, si_next = 0, xb = 0;
-        issue(ub, 0, 0, true, 0);
-        uint32_t ph0 = 0, ph1 = 0;
+        // issue cursor (units are issued in order, up to two ahead of compute)
+        int iu = ub, isi = 0, ist = 0, ixb = 0, itile = -1;
+        auto issue_next = [&]() {
+            while (iu >= W.seg[isi].z) ++isi;
+            const int t = iu / GROUPS_PER_TILE;
+            const bool nt = t != itile;
+            if (nt && itile >= 0) ixb ^= 1;
+            itile = t;
+            issue(iu, isi, ist, nt, ixb);
+            ++iu;
+            ist = (ist + 1 == NSTAGE) ? 0 : ist + 1;
+        };
+        issue_next();
+        if (iu < ue && iu != W.seg[isi].z) issue_next();    // second unit in flight (not a new segment)
+        uint32_t phase = 0;                                  // bit b: parity of stage b
+        int si = 0, cst = 0, cxb = 0, ctile = -1;
         T xi0[D], xi1[D];
         A g0[D], g1[D];
 #pragma unroll
         for (int k = 0; k < D; ++k) { xi0[k] = xi1[k] = T(0); g0[k] = g1[k] = A(0); }
 #pragma unroll 1
-        for (int u = ub, kk = 0; u < ue; ++u, ++kk) {
-            const int st = kk & 1;
-            if (st == 0) { mbar_wait(&W.bar[0], ph0); ph0 ^= 1; }
-            else         { mbar_wait(&W.bar[1], ph1); ph1 ^= 1; }
+        for (int u = ub; u < ue; ++u) {
+#ifndef MDS_EXP_NO_TMA
+            mbar_wait(&W.bar[cst], (phase >> cst) & 1);
+            phase ^= 1u << cst;
+#endif
             const int4 sg = W.seg[si];
+            const int t = u / GROUPS_PER_TILE, jj0 = (u % GROUPS_PER_TILE) * 4;
+            if (t != ctile) {
+                if (ctile >= 0) cxb ^= 1;
+                ctile = t;
+            }
             if (u == sg.y) {                          // first unit of a segment: its 64 rows
 #pragma unroll
                 for (int k = 0; k < D; ++k) {
@@ -264,25 +306,28 @@ pass_kernel(PassArgs a) {
                     xi1[k] = (T)W.xrow[(lane + 32) * D + k];
                 }
             }
-            const int t = u / GROUPS_PER_TILE, jj0 = (u % GROUPS_PER_TILE) * 4;
-            const int xcur = xb;
-            if (u + 1 < ue) {                         // prefetch the next unit
-                if (u + 1 >= W.seg[si_next].z) ++si_next;
-                const bool nt = (u + 1) / GROUPS_PER_TILE != t;
-                if (nt) xb ^= 1;
-                __syncwarp();                         // all lanes are done with y[st^1], xrow, xcol[xb]
-                issue(u + 1, si_next, st ^ 1, nt, xb);
+            __syncwarp();                             // all lanes are done with the stage being refilled
+#ifndef MDS_EXP_NO_TMA
+            if (iu < ue) {
+                // keep two units in flight; a segment's first unit (row-x copy into
+                // the single xrow buffer) waits until the current segment's rows are read
+                int s2 = isi;
+                while (iu >= W.seg[s2].z) ++s2;
+                const bool first_of_seg = (iu == W.seg[s2].y);
+                if (!first_of_seg || iu == u + 1) issue_next();
             }
-            const double* __restrict__ xc = W.xcol[xcur] + jj0 * D;
-            double* __restrict__ cslab = a.slabs + ((size_t)a.nseg + t) * TB * D + (size_t)jj0 * D;
-#pragma unroll 1
-            for (int h = 0; h < 2; ++h) {             // two column pairs: 4 pairs per lane in lock-step
+#endif
+            const T* __restrict__ yst = W.y[cst];
+            const double* __restrict__ xc = W.xcol[cxb] + jj0 * D;
+            T cv[4][D];
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {             // positions 2h, 2h+1: 4 pairs per lane in lock-step
                 T ys[4], ss[4], dd[4][D];
 #pragma unroll
                 for (int qq = 0; qq < 2; ++qq) {
-                    const int q = 2 * h + qq;
-                    ys[2 * qq] = W.y[st][q * TB + lane];
-                    ys[2 * qq + 1] = W.y[st][q * TB + lane + 32];
+                    const int q = (2 * h + qq) ^ m;   // column of position 2h + qq
+                    ys[2 * qq] = yst[q * TB + lane];
+                    ys[2 * qq + 1] = yst[q * TB + lane + 32];
                     T sa = T(0), sb = T(0);
 #pragma unroll
                     for (int k = 0; k < D; ++k) {
@@ -298,12 +343,11 @@ pass_kernel(PassArgs a) {
                 T ll[4], uu[4];
                 Pair<T, TRUNC>::eval4(ss, ys, a.P, ll, uu);
                 T lsum = T(0);
-                T cv[2][D];
 #pragma unroll
                 for (int i = 0; i < 4; ++i) {
-                    const bool m = is_missing(ys[i]);
-                    if (!m) lsum += ll[i];                // predicated, no select
-                    uu[i] = m ? T(0) : uu[i];
+                    const bool mi = is_missing(ys[i]);
+                    if (!mi) lsum += ll[i];               // predicated, no select
+                    uu[i] = mi ? T(0) : uu[i];
                 }
 #pragma unroll
                 for (int k = 0; k < D; ++k) {
@@ -311,16 +355,28 @@ pass_kernel(PassArgs a) {
                     const T va1 = uu[2] * dd[2][k], vb1 = uu[3] * dd[3][k];
                     g0[k] -= A(va0 + va1);
                     g1[k] -= A(vb0 + vb1);
-                    cv[0][k] = va0 + vb0;
-                    cv[1][k] = va1 + vb1;
+                    if (h == 0) {
+                        cv[0][k] = va0 + vb0;
+                        cv[1][k] = va1 + vb1;
+                    } else {
+                        cv[2][k] = va0 + vb0;
+                        cv[3][k] = va1 + vb1;
+                    }
                 }
                 lik_w += A(lsum);
-#pragma unroll
-                for (int k = 0; k < D; ++k) {
-                    const T cs = reduce_scatter2(cv[0][k], cv[1][k], lane);
-                    if ((lane & 15) == 0) cslab[(2 * h + (lane >> 4)) * D + k] = A(cs);
-                }
             }
+            double* __restrict__ cslab = a.slabs + ((size_t)a.nseg + t) * TB * D + (size_t)jj0 * D;
+#ifndef MDS_EXP_NO_COLRED
+#pragma unroll
+            for (int k = 0; k < D; ++k) {
+                const T cs = reduce_scatter4_perm(cv[0][k], cv[1][k], cv[2][k], cv[3][k]);
+                if ((lane & 7) == 0) cslab[m * D + k] = A(cs);
+            }
+#else
+#pragma unroll
+            for (int k = 0; k < D; ++k) lik_w += A(cv[0][k] + cv[1][k] + cv[2][k] + cv[3][k]);
+            (void)cslab;
+#endif
             if (u + 1 == sg.z) {                      // last unit of the segment: its row partial
                 double* __restrict__ rslab = a.slabs + (size_t)(ws0 + si) * TB * D;
 #pragma unroll
@@ -332,6 +388,7 @@ pass_kernel(PassArgs a) {
                 }
                 ++si;
             }
+            cst = (cst + 1 == NSTAGE) ? 0 : cst + 1;
         }
     }
 #pragma unroll
