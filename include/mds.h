@@ -238,6 +238,28 @@ const char *mds_last_error(mds_ctx ctx);
 /* Static text for a status code. */
 const char *mds_status_string(mds_status s);
 
+/* Host-only work plan (no device needed): how a context with these
+ * arguments splits the triangle for a pass kernel of ctas x warps_per_cta
+ * warps.  Validates the plan's invariants (the warps' unit ranges tile the
+ * local units in order without crossing tile-rows; every partial slab is in
+ * exactly one row block's reduction list).  owned_rows (n bytes, nullable)
+ * gets 1 for rows whose tile-row this rank owns.  Errors: MDS_E_INVALID_ARG,
+ * MDS_E_UNSUPPORTED (too many segments per warp), MDS_E_STATE (a violated
+ * invariant: a bug). */
+typedef struct {
+    int64_t tile_rows;            /* tile-rows owned */
+    int64_t tiles;                /* 64x64 tiles stored */
+    int64_t pair_slots;           /* tiles * 4096 (computed slots incl. padding) */
+    int64_t pairs;                /* real unordered pairs (i > j, i < n) owned */
+    int64_t segments;             /* row-partial slabs */
+    int64_t slabs;                /* segments + tiles */
+    int64_t max_slabs_per_block;  /* longest reduction list */
+    int64_t min_units_per_warp, max_units_per_warp;
+    int64_t ranges_per_warp;      /* a warp's range is split into this many segment tables */
+} mds_plan_info;
+mds_status mds_plan(int64_t n, int32_t rank, int32_t world, int32_t ctas, int32_t warps_per_cta,
+                    mds_plan_info *info, uint8_t *owned_rows);
+
 /* Library version "major.minor.patch". */
 const char *mds_version(void);
 

@@ -27,7 +27,7 @@ EXPORTS = [
     "mds_evaluate_partial_device", "mds_combine_partials_device",
     "mds_observed_pairs", "mds_zero_distance_pairs", "mds_set_timing", "mds_last_timing",
     "mds_hmc_trajectory", "mds_hmc_run", "mds_leapfrog_device", "mds_get_locations", "mds_get_momentum",
-    "mds_set_allgather",
+    "mds_set_allgather", "mds_plan",
     "mds_last_error", "mds_status_string", "mds_version", "mds_device_info", "mds_measure_fma_peaks",
 ]
 
@@ -36,6 +36,12 @@ class MDSError(RuntimeError):
     def __init__(self, status: int, msg: str):
         super().__init__("%s: %s" % (STATUS.get(status, status), msg))
         self.status = status
+
+
+class PlanInfo(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_int64) for n in ("tile_rows", "tiles", "pair_slots", "pairs", "segments", "slabs",
+                                              "max_slabs_per_block", "min_units_per_warp", "max_units_per_warp",
+                                              "ranges_per_warp")]
 
 
 class HmcConfig(ctypes.Structure):
@@ -86,6 +92,7 @@ def _load():
         "mds_get_locations": [vp, dp],
         "mds_get_momentum": [vp, dp],
         "mds_set_allgather": [vp, ALLGATHER_FN, vp],
+        "mds_plan": [i64, i32, i32, i32, i32, P(PlanInfo), vp],
         "mds_device_info": [P(i32), P(i32), P(i32)],
         "mds_measure_fma_peaks": [P(ctypes.c_double), P(ctypes.c_double)],
     }
@@ -245,6 +252,14 @@ def mds_get_momentum(ctx, p):
 def mds_set_allgather(ctx, fn, user=None):
     """fn: an ALLGATHER_FN instance (keep a reference alive while ctx lives)."""
     _check(lib.mds_set_allgather(ctx, fn, user), ctx)
+
+
+def mds_plan(n, rank, world, ctas, warps_per_cta, owned_rows=None):
+    """Host-only work plan (no GPU needed).  owned_rows: optional uint8 array of n."""
+    info = PlanInfo()
+    _check(lib.mds_plan(int(n), int(rank), int(world), int(ctas), int(warps_per_cta), ctypes.byref(info),
+                        _ptr(owned_rows)))
+    return {f: getattr(info, f) for f, _ in PlanInfo._fields_}
 
 
 def mds_last_error(ctx):

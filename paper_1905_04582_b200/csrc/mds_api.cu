@@ -8,6 +8,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <climits>
 #include <string>
 #include <vector>
 
@@ -41,6 +42,7 @@ struct mds_ctx_s {
     int wpc = 0;                     // its warps per CTA
     size_t smem = 0;                 // its dynamic shared memory
     int nseg = 0;
+    int vpw = 1;
     int* d_warp_seg = nullptr;
     int4* d_segs = nullptr;
     int* d_blk_ptr = nullptr;
@@ -213,6 +215,7 @@ PassArgs base_args(mds_ctx c, const double* xeval) {
     a.blk_ptr = c->d_blk_ptr;
     a.blk_slab = c->d_blk_slab;
     a.nseg = c->nseg;
+    a.vpw = c->vpw;
     a.nb = c->nb;
     a.n = c->n;
     a.slabs = c->d_slabs;
@@ -303,12 +306,110 @@ mds_status eval_internal(mds_ctx c) {
     return MDS_OK;
 }
 
-// Static schedule of the persistent pass.  The local tiles' column-group
-// units (16 per tile, in tile order) are cut into GW = wpc G equal contiguous
-// ranges, one per warp; each range is cut at tile-row boundaries into
-// segments (I, u0, u1, tbase).  The CSR lists, for each row block b, its row
-// slabs (the segments of tile-row b, in order) and then the column slabs of
-// the local tiles (I, b), I ascending: the fixed order of the reduction.
+// ---------------------------------------------------------------- the plan
+// Host-only description of a context's work split (no device needed; also
+// exported through mds_plan for CPU tests).  Tile-rows are owned cyclically
+// (I mod world == rank).  The local tiles' column-group units (16 per tile, in
+// tile order) are cut into GW = ctas * wpc equal contiguous ranges, one per
+// warp; each range is cut at tile-row boundaries into segments (I, u0, u1,
+// tbase).  The CSR lists, for each row block b, its row slabs (the segments of
+// tile-row b, in order) and then the column slabs of the local tiles (I, b),
+// I ascending: the fixed order of the reduction.
+struct Plan {
+    int nb = 0;
+    int vpw = 1;                      // virtual ranges per warp
+    std::vector<int> tiles, row_local;
+    std::vector<int> warp_seg;
+    std::vector<int4> segs;
+    std::vector<int> ptr, slab;
+};
+
+// segments per virtual range: MAXSEG_W, or less for tests (MDS_DEBUG_MAXSEG)
+int max_segments() {
+    const char* e = std::getenv("MDS_DEBUG_MAXSEG");
+    const int v = e ? std::atoi(e) : 0;
+    return (v >= 1 && v < MAXSEG_W) ? v : MAXSEG_W;
+}
+
+bool make_plan(int64_t n, int rank, int world, int64_t ctas, int wpc, Plan& P, std::string* why) {
+    P = Plan();
+    const int maxseg = max_segments();
+    P.nb = (int)((n + TB - 1) / TB);
+    P.row_local.assign(P.nb, -1);
+    for (int I = 0; I < P.nb; ++I) {
+        if (I % world != rank) continue;
+        P.row_local[I] = (int)P.tiles.size();
+        for (int J = 0; J <= I; ++J) P.tiles.push_back((I << 16) | J);
+    }
+    const int64_t ntl = (int64_t)P.tiles.size();
+    const int64_t U = (int64_t)GROUPS_PER_TILE * ntl;
+    const int64_t GW = (int64_t)wpc * ctas;
+    // each warp's contiguous range is split into vpw virtual ranges; grow vpw
+    // until no virtual range spans more than MAXSEG_W tile-row segments
+    for (P.vpw = 1;; P.vpw *= 2) {
+        const int64_t V = GW * P.vpw;
+        P.warp_seg.assign(V + 1, 0);
+        P.segs.clear();
+        bool fits = true;
+        for (int64_t w = 0; w < V && fits; ++w) {
+            int64_t u = (U * w) / V, u1 = (U * (w + 1)) / V;
+            int nsw = 0;
+            while (u < u1) {
+                const int t = (int)(u / GROUPS_PER_TILE);
+                const int I = P.tiles[t] >> 16;
+                const int64_t row_end = (int64_t)GROUPS_PER_TILE * (P.row_local[I] + I + 1);
+                const int64_t e = std::min(u1, row_end);
+                P.segs.push_back(make_int4(I, (int)u, (int)e, P.row_local[I]));
+                u = e;
+                ++nsw;
+            }
+            fits = nsw <= maxseg;
+            P.warp_seg[w + 1] = (int)P.segs.size();
+        }
+        if (fits) break;
+        if (P.vpw > (1 << 20)) {
+            if (why) *why = "schedule: cannot bound segments per warp";
+            return false;
+        }
+    }
+    const int nseg = (int)P.segs.size();
+    P.ptr.assign(P.nb + 1, 0);
+    std::vector<std::vector<int>> rows_of(P.nb);
+    for (int s2 = 0; s2 < nseg; ++s2) rows_of[P.segs[s2].x].push_back(s2);
+    for (int b = 0; b < P.nb; ++b) {
+        P.ptr[b] = (int)P.slab.size();
+        for (int s2 : rows_of[b]) P.slab.push_back(s2);
+        for (int I = b; I < P.nb; ++I)
+            if (P.row_local[I] >= 0) P.slab.push_back(nseg + P.row_local[I] + b);
+    }
+    P.ptr[P.nb] = (int)P.slab.size();
+    return true;
+}
+
+// Invariants of a plan (used by mds_plan; a failure is a bug).
+bool check_plan(const Plan& P, std::string* why) {
+    const int64_t U = (int64_t)GROUPS_PER_TILE * (int64_t)P.tiles.size();
+    int64_t next = 0;
+    for (const int4& sg : P.segs) {           // segments tile the unit range in order
+        if (sg.y != next || sg.z <= sg.y) { if (why) *why = "segments not contiguous"; return false; }
+        const int t0 = sg.y / GROUPS_PER_TILE, t1 = (sg.z - 1) / GROUPS_PER_TILE;
+        if ((P.tiles[t0] >> 16) != sg.x || (P.tiles[t1] >> 16) != sg.x || P.row_local[sg.x] != sg.w) {
+            if (why) *why = "segment crosses a tile-row";
+            return false;
+        }
+        next = sg.z;
+    }
+    if (next != U) { if (why) *why = "units not covered"; return false; }
+    std::vector<int> seen(P.segs.size() + P.tiles.size(), 0);
+    for (int v : P.slab) {
+        if (v < 0 || v >= (int)seen.size()) { if (why) *why = "slab index out of range"; return false; }
+        ++seen[v];
+    }
+    for (size_t k = 0; k < seen.size(); ++k)
+        if (seen[k] != 1) { if (why) *why = "slab not listed exactly once"; return false; }
+    return true;
+}
+
 mds_status build_schedule(mds_ctx c) {
     int dev = 0, sms = 0, occ = 1 << 30;
     CK(cudaGetDevice(&dev));
@@ -329,34 +430,15 @@ mds_status build_schedule(mds_ctx c) {
     c->grid = (int)G;
     const int64_t GW = (int64_t)c->wpc * G;
 
-    std::vector<int> warp_seg(GW + 1, 0);
-    std::vector<int4> segs;
-    for (int64_t w = 0; w < GW; ++w) {
-        int64_t u = (U * w) / GW, u1 = (U * (w + 1)) / GW;
-        int nsw = 0;
-        while (u < u1) {
-            const int t = (int)(u / GROUPS_PER_TILE);
-            const int I = c->tiles[t] >> 16;
-            const int64_t row_end = (int64_t)GROUPS_PER_TILE * (c->row_local[I] + I + 1);
-            const int64_t e = std::min(u1, row_end);
-            segs.push_back(make_int4(I, (int)u, (int)e, c->row_local[I]));
-            u = e;
-            ++nsw;
-        }
-        if (nsw > MAXSEG_W) return fail(c, MDS_E_UNSUPPORTED, "schedule: too many segments per warp");
-        warp_seg[w + 1] = (int)segs.size();
-    }
+    Plan P;
+    std::string why;
+    if (!make_plan(c->n, c->rank, c->world, G, c->wpc, P, &why)) return fail(c, MDS_E_UNSUPPORTED, why);
+    const std::vector<int>& warp_seg = P.warp_seg;
+    const std::vector<int4>& segs = P.segs;
+    const std::vector<int>& ptr = P.ptr;
+    const std::vector<int>& slab = P.slab;
     c->nseg = (int)segs.size();
-    std::vector<int> ptr(c->nb + 1, 0), slab;
-    std::vector<std::vector<int>> rows_of(c->nb);
-    for (int s = 0; s < c->nseg; ++s) rows_of[segs[s].x].push_back(s);
-    for (int b = 0; b < c->nb; ++b) {
-        ptr[b] = (int)slab.size();
-        for (int s : rows_of[b]) slab.push_back(s);
-        for (int I = b; I < c->nb; ++I)
-            if (c->row_local[I] >= 0) slab.push_back(c->nseg + c->row_local[I] + b);
-    }
-    ptr[c->nb] = (int)slab.size();
+    c->vpw = P.vpw;
 
     mds_status st;
     const size_t nslab = (size_t)(c->nseg + std::max(c->ntl, 1));
@@ -409,7 +491,10 @@ mds_status create_impl(int64_t n, int32_t d, int32_t precision, int32_t truncati
     if (n < 2 || d < 1 || d > MDS_D_MAX || (precision != MDS_F64 && precision != MDS_F32) ||
         (truncation != 0 && truncation != 1) || world < 1 || rank < 0 || rank >= world)
         return MDS_E_INVALID_ARG;
-    if ((n + TB - 1) / TB > 0xffff) return MDS_E_INVALID_ARG;
+    {   // tile codes hold I, J in 16 bits; unit and slab indices are int32
+        const int64_t nb = (n + TB - 1) / TB;
+        if (nb > 0xffff || (nb * (nb + 1) / 2) * GROUPS_PER_TILE > 0x7fffffffLL) return MDS_E_INVALID_ARG;
+    }
     mds_ctx c = new (std::nothrow) mds_ctx_s();
     if (!c) return MDS_E_OOM;
     mds_status st = check_device(c);
@@ -427,12 +512,11 @@ mds_status create_impl(int64_t n, int32_t d, int32_t precision, int32_t truncati
     c->nb = (int)((n + TB - 1) / TB);
     c->npad = (int64_t)c->nb * TB;
 
-    // tile-row ownership: cyclic (I mod world == rank), SURVEY 8(e)
-    c->row_local.assign(c->nb, -1);
-    for (int I = 0; I < c->nb; ++I) {
-        if (I % world != rank) continue;
-        c->row_local[I] = (int)c->tiles.size();
-        for (int J = 0; J <= I; ++J) c->tiles.push_back((I << 16) | J);
+    {   // tile-row ownership: cyclic (I mod world == rank), SURVEY 8(e)
+        Plan P;
+        make_plan(n, rank, world, 0, 1, P, nullptr);
+        c->tiles = P.tiles;
+        c->row_local = P.row_local;
     }
     c->ntl = (int)c->tiles.size();
     c->row_supplied.assign(n, 0);
@@ -817,6 +901,46 @@ mds_status mds_last_timing(mds_ctx c, float* pair_ms, float* reduce_ms) {
     report_phases(c);
     if (pair_ms) *pair_ms = passes ? (float)(sp / passes) : 0.f;
     if (reduce_ms) *reduce_ms = passes ? (float)(sr / passes) : 0.f;
+    return MDS_OK;
+}
+
+mds_status mds_plan(int64_t n, int32_t rank, int32_t world, int32_t ctas, int32_t warps_per_cta, mds_plan_info* info,
+                    uint8_t* owned_rows) {
+    if (n < 2 || world < 1 || rank < 0 || rank >= world || ctas < 1 || warps_per_cta < 1 || !info ||
+        (n + TB - 1) / TB > 0xffff)
+        return MDS_E_INVALID_ARG;
+    Plan P;
+    std::string why;
+    if (!make_plan(n, rank, world, ctas, warps_per_cta, P, &why)) return MDS_E_UNSUPPORTED;
+    if (!check_plan(P, &why)) return MDS_E_STATE;
+    mds_plan_info r{};
+    int64_t pairs = 0;
+    for (int I = 0; I < P.nb; ++I) {
+        if (P.row_local[I] < 0) continue;
+        ++r.tile_rows;
+        for (int64_t i = (int64_t)I * TB; i < std::min<int64_t>(n, (int64_t)(I + 1) * TB); ++i) pairs += i;
+    }
+    if (owned_rows)
+        for (int64_t i = 0; i < n; ++i) owned_rows[i] = P.row_local[i / TB] >= 0 ? 1 : 0;
+    r.tiles = (int64_t)P.tiles.size();
+    r.pair_slots = r.tiles * TB * TB;
+    r.pairs = pairs;
+    r.segments = (int64_t)P.segs.size();
+    r.slabs = r.segments + r.tiles;
+    int64_t mx = 0, umin = INT64_MAX, umax = 0;
+    for (int b = 0; b < P.nb; ++b) mx = std::max<int64_t>(mx, P.ptr[b + 1] - P.ptr[b]);
+    const int64_t GW = (int64_t)ctas * warps_per_cta, U = (int64_t)GROUPS_PER_TILE * r.tiles;
+    const int64_t V = GW * P.vpw;
+    for (int64_t w = 0; w < GW; ++w) {
+        const int64_t u = (U * (w + 1) * P.vpw) / V - (U * w * P.vpw) / V;
+        umin = std::min(umin, u);
+        umax = std::max(umax, u);
+    }
+    r.max_slabs_per_block = mx;
+    r.min_units_per_warp = umin;
+    r.max_units_per_warp = umax;
+    r.ranges_per_warp = P.vpw;
+    *info = r;
     return MDS_OK;
 }
 

@@ -155,6 +155,7 @@ struct PassArgs {
     double* gl;
     double* xnext;
     double eps, heps, inv_tau2;
+    int vpw;                     // virtual unit ranges per warp (warp_seg has GW * vpw + 1 entries)
     SigmaParams P;
     unsigned long long* prof;    // optional [G][4] globaltimer stamps (start, end A, after sync, end)
 };
@@ -215,11 +216,17 @@ struct WarpStage {
 // budgets blocks in 4-warp granules: 12 warps -> 168 regs, 8 -> 255); fp64
 // needs ~150 for 4 interleaved pairs (tools/pair_probe.cu), more at larger D.
 template <typename T, int D> struct WarpsPerCTA {
-    static constexpr int value = sizeof(T) == 8 ? (D <= 3 ? 12 : 8) : (D <= 2 ? 24 : 16);
+    static constexpr int value = sizeof(T) == 8 ? (D <= 3 ? 12 : 8) : (D <= 2 ? 24 : (D <= 6 ? 16 : 12));
 };
 
 template <typename T, int D>
 constexpr size_t pass_smem_bytes() { return WarpsPerCTA<T, D>::value * sizeof(WarpStage<T, D>); }
+// dynamic staging + the static reduction buffers must fit the 227 KB of one CTA
+static_assert(pass_smem_bytes<double, 8>() + 2 * 8 * 256 <= 227 * 1024, "smem");
+static_assert(pass_smem_bytes<float, 8>() + 2 * 12 * 256 <= 227 * 1024, "smem");
+static_assert(pass_smem_bytes<float, 6>() + 2 * 16 * 256 <= 227 * 1024, "smem");
+static_assert(pass_smem_bytes<float, 2>() + 2 * 24 * 256 <= 227 * 1024, "smem");
+static_assert(pass_smem_bytes<double, 3>() + 2 * 12 * 256 <= 227 * 1024, "smem");
 
 template <typename T, int D, bool TRUNC, int MODE>
 __global__ void __launch_bounds__(WarpsPerCTA<T, D>::value * 32, 1)
@@ -237,18 +244,25 @@ pass_kernel(PassArgs a) {
     if (a.prof && threadIdx.x == 0) a.prof[blockIdx.x * 4 + 0] = gtimer();
 
     // ------------------------------------------------------------ phase A (per warp)
-    const int ws0 = a.warp_seg[gw], ws1 = a.warp_seg[gw + 1];
-    const int nsw = ws1 - ws0;
-    if (lane < nsw) W.seg[lane] = a.segs[ws0 + lane];
+    // a warp's contiguous unit range is processed as vpw consecutive virtual
+    // ranges of at most MAXSEG_W segments each (their segment table fits smem)
     if (lane == 0) {
 #pragma unroll
         for (int b = 0; b < NSTAGE; ++b) mbar_init(&W.bar[b], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         fence_async_smem();
     }
-    __syncwarp();
-
     A lik_w = A(0);
+    uint32_t phase = 0;                      // bit b: parity of stage b (persists across ranges)
+    int cst = 0;                             // stage of the next unit to compute
+#pragma unroll 1
+    for (int vv = 0; vv < a.vpw; ++vv) {
+    const int vw = gw * a.vpw + vv;
+    const int ws0 = a.warp_seg[vw], ws1 = a.warp_seg[vw + 1];
+    const int nsw = ws1 - ws0;
+    __syncwarp();
+    if (lane < nsw) W.seg[lane] = a.segs[ws0 + lane];
+    __syncwarp();
     if (nsw > 0) {
         constexpr uint32_t YB = 4 * TB * sizeof(T), XB = TB * D * sizeof(double);
         const int ub = W.seg[0].y, ue = W.seg[nsw - 1].z;
@@ -268,7 +282,7 @@ pass_kernel(PassArgs a) {
             }
         };
         // issue cursor (units are issued in order, up to two ahead of compute)
-        int iu = ub, isi = 0, ist = 0, ixb = 0, itile = -1;
+        int iu = ub, isi = 0, ist = cst, ixb = 0, itile = -1;
         auto issue_next = [&]() {
             while (iu >= W.seg[isi].z) ++isi;
             const int t = iu / GROUPS_PER_TILE;
@@ -281,8 +295,7 @@ pass_kernel(PassArgs a) {
         };
         issue_next();
         if (iu < ue && iu != W.seg[isi].z) issue_next();    // second unit in flight (not a new segment)
-        uint32_t phase = 0;                                  // bit b: parity of stage b
-        int si = 0, cst = 0, cxb = 0, ctile = -1;
+        int si = 0, cxb = 0, ctile = -1;
         T xi0[D], xi1[D];
         A g0[D], g1[D];
 #pragma unroll
@@ -391,6 +404,7 @@ pass_kernel(PassArgs a) {
             cst = (cst + 1 == NSTAGE) ? 0 : cst + 1;
         }
     }
+    }   // virtual ranges
 #pragma unroll
     for (int m = 16; m >= 1; m >>= 1) lik_w += __shfl_xor_sync(0xffffffffu, lik_w, m);
     if (lane == 0) a.likpart[gw] = lik_w;

@@ -352,3 +352,26 @@ def test_hmc_run_c1_chain(mds):
         ll, _ = c.log_likelihood_and_gradient()
     assert st["final_loglik"] == pytest.approx(oracle.loglik_grad(y, x, w.sigma, 1)["loglik"], rel=1e-10)
     assert ll == pytest.approx(st["final_loglik"], rel=1e-12)
+
+
+def test_virtual_ranges_and_wide_d(mds):
+    """Warp ranges split into several segment tables (forced small with
+    MDS_DEBUG_MAXSEG), and the widest D in both precisions."""
+    import os
+    w, y, x = instance(2500, 2, 0.05, seed=44)
+    ref = oracle.loglik_grad(y, x, w.sigma, 1)
+    os.environ["MDS_DEBUG_MAXSEG"] = "2"
+    try:
+        ll, g = run_gpu(mds, w.n, w.d, y, x, w.sigma)
+    finally:
+        del os.environ["MDS_DEBUG_MAXSEG"]
+    assert_fp64_parity(ll, g, ref, "maxseg=2")
+    for d in (7, 8):
+        w, y, x = instance(700, d, 0.1, seed=50 + d)
+        ref = oracle.loglik_grad(y, x, w.sigma, 1)
+        ll, g = run_gpu(mds, w.n, d, y, x, w.sigma)
+        assert_fp64_parity(ll, g, ref, "d=%d" % d)
+        y32 = y.astype(np.float32).astype(np.float64)
+        x32 = x.astype(np.float32).astype(np.float64)
+        ll, g = run_gpu(mds, w.n, d, y, x, w.sigma, prec="f32")
+        fp32_check(ll, g, oracle.loglik_grad(y32, x32, w.sigma, 1))

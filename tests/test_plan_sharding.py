@@ -1,0 +1,103 @@
+"""Host-side logic of the sharded path, on CPU (no GPU needed).
+
+mds_plan exposes the work split the library uses (tile-row ownership, the
+persistent kernel's warp ranges and segments, the fixed-order reduction lists)
+and checks its invariants.  The world_size-2 test runs two gloo processes that
+each plan their shard, exchange over torch.distributed (the same all-gather the
+GPU path uses through mds_set_allgather) and verify the shards partition the
+triangle and that a rank-ordered combine gives identical results on both ranks.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+import paper_1905_04582_b200 as mds
+
+
+@pytest.mark.parametrize("n", [2, 3, 63, 64, 65, 1000, 5392, 30000])
+@pytest.mark.parametrize("world", [1, 2, 3, 8])
+def test_shards_partition_the_triangle(n, world):
+    cover = np.zeros(n, dtype=np.int64)
+    total = 0
+    for r in range(world):
+        own = np.zeros(n, dtype=np.uint8)
+        info = mds.mds_plan(n, r, world, 148, 12, own)
+        cover += own
+        total += info["pairs"]
+        assert info["slabs"] == info["segments"] + info["tiles"]
+        assert info["max_units_per_warp"] - info["min_units_per_warp"] <= 1   # balanced warps
+    assert total == n * (n - 1) // 2
+    assert np.all(cover == 1)
+
+
+def test_plan_scales_to_c5():
+    info = mds.mds_plan(100000, 0, 1, 148, 12)
+    assert info["pairs"] == 100000 * 99999 // 2
+    assert info["pair_slots"] >= info["pairs"]
+    assert info["pair_slots"] / info["pairs"] < 1.002       # padding overhead ~0.1%
+
+
+def test_plan_rejects_bad_arguments():
+    for args in [(1, 0, 1, 148, 12), (100, 2, 2, 148, 12), (100, 0, 1, 0, 12), (100, 0, 0, 148, 12)]:
+        with pytest.raises(mds.MDSError):
+            mds.mds_plan(*args)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, n, q):
+    import torch
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_1905_04582_b200 as m
+        own = np.zeros(n, dtype=np.uint8)
+        info = m.mds_plan(n, rank, world, 148, 12, own)
+        # this rank's "partial": per row, the number of pairs (i, j<i) it owns,
+        # plus a trailing scalar (its pair total) -- the n*d + 1 layout of the GPU partial
+        part = torch.zeros(n + 1, dtype=torch.float64)
+        rows = torch.from_numpy(own.astype(np.float64))
+        part[:n] = rows * torch.arange(n, dtype=torch.float64)
+        part[n] = float(info["pairs"])
+        gathered = torch.empty(world * (n + 1), dtype=torch.float64)
+        dist.all_gather_into_tensor(gathered, part)
+        g = gathered.view(world, n + 1)
+        combined = g[0].clone()
+        for r in range(1, world):            # rank-ordered sum, as combine_kernel
+            combined += g[r]
+        ok = bool(torch.all(combined[:n] == torch.arange(n, dtype=torch.float64))) and \
+            combined[n].item() == n * (n - 1) // 2
+        # identical on every rank
+        chk = torch.tensor([combined.sum().item()], dtype=torch.float64)
+        allv = [torch.zeros(1, dtype=torch.float64) for _ in range(world)]
+        dist.all_gather(allv, chk)
+        same = all(v.item() == allv[0].item() for v in allv)
+        q.put((rank, ok and same))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("n", [1000, 5392])
+def test_gloo_world2_partition_and_combine(n):
+    import torch.multiprocessing as tmp
+    ctx = tmp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, n, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+    assert sorted(r for r, _ in res) == [0, 1]
+    assert all(ok for _, ok in res)
