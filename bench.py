@@ -222,7 +222,11 @@ def run_ours(args):
     clocks = ClockSampler(torch.cuda.current_device())
     ev0 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ev1 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    ctx.set_timing(True)
+    # the library's timing mode (events around every launch) perturbs
+    # back-to-back cooperative launches by ~8 us/step; unsharded, a step IS one
+    # pass-kernel launch, so the per-step events below are the kernel's launch
+    # duration.  Sharded steps have several kernels + NCCL: timing mode is on.
+    ctx.set_timing(world > 1)
     clocks.start()
     time.sleep(0.2)
     if world > 1:
@@ -237,9 +241,12 @@ def run_ours(args):
     if world > 1:
         dist.barrier()
     clk = clocks.stop()
-    pair_ms, red_ms = ctx.last_timing()
-    ctx.set_timing(False)
     step_ms = np.array([a.elapsed_time(b) for a, b in zip(ev0, ev1)])
+    if world > 1:
+        pair_ms, red_ms = ctx.last_timing()
+    else:
+        pair_ms, red_ms = float(step_ms.mean()), 0.0
+    ctx.set_timing(False)
     tot_ms = float(step_ms.sum())
     if world > 1:
         t = torch.tensor([tot_ms, pair_ms], dtype=torch.float64, device="cuda")

@@ -235,6 +235,7 @@ pass_kernel(PassArgs a) {
     constexpr int WPC = WarpsPerCTA<T, D>::value;
     extern __shared__ __align__(128) unsigned char dsm[];
     __shared__ A red[WPC][32];
+    __shared__ A red2[WPC][32];
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int gw = blockIdx.x * WPC + warp;
@@ -419,62 +420,81 @@ pass_kernel(PassArgs a) {
     if (a.prof && threadIdx.x == 0) a.prof[blockIdx.x * 4 + 2] = gtimer();
 
     // ------------------------------------------------------------ phase B
-    // job = (row block b, chunk of 32 slab elements); warp w sums slabs w, w+WPC, ..
-    const int chunks = (TB * D + 31) / 32;
+    // job = (row block b, chunk of 64 slab elements, 2 per lane); warp w sums
+    // slabs w, w + WPC, ... in order, 8 slab indices then 16 values in flight
+    constexpr int CH = 64;
+    const int chunks = (TB * D + CH - 1) / CH;
     const int jobs = a.nb * chunks;
     for (int job = blockIdx.x; job < jobs; job += gridDim.x) {
         const int b = job / chunks, ch = job % chunks;
-        const int el = ch * 32 + lane;            // element inside the slab (ii * D + k)
+        const int e0 = ch * CH + lane, e1 = e0 + 32;       // elements inside the slab (ii * D + k)
+        const bool v0 = e0 < TB * D, v1 = e1 < TB * D;
         const int q0 = a.blk_ptr[b], q1 = a.blk_ptr[b + 1];
-        A acc = A(0);
-        if (el < TB * D) {
-            int q = q0 + warp;
-            for (; q + 3 * WPC < q1; q += 4 * WPC) {   // 4 independent loads in flight
-                A v[4];
+        A acc0 = A(0), acc1 = A(0);
+        int q = q0 + warp;
+        for (; q + 7 * WPC < q1; q += 8 * WPC) {
+            int id[8];
 #pragma unroll
-                for (int r = 0; r < 4; ++r) v[r] = a.slabs[(size_t)a.blk_slab[q + r * WPC] * TB * D + el];
+            for (int r = 0; r < 8; ++r) id[r] = __ldg(a.blk_slab + q + r * WPC);
+            A x0[8], x1[8];
 #pragma unroll
-                for (int r = 0; r < 4; ++r) acc += v[r];
+            for (int r = 0; r < 8; ++r) {
+                const double* sp = a.slabs + (size_t)id[r] * TB * D;
+                x0[r] = v0 ? sp[e0] : A(0);
+                x1[r] = v1 ? sp[e1] : A(0);
             }
-            for (; q < q1; q += WPC) acc += a.slabs[(size_t)a.blk_slab[q] * TB * D + el];
-        }
-        red[warp][lane] = acc;
-        __syncthreads();
-        if (warp == 0 && el < TB * D) {
-            A g = red[0][lane];
 #pragma unroll
-            for (int w = 1; w < WPC; ++w) g += red[w][lane];
-            const int64_t e = (int64_t)b * TB * D + el;
-            if (e < a.n * D) {
-                if (MODE == MODE_EVAL) {
-                    a.grad[e] = g;
-                } else {
-                    // leapfrog: the pass ran at xnext = x + eps (p + eps/2 gl)
-                    const double xe = a.xeval[e];
-                    const double ph = __fma_rn(a.heps, a.gl[e], a.p[e]);   // first half-kick
-                    const double gn = g - xe * a.inv_tau2;                  // grad log pi at xnext
-                    const double pn = __fma_rn(a.heps, gn, ph);             // second half-kick
-                    a.grad[e] = g;
-                    a.x[e] = xe;
-                    a.p[e] = pn;
-                    a.gl[e] = gn;
-                    a.xnext[e] = drift(xe, pn, gn, a.eps, a.heps);           // next step's drift
+            for (int r = 0; r < 8; ++r) {
+                acc0 += x0[r];
+                acc1 += x1[r];
+            }
+        }
+        for (; q < q1; q += WPC) {
+            const double* sp = a.slabs + (size_t)__ldg(a.blk_slab + q) * TB * D;
+            if (v0) acc0 += sp[e0];
+            if (v1) acc1 += sp[e1];
+        }
+        red[warp][lane] = acc0;
+        red2[warp][lane] = acc1;
+        __syncthreads();
+        if (warp < 2) {
+            const int el = warp == 0 ? e0 : e1;
+            if (el < TB * D) {
+                A g = warp == 0 ? red[0][lane] : red2[0][lane];
+#pragma unroll
+                for (int w = 1; w < WPC; ++w) g += warp == 0 ? red[w][lane] : red2[w][lane];
+                const int64_t e = (int64_t)b * TB * D + el;
+                if (e < a.n * D) {
+                    if (MODE == MODE_EVAL) {
+                        a.grad[e] = g;
+                    } else {
+                        // leapfrog: the pass ran at xnext = x + eps (p + eps/2 gl)
+                        const double xe = a.xeval[e];
+                        const double ph = __fma_rn(a.heps, a.gl[e], a.p[e]);   // first half-kick
+                        const double gn = g - xe * a.inv_tau2;                  // grad log pi at xnext
+                        const double pn = __fma_rn(a.heps, gn, ph);             // second half-kick
+                        a.grad[e] = g;
+                        a.x[e] = xe;
+                        a.p[e] = pn;
+                        a.gl[e] = gn;
+                        a.xnext[e] = drift(xe, pn, gn, a.eps, a.heps);           // next step's drift
+                    }
                 }
             }
         }
         __syncthreads();
     }
-    if (blockIdx.x == 0) {
-        // log L: fixed-order strided partial sums + tree over the warp partials
+    // log L on the last CTA (the one with the fewest reduction jobs): fixed-order
+    // strided partial sums over the warp partials, then warps in order
+    if (blockIdx.x == gridDim.x - 1) {
         const int GW = gridDim.x * WPC;
         A s = A(0);
         for (int q = threadIdx.x; q < GW; q += WPC * 32) s += a.likpart[q];
-        __shared__ A lr[WPC * 32];
-        lr[threadIdx.x] = s;
+        red[warp][lane] = s;
         __syncthreads();
         if (threadIdx.x < 32) {
             A t = A(0);
-            for (int w = 0; w < WPC; ++w) t += lr[w * 32 + threadIdx.x];
+            for (int w = 0; w < WPC; ++w) t += red[w][threadIdx.x];
 #pragma unroll
             for (int m = 16; m >= 1; m >>= 1) t += __shfl_xor_sync(0xffffffffu, t, m);
             if (threadIdx.x == 0) *a.lik = t;
