@@ -748,6 +748,8 @@ mds_status mds_set_sigma(mds_ctx c, double sigma) {
     P.half_inv_sigma2 = 0.5 / (sigma * sigma);
     P.k0 = -0.5 * std::log(2.0 * pi * sigma * sigma);
     P.cg = 1.0 / (sigma * std::sqrt(2.0 * pi));
+    P.ks = KAPPA64 * sigma;
+    P.two_ks = 2.0 * KAPPA64 * sigma;
     P.inv_sigma_f = (float)P.inv_sigma;
     P.inv_sigma2_f = (float)P.inv_sigma2;
     P.half_inv_sigma2_f = (float)P.half_inv_sigma2;

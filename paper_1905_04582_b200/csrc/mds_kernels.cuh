@@ -46,31 +46,15 @@ enum Mode { MODE_EVAL = 0, MODE_LEAPFROG = 2 };
 template <typename T, bool TRUNC> struct Pair;
 template <bool TRUNC> struct Pair<double, TRUNC> {
     __device__ __forceinline__ static void eval4(const double (&s)[4], const double (&y)[4], const SigmaParams& P,
-                                                 double (&l)[4], double (&u)[4]) {
-        pair_f64_n<TRUNC, 4>(s, y, P, l, u);
-    }
-    // the two rows of one column, evaluated in lock-step (mds_math.cuh)
-    __device__ __forceinline__ static void eval2(double sa, double sb, double ya, double yb, const SigmaParams& P,
-                                                 double& la, double& ua, double& lb, double& ub) {
-        const double s[2] = {sa, sb}, y[2] = {ya, yb};
-        double l[2], u[2];
-        pair_f64_n<TRUNC, 2>(s, y, P, l, u);
-        la = l[0];
-        ua = u[0];
-        lb = l[1];
-        ub = u[1];
+                                                 const double* exptab, double (&l)[4], double (&u)[4]) {
+        pair_f64_n<TRUNC, 4>(s, y, P, exptab, l, u);
     }
 };
 template <bool TRUNC> struct Pair<float, TRUNC> {
     __device__ __forceinline__ static void eval4(const float (&s)[4], const float (&y)[4], const SigmaParams& P,
-                                                 float (&l)[4], float (&u)[4]) {
+                                                 const double*, float (&l)[4], float (&u)[4]) {
 #pragma unroll
         for (int i = 0; i < 4; ++i) pair_f32<TRUNC>(s[i], y[i], P, l[i], u[i]);
-    }
-    __device__ __forceinline__ static void eval2(float sa, float sb, float ya, float yb, const SigmaParams& P,
-                                                 float& la, float& ua, float& lb, float& ub) {
-        pair_f32<TRUNC>(sa, ya, P, la, ua);
-        pair_f32<TRUNC>(sb, yb, P, lb, ub);
     }
 };
 
@@ -236,6 +220,9 @@ pass_kernel(PassArgs a) {
     extern __shared__ __align__(128) unsigned char dsm[];
     __shared__ A red[WPC][32];
     __shared__ A red2[WPC][32];
+    __shared__ double exptab[64];
+    if (threadIdx.x < 64) exptab[threadIdx.x] = EXPT64_TAB[threadIdx.x];
+    __syncthreads();
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int gw = blockIdx.x * WPC + warp;
@@ -355,7 +342,7 @@ pass_kernel(PassArgs a) {
                     ss[2 * qq + 1] = sb;
                 }
                 T ll[4], uu[4];
-                Pair<T, TRUNC>::eval4(ss, ys, a.P, ll, uu);
+                Pair<T, TRUNC>::eval4(ss, ys, a.P, exptab, ll, uu);
                 T lsum = T(0);
 #pragma unroll
                 for (int i = 0; i < 4; ++i) {

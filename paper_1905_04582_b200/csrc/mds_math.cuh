@@ -8,15 +8,16 @@
 // +u (x_i - x_j) to g_j.  The pair's v = u (x_i - x_j) is formed by the caller.
 //
 // Device math, t >= 0 always on this path:
-//   E      = exp(-t^2/2) = exp(-s/(2 sigma^2))     -- one exp, argument from s directly
+//   E      = exp(-t^2/2) = exp(-s/(2 sigma^2))     -- one exp, argument from s directly:
+//            2^n 2^(j/64) p(r), 64-entry table in shared memory, degree-5 p
 //   Q      = 1 - Phi(t) = E q(w),  q = erfcx(t/sqrt2)/2 as a minimax polynomial in
 //            w = (t-K)/(t+K) (one reciprocal); absolute error of Q <= 3e-16
 //   1/Phi, 1/(1+Phi) from ONE reciprocal of Phi(1+Phi)
 //   log Phi = log1p(-Q) = -2 atanh(Q/(2-Q))        -- polynomial in z = (Q/(2-Q))^2 <= 1/9
 //   phi/Phi = E / (sqrt(2 pi) Phi)                 -- shares E with Q
 // The reciprocal and rsqrt seeds come from MUFU (rcp/rsqrt.approx) refined by one
-// cubic Newton step.  About 80 FP64 instructions per pair (D = 2) instead of ~160
-// for libdevice erfc/log1p/exp/div.
+// cubic Newton step.  About 65 FP64 instructions per pair of math (+ ~8 for the
+// distance and the sums, D = 2) instead of ~160 for libdevice erfc/log1p/exp/div.
 #pragma once
 #include <cstdint>
 #include "mds_coeffs.h"
@@ -30,6 +31,8 @@ struct SigmaParams {
     double half_inv_sigma2;  // 1/(2 sigma^2)
     double k0;               // -1/2 log(2 pi sigma^2)
     double cg;               // 1/(sigma sqrt(2 pi))
+    double ks;               // KAPPA64 * sigma: w = (d - ks)/(d + ks) = (t - K)/(t + K)
+    double two_ks;           // 2 KAPPA64 sigma
     float inv_sigma_f, inv_sigma2_f, half_inv_sigma2_f, k0_f, cg_f;
 };
 
@@ -135,55 +138,7 @@ __device__ __forceinline__ bool is_missing(float y) {
     return (uint32_t)__float_as_uint(y) == CANON_NAN_F32;
 }
 
-// ---------------------------------------------------------------- fp64 pair
-template <bool TRUNC>
-__device__ __forceinline__ void pair_f64(double s, double y, const SigmaParams& P,
-                                         double& ell, double& u) {
-    // s >= 2^-1007 for the rsqrt seed (integer max on the high word; s >= 0).
-    const double sc = __hiloint2double(max(__double2hiint(s), 0x01000000), __double2loint(s));
-    const double r0 = rsqrt_seed(sc);
-    const double h = sc * r0;
-    const double e = fma(-h, r0, 1.0);               // 1 - s r0^2
-    const double c = fma(e, 0.375, 0.5);
-    const double re = r0 * e;
-    const double rs = fma(re, c, r0);                // 1/d  (cubic step)
-    const double d = s * rs;                         // exactly 0 when s == 0
-    const double res = y - d;
-    double l = fma(-(res * P.half_inv_sigma2), res, P.k0);
-    if (TRUNC) {
-        const double t = d * P.inv_sigma;
-        double a = s * P.half_inv_sigma2;            // t^2/2 >= 0
-        a = __hiloint2double(min(__double2hiint(a), 0x4085E000), __double2loint(a));  // a <= ~700
-        // E = exp(-a): k = rint(-a log2 e), r = -a - k ln2, E = 2^k p(r)
-        const double MAGIC = 6755399441055744.0;     // 1.5 * 2^52
-        const double kd = fma(a, -1.4426950408889634, MAGIC);
-        const int k = __double2loint(kd);
-        const double fk = kd - MAGIC;
-        double r = fma(fk, -0.6931471805599453, -a);
-        r = fma(fk, -2.3190468138462996e-17, r);
-        const double p = horner<EXP64_DEG>(EXP64_C, r);
-        const double E = __hiloint2double(__double2hiint(p) + (int)((unsigned)k << 20), __double2loint(p));
-        // Q = 1 - Phi(t) = E q(w), w = (t - K)/(t + K)
-        const double rden = rcp_refined(t + KAPPA64);
-        const double w = fma(-2.0 * KAPPA64, rden, 1.0);
-        const double q = horner<Q64_DEG>(Q64_C, w);
-        const double Q = E * q;
-        const double Phi = 1.0 - Q;
-        const double opp = 2.0 - Q;                  // 1 + Phi
-        const double rp = rcp_refined(Phi * opp);    // 1/(Phi (1 + Phi))
-        const double invPhi = opp * rp;
-        const double invOpp = Phi * rp;
-        const double G = (E * P.cg) * invPhi;        // phi(t) / (sigma Phi(t))
-        const double sa = Q * invOpp;                // Q/(2 - Q), in [0, 1/3]
-        const double at = horner<ATANH64_DEG>(ATANH64_C, sa * sa);
-        l = fma(sa, at, l);                          // - log Phi = 2 atanh(sa)
-        u = fma(-res, P.inv_sigma2, G) * rs;
-    } else {
-        u = (-res * P.inv_sigma2) * rs;
-    }
-    ell = l;
-}
-
+// ---------------------------------------------------------------- fp64 pairs
 // NP independent pairs in lock-step: every step is issued for all NP pairs
 // before the next, so the FP64 dependency chains (Horner steps, Newton steps)
 // of different pairs interleave in the instruction stream and hide the DFMA
@@ -191,7 +146,7 @@ __device__ __forceinline__ void pair_f64(double s, double y, const SigmaParams& 
 // pair_f64, operation for operation.
 template <bool TRUNC, int NP>
 __device__ __forceinline__ void pair_f64_n(const double (&s)[NP], const double (&y)[NP], const SigmaParams& P,
-                                           double (&ell)[NP], double (&u)[NP]) {
+                                           const double* __restrict__ exptab, double (&ell)[NP], double (&u)[NP]) {
     double rs[NP], d[NP], res[NP], l[NP];
 #pragma unroll
     for (int i = 0; i < NP; ++i) {
@@ -210,41 +165,39 @@ __device__ __forceinline__ void pair_f64_n(const double (&s)[NP], const double (
         l[i] = fma(-(res[i] * P.half_inv_sigma2), res[i], P.k0);
     }
     if (TRUNC) {
-        double t[NP], a[NP], r[NP], E[NP], w[NP];
+        // E = exp(-a), a = t^2/2 = s/(2 sigma^2): k = rint(-64 a / ln2), E = 2^(k>>6) 2^((k&63)/64) p(r),
+        // |r| <= ln2/128 (table in shared memory, degree-5 polynomial)
+        double r[NP], E[NP], w[NP], den[NP], y0[NP];
         int k[NP];
-        const double MAGIC = 6755399441055744.0;
+        const double MAGIC = 6755399441055744.0;   // 1.5 * 2^52
 #pragma unroll
         for (int i = 0; i < NP; ++i) {
-            t[i] = d[i] * P.inv_sigma;
-            a[i] = s[i] * P.half_inv_sigma2;
-            a[i] = __hiloint2double(min(__double2hiint(a[i]), 0x4085E000), __double2loint(a[i]));
-            const double kd = fma(a[i], -1.4426950408889634, MAGIC);
+            double a = s[i] * P.half_inv_sigma2;
+            a = __hiloint2double(min(__double2hiint(a), 0x4085E000), __double2loint(a));   // a <= ~700
+            const double kd = fma(a, -92.33248261689366, MAGIC);                          // 64 / ln2
             k[i] = __double2loint(kd);
             const double fk = kd - MAGIC;
-            r[i] = fma(fk, -0.6931471805599453, -a[i]);
-            r[i] = fma(fk, -2.3190468138462996e-17, r[i]);
-        }
-        // rcp seeds for (t + K) issued early: the MUFU latency overlaps the exp polynomial
-        double den[NP], y0[NP];
-#pragma unroll
-        for (int i = 0; i < NP; ++i) {
-            den[i] = t[i] + KAPPA64;
+            r[i] = fma(fk, -0.010830424696249145, -a);                                    // ln2/64 hi
+            r[i] = fma(fk, -3.6235106466348432e-19, r[i]);                                // ln2/64 lo
+            // w = (t - K)/(t + K) = (d - K sigma)/(d + K sigma): MUFU seed issued early
+            den[i] = d[i] + P.ks;
             y0[i] = rcp_seed(den[i]);
         }
         double p[NP];
 #pragma unroll
-        for (int i = 0; i < NP; ++i) p[i] = EXP64_C[EXP64_DEG];
+        for (int i = 0; i < NP; ++i) p[i] = EXPT64_C[EXPT64_DEG];
 #pragma unroll
-        for (int j = EXP64_DEG - 1; j >= 0; --j)
+        for (int j = EXPT64_DEG - 1; j >= 0; --j)
 #pragma unroll
-            for (int i = 0; i < NP; ++i) p[i] = fma(p[i], r[i], EXP64_C[j]);
+            for (int i = 0; i < NP; ++i) p[i] = fma(p[i], r[i], EXPT64_C[j]);
 #pragma unroll
         for (int i = 0; i < NP; ++i) {
-            E[i] = __hiloint2double(__double2hiint(p[i]) + (int)((unsigned)k[i] << 20), __double2loint(p[i]));
+            const double pt = p[i] * exptab[k[i] & 63];
+            E[i] = __hiloint2double(__double2hiint(pt) + (int)((unsigned)(k[i] >> 6) << 20), __double2loint(pt));
             const double e1 = fma(-den[i], y0[i], 1.0);
             const double ee = fma(e1, e1, e1);
             const double rden = fma(ee, y0[i], y0[i]);
-            w[i] = fma(-2.0 * KAPPA64, rden, 1.0);
+            w[i] = fma(-P.two_ks, rden, 1.0);
         }
         double q[NP];
 #pragma unroll

@@ -7,12 +7,15 @@ using namespace mdsk;
 
 template <int NP, int WPC>
 __global__ void __launch_bounds__(WPC * 32, 1) probe(double* out, int iters, SigmaParams P) {
+    __shared__ double tab[64];
+    if (threadIdx.x < 64) tab[threadIdx.x] = EXPT64_TAB[threadIdx.x];
+    __syncthreads();
     double s[NP], y[NP], acc = 0.0;
 #pragma unroll
     for (int i = 0; i < NP; ++i) { s[i] = 1.0 + 0.37 * i + threadIdx.x * 1e-4; y[i] = 1.1 + 0.1 * i; }
     for (int it = 0; it < iters; ++it) {
         double l[NP], u[NP];
-        pair_f64_n<true, NP>(s, y, P, l, u);
+        pair_f64_n<true, NP>(s, y, P, tab, l, u);
 #pragma unroll
         for (int i = 0; i < NP; ++i) { acc += l[i]; s[i] += u[i] * 1e-12; }
     }

@@ -13,6 +13,8 @@ template <int LEVEL, int WPC>
 __global__ void __launch_bounds__(WPC * 32, 1) probe(double* out, int units, SigmaParams P) {
     __shared__ double ys[WPC][256];
     __shared__ double xc[64 * 2];
+    __shared__ double tab[64];
+    if (threadIdx.x < 64) tab[threadIdx.x] = EXPT64_TAB[threadIdx.x];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, m = (lane >> 3) & 3;
     for (int i = threadIdx.x; i < WPC * 256; i += blockDim.x) ys[i / 256][i % 256] = 0.5 + 0.001 * (i % 97);
     for (int i = threadIdx.x; i < 128; i += blockDim.x) xc[i] = 0.01 * i;
@@ -49,7 +51,7 @@ __global__ void __launch_bounds__(WPC * 32, 1) probe(double* out, int units, Sig
                 }
             }
             double ll[4], uu[4];
-            pair_f64_n<true, 4>(ss, yy, P, ll, uu);
+            pair_f64_n<true, 4>(ss, yy, P, tab, ll, uu);
             if (LEVEL >= 2) {
                 double lsum = 0;
 #pragma unroll
