@@ -454,14 +454,17 @@ mds_status build_schedule(mds_ctx c) {
     if (!slab.empty()) CK(cudaMemcpy(c->d_blk_slab, slab.data(), slab.size() * sizeof(int), cudaMemcpyHostToDevice));
     CK(cudaMemset(c->d_slabs, 0, nslab * TB * c->d * sizeof(double)));
     const char* pe = std::getenv("MDS_PROFILE_PHASES");
-    if (pe && pe[0] == '1' && (st = dalloc(c, &c->d_prof, (size_t)G * 4))) return st;
+    if (pe && pe[0] == '1') {
+        if ((st = dalloc(c, &c->d_prof, (size_t)G * 6))) return st;
+        CK(cudaMemset(c->d_prof, 0, (size_t)G * 6 * sizeof(unsigned long long)));
+    }
     return MDS_OK;
 }
 
 // MDS_PROFILE_PHASES=1: per-CTA phase times of the last pass, printed to stderr
 void report_phases(mds_ctx c) {
     if (!c->d_prof) return;
-    std::vector<unsigned long long> h((size_t)c->grid * 4);
+    std::vector<unsigned long long> h((size_t)c->grid * 6);
     if (cudaMemcpy(h.data(), c->d_prof, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost)) return;
     unsigned long long t0 = ~0ull, t3 = 0;
     std::vector<double> a, w, b;
@@ -482,6 +485,19 @@ void report_phases(mds_ctx c) {
     };
     std::fprintf(stderr, "[mds phases us] span %.2f | A end: %s | sync wait: %s | B: %s\n", (t3 - t0) * 1e-3,
                  st(a).c_str(), st(w).c_str(), st(b).c_str());
+    // slowest CTAs: SM id, phase-A end, units whose TMA data had not landed (cumulative)
+    std::vector<int> idx(c->grid);
+    for (int g = 0; g < c->grid; ++g) idx[g] = g;
+    std::sort(idx.begin(), idx.end(), [&](int x, int y) { return a[x] > a[y]; });
+    std::fprintf(stderr, "[mds phases] slowest (cta sm A_end not_ready):");
+    for (int q = 0; q < std::min(8, c->grid); ++q)
+        std::fprintf(stderr, " (%d %llu %.1f %llu)", idx[q], h[(size_t)c->grid * 5 + idx[q]], a[idx[q]],
+                     h[(size_t)c->grid * 4 + idx[q]]);
+    std::fprintf(stderr, "\n[mds phases] fastest:");
+    for (int q = c->grid - 1; q >= std::max(0, c->grid - 8); --q)
+        std::fprintf(stderr, " (%d %llu %.1f %llu)", idx[q], h[(size_t)c->grid * 5 + idx[q]], a[idx[q]],
+                     h[(size_t)c->grid * 4 + idx[q]]);
+    std::fprintf(stderr, "\n");
 }
 
 mds_status create_impl(int64_t n, int32_t d, int32_t precision, int32_t truncation, int32_t rank, int32_t world,

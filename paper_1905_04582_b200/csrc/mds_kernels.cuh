@@ -173,21 +173,28 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
         "r"(parity)
         : "memory");
 }
+// one try_wait probe (profiling: was the stage already complete?)
+__device__ __forceinline__ bool mbar_ready(uint64_t* b, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(ok)
+        : "r"(smem_u32(b)), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
 __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
 // per-warp staging area (dynamic shared memory).  One TMA bulk copy per unit
-// brings its 4 tile columns of y (double buffered); x of the tile's 64 columns
-// is copied once per tile (double buffered), x of the segment's 64 rows once
-// per segment (single buffer: it is moved to registers before the next copy;
-// with two units in flight the next segment's copy is issued only once the
-// current segment's first unit has read it).
+// brings its 4 tile columns of y (NSTAGE-deep ring); x of the tile's 64
+// columns is copied once per tile into xcol[t & 1].  x of the segment's 64
+// rows is read straight into registers at the segment start.
 constexpr int NSTAGE = 3;        // y stages in flight per warp (prefetch two units ahead)
 
 template <typename T, int D>
 struct WarpStage {
     uint64_t bar[NSTAGE];
     uint64_t pad_;
-    double xrow[TB * D];
     double xcol[2][TB * D];
     T y[NSTAGE][4 * TB];
     int4 seg[MAXSEG_W];
@@ -241,6 +248,7 @@ pass_kernel(PassArgs a) {
         fence_async_smem();
     }
     A lik_w = A(0);
+    unsigned not_ready = 0;                  // profiling: units whose data had not landed yet
     uint32_t phase = 0;                      // bit b: parity of stage b (persists across ranges)
     int cst = 0;                             // stage of the next unit to compute
 #pragma unroll 1
@@ -255,141 +263,115 @@ pass_kernel(PassArgs a) {
         constexpr uint32_t YB = 4 * TB * sizeof(T), XB = TB * D * sizeof(double);
         const int ub = W.seg[0].y, ue = W.seg[nsw - 1].z;
         const int m = (lane >> 3) & 3;           // this lane's column order: position p <-> column p ^ m
-        // staging copies of unit u (segment si) into y stage st; new_tile -> x of
-        // its column block into xcol[xb]; first unit of a segment -> x of its rows
-        auto issue = [&](int u, int si, int st, bool new_tile, int xb) {
-            if (lane == 0) {
-                const int4 sg = W.seg[si];
-                const int t = u / GROUPS_PER_TILE, jj0 = (u % GROUPS_PER_TILE) * 4;
-                const bool first = (u == sg.y);
-                fence_async_smem();
-                mbar_arrive_tx(&W.bar[st], YB + (new_tile ? XB : 0) + (first ? XB : 0));
-                bulk_g2s(W.y[st], Y + (size_t)t * TB * TB + (size_t)jj0 * TB, YB, &W.bar[st]);
-                if (new_tile) bulk_g2s(W.xcol[xb], X + (size_t)(t - sg.w) * TB * D, XB, &W.bar[st]);
-                if (first) bulk_g2s(W.xrow, X + (size_t)sg.x * TB * D, XB, &W.bar[st]);
+        // issue cursor: units are staged in order, two ahead of compute; tile t's
+        // column x goes to xcol[t & 1] (consecutive tiles alternate)
+        int iu = ub, isi = 0, iend = W.seg[0].z, itb = W.seg[0].w, ist = cst;
+        auto issue_one = [&]() {
+            if (iu >= iend) {
+                ++isi;
+                iend = W.seg[isi].z;
+                itb = W.seg[isi].w;
             }
-        };
-        // issue cursor (units are issued in order, up to two ahead of compute)
-        int iu = ub, isi = 0, ist = cst, ixb = 0, itile = -1;
-        auto issue_next = [&]() {
-            while (iu >= W.seg[isi].z) ++isi;
-            const int t = iu / GROUPS_PER_TILE;
-            const bool nt = t != itile;
-            if (nt && itile >= 0) ixb ^= 1;
-            itile = t;
-            issue(iu, isi, ist, nt, ixb);
+            const int t = iu >> 4, jj0 = (iu & 15) << 2;
+            const bool nt = ((iu & 15) == 0) || iu == ub;
+            if (lane == 0) {
+                fence_async_smem();
+                mbar_arrive_tx(&W.bar[ist], YB + (nt ? XB : 0));
+                bulk_g2s(W.y[ist], Y + (size_t)t * TB * TB + (size_t)jj0 * TB, YB, &W.bar[ist]);
+                if (nt) bulk_g2s(W.xcol[t & 1], X + (size_t)(t - itb) * TB * D, XB, &W.bar[ist]);
+            }
             ++iu;
             ist = (ist + 1 == NSTAGE) ? 0 : ist + 1;
         };
-        issue_next();
-        if (iu < ue && iu != W.seg[isi].z) issue_next();    // second unit in flight (not a new segment)
-        int si = 0, cxb = 0, ctile = -1;
-        T xi0[D], xi1[D];
-        A g0[D], g1[D];
-#pragma unroll
-        for (int k = 0; k < D; ++k) { xi0[k] = xi1[k] = T(0); g0[k] = g1[k] = A(0); }
+#ifndef MDS_EXP_NO_TMA
+        issue_one();
+        if (iu < ue) issue_one();
+#endif
 #pragma unroll 1
-        for (int u = ub; u < ue; ++u) {
-#ifndef MDS_EXP_NO_TMA
-            mbar_wait(&W.bar[cst], (phase >> cst) & 1);
-            phase ^= 1u << cst;
-#endif
+        for (int si = 0; si < nsw; ++si) {
             const int4 sg = W.seg[si];
-            const int t = u / GROUPS_PER_TILE, jj0 = (u % GROUPS_PER_TILE) * 4;
-            if (t != ctile) {
-                if (ctile >= 0) cxb ^= 1;
-                ctile = t;
-            }
-            if (u == sg.y) {                          // first unit of a segment: its 64 rows
+            T xi0[D], xi1[D];
+            A g0[D], g1[D];
 #pragma unroll
-                for (int k = 0; k < D; ++k) {
-                    xi0[k] = (T)W.xrow[lane * D + k];
-                    xi1[k] = (T)W.xrow[(lane + 32) * D + k];
-                }
+            for (int k = 0; k < D; ++k) {          // the segment's 64 rows (2 per lane)
+                xi0[k] = (T)X[((size_t)sg.x * TB + lane) * D + k];
+                xi1[k] = (T)X[((size_t)sg.x * TB + lane + 32) * D + k];
+                g0[k] = g1[k] = A(0);
             }
-            __syncwarp();                             // all lanes are done with the stage being refilled
+#pragma unroll 1
+            for (int u = sg.y; u < sg.z; ++u) {
 #ifndef MDS_EXP_NO_TMA
-            if (iu < ue) {
-                // keep two units in flight; a segment's first unit (row-x copy into
-                // the single xrow buffer) waits until the current segment's rows are read
-                int s2 = isi;
-                while (iu >= W.seg[s2].z) ++s2;
-                const bool first_of_seg = (iu == W.seg[s2].y);
-                if (!first_of_seg || iu == u + 1) issue_next();
-            }
+                if (a.prof && lane == 0 && !mbar_ready(&W.bar[cst], (phase >> cst) & 1)) ++not_ready;
+                mbar_wait(&W.bar[cst], (phase >> cst) & 1);
+                phase ^= 1u << cst;
+                __syncwarp();                         // all lanes are done with the stage being refilled
+                if (iu < ue) issue_one();
 #endif
-            const T* __restrict__ yst = W.y[cst];
-            const double* __restrict__ xc = W.xcol[cxb] + jj0 * D;
-            T cv[4][D];
+                const int t = u >> 4, jj0 = (u & 15) << 2;
+                const T* __restrict__ yst = W.y[cst];
+                const double* __restrict__ xc = W.xcol[t & 1] + jj0 * D;
+                T cv[4][D];
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {             // positions 2h, 2h+1: 4 pairs per lane in lock-step
-                T ys[4], ss[4], dd[4][D];
+                for (int h = 0; h < 2; ++h) {         // positions 2h, 2h+1: 4 pairs per lane in lock-step
+                    T ys[4], ss[4], dd[4][D];
 #pragma unroll
-                for (int qq = 0; qq < 2; ++qq) {
-                    const int q = (2 * h + qq) ^ m;   // column of position 2h + qq
-                    ys[2 * qq] = yst[q * TB + lane];
-                    ys[2 * qq + 1] = yst[q * TB + lane + 32];
-                    T sa = T(0), sb = T(0);
+                    for (int qq = 0; qq < 2; ++qq) {
+                        const int q = (2 * h + qq) ^ m;   // column of position 2h + qq
+                        ys[2 * qq] = yst[q * TB + lane];
+                        ys[2 * qq + 1] = yst[q * TB + lane + 32];
+                        T sa = T(0), sb = T(0);
+#pragma unroll
+                        for (int k = 0; k < D; ++k) {
+                            const T xjk = (T)xc[q * D + k];
+                            dd[2 * qq][k] = xi0[k] - xjk;
+                            dd[2 * qq + 1][k] = xi1[k] - xjk;
+                            sa = fma(dd[2 * qq][k], dd[2 * qq][k], sa);
+                            sb = fma(dd[2 * qq + 1][k], dd[2 * qq + 1][k], sb);
+                        }
+                        ss[2 * qq] = sa;
+                        ss[2 * qq + 1] = sb;
+                    }
+                    T ll[4], uu[4];
+                    Pair<T, TRUNC>::eval4(ss, ys, a.P, exptab, ll, uu);
+                    T lsum = T(0);
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        const bool mi = is_missing(ys[i]);
+                        if (!mi) lsum += ll[i];               // predicated, no select
+                        uu[i] = mi ? T(0) : uu[i];
+                    }
 #pragma unroll
                     for (int k = 0; k < D; ++k) {
-                        const T xjk = (T)xc[q * D + k];
-                        dd[2 * qq][k] = xi0[k] - xjk;
-                        dd[2 * qq + 1][k] = xi1[k] - xjk;
-                        sa = fma(dd[2 * qq][k], dd[2 * qq][k], sa);
-                        sb = fma(dd[2 * qq + 1][k], dd[2 * qq + 1][k], sb);
+                        const T va0 = uu[0] * dd[0][k], vb0 = uu[1] * dd[1][k];
+                        const T va1 = uu[2] * dd[2][k], vb1 = uu[3] * dd[3][k];
+                        g0[k] -= A(va0 + va1);
+                        g1[k] -= A(vb0 + vb1);
+                        cv[2 * h][k] = va0 + vb0;
+                        cv[2 * h + 1][k] = va1 + vb1;
                     }
-                    ss[2 * qq] = sa;
-                    ss[2 * qq + 1] = sb;
+                    lik_w += A(lsum);
                 }
-                T ll[4], uu[4];
-                Pair<T, TRUNC>::eval4(ss, ys, a.P, exptab, ll, uu);
-                T lsum = T(0);
-#pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                    const bool mi = is_missing(ys[i]);
-                    if (!mi) lsum += ll[i];               // predicated, no select
-                    uu[i] = mi ? T(0) : uu[i];
-                }
-#pragma unroll
-                for (int k = 0; k < D; ++k) {
-                    const T va0 = uu[0] * dd[0][k], vb0 = uu[1] * dd[1][k];
-                    const T va1 = uu[2] * dd[2][k], vb1 = uu[3] * dd[3][k];
-                    g0[k] -= A(va0 + va1);
-                    g1[k] -= A(vb0 + vb1);
-                    if (h == 0) {
-                        cv[0][k] = va0 + vb0;
-                        cv[1][k] = va1 + vb1;
-                    } else {
-                        cv[2][k] = va0 + vb0;
-                        cv[3][k] = va1 + vb1;
-                    }
-                }
-                lik_w += A(lsum);
-            }
-            double* __restrict__ cslab = a.slabs + ((size_t)a.nseg + t) * TB * D + (size_t)jj0 * D;
+                double* __restrict__ cslab = a.slabs + ((size_t)a.nseg + t) * TB * D + (size_t)jj0 * D;
 #ifndef MDS_EXP_NO_COLRED
 #pragma unroll
-            for (int k = 0; k < D; ++k) {
-                const T cs = reduce_scatter4_perm(cv[0][k], cv[1][k], cv[2][k], cv[3][k]);
-                if ((lane & 7) == 0) cslab[m * D + k] = A(cs);
-            }
+                for (int k = 0; k < D; ++k) {
+                    const T cs = reduce_scatter4_perm(cv[0][k], cv[1][k], cv[2][k], cv[3][k]);
+                    if ((lane & 7) == 0) cslab[m * D + k] = A(cs);
+                }
 #else
 #pragma unroll
-            for (int k = 0; k < D; ++k) lik_w += A(cv[0][k] + cv[1][k] + cv[2][k] + cv[3][k]);
-            (void)cslab;
+                for (int k = 0; k < D; ++k) lik_w += A(cv[0][k] + cv[1][k] + cv[2][k] + cv[3][k]);
+                (void)cslab;
 #endif
-            if (u + 1 == sg.z) {                      // last unit of the segment: its row partial
-                double* __restrict__ rslab = a.slabs + (size_t)(ws0 + si) * TB * D;
-#pragma unroll
-                for (int k = 0; k < D; ++k) {
-                    rslab[lane * D + k] = g0[k];
-                    rslab[(lane + 32) * D + k] = g1[k];
-                    g0[k] = A(0);
-                    g1[k] = A(0);
-                }
-                ++si;
+                cst = (cst + 1 == NSTAGE) ? 0 : cst + 1;
             }
-            cst = (cst + 1 == NSTAGE) ? 0 : cst + 1;
+            // the segment's row partial
+            double* __restrict__ rslab = a.slabs + (size_t)(ws0 + si) * TB * D;
+#pragma unroll
+            for (int k = 0; k < D; ++k) {
+                rslab[lane * D + k] = g0[k];
+                rslab[(lane + 32) * D + k] = g1[k];
+            }
         }
     }
     }   // virtual ranges
@@ -399,8 +381,14 @@ pass_kernel(PassArgs a) {
 
     // ------------------------------------------------------------ barrier
     if (a.prof) {
+        if (lane == 0) atomicAdd(&a.prof[gridDim.x * 4 + blockIdx.x], (unsigned long long)not_ready);
         __syncthreads();
-        if (threadIdx.x == 0) a.prof[blockIdx.x * 4 + 1] = gtimer();
+        if (threadIdx.x == 0) {
+            a.prof[blockIdx.x * 4 + 1] = gtimer();
+            unsigned smid;
+            asm("mov.u32 %0, %%smid;" : "=r"(smid));
+            a.prof[gridDim.x * 5 + blockIdx.x] = smid;
+        }
     }
     __threadfence();
     cg::this_grid().sync();
