@@ -38,7 +38,8 @@ namespace mdsk {
 namespace cg = cooperative_groups;
 
 constexpr int TB = 64;              // tile edge B
-constexpr int GROUPS_PER_TILE = TB / 4;
+constexpr int UCOLS = 8;                    // tile columns per unit (two 4-column reduce groups)
+constexpr int GROUPS_PER_TILE = TB / UCOLS; // units per tile
 constexpr int PT = 128;             // threads per CTA of the small helper kernels
 
 enum Mode { MODE_EVAL = 0, MODE_LEAPFROG = 2 };
@@ -189,14 +190,14 @@ __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.a
 // brings its 4 tile columns of y (NSTAGE-deep ring); x of the tile's 64
 // columns is copied once per tile into xcol[t & 1].  x of the segment's 64
 // rows is read straight into registers at the segment start.
-constexpr int NSTAGE = 3;        // y stages in flight per warp (prefetch two units ahead)
+constexpr int NSTAGE = 3;        // y stages per warp (prefetch two units ahead)
 
 template <typename T, int D>
 struct WarpStage {
     uint64_t bar[NSTAGE];
     uint64_t pad_;
     double xcol[2][TB * D];
-    T y[NSTAGE][4 * TB];
+    T y[NSTAGE][UCOLS * TB];
     int4 seg[MAXSEG_W];
 };
 
@@ -260,7 +261,7 @@ pass_kernel(PassArgs a) {
     if (lane < nsw) W.seg[lane] = a.segs[ws0 + lane];
     __syncwarp();
     if (nsw > 0) {
-        constexpr uint32_t YB = 4 * TB * sizeof(T), XB = TB * D * sizeof(double);
+        constexpr uint32_t YB = UCOLS * TB * sizeof(T), XB = TB * D * sizeof(double);
         const int ub = W.seg[0].y, ue = W.seg[nsw - 1].z;
         const int m = (lane >> 3) & 3;           // this lane's column order: position p <-> column p ^ m
         // issue cursor: units are staged in order, two ahead of compute; tile t's
@@ -272,8 +273,8 @@ pass_kernel(PassArgs a) {
                 iend = W.seg[isi].z;
                 itb = W.seg[isi].w;
             }
-            const int t = iu >> 4, jj0 = (iu & 15) << 2;
-            const bool nt = ((iu & 15) == 0) || iu == ub;
+            const int t = iu / GROUPS_PER_TILE, jj0 = (iu % GROUPS_PER_TILE) * UCOLS;
+            const bool nt = (iu % GROUPS_PER_TILE == 0) || iu == ub;
             if (lane == 0) {
                 fence_async_smem();
                 mbar_arrive_tx(&W.bar[ist], YB + (nt ? XB : 0));
@@ -307,8 +308,11 @@ pass_kernel(PassArgs a) {
                 __syncwarp();                         // all lanes are done with the stage being refilled
                 if (iu < ue) issue_one();
 #endif
-                const int t = u >> 4, jj0 = (u & 15) << 2;
-                const T* __restrict__ yst = W.y[cst];
+                const int t = u / GROUPS_PER_TILE, jb = (u % GROUPS_PER_TILE) * UCOLS;
+#pragma unroll 1
+                for (int c4 = 0; c4 < UCOLS / 4; ++c4) {  // 4-column reduce groups of the unit
+                const int jj0 = jb + 4 * c4;
+                const T* __restrict__ yst = W.y[cst] + 4 * c4 * TB;
                 const double* __restrict__ xc = W.xcol[t & 1] + jj0 * D;
                 T cv[4][D];
 #pragma unroll
@@ -363,6 +367,7 @@ pass_kernel(PassArgs a) {
                 for (int k = 0; k < D; ++k) lik_w += A(cv[0][k] + cv[1][k] + cv[2][k] + cv[3][k]);
                 (void)cslab;
 #endif
+                }   // 4-column groups
                 cst = (cst + 1 == NSTAGE) ? 0 : cst + 1;
             }
             // the segment's row partial
