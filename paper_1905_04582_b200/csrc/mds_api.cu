@@ -43,6 +43,7 @@ struct mds_ctx_s {
     size_t smem = 0;                 // its dynamic shared memory
     int nseg = 0;
     int vpw = 1;
+    int epl = 1;                     // phase B elements per lane
     int* d_warp_seg = nullptr;
     int4* d_segs = nullptr;
     int* d_blk_ptr = nullptr;
@@ -216,6 +217,7 @@ PassArgs base_args(mds_ctx c, const double* xeval) {
     a.blk_slab = c->d_blk_slab;
     a.nseg = c->nseg;
     a.vpw = c->vpw;
+    a.epl = c->epl;
     a.nb = c->nb;
     a.n = c->n;
     a.slabs = c->d_slabs;
@@ -439,6 +441,11 @@ mds_status build_schedule(mds_ctx c) {
     const std::vector<int>& slab = P.slab;
     c->nseg = (int)segs.size();
     c->vpw = P.vpw;
+    // phase B: smallest elements-per-lane that fits the jobs in one grid round
+    for (c->epl = 1; c->epl < 4; c->epl *= 2) {
+        const int64_t chunks = (TB * c->d + 32 * c->epl - 1) / (32 * c->epl);
+        if (chunks * c->nb <= G - 1) break;
+    }
 
     mds_status st;
     const size_t nslab = (size_t)(c->nseg + std::max(c->ntl, 1));

@@ -39,7 +39,8 @@ namespace cg = cooperative_groups;
 
 constexpr int TB = 64;              // tile edge B
 constexpr int UCOLS = 8;                    // tile columns per unit (two 4-column reduce groups)
-constexpr int GROUPS_PER_TILE = TB / UCOLS; // units per tile
+constexpr int UNITS_PER_TILE = TB / UCOLS;  // 8-column units per tile (one bulk copy each)
+constexpr int GROUPS_PER_TILE = TB / 4;     // 4-column groups per tile: the schedule's granule
 constexpr int PT = 128;             // threads per CTA of the small helper kernels
 
 enum Mode { MODE_EVAL = 0, MODE_LEAPFROG = 2 };
@@ -141,6 +142,7 @@ struct PassArgs {
     double* xnext;
     double eps, heps, inv_tau2;
     int vpw;                     // virtual unit ranges per warp (warp_seg has GW * vpw + 1 entries)
+    int epl;                     // phase B: slab elements per lane (1, 2 or 4)
     SigmaParams P;
     unsigned long long* prof;    // optional [G][4] globaltimer stamps (start, end A, after sync, end)
 };
@@ -214,11 +216,13 @@ template <typename T, int D> struct WarpsPerCTA {
 template <typename T, int D>
 constexpr size_t pass_smem_bytes() { return WarpsPerCTA<T, D>::value * sizeof(WarpStage<T, D>); }
 // dynamic staging + the static reduction buffers must fit the 227 KB of one CTA
-static_assert(pass_smem_bytes<double, 8>() + 2 * 8 * 256 <= 227 * 1024, "smem");
-static_assert(pass_smem_bytes<float, 8>() + 2 * 12 * 256 <= 227 * 1024, "smem");
-static_assert(pass_smem_bytes<float, 6>() + 2 * 16 * 256 <= 227 * 1024, "smem");
-static_assert(pass_smem_bytes<float, 2>() + 2 * 24 * 256 <= 227 * 1024, "smem");
-static_assert(pass_smem_bytes<double, 3>() + 2 * 12 * 256 <= 227 * 1024, "smem");
+// (phase B reuses the staging area for its 4 x warps x 32 partial sums)
+static_assert(pass_smem_bytes<double, 8>() + 512 <= 227 * 1024, "smem");
+static_assert(pass_smem_bytes<float, 8>() + 512 <= 227 * 1024, "smem");
+static_assert(pass_smem_bytes<float, 6>() + 512 <= 227 * 1024, "smem");
+static_assert(pass_smem_bytes<float, 2>() + 512 <= 227 * 1024, "smem");
+static_assert(pass_smem_bytes<double, 3>() + 512 <= 227 * 1024, "smem");
+static_assert(sizeof(WarpStage<float, 1>) >= 4 * 32 * sizeof(double), "phase B buffer");
 
 template <typename T, int D, bool TRUNC, int MODE>
 __global__ void __launch_bounds__(WarpsPerCTA<T, D>::value * 32, 1)
@@ -226,8 +230,6 @@ pass_kernel(PassArgs a) {
     using A = double;
     constexpr int WPC = WarpsPerCTA<T, D>::value;
     extern __shared__ __align__(128) unsigned char dsm[];
-    __shared__ A red[WPC][32];
-    __shared__ A red2[WPC][32];
     __shared__ double exptab[64];
     if (threadIdx.x < 64) exptab[threadIdx.x] = EXPT64_TAB[threadIdx.x];
     __syncthreads();
@@ -262,19 +264,21 @@ pass_kernel(PassArgs a) {
     __syncwarp();
     if (nsw > 0) {
         constexpr uint32_t YB = UCOLS * TB * sizeof(T), XB = TB * D * sizeof(double);
-        const int ub = W.seg[0].y, ue = W.seg[nsw - 1].z;
+        // segments are in 4-column groups (g); the warp works in 8-column units
+        // u = g / 2, whose first/last may be half inside the warp's range
+        const int ub = W.seg[0].y >> 1, ue = (W.seg[nsw - 1].z + 1) >> 1;
         const int m = (lane >> 3) & 3;           // this lane's column order: position p <-> column p ^ m
         // issue cursor: units are staged in order, two ahead of compute; tile t's
         // column x goes to xcol[t & 1] (consecutive tiles alternate)
-        int iu = ub, isi = 0, iend = W.seg[0].z, itb = W.seg[0].w, ist = cst;
+        int iu = ub, isi = 0, iend = (W.seg[0].z + 1) >> 1, itb = W.seg[0].w, ist = cst;
         auto issue_one = [&]() {
             if (iu >= iend) {
                 ++isi;
-                iend = W.seg[isi].z;
+                iend = (W.seg[isi].z + 1) >> 1;
                 itb = W.seg[isi].w;
             }
-            const int t = iu / GROUPS_PER_TILE, jj0 = (iu % GROUPS_PER_TILE) * UCOLS;
-            const bool nt = (iu % GROUPS_PER_TILE == 0) || iu == ub;
+            const int t = iu / UNITS_PER_TILE, jj0 = (iu % UNITS_PER_TILE) * UCOLS;
+            const bool nt = (iu % UNITS_PER_TILE == 0) || iu == ub;
             if (lane == 0) {
                 fence_async_smem();
                 mbar_arrive_tx(&W.bar[ist], YB + (nt ? XB : 0));
@@ -300,7 +304,9 @@ pass_kernel(PassArgs a) {
                 g0[k] = g1[k] = A(0);
             }
 #pragma unroll 1
-            for (int u = sg.y; u < sg.z; ++u) {
+            for (int u = sg.y >> 1; u < (sg.z + 1) >> 1; ++u) {
+                // the unit's 4-column groups inside this segment: [c4b, c4e)
+                const int c4b = (2 * u < sg.y) ? 1 : 0, c4e = (2 * u + 1 < sg.z) ? 2 : 1;
 #ifndef MDS_EXP_NO_TMA
                 if (a.prof && lane == 0 && !mbar_ready(&W.bar[cst], (phase >> cst) & 1)) ++not_ready;
                 mbar_wait(&W.bar[cst], (phase >> cst) & 1);
@@ -308,9 +314,9 @@ pass_kernel(PassArgs a) {
                 __syncwarp();                         // all lanes are done with the stage being refilled
                 if (iu < ue) issue_one();
 #endif
-                const int t = u / GROUPS_PER_TILE, jb = (u % GROUPS_PER_TILE) * UCOLS;
+                const int t = u / UNITS_PER_TILE, jb = (u % UNITS_PER_TILE) * UCOLS;
 #pragma unroll 1
-                for (int c4 = 0; c4 < UCOLS / 4; ++c4) {  // 4-column reduce groups of the unit
+                for (int c4 = c4b; c4 < c4e; ++c4) {       // 4-column reduce groups of the unit
                 const int jj0 = jb + 4 * c4;
                 const T* __restrict__ yst = W.y[cst] + 4 * c4 * TB;
                 const double* __restrict__ xc = W.xcol[t & 1] + jj0 * D;
@@ -400,50 +406,60 @@ pass_kernel(PassArgs a) {
     if (a.prof && threadIdx.x == 0) a.prof[blockIdx.x * 4 + 2] = gtimer();
 
     // ------------------------------------------------------------ phase B
-    // job = (row block b, chunk of 64 slab elements, 2 per lane); warp w sums
-    // slabs w, w + WPC, ... in order, 8 slab indices then 16 values in flight
-    constexpr int CH = 64;
+    // job = (row block b, chunk of 32 * epl slab elements, epl per lane; the host
+    // picks epl in {1, 2, 4} so that the jobs fit the grid in one round); warp w
+    // sums slabs w, w + WPC, ... in order with 8 slab indices in flight
+    constexpr int EPLMAX = 4;
+    // the staging area is free after the grid barrier: reuse it for the sums
+    A (*red)[WPC][32] = reinterpret_cast<A (*)[WPC][32]>(dsm);
+    const int epl = a.epl;
+    const int CH = 32 * epl;
     const int chunks = (TB * D + CH - 1) / CH;
     const int jobs = a.nb * chunks;
     for (int job = blockIdx.x; job < jobs; job += gridDim.x) {
         const int b = job / chunks, ch = job % chunks;
-        const int e0 = ch * CH + lane, e1 = e0 + 32;       // elements inside the slab (ii * D + k)
-        const bool v0 = e0 < TB * D, v1 = e1 < TB * D;
         const int q0 = a.blk_ptr[b], q1 = a.blk_ptr[b + 1];
-        A acc0 = A(0), acc1 = A(0);
+        A acc[EPLMAX];
+        int el[EPLMAX];
+#pragma unroll
+        for (int ee = 0; ee < EPLMAX; ++ee) {
+            acc[ee] = A(0);
+            el[ee] = ch * CH + ee * 32 + lane;
+        }
         int q = q0 + warp;
         for (; q + 7 * WPC < q1; q += 8 * WPC) {
             int id[8];
 #pragma unroll
             for (int r = 0; r < 8; ++r) id[r] = __ldg(a.blk_slab + q + r * WPC);
-            A x0[8], x1[8];
 #pragma unroll
-            for (int r = 0; r < 8; ++r) {
-                const double* sp = a.slabs + (size_t)id[r] * TB * D;
-                x0[r] = v0 ? sp[e0] : A(0);
-                x1[r] = v1 ? sp[e1] : A(0);
-            }
+            for (int ee = 0; ee < EPLMAX; ++ee) {
+                if (ee < epl && el[ee] < TB * D) {
+                    A x[8];
 #pragma unroll
-            for (int r = 0; r < 8; ++r) {
-                acc0 += x0[r];
-                acc1 += x1[r];
+                    for (int r = 0; r < 8; ++r) x[r] = a.slabs[(size_t)id[r] * TB * D + el[ee]];
+#pragma unroll
+                    for (int r = 0; r < 8; ++r) acc[ee] += x[r];
+                }
             }
         }
         for (; q < q1; q += WPC) {
             const double* sp = a.slabs + (size_t)__ldg(a.blk_slab + q) * TB * D;
-            if (v0) acc0 += sp[e0];
-            if (v1) acc1 += sp[e1];
-        }
-        red[warp][lane] = acc0;
-        red2[warp][lane] = acc1;
-        __syncthreads();
-        if (warp < 2) {
-            const int el = warp == 0 ? e0 : e1;
-            if (el < TB * D) {
-                A g = warp == 0 ? red[0][lane] : red2[0][lane];
 #pragma unroll
-                for (int w = 1; w < WPC; ++w) g += warp == 0 ? red[w][lane] : red2[w][lane];
-                const int64_t e = (int64_t)b * TB * D + el;
+            for (int ee = 0; ee < EPLMAX; ++ee)
+                if (ee < epl && el[ee] < TB * D) acc[ee] += sp[el[ee]];
+        }
+#pragma unroll
+        for (int ee = 0; ee < EPLMAX; ++ee)
+            if (ee < epl) red[ee][warp][lane] = acc[ee];
+        __syncthreads();
+        if (warp < epl) {
+            const int ee = warp;
+            const int e_in = ch * CH + ee * 32 + lane;
+            if (e_in < TB * D) {
+                A g = red[ee][0][lane];
+#pragma unroll
+                for (int w = 1; w < WPC; ++w) g += red[ee][w][lane];
+                const int64_t e = (int64_t)b * TB * D + e_in;
                 if (e < a.n * D) {
                     if (MODE == MODE_EVAL) {
                         a.grad[e] = g;
@@ -464,17 +480,17 @@ pass_kernel(PassArgs a) {
         }
         __syncthreads();
     }
-    // log L on the last CTA (the one with the fewest reduction jobs): fixed-order
-    // strided partial sums over the warp partials, then warps in order
+    // log L on the last CTA (job-free when jobs < grid): fixed-order strided
+    // partial sums over the warp partials, then warps in order
     if (blockIdx.x == gridDim.x - 1) {
         const int GW = gridDim.x * WPC;
         A s = A(0);
         for (int q = threadIdx.x; q < GW; q += WPC * 32) s += a.likpart[q];
-        red[warp][lane] = s;
+        red[0][warp][lane] = s;
         __syncthreads();
         if (threadIdx.x < 32) {
             A t = A(0);
-            for (int w = 0; w < WPC; ++w) t += red[w][threadIdx.x];
+            for (int w = 0; w < WPC; ++w) t += red[0][w][threadIdx.x];
 #pragma unroll
             for (int m = 16; m >= 1; m >>= 1) t += __shfl_xor_sync(0xffffffffu, t, m);
             if (threadIdx.x == 0) *a.lik = t;
