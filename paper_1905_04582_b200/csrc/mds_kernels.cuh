@@ -192,7 +192,7 @@ __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.a
 // brings its 4 tile columns of y (NSTAGE-deep ring); x of the tile's 64
 // columns is copied once per tile into xcol[t & 1].  x of the segment's 64
 // rows is read straight into registers at the segment start.
-constexpr int NSTAGE = 3;        // y stages per warp (prefetch two units ahead)
+constexpr int NSTAGE = 2;        // y stages per warp (the next 8-column unit is in flight)
 
 template <typename T, int D>
 struct WarpStage {
@@ -210,7 +210,7 @@ struct WarpStage {
 // budgets blocks in 4-warp granules: 12 warps -> 168 regs, 8 -> 255); fp64
 // needs ~150 for 4 interleaved pairs (tools/pair_probe.cu), more at larger D.
 template <typename T, int D> struct WarpsPerCTA {
-    static constexpr int value = sizeof(T) == 8 ? (D <= 3 ? 12 : 8) : (D <= 2 ? 24 : (D <= 6 ? 16 : 12));
+    static constexpr int value = sizeof(T) == 8 ? (D <= 2 ? 16 : (D <= 3 ? 12 : 8)) : (D <= 2 ? 24 : (D <= 6 ? 16 : 12));
 };
 
 template <typename T, int D>
@@ -222,6 +222,9 @@ static_assert(pass_smem_bytes<float, 8>() + 512 <= 227 * 1024, "smem");
 static_assert(pass_smem_bytes<float, 6>() + 512 <= 227 * 1024, "smem");
 static_assert(pass_smem_bytes<float, 2>() + 512 <= 227 * 1024, "smem");
 static_assert(pass_smem_bytes<double, 3>() + 512 <= 227 * 1024, "smem");
+static_assert(pass_smem_bytes<double, 2>() + 512 <= 227 * 1024, "smem");
+static_assert(pass_smem_bytes<double, 1>() + 512 <= 227 * 1024, "smem");
+static_assert(pass_smem_bytes<float, 1>() + 512 <= 227 * 1024, "smem");
 static_assert(sizeof(WarpStage<float, 1>) >= 4 * 32 * sizeof(double), "phase B buffer");
 
 template <typename T, int D, bool TRUNC, int MODE>
@@ -268,7 +271,7 @@ pass_kernel(PassArgs a) {
         // u = g / 2, whose first/last may be half inside the warp's range
         const int ub = W.seg[0].y >> 1, ue = (W.seg[nsw - 1].z + 1) >> 1;
         const int m = (lane >> 3) & 3;           // this lane's column order: position p <-> column p ^ m
-        // issue cursor: units are staged in order, two ahead of compute; tile t's
+        // issue cursor: units are staged in order, NSTAGE - 1 ahead of compute; tile t's
         // column x goes to xcol[t & 1] (consecutive tiles alternate)
         int iu = ub, isi = 0, iend = (W.seg[0].z + 1) >> 1, itb = W.seg[0].w, ist = cst;
         auto issue_one = [&]() {
@@ -290,7 +293,7 @@ pass_kernel(PassArgs a) {
         };
 #ifndef MDS_EXP_NO_TMA
         issue_one();
-        if (iu < ue) issue_one();
+        if (NSTAGE > 2 && iu < ue) issue_one();
 #endif
 #pragma unroll 1
         for (int si = 0; si < nsw; ++si) {
