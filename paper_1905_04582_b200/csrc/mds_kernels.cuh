@@ -195,11 +195,10 @@ __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.a
 constexpr int NSTAGE = 2;        // y stages per warp (the next 8-column unit is in flight)
 
 template <typename T, int D>
-struct WarpStage {
+struct alignas(16) WarpStage {
     uint64_t bar[NSTAGE];
-    uint64_t pad_;
-    double xcol[2][TB * D];
-    T y[NSTAGE][UCOLS * TB];
+    alignas(16) double xcol[2][TB * D];     // bulk-copy destinations: 16-byte aligned
+    alignas(16) T y[NSTAGE][UCOLS * TB];
     int4 seg[MAXSEG_W];
 };
 
