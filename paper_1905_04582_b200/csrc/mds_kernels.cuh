@@ -454,27 +454,24 @@ pass_kernel(PassArgs a) {
         const int nk = (q1 - q0 - warp + WPC - 1) / WPC;
         // prefetched ids (the first 32 entries of the warp), 8 values per element in flight
         if (first) {
-            for (; kk + 8 <= min(nk, 32); kk += 8) {
+            const int kmax = min(nk, 32);
+            for (; kk < kmax; kk += 8) {              // batches of 8 entries, padded with exact zeros
                 int id[8];
 #pragma unroll
-                for (int r = 0; r < 8; ++r) id[r] = __shfl_sync(0xffffffffu, pre_id, kk + r);
+                for (int r = 0; r < 8; ++r) id[r] = __shfl_sync(0xffffffffu, pre_id, (kk + r) & 31);
 #pragma unroll
                 for (int ee = 0; ee < EPLMAX; ++ee) {
                     if (ee < epl && el[ee] < TB * D) {
                         A x[8];
 #pragma unroll
-                        for (int r = 0; r < 8; ++r) x[r] = a.slabs[(size_t)id[r] * TB * D + el[ee]];
+                        for (int r = 0; r < 8; ++r)
+                            x[r] = (kk + r < kmax) ? a.slabs[(size_t)id[r] * TB * D + el[ee]] : A(0);
 #pragma unroll
                         for (int r = 0; r < 8; ++r) acc[ee] += x[r];
                     }
                 }
             }
-            for (; kk < min(nk, 32); ++kk) {
-                const int id = __shfl_sync(0xffffffffu, pre_id, kk);
-#pragma unroll
-                for (int ee = 0; ee < EPLMAX; ++ee)
-                    if (ee < epl && el[ee] < TB * D) acc[ee] += a.slabs[(size_t)id * TB * D + el[ee]];
-            }
+            kk = kmax;
         }
         // the rest (long lists, or a second job): ids from global memory
         int q = q0 + warp + kk * WPC;
