@@ -392,35 +392,6 @@ pass_kernel(PassArgs a) {
     for (int m = 16; m >= 1; m >>= 1) lik_w += __shfl_xor_sync(0xffffffffu, lik_w, m);
     if (lane == 0) a.likpart[gw] = lik_w;
 
-    // ------------------------------------------------------------ phase B prologue
-    // job = (row block b, chunk of 32 * epl slab elements, epl per lane; the host
-    // picks epl in {1, 2, 4} so that the jobs fit the grid in one round).  Warp w
-    // sums slabs w, w + WPC, ... of the block's list in order.  What does not
-    // depend on phase A is loaded before the barrier: the slab ids (lane k of
-    // warp w holds entry w + k*WPC) and, for a leapfrog, x_next, p and grad log pi.
-    constexpr int EPLMAX = 4;
-    const int epl = a.epl;
-    const int CH = 32 * epl;
-    const int chunks = (TB * D + CH - 1) / CH;
-    const int jobs = a.nb * chunks;
-    int pre_id = -1;
-    double pre_xe = 0.0, pre_p = 0.0, pre_gl = 0.0;
-    if ((int)blockIdx.x < jobs) {
-        const int b = blockIdx.x / chunks, ch = blockIdx.x % chunks;
-        const int q0 = a.blk_ptr[b], q1 = a.blk_ptr[b + 1];
-        const int qk = q0 + warp + lane * WPC;
-        if (qk < q1) pre_id = __ldg(a.blk_slab + qk);
-        if (MODE == MODE_LEAPFROG && warp < epl) {
-            const int e_in = ch * CH + warp * 32 + lane;
-            const int64_t e = (int64_t)b * TB * D + e_in;
-            if (e_in < TB * D && e < a.n * D) {
-                pre_xe = a.xeval[e];
-                pre_p = a.p[e];
-                pre_gl = a.gl[e];
-            }
-        }
-    }
-
     // ------------------------------------------------------------ barrier
     if (a.prof) {
         if (lane == 0) atomicAdd(&a.prof[gridDim.x * 4 + blockIdx.x], (unsigned long long)not_ready);
@@ -437,10 +408,17 @@ pass_kernel(PassArgs a) {
     if (a.prof && threadIdx.x == 0) a.prof[blockIdx.x * 4 + 2] = gtimer();
 
     // ------------------------------------------------------------ phase B
+    // job = (row block b, chunk of 32 * epl slab elements, epl per lane; the host
+    // picks epl in {1, 2, 4} so that the jobs fit the grid in one round); warp w
+    // sums slabs w, w + WPC, ... in order with 8 slab indices in flight
+    constexpr int EPLMAX = 4;
     // the staging area is free after the grid barrier: reuse it for the sums
     A (*red)[WPC][32] = reinterpret_cast<A (*)[WPC][32]>(dsm);
+    const int epl = a.epl;
+    const int CH = 32 * epl;
+    const int chunks = (TB * D + CH - 1) / CH;
+    const int jobs = a.nb * chunks;
     for (int job = blockIdx.x; job < jobs; job += gridDim.x) {
-        const bool first = job == (int)blockIdx.x;   // its ids / state were prefetched
         const int b = job / chunks, ch = job % chunks;
         const int q0 = a.blk_ptr[b], q1 = a.blk_ptr[b + 1];
         A acc[EPLMAX];
@@ -450,31 +428,7 @@ pass_kernel(PassArgs a) {
             acc[ee] = A(0);
             el[ee] = ch * CH + ee * 32 + lane;
         }
-        int kk = 0;                                   // entry index within this warp's list
-        const int nk = (q1 - q0 - warp + WPC - 1) / WPC;
-        // prefetched ids (the first 32 entries of the warp), 8 values per element in flight
-        if (first) {
-            const int kmax = min(nk, 32);
-            for (; kk < kmax; kk += 8) {              // batches of 8 entries, padded with exact zeros
-                int id[8];
-#pragma unroll
-                for (int r = 0; r < 8; ++r) id[r] = __shfl_sync(0xffffffffu, pre_id, (kk + r) & 31);
-#pragma unroll
-                for (int ee = 0; ee < EPLMAX; ++ee) {
-                    if (ee < epl && el[ee] < TB * D) {
-                        A x[8];
-#pragma unroll
-                        for (int r = 0; r < 8; ++r)
-                            x[r] = (kk + r < kmax) ? a.slabs[(size_t)id[r] * TB * D + el[ee]] : A(0);
-#pragma unroll
-                        for (int r = 0; r < 8; ++r) acc[ee] += x[r];
-                    }
-                }
-            }
-            kk = kmax;
-        }
-        // the rest (long lists, or a second job): ids from global memory
-        int q = q0 + warp + kk * WPC;
+        int q = q0 + warp;
         for (; q + 7 * WPC < q1; q += 8 * WPC) {
             int id[8];
 #pragma unroll
@@ -513,10 +467,8 @@ pass_kernel(PassArgs a) {
                         a.grad[e] = g;
                     } else {
                         // leapfrog: the pass ran at xnext = x + eps (p + eps/2 gl)
-                        const double xe = first ? pre_xe : a.xeval[e];
-                        const double pp = first ? pre_p : a.p[e];
-                        const double gg = first ? pre_gl : a.gl[e];
-                        const double ph = __fma_rn(a.heps, gg, pp);             // first half-kick
+                        const double xe = a.xeval[e];
+                        const double ph = __fma_rn(a.heps, a.gl[e], a.p[e]);   // first half-kick
                         const double gn = g - xe * a.inv_tau2;                  // grad log pi at xnext
                         const double pn = __fma_rn(a.heps, gn, ph);             // second half-kick
                         a.grad[e] = g;
