@@ -267,6 +267,15 @@ const char *mds_version(void);
  * if there is no device). */
 mds_status mds_device_info(int32_t *sm_count, int32_t *cc_major, int32_t *cc_minor);
 
+/* Timing utility (not part of the method): overwrite `bytes` of the device
+ * buffer `dev_buf` (caller-owned, >= 16 bytes; use more than the 126 MB L2)
+ * on the context's stream, launched with the pass kernel's grid, block size and
+ * dynamic shared memory so the SMs keep the pass kernel's L1/shared split
+ * between timed passes (a flush with another split makes the next pass
+ * reconfigure the SMs inside the timed region).  Errors: MDS_E_INVALID_ARG,
+ * MDS_E_CUDA. */
+mds_status mds_l2_flush(mds_ctx ctx, void *dev_buf, size_t bytes);
+
 /* Measure this device's FP64 (dfma) and FP32 (ffma) lane throughput with a
  * register-resident dependent-chain microbenchmark; results in lane-FMA/s.
  * Used for the ALU roofline denominator. */

@@ -128,6 +128,11 @@ class MDS:
     def set_timing(self, on: bool = True):
         _abi.mds_set_timing(self.ctx, on)
 
+    def l2_flush(self, buf):
+        """Overwrite the device tensor `buf` (> L2) with the pass kernel's launch
+        shape (timing utility, mds_l2_flush)."""
+        _abi.mds_l2_flush(self.ctx, buf.data_ptr(), buf.numel() * buf.element_size())
+
     def last_timing(self):
         return _abi.mds_last_timing(self.ctx)
 

@@ -28,7 +28,7 @@ EXPORTS = [
     "mds_observed_pairs", "mds_zero_distance_pairs", "mds_set_timing", "mds_last_timing",
     "mds_hmc_trajectory", "mds_hmc_run", "mds_leapfrog_device", "mds_get_locations", "mds_get_momentum",
     "mds_set_allgather", "mds_plan",
-    "mds_last_error", "mds_status_string", "mds_version", "mds_device_info", "mds_measure_fma_peaks",
+    "mds_last_error", "mds_status_string", "mds_version", "mds_device_info", "mds_measure_fma_peaks", "mds_l2_flush",
 ]
 
 
@@ -95,6 +95,7 @@ def _load():
         "mds_plan": [i64, i32, i32, i32, i32, P(PlanInfo), vp],
         "mds_device_info": [P(i32), P(i32), P(i32)],
         "mds_measure_fma_peaks": [P(ctypes.c_double), P(ctypes.c_double)],
+        "mds_l2_flush": [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t],
     }
     for name, args in sig.items():
         f = getattr(lib, name)
@@ -216,6 +217,10 @@ def mds_zero_distance_pairs(ctx):
 
 def mds_set_timing(ctx, enable):
     _check(lib.mds_set_timing(ctx, int(bool(enable))), ctx)
+
+
+def mds_l2_flush(ctx, dev_ptr, nbytes):
+    _check(lib.mds_l2_flush(ctx, ctypes.c_void_p(dev_ptr), ctypes.c_size_t(nbytes)), ctx)
 
 
 def mds_last_timing(ctx):

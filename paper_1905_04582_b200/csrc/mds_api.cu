@@ -999,6 +999,19 @@ mds_status mds_device_info(int32_t* sm_count, int32_t* cc_major, int32_t* cc_min
     return MDS_OK;
 }
 
+mds_status mds_l2_flush(mds_ctx c, void* dev_buf, size_t bytes) {
+    if (!c || !dev_buf || bytes < 16) return MDS_E_INVALID_ARG;
+    static bool attr_set = false;
+    if (!attr_set) {
+        if (cudaFuncSetAttribute(l2_flush_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem))
+            return fail(c, MDS_E_CUDA, "l2_flush attribute");
+        attr_set = true;
+    }
+    l2_flush_kernel<<<c->grid, 32 * c->wpc, c->smem, c->stream>>>((uint4*)dev_buf, bytes / 16, 0x3c3c3c3cu);
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? MDS_OK : fail(c, MDS_E_CUDA, cudaGetErrorString(e));
+}
+
 mds_status mds_measure_fma_peaks(double* fp64, double* fp32) {
     int dev = 0, sms = 0;
     if (cudaGetDevice(&dev) != cudaSuccess) {

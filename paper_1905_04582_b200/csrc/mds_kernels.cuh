@@ -38,8 +38,6 @@ namespace mdsk {
 namespace cg = cooperative_groups;
 
 constexpr int TB = 64;              // tile edge B
-constexpr int UCOLS = 8;                    // tile columns per unit (two 4-column reduce groups)
-constexpr int UNITS_PER_TILE = TB / UCOLS;  // 8-column units per tile (one bulk copy each)
 constexpr int GROUPS_PER_TILE = TB / 4;     // 4-column groups per tile: the schedule's granule
 constexpr int PT = 128;             // threads per CTA of the small helper kernels
 
@@ -189,27 +187,36 @@ __device__ __forceinline__ bool mbar_ready(uint64_t* b, uint32_t parity) {
 __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
 // per-warp staging area (dynamic shared memory).  One TMA bulk copy per unit
-// brings its 4 tile columns of y (NSTAGE-deep ring); x of the tile's 64
+// brings its UCOLS tile columns of y (NSTAGE-deep ring); x of the tile's 64
 // columns is copied once per tile into xcol[t & 1].  x of the segment's 64
 // rows is read straight into registers at the segment start.
-constexpr int NSTAGE = 2;        // y stages per warp (the next 8-column unit is in flight)
+constexpr int NSTAGE = 2;        // y stages per warp (the next unit is in flight)
+
+// Warps per CTA and tile columns per unit (one bulk copy each; a multiple of
+// the 4-column reduce group).  ONE CTA per SM with as many warps as the register
+// file holds: warps of one CTA progress evenly, while several CTAs per SM drift
+// apart by up to ~1.6x (issue arbitration; measured with MDS_PROFILE_PHASES),
+// which a grid barrier turns into idle time.  Warps per CTA bound the registers
+// per thread (ptxas budgets blocks in 4-warp granules: 16 warps -> 128 regs,
+// 12 -> 168, 8 -> 255); fp64 needs ~128-150 for 4 interleaved pairs
+// (tools/pair_probe.cu), more at larger D.  Wider units halve the per-unit
+// issue/wait overhead where the 2-stage ring still fits shared memory.
+template <typename T, int D> struct KernelShape {
+    // fp64: 16-column units (8 KB copies) wherever 2 stages fit: D <= 2 at 12
+    // warps (A/B on one box vs 8-column units at 16 warps: 150.0 vs 144.6 G
+    // pair-evals/s on C2), D >= 4 at 8 warps; D = 3 keeps 8-column units
+    static constexpr int wpc = sizeof(T) == 8 ? (D <= 3 ? 12 : 8) : (D <= 2 ? 24 : (D <= 6 ? 16 : 12));
+    static constexpr int ucols = (sizeof(T) == 8 && D != 3) ? 16 : 8;
+};
+template <typename T, int D> struct WarpsPerCTA { static constexpr int value = KernelShape<T, D>::wpc; };
 
 template <typename T, int D>
 struct alignas(16) WarpStage {
+    static constexpr int UC = KernelShape<T, D>::ucols;
     uint64_t bar[NSTAGE];
     alignas(16) double xcol[2][TB * D];     // bulk-copy destinations: 16-byte aligned
-    alignas(16) T y[NSTAGE][UCOLS * TB];
+    alignas(16) T y[NSTAGE][UC * TB];
     int4 seg[MAXSEG_W];
-};
-
-// ONE CTA per SM with as many warps as the register file holds: warps of one
-// CTA progress evenly, while several CTAs per SM drift apart by up to ~1.6x
-// (issue arbitration; measured with MDS_PROFILE_PHASES), which a grid barrier
-// turns into idle time.  Warps per CTA bound the registers per thread (ptxas
-// budgets blocks in 4-warp granules: 12 warps -> 168 regs, 8 -> 255); fp64
-// needs ~150 for 4 interleaved pairs (tools/pair_probe.cu), more at larger D.
-template <typename T, int D> struct WarpsPerCTA {
-    static constexpr int value = sizeof(T) == 8 ? (D <= 2 ? 16 : (D <= 3 ? 12 : 8)) : (D <= 2 ? 24 : (D <= 6 ? 16 : 12));
 };
 
 template <typename T, int D>
@@ -217,6 +224,7 @@ constexpr size_t pass_smem_bytes() { return WarpsPerCTA<T, D>::value * sizeof(Wa
 // dynamic staging + the static reduction buffers must fit the 227 KB of one CTA
 // (phase B reuses the staging area for its 4 x warps x 32 partial sums)
 static_assert(pass_smem_bytes<double, 8>() + 512 <= 227 * 1024, "smem");
+static_assert(pass_smem_bytes<double, 4>() + 512 <= 227 * 1024, "smem");
 static_assert(pass_smem_bytes<float, 8>() + 512 <= 227 * 1024, "smem");
 static_assert(pass_smem_bytes<float, 6>() + 512 <= 227 * 1024, "smem");
 static_assert(pass_smem_bytes<float, 2>() + 512 <= 227 * 1024, "smem");
@@ -231,6 +239,9 @@ __global__ void __launch_bounds__(WarpsPerCTA<T, D>::value * 32, 1)
 pass_kernel(PassArgs a) {
     using A = double;
     constexpr int WPC = WarpsPerCTA<T, D>::value;
+    constexpr int UCOLS = KernelShape<T, D>::ucols;     // tile columns per unit
+    constexpr int GPU = UCOLS / 4;                      // 4-column groups per unit
+    constexpr int UNITS_PER_TILE = TB / UCOLS;
     extern __shared__ __align__(128) unsigned char dsm[];
     __shared__ double exptab[64];
     if (threadIdx.x < 64) exptab[threadIdx.x] = EXPT64_TAB[threadIdx.x];
@@ -266,23 +277,27 @@ pass_kernel(PassArgs a) {
     __syncwarp();
     if (nsw > 0) {
         constexpr uint32_t YB = UCOLS * TB * sizeof(T), XB = TB * D * sizeof(double);
-        // segments are in 4-column groups (g); the warp works in 8-column units
-        // u = g / 2, whose first/last may be half inside the warp's range
-        const int ub = W.seg[0].y >> 1, ue = (W.seg[nsw - 1].z + 1) >> 1;
+        // segments are in 4-column groups (g); the warp works in UCOLS-column units
+        // u = g / GPU, whose first/last may be partly outside the warp's range
+        const int ub = W.seg[0].y / GPU, ue = (W.seg[nsw - 1].z + GPU - 1) / GPU;
         const int m = (lane >> 3) & 3;           // this lane's column order: position p <-> column p ^ m
         // issue cursor: units are staged in order, NSTAGE - 1 ahead of compute; tile t's
         // column x goes to xcol[t & 1] (consecutive tiles alternate)
-        int iu = ub, isi = 0, iend = (W.seg[0].z + 1) >> 1, itb = W.seg[0].w, ist = cst;
+        int iu = ub, isi = 0, iend = (W.seg[0].z + GPU - 1) / GPU, itb = W.seg[0].w, ist = cst;
         auto issue_one = [&]() {
             if (iu >= iend) {
                 ++isi;
-                iend = (W.seg[isi].z + 1) >> 1;
+                iend = (W.seg[isi].z + GPU - 1) / GPU;
                 itb = W.seg[isi].w;
             }
             const int t = iu / UNITS_PER_TILE, jj0 = (iu % UNITS_PER_TILE) * UCOLS;
             const bool nt = (iu % UNITS_PER_TILE == 0) || iu == ub;
             if (lane == 0) {
-                fence_async_smem();
+                // WAR on the stage (generic LDS reads of the unit before, async-proxy
+                // writes now) is ordered by the __syncwarp after the wait below, as in
+                // an mbarrier consumer-release / producer-acquire pipeline: no proxy
+                // fence (it compiles to MEMBAR.ALL.CTA, which waits for this lane's
+                // outstanding column-slab stores)
                 mbar_arrive_tx(&W.bar[ist], YB + (nt ? XB : 0));
                 bulk_g2s(W.y[ist], Y + (size_t)t * TB * TB + (size_t)jj0 * TB, YB, &W.bar[ist]);
                 if (nt) bulk_g2s(W.xcol[t & 1], X + (size_t)(t - itb) * TB * D, XB, &W.bar[ist]);
@@ -306,9 +321,9 @@ pass_kernel(PassArgs a) {
                 g0[k] = g1[k] = A(0);
             }
 #pragma unroll 1
-            for (int u = sg.y >> 1; u < (sg.z + 1) >> 1; ++u) {
+            for (int u = sg.y / GPU; u < (sg.z + GPU - 1) / GPU; ++u) {
                 // the unit's 4-column groups inside this segment: [c4b, c4e)
-                const int c4b = (2 * u < sg.y) ? 1 : 0, c4e = (2 * u + 1 < sg.z) ? 2 : 1;
+                const int c4b = max(sg.y - GPU * u, 0), c4e = min(sg.z - GPU * u, GPU);
 #ifndef MDS_EXP_NO_TMA
                 if (a.prof && lane == 0 && !mbar_ready(&W.bar[cst], (phase >> cst) & 1)) ++not_ready;
                 mbar_wait(&W.bar[cst], (phase >> cst) & 1);
@@ -368,7 +383,11 @@ pass_kernel(PassArgs a) {
 #pragma unroll
                 for (int k = 0; k < D; ++k) {
                     const T cs = reduce_scatter4_perm(cv[0][k], cv[1][k], cv[2][k], cv[3][k]);
+#ifndef MDS_EXP_NO_CSTORE
                     if ((lane & 7) == 0) cslab[m * D + k] = A(cs);
+#else
+                    lik_w += A(cs);
+#endif
                 }
 #else
 #pragma unroll
@@ -546,6 +565,16 @@ __global__ void fill_nan_kernel(T* p, size_t count) {
     if (sizeof(T) == 8) nanv = (T)__hiloint2double((int)CANON_NAN_HI64, 0);
     else nanv = (T)__int_as_float((int)CANON_NAN_F32);
     for (; k < count; k += stride) p[k] = nanv;
+}
+
+// L2 flush for timing loops: overwrite a buffer larger than L2 with 16-byte
+// stores.  Launched with the pass kernel's block size and dynamic shared memory
+// so the SMs keep the same L1/shared-memory split between timed passes.
+__global__ void l2_flush_kernel(uint4* p, size_t count16, unsigned v) {
+    size_t k = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const size_t stride = (size_t)gridDim.x * blockDim.x;
+    const uint4 w = make_uint4(v, v, v, v);
+    for (; k < count16; k += stride) p[k] = w;
 }
 
 // count observed (non-canonical-NaN) slots of the local tiles
