@@ -47,7 +47,7 @@ struct mds_ctx_s {
     int* d_warp_seg = nullptr;
     int4* d_segs = nullptr;
     int* d_blk_ptr = nullptr;
-    int* d_blk_slab = nullptr;
+    int* d_slab_pos = nullptr;       // storage row of each logical slab (block-contiguous)
     double* d_slabs = nullptr;       // (nseg + ntl) x B x d
     double* d_likpart = nullptr;     // [wpc * grid] (one per warp)
 
@@ -152,7 +152,7 @@ mds_status dalloc(mds_ctx c, T** p, size_t count) {
 
 void free_all(mds_ctx c) {
     void* ps[] = {c->d_tiles, c->d_row_local, c->d_warp_seg, c->d_segs, c->d_blk_ptr,
-                  c->d_blk_slab, c->d_slabs, c->d_likpart, c->d_y, c->d_x, c->d_grad, c->d_lik, c->d_stage,
+                  c->d_slab_pos, c->d_slabs, c->d_likpart, c->d_y, c->d_x, c->d_grad, c->d_lik, c->d_stage,
                   c->d_bad, c->d_count, c->d_partial, c->d_gathered, c->d_p, c->d_gl, c->d_xnext, c->d_xsave,
                   c->d_glsave, c->d_liksave, c->d_H, c->d_H0, c->d_prof};
     for (void* p : ps)
@@ -214,7 +214,7 @@ PassArgs base_args(mds_ctx c, const double* xeval) {
     a.warp_seg = c->d_warp_seg;
     a.segs = c->d_segs;
     a.blk_ptr = c->d_blk_ptr;
-    a.blk_slab = c->d_blk_slab;
+    a.slab_pos = c->d_slab_pos;
     a.nseg = c->nseg;
     a.vpw = c->vpw;
     a.epl = c->epl;
@@ -452,18 +452,22 @@ mds_status build_schedule(mds_ctx c) {
     if ((st = dalloc(c, &c->d_warp_seg, warp_seg.size()))) return st;
     if ((st = dalloc(c, &c->d_segs, std::max<size_t>(segs.size(), 1)))) return st;
     if ((st = dalloc(c, &c->d_blk_ptr, ptr.size()))) return st;
-    if ((st = dalloc(c, &c->d_blk_slab, std::max<size_t>(slab.size(), 1)))) return st;
+    // storage row of each logical slab = its position in the CSR order, so that
+    // every row block's slabs are contiguous for phase B
+    std::vector<int> pos(slab.size());
+    for (size_t q = 0; q < slab.size(); ++q) pos[slab[q]] = (int)q;
+    if ((st = dalloc(c, &c->d_slab_pos, std::max<size_t>(pos.size(), 1)))) return st;
     if ((st = dalloc(c, &c->d_slabs, nslab * TB * c->d))) return st;
     if ((st = dalloc(c, &c->d_likpart, (size_t)GW))) return st;
     CK(cudaMemcpy(c->d_warp_seg, warp_seg.data(), warp_seg.size() * sizeof(int), cudaMemcpyHostToDevice));
     if (!segs.empty()) CK(cudaMemcpy(c->d_segs, segs.data(), segs.size() * sizeof(int4), cudaMemcpyHostToDevice));
     CK(cudaMemcpy(c->d_blk_ptr, ptr.data(), ptr.size() * sizeof(int), cudaMemcpyHostToDevice));
-    if (!slab.empty()) CK(cudaMemcpy(c->d_blk_slab, slab.data(), slab.size() * sizeof(int), cudaMemcpyHostToDevice));
+    if (!pos.empty()) CK(cudaMemcpy(c->d_slab_pos, pos.data(), pos.size() * sizeof(int), cudaMemcpyHostToDevice));
     CK(cudaMemset(c->d_slabs, 0, nslab * TB * c->d * sizeof(double)));
     const char* pe = std::getenv("MDS_PROFILE_PHASES");
     if (pe && pe[0] == '1') {
-        if ((st = dalloc(c, &c->d_prof, (size_t)G * 6))) return st;
-        CK(cudaMemset(c->d_prof, 0, (size_t)G * 6 * sizeof(unsigned long long)));
+        if ((st = dalloc(c, &c->d_prof, (size_t)G * 7))) return st;
+        CK(cudaMemset(c->d_prof, 0, (size_t)G * 7 * sizeof(unsigned long long)));
     }
     return MDS_OK;
 }
@@ -471,10 +475,10 @@ mds_status build_schedule(mds_ctx c) {
 // MDS_PROFILE_PHASES=1: per-CTA phase times of the last pass, printed to stderr
 void report_phases(mds_ctx c) {
     if (!c->d_prof) return;
-    std::vector<unsigned long long> h((size_t)c->grid * 6);
+    std::vector<unsigned long long> h((size_t)c->grid * 7);
     if (cudaMemcpy(h.data(), c->d_prof, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost)) return;
     unsigned long long t0 = ~0ull, t3 = 0;
-    std::vector<double> a, w, b;
+    std::vector<double> a, w, b, s0, f0;
     for (int g = 0; g < c->grid; ++g) {
         t0 = std::min(t0, h[4 * g]);
         t3 = std::max(t3, h[4 * g + 3]);
@@ -483,6 +487,8 @@ void report_phases(mds_ctx c) {
         a.push_back((h[4 * g + 1] - t0) * 1e-3);
         w.push_back((h[4 * g + 2] - h[4 * g + 1]) * 1e-3);
         b.push_back((h[4 * g + 3] - h[4 * g + 2]) * 1e-3);
+        s0.push_back((h[4 * g] - t0) * 1e-3);
+        if (h[(size_t)c->grid * 6 + g]) f0.push_back((h[(size_t)c->grid * 6 + g] - t0) * 1e-3);
     }
     auto st = [](std::vector<double> v) {
         std::sort(v.begin(), v.end());
@@ -492,6 +498,9 @@ void report_phases(mds_ctx c) {
     };
     std::fprintf(stderr, "[mds phases us] span %.2f | A end: %s | sync wait: %s | B: %s\n", (t3 - t0) * 1e-3,
                  st(a).c_str(), st(w).c_str(), st(b).c_str());
+    if (!f0.empty())
+        std::fprintf(stderr, "[mds phases us] CTA start: %s | warp 0 first unit landed: %s\n", st(s0).c_str(),
+                     st(f0).c_str());
     // slowest CTAs: SM id, phase-A end, units whose TMA data had not landed (cumulative)
     std::vector<int> idx(c->grid);
     for (int g = 0; g < c->grid; ++g) idx[g] = g;

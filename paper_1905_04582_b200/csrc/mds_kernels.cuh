@@ -122,8 +122,9 @@ struct PassArgs {
     // schedule (per global warp gw = blockIdx.x * 4 + warp)
     const int* warp_seg;         // [GW + 1] segment range per warp
     const int4* segs;            // [S] (I, u0, u1, tbase): tile-row, unit range, local index of tile (I, 0)
-    const int* blk_ptr;          // [nb + 1] CSR of slabs per row block
-    const int* blk_slab;         // slab indices
+    const int* blk_ptr;          // [nb + 1] slabs of row block b: storage rows [blk_ptr[b], blk_ptr[b+1])
+    const int* slab_pos;         // [S + ntl] storage row of segment s's row slab (s) and of
+                                 // local tile t's column slab (S + t): block-contiguous order
     int nseg;                    // S
     int nb;
     int64_t n;
@@ -217,6 +218,7 @@ struct alignas(16) WarpStage {
     alignas(16) double xcol[2][TB * D];     // bulk-copy destinations: 16-byte aligned
     alignas(16) T y[NSTAGE][UC * TB];
     int4 seg[MAXSEG_W];
+    int spos[MAXSEG_W];                     // storage rows of the segments' row slabs
 };
 
 template <typename T, int D>
@@ -244,25 +246,27 @@ pass_kernel(PassArgs a) {
     constexpr int UNITS_PER_TILE = TB / UCOLS;
     extern __shared__ __align__(128) unsigned char dsm[];
     __shared__ double exptab[64];
-    if (threadIdx.x < 64) exptab[threadIdx.x] = EXPT64_TAB[threadIdx.x];
-    __syncthreads();
-
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int gw = blockIdx.x * WPC + warp;
     WarpStage<T, D>& W = reinterpret_cast<WarpStage<T, D>*>(dsm)[warp];
     const T* __restrict__ Y = static_cast<const T*>(a.y);
     const double* __restrict__ X = a.xeval;
-    if (a.prof && threadIdx.x == 0) a.prof[blockIdx.x * 4 + 0] = gtimer();
+    constexpr uint32_t YB = UCOLS * TB * sizeof(T), XB = TB * D * sizeof(double);
 
     // ------------------------------------------------------------ phase A (per warp)
     // a warp's contiguous unit range is processed as vpw consecutive virtual
-    // ranges of at most MAXSEG_W segments each (their segment table fits smem)
+    // ranges of at most MAXSEG_W segments each (their segment table fits smem).
+    // (Issuing the first unit's copy from the range bounds before the segment
+    // tables arrive measured 1.4% slower: A/B on one box, 146.9 vs 148.4.)
     if (lane == 0) {
 #pragma unroll
         for (int b = 0; b < NSTAGE; ++b) mbar_init(&W.bar[b], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         fence_async_smem();
     }
+    if (threadIdx.x < 64) exptab[threadIdx.x] = EXPT64_TAB[threadIdx.x];
+    __syncthreads();
+    if (a.prof && threadIdx.x == 0) a.prof[blockIdx.x * 4 + 0] = gtimer();
     A lik_w = A(0);
     unsigned not_ready = 0;                  // profiling: units whose data had not landed yet
     uint32_t phase = 0;                      // bit b: parity of stage b (persists across ranges)
@@ -273,10 +277,12 @@ pass_kernel(PassArgs a) {
     const int ws0 = a.warp_seg[vw], ws1 = a.warp_seg[vw + 1];
     const int nsw = ws1 - ws0;
     __syncwarp();
-    if (lane < nsw) W.seg[lane] = a.segs[ws0 + lane];
+    if (lane < nsw) {
+        W.seg[lane] = a.segs[ws0 + lane];
+        W.spos[lane] = __ldg(a.slab_pos + ws0 + lane);
+    }
     __syncwarp();
     if (nsw > 0) {
-        constexpr uint32_t YB = UCOLS * TB * sizeof(T), XB = TB * D * sizeof(double);
         // segments are in 4-column groups (g); the warp works in UCOLS-column units
         // u = g / GPU, whose first/last may be partly outside the warp's range
         const int ub = W.seg[0].y / GPU, ue = (W.seg[nsw - 1].z + GPU - 1) / GPU;
@@ -327,11 +333,16 @@ pass_kernel(PassArgs a) {
 #ifndef MDS_EXP_NO_TMA
                 if (a.prof && lane == 0 && !mbar_ready(&W.bar[cst], (phase >> cst) & 1)) ++not_ready;
                 mbar_wait(&W.bar[cst], (phase >> cst) & 1);
+                if (a.prof && threadIdx.x == 0 && not_ready < 0x80000000u) {   // first unit of warp 0 landed
+                    a.prof[gridDim.x * 6 + blockIdx.x] = gtimer();
+                    not_ready |= 0x80000000u;
+                }
                 phase ^= 1u << cst;
                 __syncwarp();                         // all lanes are done with the stage being refilled
                 if (iu < ue) issue_one();
 #endif
                 const int t = u / UNITS_PER_TILE, jb = (u % UNITS_PER_TILE) * UCOLS;
+                const int cpos = __ldg(a.slab_pos + a.nseg + t);    // used after the groups' math
 #pragma unroll 1
                 for (int c4 = c4b; c4 < c4e; ++c4) {       // 4-column reduce groups of the unit
                 const int jj0 = jb + 4 * c4;
@@ -378,7 +389,7 @@ pass_kernel(PassArgs a) {
                     }
                     lik_w += A(lsum);
                 }
-                double* __restrict__ cslab = a.slabs + ((size_t)a.nseg + t) * TB * D + (size_t)jj0 * D;
+                double* __restrict__ cslab = a.slabs + (size_t)cpos * TB * D + (size_t)jj0 * D;
 #ifndef MDS_EXP_NO_COLRED
 #pragma unroll
                 for (int k = 0; k < D; ++k) {
@@ -398,7 +409,7 @@ pass_kernel(PassArgs a) {
                 cst = (cst + 1 == NSTAGE) ? 0 : cst + 1;
             }
             // the segment's row partial
-            double* __restrict__ rslab = a.slabs + (size_t)(ws0 + si) * TB * D;
+            double* __restrict__ rslab = a.slabs + (size_t)W.spos[si] * TB * D;
 #pragma unroll
             for (int k = 0; k < D; ++k) {
                 rslab[lane * D + k] = g0[k];
@@ -413,7 +424,7 @@ pass_kernel(PassArgs a) {
 
     // ------------------------------------------------------------ barrier
     if (a.prof) {
-        if (lane == 0) atomicAdd(&a.prof[gridDim.x * 4 + blockIdx.x], (unsigned long long)not_ready);
+        if (lane == 0) atomicAdd(&a.prof[gridDim.x * 4 + blockIdx.x], (unsigned long long)(not_ready & 0x7fffffffu));
         __syncthreads();
         if (threadIdx.x == 0) {
             a.prof[blockIdx.x * 4 + 1] = gtimer();
@@ -422,6 +433,13 @@ pass_kernel(PassArgs a) {
             a.prof[gridDim.x * 5 + blockIdx.x] = smid;
         }
     }
+    // (Loading phase B's static inputs -- block pointers, leapfrog state -- before
+    // the barrier measured 0.4% slower: A/B on one box.)
+    constexpr int EPLMAX = 4;
+    const int epl = a.epl;
+    const int CH = 32 * epl;
+    const int chunks = (TB * D + CH - 1) / CH;
+    const int jobs = a.nb * chunks;
     __threadfence();
     cg::this_grid().sync();
     if (a.prof && threadIdx.x == 0) a.prof[blockIdx.x * 4 + 2] = gtimer();
@@ -430,16 +448,11 @@ pass_kernel(PassArgs a) {
     // job = (row block b, chunk of 32 * epl slab elements, epl per lane; the host
     // picks epl in {1, 2, 4} so that the jobs fit the grid in one round); warp w
     // sums slabs w, w + WPC, ... in order with 8 slab indices in flight
-    constexpr int EPLMAX = 4;
     // the staging area is free after the grid barrier: reuse it for the sums
     A (*red)[WPC][32] = reinterpret_cast<A (*)[WPC][32]>(dsm);
-    const int epl = a.epl;
-    const int CH = 32 * epl;
-    const int chunks = (TB * D + CH - 1) / CH;
-    const int jobs = a.nb * chunks;
     for (int job = blockIdx.x; job < jobs; job += gridDim.x) {
         const int b = job / chunks, ch = job % chunks;
-        const int q0 = a.blk_ptr[b], q1 = a.blk_ptr[b + 1];
+        const int q0 = a.blk_ptr[b], nq = a.blk_ptr[b + 1] - q0;
         A acc[EPLMAX];
         int el[EPLMAX];
 #pragma unroll
@@ -447,27 +460,32 @@ pass_kernel(PassArgs a) {
             acc[ee] = A(0);
             el[ee] = ch * CH + ee * 32 + lane;
         }
-        int q = q0 + warp;
-        for (; q + 7 * WPC < q1; q += 8 * WPC) {
-            int id[8];
-#pragma unroll
-            for (int r = 0; r < 8; ++r) id[r] = __ldg(a.blk_slab + q + r * WPC);
+        // leapfrog state of the element this warp updates below (independent of the sums)
+        double pre_xe = 0, pre_p = 0, pre_gl = 0;
+        const int e_up = ch * CH + warp * 32 + lane;
+        const int64_t e_glb = (int64_t)b * TB * D + e_up;
+        if (MODE == MODE_LEAPFROG && warp < epl && e_up < TB * D && e_glb < a.n * D) {
+            pre_xe = a.xeval[e_glb];
+            pre_p = a.p[e_glb];
+            pre_gl = a.gl[e_glb];
+        }
+        // block b's slabs are contiguous: warp w sums rows w, w + WPC, ... in order,
+        // 8 rows in flight (rows past the end add exact zeros)
+        const double* __restrict__ sb = a.slabs + (size_t)q0 * TB * D;
+        for (int k0 = warp; k0 < nq; k0 += 8 * WPC) {
 #pragma unroll
             for (int ee = 0; ee < EPLMAX; ++ee) {
                 if (ee < epl && el[ee] < TB * D) {
                     A x[8];
 #pragma unroll
-                    for (int r = 0; r < 8; ++r) x[r] = a.slabs[(size_t)id[r] * TB * D + el[ee]];
+                    for (int r = 0; r < 8; ++r) {
+                        const int k = k0 + r * WPC;
+                        x[r] = k < nq ? sb[(size_t)k * TB * D + el[ee]] : A(0);
+                    }
 #pragma unroll
                     for (int r = 0; r < 8; ++r) acc[ee] += x[r];
                 }
             }
-        }
-        for (; q < q1; q += WPC) {
-            const double* sp = a.slabs + (size_t)__ldg(a.blk_slab + q) * TB * D;
-#pragma unroll
-            for (int ee = 0; ee < EPLMAX; ++ee)
-                if (ee < epl && el[ee] < TB * D) acc[ee] += sp[el[ee]];
         }
 #pragma unroll
         for (int ee = 0; ee < EPLMAX; ++ee)
@@ -486,8 +504,8 @@ pass_kernel(PassArgs a) {
                         a.grad[e] = g;
                     } else {
                         // leapfrog: the pass ran at xnext = x + eps (p + eps/2 gl)
-                        const double xe = a.xeval[e];
-                        const double ph = __fma_rn(a.heps, a.gl[e], a.p[e]);   // first half-kick
+                        const double xe = pre_xe;
+                        const double ph = __fma_rn(a.heps, pre_gl, pre_p);    // first half-kick
                         const double gn = g - xe * a.inv_tau2;                  // grad log pi at xnext
                         const double pn = __fma_rn(a.heps, gn, ph);             // second half-kick
                         a.grad[e] = g;
