@@ -162,6 +162,61 @@ mds_status mds_set_allgather(mds_ctx ctx, mds_allgather_fn fn, void *user);
 mds_status mds_combine_partials_device(mds_ctx ctx, const double *gathered_dev, int32_t world,
                                        double *loglik_dev, double *grad_dev);
 
+/* ---- sigma side ------------------------------------ */
+
+/* log L (Eq. 2) at the context's X and Y for another sigma
+ * (> 0, finite), into *loglik (host).  The context's sigma and cached results
+ * are unchanged.  One likelihood-only pass: the per-pair Eq. 2 term without
+ * the Eq. 6 coefficient, no gradient reduction.  Synchronises.  Errors:
+ * MDS_E_INVALID_ARG, MDS_E_STATE (inputs not set), MDS_E_CUDA, MDS_E_COMM. */
+mds_status mds_log_likelihood_at_sigma(mds_ctx ctx, double sigma, double *loglik);
+
+/* Prior of the MDS error variance: sigma^-2 ~ Gamma(shape, rate). */
+typedef struct {
+    double shape;   /* s_0 > 0 */
+    double rate;    /* r_0 > 0 */
+} mds_sigma_prior;
+
+/* One Metropolis-Hastings update of sigma^2 given X (the per-iteration
+ * sigma^2 update of PAPER.md:672; under truncation its full conditional is not
+ * of standard form, so a random walk on phi = log sigma^2 replaces Gibbs):
+ *   phi' = phi + step * z,
+ *   log r = [log L(sigma') - log L(sigma)] + [lp(phi') - lp(phi)],
+ *   lp(phi) = -shape * phi - rate * e^-phi   (Gamma density of tau = e^-phi
+ *                                             times the Jacobian tau),
+ *   accept iff log(u) < log r; then sigma <- sigma' exactly as mds_set_sigma.
+ * z ~ N(0, 1) and u ~ U(0, 1] are drawn by the caller and passed in.  Both log
+ * L values come from likelihood-only passes (log L at the current sigma is
+ * reused from the previous call while neither X, Y nor sigma changed).
+ * Outputs (either may be NULL): *accepted (0/1), *log_ratio (log r).
+ * Errors: MDS_E_INVALID_ARG (shape/rate/step <= 0, non-finite z, u outside
+ * (0, 1]), MDS_E_STATE, MDS_E_CUDA, MDS_E_COMM. */
+mds_status mds_sigma_mh_step(mds_ctx ctx, const mds_sigma_prior *prior, double step, double z, double u,
+                             int32_t *accepted, double *log_ratio);
+
+/* ---- single-location updates ---------------------- */
+
+/* Change of log L when x_i alone moves to x_new_i (host, d values), with X, Y
+ * and sigma otherwise as set ("changing the value of a
+ * single x_i invalidates only N - 1 terms"):
+ *   *delta = sum_{j != i, y_ij observed} [ ell(y_ij, ||x_new_i - x_j||) - ell(y_ij, ||x_i - x_j||) ]
+ * with ell the Eq. 2 term.  O(N d), one CTA; the context is unchanged.
+ * Synchronises.  Errors: MDS_E_INVALID_ARG (i outside [0, n), non-finite
+ * x_new_i, NULL), MDS_E_STATE, MDS_E_UNSUPPORTED (sharded context), MDS_E_CUDA. */
+mds_status mds_row_loglik_delta(mds_ctx ctx, int64_t i, const double *x_new_i, double *delta);
+
+/* k sequential single-location random-walk Metropolis updates (the sampler of
+ * Bedford et al. the paper compares HMC against), all in one
+ * device launch.  Update q: i = rows[q]; x' = x_i + step * z[q*d .. q*d+d-1];
+ * log r = Delta_i(x') - (|x'|^2 - |x_i|^2) / (2 prior_sd^2) (iid N(0, prior_sd^2)
+ * prior, reading R20; prior_sd <= 0: flat); accept iff log(u[q]) < log r, then
+ * x_i <- x'.  rows (int64), z (k x d) and u (k, in (0, 1]) are host arrays of
+ * the caller's random numbers.  X moves in place; *accepted (may be NULL)
+ * counts acceptances.  Synchronises.  Errors: MDS_E_INVALID_ARG, MDS_E_STATE,
+ * MDS_E_UNSUPPORTED (sharded context), MDS_E_OOM, MDS_E_CUDA. */
+mds_status mds_rw_sweep(mds_ctx ctx, int64_t k, const int64_t *rows, const double *z, const double *u,
+                        double step, double prior_sd, int64_t *accepted);
+
 /* ---- diagnostics ------------------------------------------------------- */
 
 /* Number of observed pairs stored by this context (this rank's share). */

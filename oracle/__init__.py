@@ -61,6 +61,12 @@ def _load():
                                          d_p, d_p, d_p]
         lib.oracle_leapfrog.argtypes = [i64, i32, d_p, d_p, d_p, ctypes.c_double, i32,
                                         ctypes.c_double, ctypes.c_double, i32, d_p, d_p, d_p]
+        lib.oracle_sigma_mh_step.argtypes = [i64, i32, d_p, d_p, ctypes.c_double, i32, ctypes.c_double,
+                                             ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_double,
+                                             d_p, P(i32), d_p]
+        lib.oracle_row_delta.argtypes = [i64, i32, d_p, d_p, i64, d_p, ctypes.c_double, i32, d_p]
+        lib.oracle_rw_sweep.argtypes = [i64, i32, d_p, d_p, ctypes.c_double, i32, i64, P(i64), d_p, d_p,
+                                        ctypes.c_double, ctypes.c_double, P(i64)]
         _lib = lib
     return _lib
 
@@ -156,3 +162,51 @@ def leapfrog(y_packed: np.ndarray, x0: np.ndarray, p0: np.ndarray, sigma: float,
     if rc:
         raise ValueError("invalid oracle arguments")
     return dict(x=x, p=p, H0=H0.value, H1=H1.value, loglik=ll.value)
+
+
+def sigma_mh_step(y_packed: np.ndarray, x: np.ndarray, sigma: float, shape: float, rate: float, step: float,
+                  z: float, u: float, truncation: int = 1):
+    """One MH step on log sigma^2 (prior sigma^-2 ~ Gamma(shape, rate)).
+    Returns dict(sigma, accepted, log_ratio)."""
+    lib = _load()
+    x = _f64(x)
+    n, d = x.shape
+    so = ctypes.c_double()
+    acc = ctypes.c_int32()
+    lr = ctypes.c_double()
+    rc = lib.oracle_sigma_mh_step(n, d, _dp(_f64(y_packed)), _dp(x), float(sigma), int(truncation), float(shape),
+                                  float(rate), float(step), float(z), float(u), ctypes.byref(so),
+                                  ctypes.byref(acc), ctypes.byref(lr))
+    if rc:
+        raise ValueError("invalid oracle arguments")
+    return dict(sigma=so.value, accepted=bool(acc.value), log_ratio=lr.value)
+
+
+def row_delta(y_packed: np.ndarray, x: np.ndarray, i: int, x_new, sigma: float, truncation: int = 1) -> float:
+    """Change of log L when x_i alone moves to x_new."""
+    lib = _load()
+    x = _f64(x)
+    n, d = x.shape
+    xn = _f64(x_new).reshape(d)
+    out = ctypes.c_double()
+    if lib.oracle_row_delta(n, d, _dp(_f64(y_packed)), _dp(x), int(i), _dp(xn), float(sigma), int(truncation),
+                            ctypes.byref(out)):
+        raise ValueError("invalid oracle arguments")
+    return out.value
+
+
+def rw_sweep(y_packed: np.ndarray, x0: np.ndarray, sigma: float, rows, z, u, step: float, prior_sd: float = 0.0,
+             truncation: int = 1):
+    """Sequential single-location random-walk Metropolis updates.  Returns (x, accepted)."""
+    lib = _load()
+    x = _f64(x0).copy()
+    n, d = x.shape
+    rows = np.ascontiguousarray(rows, dtype=np.int64)
+    z = _f64(z).reshape(rows.size, d)
+    u = _f64(u).reshape(rows.size)
+    acc = ctypes.c_int64()
+    if lib.oracle_rw_sweep(n, d, _dp(_f64(y_packed)), _dp(x), float(sigma), int(truncation), rows.size,
+                           rows.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), _dp(z), _dp(u), float(step),
+                           float(prior_sd), ctypes.byref(acc)):
+        raise ValueError("invalid oracle arguments")
+    return x, acc.value

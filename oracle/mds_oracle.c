@@ -20,6 +20,12 @@
  *   PAPER.md:821-826 (App. B)           truncation flag T: T = 0 drops the log Phi term and its
  *                                       derivative (reading R12).
  *   PAPER.md:321-336 (Sec. 2.3, Eq. 5)  leapfrog integrator for HMC (readings R19, R20).
+ *   PAPER.md:258-263                    single-location updates: "changing the value of a single
+ *                                       x_i invalidates only N - 1 terms" (row delta, random-walk
+ *                                       Metropolis sweep of Bedford et al.; reading R28).
+ *   PAPER.md:205-210, 672               sigma^-2 ~ Gamma(s_0, r_0) and the per-iteration
+ *                                       sigma^2 update: Metropolis-Hastings random walk on
+ *                                       log sigma^2 (reading R27).
  *
  * Numerics: double precision only, libm erfc/log1p/exp/sqrt, i-major order
  * (i ascending, j ascending < i), Neumaier-compensated sums for log L and the
@@ -229,5 +235,104 @@ int oracle_leapfrog(int64_t n, int32_t d, const double *y_packed, double *x, dou
     if (H1) *H1 = -(ll + prior_logpdf(m, x, prior_sd)) + kinetic(m, p);
     if (loglik_end) *loglik_end = ll;
     free(g);
+    return 0;
+}
+
+/* ---- sigma^2 update (PAPER.md:205-210 prior, PAPER.md:672 update; R27) ---- */
+/* One Metropolis-Hastings step on phi = log sigma^2 at fixed X:
+ *   phi' = phi + step * z;  sigma' = exp(phi'/2)
+ *   log r = log L(sigma') - log L(sigma) + log pi(phi') - log pi(phi)
+ * where tau = 1/sigma^2 = exp(-phi) ~ Gamma(shape, rate) (density
+ * rate^shape tau^(shape-1) e^(-rate tau) / Gamma(shape)), so the density of
+ * phi is that times |d tau/d phi| = tau:  log pi(phi) = shape log tau - rate tau + const.
+ * Accept iff log(u) < log r.  z and u are the caller's random numbers. */
+int oracle_sigma_mh_step(int64_t n, int32_t d, const double *y_packed, const double *x,
+                         double sigma, int32_t truncation, double shape, double rate,
+                         double step, double z, double u,
+                         double *sigma_out, int32_t *accepted, double *log_ratio)
+{
+    if (!(shape > 0.0) || !(rate > 0.0) || !(step > 0.0) || !(u > 0.0) || !(u <= 1.0)) return -1;
+    double phi0 = log(sigma * sigma);
+    double phi1 = phi0 + step * z;
+    double sigma1 = exp(phi1 / 2.0);
+    double ll0, ll1;
+    if (oracle_loglik_grad(n, d, y_packed, x, sigma, truncation, &ll0, NULL, NULL, NULL, NULL)) return -1;
+    if (oracle_loglik_grad(n, d, y_packed, x, sigma1, truncation, &ll1, NULL, NULL, NULL, NULL)) return -1;
+    double tau0 = exp(-phi0), tau1 = exp(-phi1);
+    double lp0 = shape * log(tau0) - rate * tau0;
+    double lp1 = shape * log(tau1) - rate * tau1;
+    double lr = (ll1 - ll0) + (lp1 - lp0);
+    int ok = isfinite(lr) && log(u) < lr;
+    if (sigma_out) *sigma_out = ok ? sigma1 : sigma;
+    if (accepted) *accepted = ok;
+    if (log_ratio) *log_ratio = lr;
+    return 0;
+}
+
+/* ---- single-location updates (R28) --------------------- */
+/* y_ij for i != j from the packed strict lower triangle (y_ij = y_ji). */
+static double y_of(const double *y_packed, int64_t i, int64_t j)
+{
+    if (i < j) { int64_t t = i; i = j; j = t; }
+    return y_packed[(i * (i - 1)) / 2 + j];
+}
+
+/* Delta = sum_{j != i observed} [ ell(y_ij, ||x_new - x_j||) - ell(y_ij, ||x_i - x_j||) ]
+ * (Eq. 2 terms), in j order with a compensated sum. */
+int oracle_row_delta(int64_t n, int32_t d, const double *y_packed, const double *x, int64_t i,
+                     const double *x_new, double sigma, int32_t truncation, double *delta)
+{
+    if (n < 2 || d < 1 || i < 0 || i >= n || !(sigma > 0.0)) return -1;
+    acc_t a = {0.0, 0.0};
+    for (int64_t j = 0; j < n; ++j) {
+        if (j == i) continue;
+        double y = y_of(y_packed, i, j);
+        if (isnan(y)) continue;
+        double sn = 0.0, so = 0.0;
+        for (int k = 0; k < d; ++k) {
+            double dn = x_new[k] - x[j * d + k], dl = x[i * d + k] - x[j * d + k];
+            sn += dn * dn;
+            so += dl * dl;
+        }
+        double en, eo;
+        oracle_pair_term(y, sqrt(sn), sigma, truncation, &en, NULL);
+        oracle_pair_term(y, sqrt(so), sigma, truncation, &eo, NULL);
+        acc_add(&a, en);
+        acc_add(&a, -eo);
+    }
+    *delta = acc_val(&a);
+    return 0;
+}
+
+/* k sequential random-walk Metropolis updates: i = rows[q],
+ * x' = x_i + step z[q], log r = Delta_i(x') + log prior(x') - log prior(x_i)
+ * (iid N(0, prior_sd^2), none if prior_sd <= 0), accept iff log(u[q]) < log r.
+ * x (n*d) is updated in place; *accepted counts. */
+int oracle_rw_sweep(int64_t n, int32_t d, const double *y_packed, double *x, double sigma, int32_t truncation,
+                    int64_t k, const int64_t *rows, const double *z, const double *u, double step,
+                    double prior_sd, int64_t *accepted)
+{
+    if (n < 2 || d < 1 || k < 0 || !(step > 0.0)) return -1;
+    double *xn = (double *)malloc((size_t)d * sizeof(double));
+    if (!xn) return -1;
+    int64_t na = 0;
+    for (int64_t q = 0; q < k; ++q) {
+        int64_t i = rows[q];
+        if (i < 0 || i >= n) { free(xn); return -1; }
+        for (int c = 0; c < d; ++c) xn[c] = x[i * d + c] + step * z[q * d + c];
+        double dl;
+        oracle_row_delta(n, d, y_packed, x, i, xn, sigma, truncation, &dl);
+        double lp = 0.0;
+        if (prior_sd > 0.0)
+            for (int c = 0; c < d; ++c)
+                lp += -(xn[c] * xn[c]) / (2.0 * prior_sd * prior_sd) + (x[i * d + c] * x[i * d + c]) / (2.0 * prior_sd * prior_sd);
+        double lr = dl + lp;
+        if (isfinite(lr) && log(u[q]) < lr) {
+            for (int c = 0; c < d; ++c) x[i * d + c] = xn[c];
+            ++na;
+        }
+    }
+    if (accepted) *accepted = na;
+    free(xn);
     return 0;
 }

@@ -173,6 +173,27 @@ class MDS:
         cfg = HmcConfig(0, int(n_steps), float(step_size), float(prior_sd), 0)
         _abi.mds_leapfrog_device(self.ctx, cfg, p0_dev)
 
+    # sigma side
+    def log_likelihood_at_sigma(self, sigma: float) -> float:
+        return _abi.mds_log_likelihood_at_sigma(self.ctx, sigma)
+
+    def sigma_mh_step(self, shape: float, rate: float, step: float, z: float, u: float):
+        """One MH update of sigma^2 (random walk on log sigma^2, caller-drawn z, u).
+        Returns (accepted, log_ratio); the context's sigma moves on acceptance."""
+        return _abi.mds_sigma_mh_step(self.ctx, shape, rate, step, z, u)
+
+    # single-location updates (SURVEY 8(f) NEXT-4)
+    def row_loglik_delta(self, i: int, x_new_i) -> float:
+        return _abi.mds_row_loglik_delta(self.ctx, i, np.ascontiguousarray(x_new_i, dtype=np.float64))
+
+    def rw_sweep(self, rows, z, u, step: float, prior_sd: float = 0.0) -> int:
+        """Sequential random-walk Metropolis updates of single locations (caller-drawn
+        rows, z, u); X moves in place.  Returns the number accepted."""
+        rows = np.ascontiguousarray(rows, dtype=np.int64)
+        z = np.ascontiguousarray(z, dtype=np.float64).reshape(rows.size, self.d)
+        u = np.ascontiguousarray(u, dtype=np.float64).reshape(rows.size)
+        return _abi.mds_rw_sweep(self.ctx, rows, z, u, step, prior_sd)
+
     # HMC
     def hmc_trajectory(self, p0: np.ndarray, step_size: float, n_leapfrog: int, prior_sd: float = 0.0):
         cfg = HmcConfig(0, int(n_leapfrog), float(step_size), float(prior_sd), 0)

@@ -28,6 +28,7 @@ EXPORTS = [
     "mds_observed_pairs", "mds_zero_distance_pairs", "mds_set_timing", "mds_last_timing",
     "mds_hmc_trajectory", "mds_hmc_run", "mds_leapfrog_device", "mds_get_locations", "mds_get_momentum",
     "mds_set_allgather", "mds_plan",
+    "mds_log_likelihood_at_sigma", "mds_sigma_mh_step", "mds_row_loglik_delta", "mds_rw_sweep",
     "mds_last_error", "mds_status_string", "mds_version", "mds_device_info", "mds_measure_fma_peaks", "mds_l2_flush",
 ]
 
@@ -52,6 +53,10 @@ class HmcConfig(ctypes.Structure):
 class HmcStats(ctypes.Structure):
     _fields_ = [("accepted", ctypes.c_int64), ("grad_evals", ctypes.c_int64), ("mean_abs_dH", ctypes.c_double),
                 ("seconds", ctypes.c_double), ("final_loglik", ctypes.c_double)]
+
+
+class SigmaPrior(ctypes.Structure):
+    _fields_ = [("shape", ctypes.c_double), ("rate", ctypes.c_double)]
 
 
 # int (*)(void* user, const double* send_dev, double* recv_dev, int64_t count, void* stream)
@@ -96,6 +101,11 @@ def _load():
         "mds_device_info": [P(i32), P(i32), P(i32)],
         "mds_measure_fma_peaks": [P(ctypes.c_double), P(ctypes.c_double)],
         "mds_l2_flush": [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t],
+        "mds_log_likelihood_at_sigma": [vp, ctypes.c_double, P(ctypes.c_double)],
+        "mds_row_loglik_delta": [vp, i64, dp, P(ctypes.c_double)],
+        "mds_rw_sweep": [vp, i64, dp, dp, dp, ctypes.c_double, ctypes.c_double, P(i64)],
+        "mds_sigma_mh_step": [vp, P(SigmaPrior), ctypes.c_double, ctypes.c_double, ctypes.c_double, P(i32),
+                              P(ctypes.c_double)],
     }
     for name, args in sig.items():
         f = getattr(lib, name)
@@ -265,6 +275,35 @@ def mds_plan(n, rank, world, ctas, warps_per_cta, owned_rows=None):
     _check(lib.mds_plan(int(n), int(rank), int(world), int(ctas), int(warps_per_cta), ctypes.byref(info),
                         _ptr(owned_rows)))
     return {f: getattr(info, f) for f, _ in PlanInfo._fields_}
+
+
+def mds_log_likelihood_at_sigma(ctx, sigma):
+    v = ctypes.c_double()
+    _check(lib.mds_log_likelihood_at_sigma(ctx, float(sigma), ctypes.byref(v)), ctx)
+    return v.value
+
+
+def mds_sigma_mh_step(ctx, shape, rate, step, z, u):
+    """Returns (accepted: bool, log_ratio: float)."""
+    pr = SigmaPrior(float(shape), float(rate))
+    acc, lr = ctypes.c_int32(), ctypes.c_double()
+    _check(lib.mds_sigma_mh_step(ctx, ctypes.byref(pr), float(step), float(z), float(u), ctypes.byref(acc),
+                                 ctypes.byref(lr)), ctx)
+    return bool(acc.value), lr.value
+
+
+def mds_row_loglik_delta(ctx, i, x_new_i):
+    v = ctypes.c_double()
+    _check(lib.mds_row_loglik_delta(ctx, int(i), _ptr(x_new_i), ctypes.byref(v)), ctx)
+    return v.value
+
+
+def mds_rw_sweep(ctx, rows, z, u, step, prior_sd):
+    """rows: int64 (k,), z: float64 (k, d), u: float64 (k,).  Returns the acceptance count."""
+    acc = ctypes.c_int64()
+    _check(lib.mds_rw_sweep(ctx, int(rows.size), _ptr(rows), _ptr(z), _ptr(u), float(step), float(prior_sd),
+                            ctypes.byref(acc)), ctx)
+    return acc.value
 
 
 def mds_last_error(ctx):

@@ -14,6 +14,7 @@
 
 #include "../../include/mds.h"
 #include "mds_kernels.cuh"
+#include "mds_row.cuh"
 
 using namespace mdsk;
 
@@ -87,11 +88,16 @@ struct mds_ctx_s {
     int64_t rows_needed = 0;
     int64_t n_obs = -1;              // -1 = recount needed
     uint64_t version = 1, eval_version = 0;
+    uint64_t mh_version = 0;         // version mh_ll (log L from a MODE_LIK pass) belongs to
+    double mh_ll = 0.0;
 
     cudaStream_t stream = nullptr;
     bool timing = false;
     std::vector<cudaEvent_t> evpool;  // timing mode: 3 events per recorded pass
     size_t ev_used = 0;               // events recorded since the last mds_last_timing
+
+    void* d_rwbuf = nullptr;         // single-location sweeps: rows, z, u, outputs
+    size_t rwbuf_bytes = 0;
 
     unsigned long long* d_prof = nullptr;   // MDS_PROFILE_PHASES=1: globaltimer stamps [grid][4]
 
@@ -154,7 +160,7 @@ void free_all(mds_ctx c) {
     void* ps[] = {c->d_tiles, c->d_row_local, c->d_warp_seg, c->d_segs, c->d_blk_ptr,
                   c->d_slab_pos, c->d_slabs, c->d_likpart, c->d_y, c->d_x, c->d_grad, c->d_lik, c->d_stage,
                   c->d_bad, c->d_count, c->d_partial, c->d_gathered, c->d_p, c->d_gl, c->d_xnext, c->d_xsave,
-                  c->d_glsave, c->d_liksave, c->d_H, c->d_H0, c->d_prof};
+                  c->d_glsave, c->d_liksave, c->d_H, c->d_H0, c->d_prof, c->d_rwbuf};
     for (void* p : ps)
         if (p) cudaFree(p);
     for (auto& e : c->evpool)
@@ -164,37 +170,16 @@ void free_all(mds_ctx c) {
 inline int64_t packed_off(int64_t i) { return i * (i - 1) / 2; }
 
 // ---------------------------------------------------------------- dispatch
-typedef void (*PassFn)(PassArgs);
-
-struct PassKernel {
-    PassFn fn;
-    size_t smem;
-    int wpc;   // warps per CTA
-};
-
-template <typename T, bool TR, int MODE, int D>
-PassKernel pk() {
-    return PassKernel{pass_kernel<T, D, TR, MODE>, pass_smem_bytes<T, D>(), WarpsPerCTA<T, D>::value};
-}
-
-template <typename T, bool TR, int MODE>
-PassKernel pass_fn_d(int d) {
-    switch (d) {
-        case 1: return pk<T, TR, MODE, 1>();
-        case 2: return pk<T, TR, MODE, 2>();
-        case 3: return pk<T, TR, MODE, 3>();
-        case 4: return pk<T, TR, MODE, 4>();
-        case 5: return pk<T, TR, MODE, 5>();
-        case 6: return pk<T, TR, MODE, 6>();
-        case 7: return pk<T, TR, MODE, 7>();
-        default: return pk<T, TR, MODE, 8>();
+// pass kernel for (MODE, precision, truncation, D); instantiated in pass_m*_*.cu
+PassKernel pass_fn_mode(int mode, int prec, int trunc, int d) {
+    const bool f = prec == MDS_F64;
+    switch (mode) {
+        case MODE_EVAL: return f ? pass_m0_f64(trunc, d) : pass_m0_f32(trunc, d);
+        case MODE_EVAL_NOLIK: return f ? pass_m1_f64(trunc, d) : pass_m1_f32(trunc, d);
+        case MODE_LEAPFROG: return f ? pass_m2_f64(trunc, d) : pass_m2_f32(trunc, d);
+        case MODE_LEAPFROG_NOLIK: return f ? pass_m3_f64(trunc, d) : pass_m3_f32(trunc, d);
+        default: return f ? pass_m4_f64(trunc, d) : pass_m4_f32(trunc, d);
     }
-}
-
-template <int MODE>
-PassKernel pass_fn(int prec, int trunc, int d) {
-    if (prec == MDS_F64) return trunc ? pass_fn_d<double, true, MODE>(d) : pass_fn_d<double, false, MODE>(d);
-    return trunc ? pass_fn_d<float, true, MODE>(d) : pass_fn_d<float, false, MODE>(d);
 }
 
 // timing mode: the next event of the pool (grown on demand)
@@ -244,11 +229,12 @@ mds_status launch_coop(mds_ctx c, PassKernel k, PassArgs& a, cudaStream_t s) {
 
 // A fused pass at xeval.  EVAL: (grad_out, lik_out) <- full result.  With a
 // leapfrog state (lf = true): the pass runs at xnext and applies the leapfrog
-// update (x, p, gl, xnext, grad, lik).  Sharded contexts go through the local
-// partial, the exchange callback and the rank-ordered combine.  In timing mode
-// three events bracket the pass kernel and the post-kernel work.
+// update (x, p, gl, xnext, grad, lik).  want_lik = false skips log L (the
+// gradient-only variant; *lik_out is then NaN).  Sharded contexts go through
+// the local partial, the exchange callback and the rank-ordered combine.  In
+// timing mode three events bracket the pass kernel and the post-kernel work.
 mds_status run_pass(mds_ctx c, const double* xeval, double* grad_out, double* lik_out, bool lf, double eps,
-                    double inv_tau2, cudaStream_t s, bool timed) {
+                    double inv_tau2, cudaStream_t s, bool timed, bool want_lik = true) {
     timed = timed && c->timing;
     const int64_t nd = c->n * c->d;
     PassArgs a = base_args(c, xeval);
@@ -264,15 +250,16 @@ mds_status run_pass(mds_ctx c, const double* xeval, double* grad_out, double* li
     if (c->world == 1) {
         a.grad = grad_out;
         a.lik = lik_out;
-        st = lf ? launch_coop(c, pass_fn<MODE_LEAPFROG>(c->prec, c->trunc, c->d), a, s)
-                : launch_coop(c, pass_fn<MODE_EVAL>(c->prec, c->trunc, c->d), a, s);
+        const int mode = lf ? (want_lik ? MODE_LEAPFROG : MODE_LEAPFROG_NOLIK)
+                            : (want_lik ? MODE_EVAL : MODE_EVAL_NOLIK);
+        st = launch_coop(c, pass_fn_mode(mode, c->prec, c->trunc, c->d), a, s);
         if (st) return st;
         if (timed) CK(cudaEventRecord(next_event(c), s));
     } else {
         if (!c->ag_fn) return fail(c, MDS_E_STATE, "sharded context: register the exchange with mds_set_allgather");
         a.grad = c->d_partial;
         a.lik = c->d_partial + nd;
-        st = launch_coop(c, pass_fn<MODE_EVAL>(c->prec, c->trunc, c->d), a, s);
+        st = launch_coop(c, pass_fn_mode(want_lik ? MODE_EVAL : MODE_EVAL_NOLIK, c->prec, c->trunc, c->d), a, s);
         if (st) return st;
         if (timed) CK(cudaEventRecord(next_event(c), s));
         if (c->ag_fn(c->ag_user, c->d_partial, c->d_gathered, nd + 1, (void*)s) != 0)
@@ -286,6 +273,54 @@ mds_status run_pass(mds_ctx c, const double* xeval, double* grad_out, double* li
     if (timed) CK(cudaEventRecord(next_event(c), s));
     CK(cudaGetLastError());
     return MDS_OK;
+}
+
+SigmaParams sigma_params(double sigma);
+
+// log L only (MODE_LIK) at the context's X for the SigmaParams given, into the
+// device double lik_out; sharded: local partial -> exchange -> rank-ordered sum
+mds_status run_lik_pass(mds_ctx c, const SigmaParams& P, double* lik_out, cudaStream_t s) {
+    PassArgs a = base_args(c, c->d_x);
+    a.P = P;
+    const PassKernel k = pass_fn_mode(MODE_LIK, c->prec, c->trunc, c->d);
+    if (c->world == 1) {
+        a.lik = lik_out;
+        return launch_coop(c, k, a, s);
+    }
+    if (!c->ag_fn) return fail(c, MDS_E_STATE, "sharded context: register the exchange with mds_set_allgather");
+    double* part = c->d_partial + c->n * c->d;
+    a.lik = part;
+    mds_status st = launch_coop(c, k, a, s);
+    if (st) return st;
+    if (c->ag_fn(c->ag_user, part, c->d_gathered, 1, (void*)s) != 0)
+        return fail(c, MDS_E_COMM, "all-gather callback failed");
+    combine_kernel<<<1, 32, 0, s>>>(c->d_gathered, c->world, 1, nullptr, lik_out);
+    CK(cudaGetLastError());
+    return MDS_OK;
+}
+
+mds_status rw_scratch(mds_ctx c, size_t bytes) {
+    if (c->rwbuf_bytes >= bytes) return MDS_OK;
+    if (c->d_rwbuf) cudaFree(c->d_rwbuf);
+    c->d_rwbuf = nullptr;
+    c->rwbuf_bytes = 0;
+    cudaError_t e = cudaMalloc(&c->d_rwbuf, bytes);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return fail(c, MDS_E_OOM, "cudaMalloc of sweep scratch failed");
+    }
+    c->rwbuf_bytes = bytes;
+    return MDS_OK;
+}
+
+RowArgs row_args(mds_ctx c) {
+    RowArgs a{};
+    a.y = c->d_y;
+    a.row_local = c->d_row_local;
+    a.x = c->d_x;
+    a.n = c->n;
+    a.P = c->P;
+    return a;
 }
 
 mds_status ready(mds_ctx c) {
@@ -416,7 +451,8 @@ mds_status build_schedule(mds_ctx c) {
     int dev = 0, sms = 0, occ = 1 << 30;
     CK(cudaGetDevice(&dev));
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    PassKernel ks[2] = {pass_fn<MODE_EVAL>(c->prec, c->trunc, c->d), pass_fn<MODE_LEAPFROG>(c->prec, c->trunc, c->d)};
+    PassKernel ks[5];
+    for (int m = 0; m < 5; ++m) ks[m] = pass_fn_mode(m, c->prec, c->trunc, c->d);
     for (PassKernel k : ks) {
         CK(cudaFuncSetAttribute(k.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k.smem));
         int o = 0;
@@ -772,9 +808,146 @@ mds_status mds_set_locations_device(mds_ctx c, const double* x_dev) {
 mds_status mds_set_sigma(mds_ctx c, double sigma) {
     GUARD(c);
     if (!(sigma > 0.0) || !std::isfinite(sigma)) return fail(c, MDS_E_INVALID_ARG, "sigma must be > 0 and finite");
-    const double pi = 3.14159265358979323846;
     c->sigma = sigma;
-    SigmaParams& P = c->P;
+    c->P = sigma_params(sigma);
+    c->sigma_set = true;
+    ++c->version;
+    return MDS_OK;
+}
+
+mds_status mds_log_likelihood_at_sigma(mds_ctx c, double sigma, double* loglik) {
+    GUARD(c);
+    if (!loglik) return fail(c, MDS_E_INVALID_ARG, "NULL output");
+    if (!(sigma > 0.0) || !std::isfinite(sigma)) return fail(c, MDS_E_INVALID_ARG, "sigma must be > 0 and finite");
+    mds_status st = ready(c);
+    if (st) return st;
+    st = run_lik_pass(c, sigma_params(sigma), c->d_lik + 2, c->stream);
+    if (st) return st;
+    CK(cudaMemcpyAsync(loglik, c->d_lik + 2, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    return MDS_OK;
+}
+
+mds_status mds_row_loglik_delta(mds_ctx c, int64_t i, const double* x_new_i, double* delta) {
+    GUARD(c);
+    if (!x_new_i || !delta) return fail(c, MDS_E_INVALID_ARG, "NULL argument");
+    if (i < 0 || i >= c->n) return fail(c, MDS_E_INVALID_ARG, "row index out of range");
+    for (int k = 0; k < c->d; ++k)
+        if (!std::isfinite(x_new_i[k])) return fail(c, MDS_E_INVALID_ARG, "non-finite location");
+    if (c->world != 1) return fail(c, MDS_E_UNSUPPORTED, "single-location updates need an unsharded context");
+    mds_status st = ready(c);
+    if (st) return st;
+    if ((st = rw_scratch(c, 2 * sizeof(double) * 8))) return st;
+    double* dx = static_cast<double*>(c->d_rwbuf);
+    CK(cudaMemcpyAsync(dx, x_new_i, c->d * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    RowArgs a = row_args(c);
+    a.i0 = i;
+    a.xnew = dx;
+    a.delta = dx + 8;
+    a.K = 0;
+    row_fn(c->prec == MDS_F64, c->trunc, c->d)<<<1, ROW_THREADS, 0, c->stream>>>(a);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(delta, dx + 8, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    return MDS_OK;
+}
+
+mds_status mds_rw_sweep(mds_ctx c, int64_t k, const int64_t* rows, const double* z, const double* u, double step,
+                        double prior_sd, int64_t* accepted) {
+    GUARD(c);
+    if (k < 0 || (k > 0 && (!rows || !z || !u))) return fail(c, MDS_E_INVALID_ARG, "bad sweep arrays");
+    if (!(step > 0.0) || !std::isfinite(step) || !std::isfinite(prior_sd))
+        return fail(c, MDS_E_INVALID_ARG, "need step > 0 and finite prior_sd");
+    for (int64_t q = 0; q < k; ++q) {
+        if (rows[q] < 0 || rows[q] >= c->n) return fail(c, MDS_E_INVALID_ARG, "row index out of range");
+        if (!(u[q] > 0.0) || !(u[q] <= 1.0)) return fail(c, MDS_E_INVALID_ARG, "u must lie in (0, 1]");
+        for (int j = 0; j < c->d; ++j)
+            if (!std::isfinite(z[q * c->d + j])) return fail(c, MDS_E_INVALID_ARG, "non-finite z");
+    }
+    if (c->world != 1) return fail(c, MDS_E_UNSUPPORTED, "single-location updates need an unsharded context");
+    mds_status st = ready(c);
+    if (st) return st;
+    if (k == 0) {
+        if (accepted) *accepted = 0;
+        return MDS_OK;
+    }
+    const size_t zb = (size_t)k * c->d * sizeof(double), rb = (size_t)k * sizeof(int64_t), ub = (size_t)k * 8;
+    if ((st = rw_scratch(c, 64 + rb + zb + ub))) return st;
+    char* base = static_cast<char*>(c->d_rwbuf);
+    unsigned long long* dacc = reinterpret_cast<unsigned long long*>(base);
+    int64_t* drows = reinterpret_cast<int64_t*>(base + 64);
+    double* dz = reinterpret_cast<double*>(base + 64 + rb);
+    double* du = reinterpret_cast<double*>(base + 64 + rb + zb);
+    CK(cudaMemcpyAsync(drows, rows, rb, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(dz, z, zb, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(du, u, ub, cudaMemcpyHostToDevice, c->stream));
+    RowArgs a = row_args(c);
+    a.K = k;
+    a.rows = drows;
+    a.z = dz;
+    a.u = du;
+    a.step = step;
+    a.inv_tau2 = prior_sd > 0.0 ? 1.0 / (prior_sd * prior_sd) : 0.0;
+    a.accepted = dacc;
+    row_fn(c->prec == MDS_F64, c->trunc, c->d)<<<1, ROW_THREADS, 0, c->stream>>>(a);
+    CK(cudaGetLastError());
+    unsigned long long na = 0;
+    CK(cudaMemcpyAsync(&na, dacc, sizeof(na), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    if (accepted) *accepted = (int64_t)na;
+    ++c->version;      // X moved (possibly)
+    return MDS_OK;
+}
+
+mds_status mds_sigma_mh_step(mds_ctx c, const mds_sigma_prior* prior, double step, double z, double u,
+                             int32_t* accepted, double* log_ratio) {
+    GUARD(c);
+    if (!prior || !(prior->shape > 0.0) || !(prior->rate > 0.0) || !std::isfinite(prior->shape) ||
+        !std::isfinite(prior->rate))
+        return fail(c, MDS_E_INVALID_ARG, "sigma prior needs shape > 0 and rate > 0");
+    if (!(step > 0.0) || !std::isfinite(step) || !std::isfinite(z) || !(u > 0.0) || !(u <= 1.0))
+        return fail(c, MDS_E_INVALID_ARG, "need step > 0, finite z and u in (0, 1]");
+    mds_status st = ready(c);
+    if (st) return st;
+    const double phi0 = 2.0 * std::log(c->sigma);          // phi = log sigma^2
+    const double phi1 = phi0 + step * z;
+    const double sigma1 = std::exp(0.5 * phi1);
+    if (!(sigma1 > 0.0) || !std::isfinite(sigma1)) return fail(c, MDS_E_INVALID_ARG, "proposal sigma out of range");
+    // log L at the current sigma: cached from the previous step when nothing changed
+    if (c->mh_version != c->version) {
+        st = run_lik_pass(c, c->P, c->d_lik + 2, c->stream);
+        if (st) return st;
+    }
+    st = run_lik_pass(c, sigma_params(sigma1), c->d_lik + 3, c->stream);
+    if (st) return st;
+    double ll[2] = {c->mh_ll, 0.0};
+    if (c->mh_version != c->version)
+        CK(cudaMemcpyAsync(&ll[0], c->d_lik + 2, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(&ll[1], c->d_lik + 3, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    // log prior of phi: tau = 1/sigma^2 = e^-phi ~ Gamma(shape, rate), Jacobian |dtau/dphi| = tau
+    auto lp = [&](double phi) { return -prior->shape * phi - prior->rate * std::exp(-phi); };
+    const double lr = (ll[1] - ll[0]) + (lp(phi1) - lp(phi0));
+    const bool ok = std::isfinite(lr) && std::log(u) < lr;
+    if (log_ratio) *log_ratio = lr;
+    if (accepted) *accepted = ok ? 1 : 0;
+    if (ok) {
+        st = mds_set_sigma(c, sigma1);
+        if (st) return st;
+        c->mh_ll = ll[1];
+    } else {
+        c->mh_ll = ll[0];
+    }
+    c->mh_version = c->version;
+    return MDS_OK;
+}
+
+}  // extern "C"
+
+namespace {
+SigmaParams sigma_params(double sigma) {
+    const double pi = 3.14159265358979323846;
+    SigmaParams P{};
     P.inv_sigma = 1.0 / sigma;
     P.inv_sigma2 = 1.0 / (sigma * sigma);
     P.half_inv_sigma2 = 0.5 / (sigma * sigma);
@@ -787,10 +960,11 @@ mds_status mds_set_sigma(mds_ctx c, double sigma) {
     P.half_inv_sigma2_f = (float)P.half_inv_sigma2;
     P.k0_f = (float)P.k0;
     P.cg_f = (float)P.cg;
-    c->sigma_set = true;
-    ++c->version;
-    return MDS_OK;
+    return P;
 }
+}  // namespace
+
+extern "C" {
 
 mds_status mds_log_likelihood_and_gradient(mds_ctx c, double* loglik, double* grad) {
     GUARD(c);
@@ -831,7 +1005,7 @@ mds_status mds_evaluate_partial_device(mds_ctx c, double* part_dev) {
     PassArgs a = base_args(c, c->d_x);
     a.grad = part_dev;
     a.lik = part_dev + c->n * c->d;
-    return launch_coop(c, pass_fn<MODE_EVAL>(c->prec, c->trunc, c->d), a, c->stream);
+    return launch_coop(c, pass_fn_mode(MODE_EVAL, c->prec, c->trunc, c->d), a, c->stream);
 }
 
 mds_status mds_set_allgather(mds_ctx c, mds_allgather_fn fn, void* user) {

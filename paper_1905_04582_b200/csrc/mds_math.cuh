@@ -142,9 +142,14 @@ __device__ __forceinline__ bool is_missing(float y) {
 // NP independent pairs in lock-step: every step is issued for all NP pairs
 // before the next, so the FP64 dependency chains (Horner steps, Newton steps)
 // of different pairs interleave in the instruction stream and hide the DFMA
-// latency (a single pair is one long dependent chain).  Same arithmetic as
-// pair_f64, operation for operation.
-template <bool TRUNC, int NP>
+// latency (a single pair is one long dependent chain).
+// WL: form ell (the Eq. 2 term); WG: form u (the Eq. 6 coefficient / d).  The
+// pass variants that need only one of them (gradient-only leapfrog steps,
+// likelihood-only sigma sweeps) drop the other's work:
+//   WL && WG : one reciprocal of Phi (2 - Q) gives 1/Phi and 1/(2 - Q)
+//   WG only  : 1/Phi alone (no atanh series)
+//   WL only  : 1/(2 - Q) alone (no phi/Phi)
+template <bool TRUNC, int NP, bool WL = true, bool WG = true>
 __device__ __forceinline__ void pair_f64_n(const double (&s)[NP], const double (&y)[NP], const SigmaParams& P,
                                            const double* __restrict__ exptab, double (&ell)[NP], double (&u)[NP]) {
     double rs[NP], d[NP], res[NP], l[NP];
@@ -162,7 +167,7 @@ __device__ __forceinline__ void pair_f64_n(const double (&s)[NP], const double (
     for (int i = 0; i < NP; ++i) {
         d[i] = s[i] * rs[i];
         res[i] = y[i] - d[i];
-        l[i] = fma(-(res[i] * P.half_inv_sigma2), res[i], P.k0);
+        if (WL) l[i] = fma(-(res[i] * P.half_inv_sigma2), res[i], P.k0);
     }
     if (TRUNC) {
         // E = exp(-a), a = t^2/2 = s/(2 sigma^2): k = rint(-64 a / ln2), E = 2^(k>>6) 2^((k&63)/64) p(r),
@@ -212,7 +217,7 @@ __device__ __forceinline__ void pair_f64_n(const double (&s)[NP], const double (
             Q[i] = E[i] * q[i];
             Phi[i] = 1.0 - Q[i];
             opp[i] = 2.0 - Q[i];
-            prod[i] = Phi[i] * opp[i];
+            prod[i] = (WL && WG) ? Phi[i] * opp[i] : (WG ? Phi[i] : opp[i]);
             z0[i] = rcp_seed(prod[i]);
         }
         double sa[NP], zz[NP], G[NP];
@@ -221,36 +226,43 @@ __device__ __forceinline__ void pair_f64_n(const double (&s)[NP], const double (
             const double f1 = fma(-prod[i], z0[i], 1.0);
             const double f2 = fma(f1, f1, f1);
             const double rp = fma(f2, z0[i], z0[i]);
-            const double invPhi = opp[i] * rp;
-            const double invOpp = Phi[i] * rp;
-            G[i] = (E[i] * P.cg) * invPhi;
-            sa[i] = Q[i] * invOpp;
-            zz[i] = sa[i] * sa[i];
+            if (WG) {
+                const double invPhi = WL ? opp[i] * rp : rp;
+                G[i] = (E[i] * P.cg) * invPhi;
+            }
+            if (WL) {
+                const double invOpp = WG ? Phi[i] * rp : rp;
+                sa[i] = Q[i] * invOpp;
+                zz[i] = sa[i] * sa[i];
+            }
         }
-        double at[NP];
+        if (WL) {
+            double at[NP];
 #pragma unroll
-        for (int i = 0; i < NP; ++i) at[i] = ATANH64_C[ATANH64_DEG];
+            for (int i = 0; i < NP; ++i) at[i] = ATANH64_C[ATANH64_DEG];
 #pragma unroll
-        for (int j = ATANH64_DEG - 1; j >= 0; --j)
+            for (int j = ATANH64_DEG - 1; j >= 0; --j)
 #pragma unroll
-            for (int i = 0; i < NP; ++i) at[i] = fma(at[i], zz[i], ATANH64_C[j]);
+                for (int i = 0; i < NP; ++i) at[i] = fma(at[i], zz[i], ATANH64_C[j]);
 #pragma unroll
-        for (int i = 0; i < NP; ++i) {
-            ell[i] = fma(sa[i], at[i], l[i]);
-            u[i] = fma(-res[i], P.inv_sigma2, G[i]) * rs[i];
+            for (int i = 0; i < NP; ++i) ell[i] = fma(sa[i], at[i], l[i]);
+        }
+        if (WG) {
+#pragma unroll
+            for (int i = 0; i < NP; ++i) u[i] = fma(-res[i], P.inv_sigma2, G[i]) * rs[i];
         }
     } else {
 #pragma unroll
         for (int i = 0; i < NP; ++i) {
-            ell[i] = l[i];
-            u[i] = (-res[i] * P.inv_sigma2) * rs[i];
+            if (WL) ell[i] = l[i];
+            if (WG) u[i] = (-res[i] * P.inv_sigma2) * rs[i];
         }
     }
 }
 
 // ---------------------------------------------------------------- fp32 pair
 // fp32 storage and per-pair math (reading R15); MUFU rsqrt/ex2/rcp/lg2.
-template <bool TRUNC>
+template <bool TRUNC, bool WL = true, bool WG = true>
 __device__ __forceinline__ void pair_f32(float s, float y, const SigmaParams& P,
                                          float& ell, float& u) {
     const float sc = fmaxf(s, 1e-30f);
@@ -269,12 +281,12 @@ __device__ __forceinline__ void pair_f32(float s, float y, const SigmaParams& P,
         const float Phi = 1.0f - Q;
         const float invPhi = rcp_f(Phi);
         const float G = (E * P.cg_f) * invPhi;
-        l = fmaf(-0.693147181f, lg2_f(Phi), l);      // - log Phi
-        u = fmaf(-res, P.inv_sigma2_f, G) * rs;
+        if (WL) l = fmaf(-0.693147181f, lg2_f(Phi), l);      // - log Phi
+        if (WG) u = fmaf(-res, P.inv_sigma2_f, G) * rs;
     } else {
-        u = (-res * P.inv_sigma2_f) * rs;
+        if (WG) u = (-res * P.inv_sigma2_f) * rs;
     }
-    ell = l;
+    if (WL) ell = l;
 }
 
 }  // namespace mdsk

@@ -1,0 +1,589 @@
+// mds_pass.cuh -- the sm_100a pass kernel of the fused MDS likelihood+gradient pass.
+// (Instantiated per mode and precision in pass_m<MODE>_<prec>.cu; the helper
+// kernels live in mds_kernels.cuh.)
+//
+// Data layout in HBM:
+//   Y   : the strict lower triangle cut into B x B tiles (I, J), I >= J, B = 64.
+//         Only this rank's tile-rows are stored, tile-major in (I, J) order;
+//         inside a tile the layout is column-major, y(ii, jj) at [jj*B + ii], so
+//         the 32 lanes of a warp (consecutive rows) read one 256 B line per column.
+//         Slots that are not an observed pair (missing y, i <= j in diagonal
+//         tiles, padding rows/columns >= n) hold the canonical NaN, so the pair
+//         loop has no bounds or i > j test.
+//   X   : fp64 master, n_pad x D row-major, padding rows zero (plus p, grad log pi
+//         and the drifted X of the next leapfrog step, same layout).
+//   slab: B x D fp64 partial sums. Slabs [0, S) are row-segment partials, slabs
+//         [S, S + ntl) the column partials of each local tile.
+//
+// ONE persistent cooperative kernel per pass:
+//   phase A  grid = resident CTAs; CTA c owns the column-group units
+//            [c U/G, (c+1) U/G) of the tile list (U = 16 column-groups x tiles),
+//            cut into tile-row segments.  Warp w of the CTA takes units w, w+4, ..
+//            of a segment; lane l evaluates rows l and l+32 against the 4 columns
+//            of a unit: 8 pairs, Eq. 2 term and Eq. 6 coefficient each.  Row sums
+//            stay in registers for the whole segment (Alg. 2's per-row reduction,
+//            PAPER.md:786-805); the column side (each unordered pair is computed
+//            once, so it is new) is summed over the 64 rows by a 2-row add + a
+//            4-column reduce-scatter and stored once per column; log L partials
+//            per CTA (Alg. 1's binary tree).  No atomics.
+//   barrier  cooperative grid sync.
+//   phase B  fixed-order reduction: g_i = sum of the row-segment slabs and column
+//            slabs touching row block i/B (CSR built on the host), then either
+//            the result (EVAL), the sharded partial (PARTIAL), or the leapfrog
+//            update (LEAPFROG: second half-kick, next drift).  CTA 0 sums log L.
+#pragma once
+#include <cooperative_groups.h>
+#include <cstdint>
+#include "mds_math.cuh"
+
+namespace mdsk {
+namespace cg = cooperative_groups;
+
+constexpr int TB = 64;              // tile edge B
+constexpr int GROUPS_PER_TILE = TB / 4;     // 4-column groups per tile: the schedule's granule
+constexpr int PT = 128;             // threads per CTA of the small helper kernels
+
+// What one pass computes (template parameter MODE of pass_kernel):
+//   EVAL            log L and gradient (Eq. 2 + Eq. 6)
+//   EVAL_NOLIK      gradient only (sharded leapfrog steps that need no log L)
+//   LEAPFROG        log L, gradient and the leapfrog update (Eq. 5)
+//   LEAPFROG_NOLIK  gradient + leapfrog update: steps 1..L-1 of a trajectory,
+//                   whose log L nobody reads
+//   LIK             log L only, at the SigmaParams passed (sigma-side sweep for
+//                   the MH update of sigma^2; no gradient, no slabs)
+enum Mode { MODE_EVAL = 0, MODE_EVAL_NOLIK = 1, MODE_LEAPFROG = 2, MODE_LEAPFROG_NOLIK = 3, MODE_LIK = 4 };
+template <int MODE> struct ModeTraits {
+    static constexpr bool LF = MODE == MODE_LEAPFROG || MODE == MODE_LEAPFROG_NOLIK;   // leapfrog update
+    static constexpr bool WL = !(MODE == MODE_EVAL_NOLIK || MODE == MODE_LEAPFROG_NOLIK);  // log L wanted
+    static constexpr bool WG = MODE != MODE_LIK;                                        // gradient wanted
+};
+
+template <typename T, bool TRUNC> struct Pair;
+template <bool TRUNC> struct Pair<double, TRUNC> {
+    template <bool WL, bool WG>
+    __device__ __forceinline__ static void eval4(const double (&s)[4], const double (&y)[4], const SigmaParams& P,
+                                                 const double* exptab, double (&l)[4], double (&u)[4]) {
+        pair_f64_n<TRUNC, 4, WL, WG>(s, y, P, exptab, l, u);
+    }
+};
+template <bool TRUNC> struct Pair<float, TRUNC> {
+    template <bool WL, bool WG>
+    __device__ __forceinline__ static void eval4(const float (&s)[4], const float (&y)[4], const SigmaParams& P,
+                                                 const double*, float (&l)[4], float (&u)[4]) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) pair_f32<TRUNC, WL, WG>(s[i], y[i], P, l[i], u[i]);
+    }
+};
+
+template <typename T>
+__device__ __forceinline__ T shfl_xor(T v, int m) { return __shfl_xor_sync(0xffffffffu, v, m); }
+
+// Sum of 4 per-lane values a0..a3 over the 32 lanes; lane L ends with the total
+// of column c = (L >> 3) & 3 (all 8 lanes of that group hold it).  Fixed order.
+template <typename T>
+__device__ __forceinline__ T reduce_scatter4(T a0, T a1, T a2, T a3, int lane) {
+    const bool b4 = lane & 16, b3 = lane & 8;
+    T k0 = b4 ? a2 : a0, k1 = b4 ? a3 : a1;
+    T s0 = b4 ? a0 : a2, s1 = b4 ? a1 : a3;
+    k0 += shfl_xor(s0, 16);
+    k1 += shfl_xor(s1, 16);
+    T k = b3 ? k1 : k0;
+    T sd = b3 ? k0 : k1;
+    k += shfl_xor(sd, 8);
+    k += shfl_xor(k, 4);
+    k += shfl_xor(k, 2);
+    k += shfl_xor(k, 1);
+    return k;
+}
+
+// Sum over the 32 lanes of 4 per-lane column values stored in the per-lane
+// order v[p] = column p ^ m, m = (L >> 3) & 3 (see the unit loop): every
+// exchange then sends a fixed register, so no selects are needed.  Lane L ends
+// with the total of column m (all 8 lanes with the same m hold it).  Fixed order.
+template <typename T>
+__device__ __forceinline__ T reduce_scatter4_perm(T v0, T v1, T v2, T v3) {
+    T k0 = v0 + shfl_xor(v2, 16);     // partner L^16 holds my columns 0,1 at its positions 2,3
+    T k1 = v1 + shfl_xor(v3, 16);
+    T k = k0 + shfl_xor(k1, 8);       // partner L^8 holds my column 0 at its position 1
+    k += shfl_xor(k, 4);
+    k += shfl_xor(k, 2);
+    k += shfl_xor(k, 1);
+    return k;
+}
+
+// Sum of 2 per-lane values over the 32 lanes; lane L ends with the total of
+// column (L >> 4) & 1.  Fixed order.
+template <typename T>
+__device__ __forceinline__ T reduce_scatter2(T a0, T a1, int lane) {
+    const bool b4 = lane & 16;
+    T k = b4 ? a1 : a0;
+    const T sd = b4 ? a0 : a1;
+    k += shfl_xor(sd, 16);
+    k += shfl_xor(k, 8);
+    k += shfl_xor(k, 4);
+    k += shfl_xor(k, 2);
+    k += shfl_xor(k, 1);
+    return k;
+}
+
+// leapfrog drift of one coordinate: x + eps (p + eps/2 gl); the same expression
+// (and rounding) wherever it is evaluated
+__device__ __forceinline__ double drift(double x, double p, double gl, double eps, double heps) {
+    return __fma_rn(eps, __fma_rn(heps, gl, p), x);
+}
+
+struct PassArgs {
+    // inputs
+    const void* y;               // local tiles [ntl][B][B]
+    const double* xeval;         // positions the pass evaluates at (n_pad x D)
+    // schedule (per global warp gw = blockIdx.x * 4 + warp)
+    const int* warp_seg;         // [GW + 1] segment range per warp
+    const int4* segs;            // [S] (I, u0, u1, tbase): tile-row, unit range, local index of tile (I, 0)
+    const int* blk_ptr;          // [nb + 1] slabs of row block b: storage rows [blk_ptr[b], blk_ptr[b+1])
+    const int* slab_pos;         // [S + ntl] storage row of segment s's row slab (s) and of
+                                 // local tile t's column slab (S + t): block-contiguous order
+    int nseg;                    // S
+    int nb;
+    int64_t n;
+    // scratch
+    double* slabs;               // (S + ntl) x B x D
+    double* likpart;             // [GW]
+    // outputs
+    double* grad;                // EVAL: d log L / dX (n x D)      (sharded: this rank's partial)
+    double* lik;                 // log L                           (sharded: partial)
+    // leapfrog state (MODE_LEAPFROG): x <- xeval, p, gl updated, xnext written
+    double* x;
+    double* p;
+    double* gl;
+    double* xnext;
+    double eps, heps, inv_tau2;
+    int vpw;                     // virtual unit ranges per warp (warp_seg has GW * vpw + 1 entries)
+    int epl;                     // phase B: slab elements per lane (1, 2 or 4)
+    SigmaParams P;
+    unsigned long long* prof;    // optional [G][4] globaltimer stamps (start, end A, after sync, end)
+};
+
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
+constexpr int MAXSEG_W = 32;    // segments per warp (host checks)
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t cnt) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(cnt) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t* b, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+// TMA bulk copy global -> shared (SASS UBLKCP), completion counted on the mbarrier
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* b) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(b))
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+    asm volatile(
+        "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}" ::"r"(
+            smem_u32(b)),
+        "r"(parity)
+        : "memory");
+}
+// one try_wait probe (profiling: was the stage already complete?)
+__device__ __forceinline__ bool mbar_ready(uint64_t* b, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(ok)
+        : "r"(smem_u32(b)), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+// per-warp staging area (dynamic shared memory).  One TMA bulk copy per unit
+// brings its UCOLS tile columns of y (NSTAGE-deep ring); x of the tile's 64
+// columns is copied once per tile into xcol[t & 1].  x of the segment's 64
+// rows is read straight into registers at the segment start.
+constexpr int NSTAGE = 2;        // y stages per warp (the next unit is in flight)
+
+// Warps per CTA and tile columns per unit (one bulk copy each; a multiple of
+// the 4-column reduce group).  ONE CTA per SM with as many warps as the register
+// file holds: warps of one CTA progress evenly, while several CTAs per SM drift
+// apart by up to ~1.6x (issue arbitration; measured with MDS_PROFILE_PHASES),
+// which a grid barrier turns into idle time.  Warps per CTA bound the registers
+// per thread (ptxas budgets blocks in 4-warp granules: 16 warps -> 128 regs,
+// 12 -> 168, 8 -> 255); fp64 needs ~128-150 for 4 interleaved pairs
+// (tools/pair_probe.cu), more at larger D.  Wider units halve the per-unit
+// issue/wait overhead where the 2-stage ring still fits shared memory.
+template <typename T, int D> struct KernelShape {
+    // fp64: 16-column units (8 KB copies) wherever 2 stages fit: D <= 2 at 12
+    // warps (A/B on one box vs 8-column units at 16 warps: 150.0 vs 144.6 G
+    // pair-evals/s on C2), D >= 4 at 8 warps; D = 3 keeps 8-column units
+    static constexpr int wpc = sizeof(T) == 8 ? (D <= 3 ? 12 : 8) : (D <= 2 ? 24 : (D <= 6 ? 16 : 12));
+    static constexpr int ucols = (sizeof(T) == 8 && D != 3) ? 16 : 8;
+};
+template <typename T, int D> struct WarpsPerCTA { static constexpr int value = KernelShape<T, D>::wpc; };
+
+template <typename T, int D>
+struct alignas(16) WarpStage {
+    static constexpr int UC = KernelShape<T, D>::ucols;
+    uint64_t bar[NSTAGE];
+    alignas(16) double xcol[2][TB * D];     // bulk-copy destinations: 16-byte aligned
+    alignas(16) T y[NSTAGE][UC * TB];
+    int4 seg[MAXSEG_W];
+    int spos[MAXSEG_W];                     // storage rows of the segments' row slabs
+};
+
+template <typename T, int D>
+constexpr size_t pass_smem_bytes() { return WarpsPerCTA<T, D>::value * sizeof(WarpStage<T, D>); }
+// dynamic staging + the static reduction buffers must fit the 227 KB of one CTA
+// (phase B reuses the staging area for its 4 x warps x 32 partial sums)
+static_assert(pass_smem_bytes<double, 8>() + 512 <= 227 * 1024, "smem");
+static_assert(pass_smem_bytes<double, 4>() + 512 <= 227 * 1024, "smem");
+static_assert(pass_smem_bytes<float, 8>() + 512 <= 227 * 1024, "smem");
+static_assert(pass_smem_bytes<float, 6>() + 512 <= 227 * 1024, "smem");
+static_assert(pass_smem_bytes<float, 2>() + 512 <= 227 * 1024, "smem");
+static_assert(pass_smem_bytes<double, 3>() + 512 <= 227 * 1024, "smem");
+static_assert(pass_smem_bytes<double, 2>() + 512 <= 227 * 1024, "smem");
+static_assert(pass_smem_bytes<double, 1>() + 512 <= 227 * 1024, "smem");
+static_assert(pass_smem_bytes<float, 1>() + 512 <= 227 * 1024, "smem");
+static_assert(sizeof(WarpStage<float, 1>) >= 4 * 32 * sizeof(double), "phase B buffer");
+
+template <typename T, int D, bool TRUNC, int MODE>
+__global__ void __launch_bounds__(WarpsPerCTA<T, D>::value * 32, 1)
+pass_kernel(PassArgs a) {
+    using A = double;
+    constexpr bool LF = ModeTraits<MODE>::LF, WL = ModeTraits<MODE>::WL, WG = ModeTraits<MODE>::WG;
+    constexpr int WPC = WarpsPerCTA<T, D>::value;
+    constexpr int UCOLS = KernelShape<T, D>::ucols;     // tile columns per unit
+    constexpr int GPU = UCOLS / 4;                      // 4-column groups per unit
+    constexpr int UNITS_PER_TILE = TB / UCOLS;
+    extern __shared__ __align__(128) unsigned char dsm[];
+    __shared__ double exptab[64];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int gw = blockIdx.x * WPC + warp;
+    WarpStage<T, D>& W = reinterpret_cast<WarpStage<T, D>*>(dsm)[warp];
+    const T* __restrict__ Y = static_cast<const T*>(a.y);
+    const double* __restrict__ X = a.xeval;
+    constexpr uint32_t YB = UCOLS * TB * sizeof(T), XB = TB * D * sizeof(double);
+
+    // ------------------------------------------------------------ phase A (per warp)
+    // a warp's contiguous unit range is processed as vpw consecutive virtual
+    // ranges of at most MAXSEG_W segments each (their segment table fits smem).
+    // (Issuing the first unit's copy from the range bounds before the segment
+    // tables arrive measured 1.4% slower: A/B on one box, 146.9 vs 148.4.)
+    if (lane == 0) {
+#pragma unroll
+        for (int b = 0; b < NSTAGE; ++b) mbar_init(&W.bar[b], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        fence_async_smem();
+    }
+    if (threadIdx.x < 64) exptab[threadIdx.x] = EXPT64_TAB[threadIdx.x];
+    __syncthreads();
+    if (a.prof && threadIdx.x == 0) a.prof[blockIdx.x * 4 + 0] = gtimer();
+    A lik_w = A(0);
+    unsigned not_ready = 0;                  // profiling: units whose data had not landed yet
+    uint32_t phase = 0;                      // bit b: parity of stage b (persists across ranges)
+    int cst = 0;                             // stage of the next unit to compute
+#pragma unroll 1
+    for (int vv = 0; vv < a.vpw; ++vv) {
+    const int vw = gw * a.vpw + vv;
+    const int ws0 = a.warp_seg[vw], ws1 = a.warp_seg[vw + 1];
+    const int nsw = ws1 - ws0;
+    __syncwarp();
+    if (lane < nsw) {
+        W.seg[lane] = a.segs[ws0 + lane];
+        W.spos[lane] = __ldg(a.slab_pos + ws0 + lane);
+    }
+    __syncwarp();
+    if (nsw > 0) {
+        // segments are in 4-column groups (g); the warp works in UCOLS-column units
+        // u = g / GPU, whose first/last may be partly outside the warp's range
+        const int ub = W.seg[0].y / GPU, ue = (W.seg[nsw - 1].z + GPU - 1) / GPU;
+        const int m = (lane >> 3) & 3;           // this lane's column order: position p <-> column p ^ m
+        // issue cursor: units are staged in order, NSTAGE - 1 ahead of compute; tile t's
+        // column x goes to xcol[t & 1] (consecutive tiles alternate)
+        int iu = ub, isi = 0, iend = (W.seg[0].z + GPU - 1) / GPU, itb = W.seg[0].w, ist = cst;
+        auto issue_one = [&]() {
+            if (iu >= iend) {
+                ++isi;
+                iend = (W.seg[isi].z + GPU - 1) / GPU;
+                itb = W.seg[isi].w;
+            }
+            const int t = iu / UNITS_PER_TILE, jj0 = (iu % UNITS_PER_TILE) * UCOLS;
+            const bool nt = (iu % UNITS_PER_TILE == 0) || iu == ub;
+            if (lane == 0) {
+                // WAR on the stage (generic LDS reads of the unit before, async-proxy
+                // writes now) is ordered by the __syncwarp after the wait below, as in
+                // an mbarrier consumer-release / producer-acquire pipeline: no proxy
+                // fence (it compiles to MEMBAR.ALL.CTA, which waits for this lane's
+                // outstanding column-slab stores)
+                mbar_arrive_tx(&W.bar[ist], YB + (nt ? XB : 0));
+                bulk_g2s(W.y[ist], Y + (size_t)t * TB * TB + (size_t)jj0 * TB, YB, &W.bar[ist]);
+                if (nt) bulk_g2s(W.xcol[t & 1], X + (size_t)(t - itb) * TB * D, XB, &W.bar[ist]);
+            }
+            ++iu;
+            ist = (ist + 1 == NSTAGE) ? 0 : ist + 1;
+        };
+#ifndef MDS_EXP_NO_TMA
+        issue_one();
+        if (NSTAGE > 2 && iu < ue) issue_one();
+#endif
+#pragma unroll 1
+        for (int si = 0; si < nsw; ++si) {
+            const int4 sg = W.seg[si];
+            T xi0[D], xi1[D];
+            A g0[D], g1[D];
+#pragma unroll
+            for (int k = 0; k < D; ++k) {          // the segment's 64 rows (2 per lane)
+                xi0[k] = (T)X[((size_t)sg.x * TB + lane) * D + k];
+                xi1[k] = (T)X[((size_t)sg.x * TB + lane + 32) * D + k];
+                g0[k] = g1[k] = A(0);
+            }
+#pragma unroll 1
+            for (int u = sg.y / GPU; u < (sg.z + GPU - 1) / GPU; ++u) {
+                // the unit's 4-column groups inside this segment: [c4b, c4e)
+                const int c4b = max(sg.y - GPU * u, 0), c4e = min(sg.z - GPU * u, GPU);
+#ifndef MDS_EXP_NO_TMA
+                if (a.prof && lane == 0 && !mbar_ready(&W.bar[cst], (phase >> cst) & 1)) ++not_ready;
+                mbar_wait(&W.bar[cst], (phase >> cst) & 1);
+                if (a.prof && threadIdx.x == 0 && not_ready < 0x80000000u) {   // first unit of warp 0 landed
+                    a.prof[gridDim.x * 6 + blockIdx.x] = gtimer();
+                    not_ready |= 0x80000000u;
+                }
+                phase ^= 1u << cst;
+                __syncwarp();                         // all lanes are done with the stage being refilled
+                if (iu < ue) issue_one();
+#endif
+                const int t = u / UNITS_PER_TILE, jb = (u % UNITS_PER_TILE) * UCOLS;
+                const int cpos = __ldg(a.slab_pos + a.nseg + t);    // used after the groups' math
+#pragma unroll 1
+                for (int c4 = c4b; c4 < c4e; ++c4) {       // 4-column reduce groups of the unit
+                const int jj0 = jb + 4 * c4;
+                const T* __restrict__ yst = W.y[cst] + 4 * c4 * TB;
+                const double* __restrict__ xc = W.xcol[t & 1] + jj0 * D;
+                T cv[4][D];
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {         // positions 2h, 2h+1: 4 pairs per lane in lock-step
+                    T ys[4], ss[4], dd[4][D];
+#pragma unroll
+                    for (int qq = 0; qq < 2; ++qq) {
+                        const int q = (2 * h + qq) ^ m;   // column of position 2h + qq
+                        ys[2 * qq] = yst[q * TB + lane];
+                        ys[2 * qq + 1] = yst[q * TB + lane + 32];
+                        T sa = T(0), sb = T(0);
+#pragma unroll
+                        for (int k = 0; k < D; ++k) {
+                            const T xjk = (T)xc[q * D + k];
+                            dd[2 * qq][k] = xi0[k] - xjk;
+                            dd[2 * qq + 1][k] = xi1[k] - xjk;
+                            sa = fma(dd[2 * qq][k], dd[2 * qq][k], sa);
+                            sb = fma(dd[2 * qq + 1][k], dd[2 * qq + 1][k], sb);
+                        }
+                        ss[2 * qq] = sa;
+                        ss[2 * qq + 1] = sb;
+                    }
+                    T ll[4], uu[4];
+                    Pair<T, TRUNC>::template eval4<WL, WG>(ss, ys, a.P, exptab, ll, uu);
+                    T lsum = T(0);
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        const bool mi = is_missing(ys[i]);
+                        if (WL && !mi) lsum += ll[i];         // predicated, no select
+                        if (WG) uu[i] = mi ? T(0) : uu[i];
+                    }
+                    if (WG) {
+#pragma unroll
+                        for (int k = 0; k < D; ++k) {
+                            const T va0 = uu[0] * dd[0][k], vb0 = uu[1] * dd[1][k];
+                            const T va1 = uu[2] * dd[2][k], vb1 = uu[3] * dd[3][k];
+                            g0[k] -= A(va0 + va1);
+                            g1[k] -= A(vb0 + vb1);
+                            cv[2 * h][k] = va0 + vb0;
+                            cv[2 * h + 1][k] = va1 + vb1;
+                        }
+                    }
+                    if (WL) lik_w += A(lsum);
+                }
+                double* __restrict__ cslab = a.slabs + (size_t)cpos * TB * D + (size_t)jj0 * D;
+#ifndef MDS_EXP_NO_COLRED
+#pragma unroll
+                for (int k = 0; k < (WG ? D : 0); ++k) {
+                    const T cs = reduce_scatter4_perm(cv[0][k], cv[1][k], cv[2][k], cv[3][k]);
+#ifndef MDS_EXP_NO_CSTORE
+                    if ((lane & 7) == 0) cslab[m * D + k] = A(cs);
+#else
+                    lik_w += A(cs);
+#endif
+                }
+#else
+#pragma unroll
+                for (int k = 0; k < D; ++k) lik_w += A(cv[0][k] + cv[1][k] + cv[2][k] + cv[3][k]);
+                (void)cslab;
+#endif
+                }   // 4-column groups
+                cst = (cst + 1 == NSTAGE) ? 0 : cst + 1;
+            }
+            // the segment's row partial
+            double* __restrict__ rslab = a.slabs + (size_t)W.spos[si] * TB * D;
+            if (WG) {
+#pragma unroll
+                for (int k = 0; k < D; ++k) {
+                    rslab[lane * D + k] = g0[k];
+                    rslab[(lane + 32) * D + k] = g1[k];
+                }
+            }
+        }
+    }
+    }   // virtual ranges
+#pragma unroll
+    for (int m = 16; m >= 1; m >>= 1) lik_w += __shfl_xor_sync(0xffffffffu, lik_w, m);
+    if (lane == 0) a.likpart[gw] = lik_w;
+
+    // ------------------------------------------------------------ barrier
+    if (a.prof) {
+        if (lane == 0) atomicAdd(&a.prof[gridDim.x * 4 + blockIdx.x], (unsigned long long)(not_ready & 0x7fffffffu));
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            a.prof[blockIdx.x * 4 + 1] = gtimer();
+            unsigned smid;
+            asm("mov.u32 %0, %%smid;" : "=r"(smid));
+            a.prof[gridDim.x * 5 + blockIdx.x] = smid;
+        }
+    }
+    // (Loading phase B's static inputs -- block pointers, leapfrog state -- before
+    // the barrier measured 0.4% slower: A/B on one box.)
+    constexpr int EPLMAX = 4;
+    const int epl = a.epl;
+    const int CH = 32 * epl;
+    const int chunks = (TB * D + CH - 1) / CH;
+    const int jobs = a.nb * chunks;
+    __threadfence();
+    cg::this_grid().sync();
+    if (a.prof && threadIdx.x == 0) a.prof[blockIdx.x * 4 + 2] = gtimer();
+
+    // ------------------------------------------------------------ phase B
+    // job = (row block b, chunk of 32 * epl slab elements, epl per lane; the host
+    // picks epl in {1, 2, 4} so that the jobs fit the grid in one round); warp w
+    // sums slabs w, w + WPC, ... in order with 8 slab indices in flight
+    // the staging area is free after the grid barrier: reuse it for the sums
+    A (*red)[WPC][32] = reinterpret_cast<A (*)[WPC][32]>(dsm);
+    for (int job = blockIdx.x; WG && job < jobs; job += gridDim.x) {
+        const int b = job / chunks, ch = job % chunks;
+        const int q0 = a.blk_ptr[b], nq = a.blk_ptr[b + 1] - q0;
+        A acc[EPLMAX];
+        int el[EPLMAX];
+#pragma unroll
+        for (int ee = 0; ee < EPLMAX; ++ee) {
+            acc[ee] = A(0);
+            el[ee] = ch * CH + ee * 32 + lane;
+        }
+        // leapfrog state of the element this warp updates below (independent of the sums)
+        double pre_xe = 0, pre_p = 0, pre_gl = 0;
+        const int e_up = ch * CH + warp * 32 + lane;
+        const int64_t e_glb = (int64_t)b * TB * D + e_up;
+        if (LF && warp < epl && e_up < TB * D && e_glb < a.n * D) {
+            pre_xe = a.xeval[e_glb];
+            pre_p = a.p[e_glb];
+            pre_gl = a.gl[e_glb];
+        }
+        // block b's slabs are contiguous: warp w sums rows w, w + WPC, ... in order,
+        // 8 rows in flight (rows past the end add exact zeros)
+        const double* __restrict__ sb = a.slabs + (size_t)q0 * TB * D;
+        for (int k0 = warp; k0 < nq; k0 += 8 * WPC) {
+#pragma unroll
+            for (int ee = 0; ee < EPLMAX; ++ee) {
+                if (ee < epl && el[ee] < TB * D) {
+                    A x[8];
+#pragma unroll
+                    for (int r = 0; r < 8; ++r) {
+                        const int k = k0 + r * WPC;
+                        x[r] = k < nq ? sb[(size_t)k * TB * D + el[ee]] : A(0);
+                    }
+#pragma unroll
+                    for (int r = 0; r < 8; ++r) acc[ee] += x[r];
+                }
+            }
+        }
+#pragma unroll
+        for (int ee = 0; ee < EPLMAX; ++ee)
+            if (ee < epl) red[ee][warp][lane] = acc[ee];
+        __syncthreads();
+        if (warp < epl) {
+            const int ee = warp;
+            const int e_in = ch * CH + ee * 32 + lane;
+            if (e_in < TB * D) {
+                A g = red[ee][0][lane];
+#pragma unroll
+                for (int w = 1; w < WPC; ++w) g += red[ee][w][lane];
+                const int64_t e = (int64_t)b * TB * D + e_in;
+                if (e < a.n * D) {
+                    if (!LF) {
+                        a.grad[e] = g;
+                    } else {
+                        // leapfrog: the pass ran at xnext = x + eps (p + eps/2 gl)
+                        const double xe = pre_xe;
+                        const double ph = __fma_rn(a.heps, pre_gl, pre_p);    // first half-kick
+                        const double gn = g - xe * a.inv_tau2;                  // grad log pi at xnext
+                        const double pn = __fma_rn(a.heps, gn, ph);             // second half-kick
+                        a.grad[e] = g;
+                        a.x[e] = xe;
+                        a.p[e] = pn;
+                        a.gl[e] = gn;
+                        a.xnext[e] = drift(xe, pn, gn, a.eps, a.heps);           // next step's drift
+                    }
+                }
+            }
+        }
+        __syncthreads();
+    }
+    // log L on the last CTA (job-free when jobs < grid): fixed-order strided
+    // partial sums over the warp partials, then warps in order
+    if (!WL) {
+        // nobody reads log L of this pass: mark it as not computed
+        if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) *a.lik = __longlong_as_double(0x7ff8000000000000LL);
+    } else if (blockIdx.x == gridDim.x - 1) {
+        const int GW = gridDim.x * WPC;
+        A s = A(0);
+        for (int q = threadIdx.x; q < GW; q += WPC * 32) s += a.likpart[q];
+        red[0][warp][lane] = s;
+        __syncthreads();
+        if (threadIdx.x < 32) {
+            A t = A(0);
+            for (int w = 0; w < WPC; ++w) t += red[0][w][threadIdx.x];
+#pragma unroll
+            for (int m = 16; m >= 1; m >>= 1) t += __shfl_xor_sync(0xffffffffu, t, m);
+            if (threadIdx.x == 0) *a.lik = t;
+        }
+    }
+    if (a.prof) {
+        __syncthreads();
+        if (threadIdx.x == 0) a.prof[blockIdx.x * 4 + 3] = gtimer();
+    }
+}
+
+// ------------------------------------------------------------ dispatch
+typedef void (*PassFn)(PassArgs);
+struct PassKernel {
+    PassFn fn;
+    size_t smem;
+    int wpc;   // warps per CTA
+};
+// pass_m<MODE>_<prec>(trunc, d): the instantiation for one (MODE, precision),
+// defined in csrc/pass_m<MODE>_<prec>.cu (one translation unit each)
+#define MDS_DECLARE_PASS(M)                       \
+    PassKernel pass_m##M##_f64(int trunc, int d); \
+    PassKernel pass_m##M##_f32(int trunc, int d);
+MDS_DECLARE_PASS(0)
+MDS_DECLARE_PASS(1)
+MDS_DECLARE_PASS(2)
+MDS_DECLARE_PASS(3)
+MDS_DECLARE_PASS(4)
+#undef MDS_DECLARE_PASS
+
+}  // namespace mdsk
+

@@ -1,0 +1,166 @@
+// mds_row.cu -- single-location update kernels (see mds_row.cuh).
+#include "mds_row.cuh"
+
+namespace mdsk {
+namespace {
+
+// y_ab (a > b) in the tiled triangle: tile (a/B, b/B), column-major inside
+template <typename T>
+__device__ __forceinline__ T y_pair(const T* __restrict__ Y, const int* __restrict__ row_local, int64_t a, int64_t b) {
+    const int lt = __ldg(row_local + (a >> 6));
+    return Y[((size_t)(lt + (b >> 6)) << 12) + ((b & 63) << 6) + (a & 63)];
+}
+
+template <typename T, bool TRUNC>
+__device__ __forceinline__ void ell2(T s0, T s1, T y, const SigmaParams& P, const double* exptab, T& e0, T& e1);
+template <>
+__device__ __forceinline__ void ell2<double, true>(double s0, double s1, double y, const SigmaParams& P,
+                                                   const double* exptab, double& e0, double& e1) {
+    const double s[2] = {s0, s1}, yy[2] = {y, y};
+    double l[2], u[2];
+    pair_f64_n<true, 2, true, false>(s, yy, P, exptab, l, u);
+    e0 = l[0];
+    e1 = l[1];
+}
+template <>
+__device__ __forceinline__ void ell2<double, false>(double s0, double s1, double y, const SigmaParams& P,
+                                                    const double* exptab, double& e0, double& e1) {
+    const double s[2] = {s0, s1}, yy[2] = {y, y};
+    double l[2], u[2];
+    pair_f64_n<false, 2, true, false>(s, yy, P, exptab, l, u);
+    e0 = l[0];
+    e1 = l[1];
+}
+template <>
+__device__ __forceinline__ void ell2<float, true>(float s0, float s1, float y, const SigmaParams& P, const double*,
+                                                  float& e0, float& e1) {
+    float u;
+    pair_f32<true, true, false>(s0, y, P, e0, u);
+    pair_f32<true, true, false>(s1, y, P, e1, u);
+}
+template <>
+__device__ __forceinline__ void ell2<float, false>(float s0, float s1, float y, const SigmaParams& P, const double*,
+                                                   float& e0, float& e1) {
+    float u;
+    pair_f32<false, true, false>(s0, y, P, e0, u);
+    pair_f32<false, true, false>(s1, y, P, e1, u);
+}
+
+// Delta of row i between positions xn and xo (both [D] in shared memory),
+// returned to every thread.  Fixed order: per-thread sum over its columns in
+// ascending j, warp butterfly, then the 32 warp sums in order.
+template <typename T, int D, bool TRUNC>
+__device__ double row_delta(const RowArgs& a, int64_t i, const double* xn, const double* xo, const double* exptab,
+                            double* red) {
+    const T* __restrict__ Y = static_cast<const T*>(a.y);
+    const double* X = a.x;     // not __restrict__/nc: the sweep writes X between updates
+    double acc = 0.0;
+    T xnr[D], xor_[D];
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+        xnr[k] = (T)xn[k];
+        xor_[k] = (T)xo[k];
+    }
+    for (int64_t j = threadIdx.x; j < a.n; j += ROW_THREADS) {
+        if (j == i) continue;
+        const T y = j < i ? y_pair<T>(Y, a.row_local, i, j) : y_pair<T>(Y, a.row_local, j, i);
+        if (is_missing(y)) continue;
+        T sn = T(0), so = T(0);
+#pragma unroll
+        for (int k = 0; k < D; ++k) {
+            const T xj = (T)X[j * D + k];
+            const T dn = xnr[k] - xj, dl = xor_[k] - xj;
+            sn = fma(dn, dn, sn);
+            so = fma(dl, dl, so);
+        }
+        T en, eo;
+        ell2<T, TRUNC>(sn, so, y, a.P, exptab, en, eo);
+        acc += double(en) - double(eo);
+    }
+#pragma unroll
+    for (int m = 16; m >= 1; m >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, m);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (lane == 0) red[warp] = acc;
+    __syncthreads();
+    double t = 0.0;
+    if (warp == 0) {
+        t = red[lane];
+#pragma unroll
+        for (int m = 16; m >= 1; m >>= 1) t += __shfl_xor_sync(0xffffffffu, t, m);
+        if (lane == 0) red[32] = t;
+    }
+    __syncthreads();
+    t = red[32];
+    __syncthreads();   // red is reused by the next call
+    return t;
+}
+
+template <typename T, int D, bool TRUNC>
+__global__ void __launch_bounds__(ROW_THREADS, 1) row_kernel(RowArgs a) {
+    __shared__ double exptab[64];
+    __shared__ double red[33];
+    __shared__ double xn[D], xo[D];
+    if (threadIdx.x < 64) exptab[threadIdx.x] = EXPT64_TAB[threadIdx.x];
+    if (a.K == 0) {
+        if (threadIdx.x < D) {
+            xo[threadIdx.x] = a.x[a.i0 * D + threadIdx.x];
+            xn[threadIdx.x] = a.xnew[threadIdx.x];
+        }
+        __syncthreads();
+        const double dl = row_delta<T, D, TRUNC>(a, a.i0, xn, xo, exptab, red);
+        if (threadIdx.x == 0) *a.delta = dl;
+        return;
+    }
+    unsigned long long nacc = 0;
+    for (int64_t k = 0; k < a.K; ++k) {
+        const int64_t i = a.rows[k];
+        if (threadIdx.x < D) {
+            const double v = a.x[i * D + threadIdx.x];
+            xo[threadIdx.x] = v;
+            xn[threadIdx.x] = __fma_rn(a.step, a.z[k * D + threadIdx.x], v);
+        }
+        __syncthreads();
+        const double dl = row_delta<T, D, TRUNC>(a, i, xn, xo, exptab, red);
+        // log prior change (iid N(0, tau^2)); decision in fp64 on thread 0
+        if (threadIdx.x == 0) {
+            double pn = 0.0, po = 0.0;
+#pragma unroll
+            for (int q = 0; q < D; ++q) {
+                pn = fma(xn[q], xn[q], pn);
+                po = fma(xo[q], xo[q], po);
+            }
+            const double lr = dl - 0.5 * (pn - po) * a.inv_tau2;
+            const bool ok = isfinite(lr) && log(a.u[k]) < lr;
+            if (ok) {
+#pragma unroll
+                for (int q = 0; q < D; ++q) a.x[i * D + q] = xn[q];
+                ++nacc;
+            }
+        }
+        __threadfence_block();
+        __syncthreads();   // X[i] (if accepted) is visible to the next update's column reads
+    }
+    if (threadIdx.x == 0) *a.accepted = nacc;
+}
+
+template <typename T, bool TR>
+RowFn row_fn_d(int d) {
+    switch (d) {
+        case 1: return row_kernel<T, 1, TR>;
+        case 2: return row_kernel<T, 2, TR>;
+        case 3: return row_kernel<T, 3, TR>;
+        case 4: return row_kernel<T, 4, TR>;
+        case 5: return row_kernel<T, 5, TR>;
+        case 6: return row_kernel<T, 6, TR>;
+        case 7: return row_kernel<T, 7, TR>;
+        default: return row_kernel<T, 8, TR>;
+    }
+}
+}  // namespace
+
+RowFn row_fn(int prec_is_f64, int trunc, int d) {
+    if (prec_is_f64) return trunc ? row_fn_d<double, true>(d) : row_fn_d<double, false>(d);
+    return trunc ? row_fn_d<float, true>(d) : row_fn_d<float, false>(d);
+}
+
+}  // namespace mdsk

@@ -1,0 +1,48 @@
+// mds_row.cuh -- single-location updates.
+//
+// "changing the value of a single x_i invalidates only N - 1 terms": the change
+// of log L when x_i alone moves to x', one row of the triangle,
+//   Delta_i(x') = sum_{j != i, y_ij observed} [ ell(y_ij, ||x' - x_j||) - ell(y_ij, ||x_i - x_j||) ]
+// (ell = the Eq. 2 term), is O(N D).  It drives the random-walk Metropolis
+// sampler of Bedford et al. that the paper compares against: update i, propose
+// x_i + step z, accept iff log u < Delta_i + Delta log prior.
+//
+// One CTA of 1024 threads evaluates one row: thread t takes columns
+// j = t, t + 1024, ... (y_ij gathered from the tiled triangle: for j > i the
+// 32 lanes of a warp read one contiguous 256 B run of a tile column), both
+// terms of a column in lock-step (pair_f64_n with NP = 2, likelihood only),
+// then a fixed-order block tree reduction: deterministic, no atomics.  A sweep
+// of K sequential updates is ONE launch (the updates are dependent: the CTA
+// loops, X stays in L2).
+#pragma once
+#include <cstdint>
+#include "mds_math.cuh"
+
+namespace mdsk {
+
+struct RowArgs {
+    const void* y;              // local tiles (unsharded context: all of them)
+    const int* row_local;       // [nb] local index of tile (I, 0)
+    double* x;                  // fp64 master X, n_pad x D (updated in place by the sweep)
+    int64_t n;
+    // single delta (K == 0): row i0 moved to xnew
+    int64_t i0;
+    const double* xnew;         // [D]
+    double* delta;              // out: Delta
+    // sweep (K >= 1)
+    int64_t K;
+    const int64_t* rows;        // [K]
+    const double* z;            // [K][D]
+    const double* u;            // [K]
+    double step;
+    double inv_tau2;            // iid N(0, tau^2) prior; 0 = flat
+    unsigned long long* accepted;
+    SigmaParams P;
+};
+
+typedef void (*RowFn)(RowArgs);
+constexpr int ROW_THREADS = 1024;
+// row_kernel<T, D, TRUNC> for (precision, truncation, d); defined in mds_row.cu
+RowFn row_fn(int prec_is_f64, int trunc, int d);
+
+}  // namespace mdsk

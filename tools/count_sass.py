@@ -1,7 +1,7 @@
 #!/usr/bin/env python
 """Static SASS instruction mix of the pair kernel's inner loop -> profiles/sass_counts.json.
 
-For every pass_kernel<T, D, TRUNC, LEAPFROG> instantiation in libmds.so: find the loop
+For every pass_kernel<T, D, TRUNC, MODE> instantiation in libmds.so: find the loop
 (the backward branch of the column-group loop), count its instructions by
 class, and divide by the pairs one loop trip evaluates per lane (its MUFU.RSQ count).  The
 FP64 count per pair is the 'algorithmic' FP64 work of the roofline.
@@ -26,11 +26,11 @@ def main():
     res = {}
     for f in funcs[1:]:
         name = f.split("\n", 1)[0].strip()
-        m = re.match(r"_ZN4mdsk11pass_kernelI([fd])Li(\d)ELb([01])ELi2EEEvNS_8PassArgsE", name)
+        m = re.match(r"_ZN4mdsk11pass_kernelI([fd])Li(\d)ELb([01])ELi(\d)EEEvNS_8PassArgsE", name)
         if not m:
             continue
         prec = "f64" if m.group(1) == "d" else "f32"
-        d, t = int(m.group(2)), int(m.group(3))
+        d, t, mode = int(m.group(2)), int(m.group(3)), int(m.group(4))
         lines = re.findall(r"/\*([0-9a-f]{4,})\*/\s+(.*?);", f)
         ins = [(int(a, 16), txt.strip()) for a, txt in lines]
         # backward branch of the group loop
@@ -55,7 +55,10 @@ def main():
         n64 = sum(o in FP64 for o in ops)
         n32 = sum(o in FP32 for o in ops)
         nmufu = sum(o == "MUFU" for o in ops)
-        res["%s_d%d_t%d" % (prec, d, t)] = {
+        # key: <prec>_d<D>_t<T> for the leapfrog pass (mode 2, the bench kernel),
+        # + "_m<mode>" for the other modes (mds_pass.cuh "Mode")
+        key = "%s_d%d_t%d" % (prec, d, t) + ("" if mode == 2 else "_m%d" % mode)
+        res[key] = {
             "kernel": name, "loop_instructions": len(ops),
             "pairs_per_trip": npairs,
             "fp64_per_pair": n64 / npairs, "fp32_per_pair": n32 / npairs,
