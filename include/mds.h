@@ -217,6 +217,31 @@ mds_status mds_row_loglik_delta(mds_ctx ctx, int64_t i, const double *x_new_i, d
 mds_status mds_rw_sweep(mds_ctx ctx, int64_t k, const int64_t *rows, const double *z, const double *u,
                         double step, double prior_sd, int64_t *accepted);
 
+/* ---- cross-validation ----------------------------- */
+
+/* The held-out observations of one cross-validation fold:
+ * m pairs (i[q], j[q], y[q]) with 0 <= i, j < n, i != j, y finite and >= 0
+ * (host arrays; order is kept).  Replaces any previous fold and resets the
+ * accumulator.  The caller trains on the complement: the Y given to
+ * mds_set_dissimilarities* should hold NaN (missing, R7) at these pairs; this
+ * is not checked.  Held-out terms are evaluated in fp64 whatever the context
+ * precision, with the context's truncation flag.  Errors: MDS_E_INVALID_ARG,
+ * MDS_E_OOM, MDS_E_CUDA. */
+mds_status mds_cv_set_heldout(mds_ctx ctx, int64_t m, const int64_t *i, const int64_t *j, const double *y);
+
+/* Add one posterior draw: at the context's current X and sigma, ell_q = log
+ * p(y_q | X, sigma) (the Eq. 1 density = the Eq. 2 term) of every held-out
+ * pair goes into that pair's running log-sum-exp.  Stream-ordered, no sync.
+ * Errors: MDS_E_STATE (no fold, X or sigma not set), MDS_E_CUDA. */
+mds_status mds_cv_accumulate(mds_ctx ctx);
+
+/* The fold's log pointwise predictive density over the S draws accumulated:
+ *   *lpd = sum_q log( (1/S) sum_s exp(ell_q^(s)) )
+ * (PAPER.md:389-393 without the posterior-density factor, reading R29), a
+ * fixed-order reduction; *draws (may be NULL) = S.  Synchronises.  Errors:
+ * MDS_E_INVALID_ARG (NULL lpd), MDS_E_STATE (no fold / no draw), MDS_E_CUDA. */
+mds_status mds_cv_lpd(mds_ctx ctx, double *lpd, int64_t *draws);
+
 /* ---- diagnostics ------------------------------------------------------- */
 
 /* Number of observed pairs stored by this context (this rank's share). */

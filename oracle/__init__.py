@@ -67,6 +67,7 @@ def _load():
         lib.oracle_row_delta.argtypes = [i64, i32, d_p, d_p, i64, d_p, ctypes.c_double, i32, d_p]
         lib.oracle_rw_sweep.argtypes = [i64, i32, d_p, d_p, ctypes.c_double, i32, i64, P(i64), d_p, d_p,
                                         ctypes.c_double, ctypes.c_double, P(i64)]
+        lib.oracle_cv_lpd.argtypes = [i64, i32, i64, P(i64), P(i64), d_p, i64, d_p, d_p, i32, d_p]
         _lib = lib
     return _lib
 
@@ -210,3 +211,21 @@ def rw_sweep(y_packed: np.ndarray, x0: np.ndarray, sigma: float, rows, z, u, ste
                            float(prior_sd), ctypes.byref(acc)):
         raise ValueError("invalid oracle arguments")
     return x, acc.value
+
+
+def cv_lpd(hi, hj, hy, xs, sigmas, truncation: int = 1) -> float:
+    """Held-out log pointwise predictive density over S draws.
+    xs: (S, n, d) posterior draws of X; sigmas: (S,)."""
+    lib = _load()
+    xs = _f64(xs)
+    S, n, d = xs.shape
+    hi = np.ascontiguousarray(hi, dtype=np.int64)
+    hj = np.ascontiguousarray(hj, dtype=np.int64)
+    hy = _f64(hy)
+    sg = _f64(sigmas).reshape(S)
+    out = ctypes.c_double()
+    P = ctypes.POINTER(ctypes.c_int64)
+    if lib.oracle_cv_lpd(n, d, hy.size, hi.ctypes.data_as(P), hj.ctypes.data_as(P), _dp(hy), S, _dp(xs), _dp(sg),
+                         int(truncation), ctypes.byref(out)):
+        raise ValueError("invalid oracle arguments")
+    return out.value

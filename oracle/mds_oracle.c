@@ -23,6 +23,8 @@
  *   PAPER.md:258-263                    single-location updates: "changing the value of a single
  *                                       x_i invalidates only N - 1 terms" (row delta, random-walk
  *                                       Metropolis sweep of Bedford et al.; reading R28).
+ *   PAPER.md:381-395                    cross-validated log pointwise predictive density of a
+ *                                       held-out fold over S posterior draws (reading R29).
  *   PAPER.md:205-210, 672               sigma^-2 ~ Gamma(s_0, r_0) and the per-iteration
  *                                       sigma^2 update: Metropolis-Hastings random walk on
  *                                       log sigma^2 (reading R27).
@@ -334,5 +336,39 @@ int oracle_rw_sweep(int64_t n, int32_t d, const double *y_packed, double *x, dou
     }
     if (accepted) *accepted = na;
     free(xn);
+    return 0;
+}
+
+/* ---- cross-validation lpd (R29) ------------------------ */
+/* lpd = sum_q log( (1/S) sum_s p(y_q | X_s, sigma_s) ), p the Eq. 1 density,
+ * log p = the Eq. 2 term.  Draws: xs[s*n*d ...] (S x n x d), sigmas[S].
+ * Each log-mean-exp is formed with the max shift: m + log(sum exp(l - m)) - log S. */
+int oracle_cv_lpd(int64_t n, int32_t d, int64_t m, const int64_t *hi, const int64_t *hj, const double *hy,
+                  int64_t S, const double *xs, const double *sigmas, int32_t truncation, double *lpd)
+{
+    if (n < 2 || d < 1 || m < 0 || S < 1) return -1;
+    double *l = (double *)malloc((size_t)S * sizeof(double));
+    if (!l) return -1;
+    acc_t tot = {0.0, 0.0};
+    for (int64_t q = 0; q < m; ++q) {
+        int64_t i = hi[q], j = hj[q];
+        if (i < 0 || i >= n || j < 0 || j >= n || i == j) { free(l); return -1; }
+        double mx = -INFINITY;
+        for (int64_t s = 0; s < S; ++s) {
+            const double *x = xs + s * n * d;
+            double ss = 0.0;
+            for (int k = 0; k < d; ++k) {
+                double df = x[i * d + k] - x[j * d + k];
+                ss += df * df;
+            }
+            oracle_pair_term(hy[q], sqrt(ss), sigmas[s], truncation, &l[s], NULL);
+            if (l[s] > mx) mx = l[s];
+        }
+        double se = 0.0;
+        for (int64_t s = 0; s < S; ++s) se += exp(l[s] - mx);
+        acc_add(&tot, mx + log(se) - log((double)S));
+    }
+    *lpd = acc_val(&tot);
+    free(l);
     return 0;
 }

@@ -182,6 +182,18 @@ class MDS:
         Returns (accepted, log_ratio); the context's sigma moves on acceptance."""
         return _abi.mds_sigma_mh_step(self.ctx, shape, rate, step, z, u)
 
+    # cross-validation (SURVEY 8(f) NEXT-3)
+    def cv_set_heldout(self, i, j, y):
+        _abi.mds_cv_set_heldout(self.ctx, np.ascontiguousarray(i, dtype=np.int64),
+                                np.ascontiguousarray(j, dtype=np.int64), np.ascontiguousarray(y, dtype=np.float64))
+
+    def cv_accumulate(self):
+        _abi.mds_cv_accumulate(self.ctx)
+
+    def cv_lpd(self):
+        """(lpd, draws) of the held-out fold over the draws accumulated."""
+        return _abi.mds_cv_lpd(self.ctx)
+
     # single-location updates (SURVEY 8(f) NEXT-4)
     def row_loglik_delta(self, i: int, x_new_i) -> float:
         return _abi.mds_row_loglik_delta(self.ctx, i, np.ascontiguousarray(x_new_i, dtype=np.float64))

@@ -29,6 +29,7 @@ EXPORTS = [
     "mds_hmc_trajectory", "mds_hmc_run", "mds_leapfrog_device", "mds_get_locations", "mds_get_momentum",
     "mds_set_allgather", "mds_plan",
     "mds_log_likelihood_at_sigma", "mds_sigma_mh_step", "mds_row_loglik_delta", "mds_rw_sweep",
+    "mds_cv_set_heldout", "mds_cv_accumulate", "mds_cv_lpd",
     "mds_last_error", "mds_status_string", "mds_version", "mds_device_info", "mds_measure_fma_peaks", "mds_l2_flush",
 ]
 
@@ -102,6 +103,9 @@ def _load():
         "mds_measure_fma_peaks": [P(ctypes.c_double), P(ctypes.c_double)],
         "mds_l2_flush": [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t],
         "mds_log_likelihood_at_sigma": [vp, ctypes.c_double, P(ctypes.c_double)],
+        "mds_cv_set_heldout": [vp, i64, dp, dp, dp],
+        "mds_cv_accumulate": [vp],
+        "mds_cv_lpd": [vp, P(ctypes.c_double), P(i64)],
         "mds_row_loglik_delta": [vp, i64, dp, P(ctypes.c_double)],
         "mds_rw_sweep": [vp, i64, dp, dp, dp, ctypes.c_double, ctypes.c_double, P(i64)],
         "mds_sigma_mh_step": [vp, P(SigmaPrior), ctypes.c_double, ctypes.c_double, ctypes.c_double, P(i32),
@@ -304,6 +308,22 @@ def mds_rw_sweep(ctx, rows, z, u, step, prior_sd):
     _check(lib.mds_rw_sweep(ctx, int(rows.size), _ptr(rows), _ptr(z), _ptr(u), float(step), float(prior_sd),
                             ctypes.byref(acc)), ctx)
     return acc.value
+
+
+def mds_cv_set_heldout(ctx, i, j, y):
+    """i, j: int64 arrays (m,), y: float64 (m,)."""
+    _check(lib.mds_cv_set_heldout(ctx, int(y.size), _ptr(i), _ptr(j), _ptr(y)), ctx)
+
+
+def mds_cv_accumulate(ctx):
+    _check(lib.mds_cv_accumulate(ctx), ctx)
+
+
+def mds_cv_lpd(ctx):
+    """Returns (lpd, draws)."""
+    v, s = ctypes.c_double(), ctypes.c_int64()
+    _check(lib.mds_cv_lpd(ctx, ctypes.byref(v), ctypes.byref(s)), ctx)
+    return v.value, s.value
 
 
 def mds_last_error(ctx):

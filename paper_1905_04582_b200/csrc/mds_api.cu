@@ -15,6 +15,7 @@
 #include "../../include/mds.h"
 #include "mds_kernels.cuh"
 #include "mds_row.cuh"
+#include "mds_cv.cuh"
 
 using namespace mdsk;
 
@@ -96,6 +97,15 @@ struct mds_ctx_s {
     std::vector<cudaEvent_t> evpool;  // timing mode: 3 events per recorded pass
     size_t ev_used = 0;               // events recorded since the last mds_last_timing
 
+    // cross-validation fold (held-out pairs, per-pair running log-sum-exp)
+    int2* d_cv_ij = nullptr;
+    double* d_cv_y = nullptr;
+    double* d_cv_max = nullptr;
+    double* d_cv_sum = nullptr;
+    double* d_cv_out = nullptr;
+    int64_t cv_m = -1;               // -1: no fold set
+    int64_t cv_draws = 0;
+
     void* d_rwbuf = nullptr;         // single-location sweeps: rows, z, u, outputs
     size_t rwbuf_bytes = 0;
 
@@ -160,7 +170,8 @@ void free_all(mds_ctx c) {
     void* ps[] = {c->d_tiles, c->d_row_local, c->d_warp_seg, c->d_segs, c->d_blk_ptr,
                   c->d_slab_pos, c->d_slabs, c->d_likpart, c->d_y, c->d_x, c->d_grad, c->d_lik, c->d_stage,
                   c->d_bad, c->d_count, c->d_partial, c->d_gathered, c->d_p, c->d_gl, c->d_xnext, c->d_xsave,
-                  c->d_glsave, c->d_liksave, c->d_H, c->d_H0, c->d_prof, c->d_rwbuf};
+                  c->d_glsave, c->d_liksave, c->d_H, c->d_H0, c->d_prof, c->d_rwbuf,
+                  c->d_cv_ij, c->d_cv_y, c->d_cv_max, c->d_cv_sum, c->d_cv_out};
     for (void* p : ps)
         if (p) cudaFree(p);
     for (auto& e : c->evpool)
@@ -896,6 +907,84 @@ mds_status mds_rw_sweep(mds_ctx c, int64_t k, const int64_t* rows, const double*
     CK(cudaStreamSynchronize(c->stream));
     if (accepted) *accepted = (int64_t)na;
     ++c->version;      // X moved (possibly)
+    return MDS_OK;
+}
+
+mds_status mds_cv_set_heldout(mds_ctx c, int64_t m, const int64_t* i, const int64_t* j, const double* y) {
+    GUARD(c);
+    if (m < 0 || (m > 0 && (!i || !j || !y))) return fail(c, MDS_E_INVALID_ARG, "bad held-out arrays");
+    if (m > INT_MAX) return fail(c, MDS_E_INVALID_ARG, "too many held-out pairs");
+    std::vector<int2> ij((size_t)m);
+    for (int64_t q = 0; q < m; ++q) {
+        if (i[q] < 0 || i[q] >= c->n || j[q] < 0 || j[q] >= c->n || i[q] == j[q])
+            return fail(c, MDS_E_INVALID_ARG, "held-out pair " + std::to_string(q) + " out of range or diagonal");
+        if (!(y[q] >= 0.0) || !std::isfinite(y[q]))
+            return fail(c, MDS_E_INVALID_ARG, "held-out y must be finite and >= 0");
+        ij[(size_t)q] = make_int2((int)i[q], (int)j[q]);
+    }
+    void* ps[] = {c->d_cv_ij, c->d_cv_y, c->d_cv_max, c->d_cv_sum};
+    for (void* p : ps)
+        if (p) cudaFree(p);
+    c->d_cv_ij = nullptr;
+    c->d_cv_y = c->d_cv_max = c->d_cv_sum = nullptr;
+    c->cv_m = -1;
+    c->cv_draws = 0;
+    mds_status st;
+    if ((st = dalloc(c, &c->d_cv_ij, (size_t)m)) || (st = dalloc(c, &c->d_cv_y, (size_t)m)) ||
+        (st = dalloc(c, &c->d_cv_max, (size_t)m)) || (st = dalloc(c, &c->d_cv_sum, (size_t)m)) ||
+        (!c->d_cv_out && (st = dalloc(c, &c->d_cv_out, 1))))
+        return st;
+    if (m > 0) {
+        CK(cudaMemcpy(c->d_cv_ij, ij.data(), (size_t)m * sizeof(int2), cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(c->d_cv_y, y, (size_t)m * sizeof(double), cudaMemcpyHostToDevice));
+    }
+    c->cv_m = m;
+    return MDS_OK;
+}
+
+mds_status mds_cv_accumulate(mds_ctx c) {
+    GUARD(c);
+    if (c->cv_m < 0) return fail(c, MDS_E_STATE, "no held-out fold set (mds_cv_set_heldout)");
+    if (!c->x_set) return fail(c, MDS_E_STATE, "locations not set");
+    if (!c->sigma_set) return fail(c, MDS_E_STATE, "sigma not set");
+    if (c->cv_m > 0) {
+        CvArgs a{};
+        a.ij = c->d_cv_ij;
+        a.y = c->d_cv_y;
+        a.x = c->d_x;
+        a.lmax = c->d_cv_max;
+        a.lsum = c->d_cv_sum;
+        a.m = c->cv_m;
+        a.d = c->d;
+        a.trunc = c->trunc;
+        a.first = c->cv_draws == 0;
+        a.P = c->P;
+        int sms = 148;
+        int dev = 0;
+        CK(cudaGetDevice(&dev));
+        CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+        const int64_t want = (c->cv_m + 255) / 256;
+        cv_accumulate_launch(a, (int)std::min<int64_t>(want, (int64_t)sms * 8), c->stream);
+        CK(cudaGetLastError());
+    }
+    ++c->cv_draws;
+    return MDS_OK;
+}
+
+mds_status mds_cv_lpd(mds_ctx c, double* lpd, int64_t* draws) {
+    GUARD(c);
+    if (!lpd) return fail(c, MDS_E_INVALID_ARG, "NULL output");
+    if (c->cv_m < 0) return fail(c, MDS_E_STATE, "no held-out fold set (mds_cv_set_heldout)");
+    if (c->cv_draws == 0) return fail(c, MDS_E_STATE, "no posterior draw accumulated (mds_cv_accumulate)");
+    if (draws) *draws = c->cv_draws;
+    if (c->cv_m == 0) {
+        *lpd = 0.0;
+        return MDS_OK;
+    }
+    cv_finalize_launch(c->d_cv_max, c->d_cv_sum, c->cv_m, c->cv_draws, c->d_cv_out, c->stream);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(lpd, c->d_cv_out, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
     return MDS_OK;
 }
 
