@@ -217,6 +217,34 @@ mds_status mds_row_loglik_delta(mds_ctx ctx, int64_t i, const double *x_new_i, d
 mds_status mds_rw_sweep(mds_ctx ctx, int64_t k, const int64_t *rows, const double *z, const double *u,
                         double step, double prior_sd, int64_t *accepted);
 
+/* ---- phylogenetic prior --------------------------- */
+
+/* Set the Brownian-diffusion prior of X (Eq. 3):
+ * X ~ MN(mu0, V_G, Sigma).  The forest has n_nodes nodes; node k < n is item k
+ * (a tip), nodes >= n are internal.  parent[k] is the parent node, or -1 for a
+ * root; t[k] > 0 is the branch length to the parent (x_k = x_parent +
+ * N(0, t[k] Sigma)), or for a root its prior variance factor (x_root ~
+ * N(mu0, t[k] Sigma): tau_0 for a tree root, tau_e for an unsequenced item,
+ * which is a root without children).  Trees may be
+ * multifurcating; items must be tips and internal nodes must have children.
+ * mu0: d values (NULL = 0).  sigma_cov: d x d symmetric positive definite
+ * (row-major; NULL = identity).  All host arrays, copied.  Once set, the HMC
+ * calls (mds_hmc_trajectory, mds_leapfrog_device, mds_hmc_run) target
+ * log L + log p(X) under this prior and ignore cfg->prior_sd; the prior and
+ * its gradient come from an O(n d^2) post-order / pre-order pass over the
+ * forest (the dynamic program of PAPER.md:243-246), never from V_G^-1.
+ * n_nodes == 0 removes the tree prior (back to the iid prior).  Errors:
+ * MDS_E_INVALID_ARG (bad forest: cycle, out-of-range parent, an item with
+ * children, a childless internal node, t <= 0; Sigma not SPD), MDS_E_OOM,
+ * MDS_E_CUDA. */
+mds_status mds_set_tree_prior(mds_ctx ctx, int64_t n_nodes, const int64_t *parent, const double *t,
+                              const double *mu0, const double *sigma_cov);
+
+/* log p(X) under the tree prior at the context's X, and d log p / dX (host,
+ * n x d); either may be NULL.  Synchronises.  Errors: MDS_E_STATE (no tree
+ * prior or X not set), MDS_E_CUDA. */
+mds_status mds_tree_prior(mds_ctx ctx, double *logp, double *grad);
+
 /* ---- cross-validation ----------------------------- */
 
 /* The held-out observations of one cross-validation fold:

@@ -182,6 +182,20 @@ class MDS:
         Returns (accepted, log_ratio); the context's sigma moves on acceptance."""
         return _abi.mds_sigma_mh_step(self.ctx, shape, rate, step, z, u)
 
+    # phylogenetic prior (SURVEY 8(f) NEXT-2)
+    def set_tree_prior(self, parent, t, mu0=None, sigma_cov=None):
+        f = lambda a: None if a is None else np.ascontiguousarray(a, dtype=np.float64)
+        _abi.mds_set_tree_prior(self.ctx, np.ascontiguousarray(parent, dtype=np.int64), f(t), f(mu0), f(sigma_cov))
+
+    def clear_tree_prior(self):
+        _abi.mds_set_tree_prior(self.ctx, np.zeros(0, dtype=np.int64), np.zeros(0))
+
+    def tree_prior(self):
+        """(log p(X), d log p / dX) under the tree prior at the current X."""
+        g = np.zeros((self.n, self.d))
+        lp = _abi.mds_tree_prior(self.ctx, g)
+        return lp, g
+
     # cross-validation (SURVEY 8(f) NEXT-3)
     def cv_set_heldout(self, i, j, y):
         _abi.mds_cv_set_heldout(self.ctx, np.ascontiguousarray(i, dtype=np.int64),

@@ -29,7 +29,7 @@ EXPORTS = [
     "mds_hmc_trajectory", "mds_hmc_run", "mds_leapfrog_device", "mds_get_locations", "mds_get_momentum",
     "mds_set_allgather", "mds_plan",
     "mds_log_likelihood_at_sigma", "mds_sigma_mh_step", "mds_row_loglik_delta", "mds_rw_sweep",
-    "mds_cv_set_heldout", "mds_cv_accumulate", "mds_cv_lpd",
+    "mds_cv_set_heldout", "mds_cv_accumulate", "mds_cv_lpd", "mds_set_tree_prior", "mds_tree_prior",
     "mds_last_error", "mds_status_string", "mds_version", "mds_device_info", "mds_measure_fma_peaks", "mds_l2_flush",
 ]
 
@@ -104,6 +104,8 @@ def _load():
         "mds_l2_flush": [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t],
         "mds_log_likelihood_at_sigma": [vp, ctypes.c_double, P(ctypes.c_double)],
         "mds_cv_set_heldout": [vp, i64, dp, dp, dp],
+        "mds_set_tree_prior": [vp, i64, dp, dp, dp, dp],
+        "mds_tree_prior": [vp, dp, dp],
         "mds_cv_accumulate": [vp],
         "mds_cv_lpd": [vp, P(ctypes.c_double), P(i64)],
         "mds_row_loglik_delta": [vp, i64, dp, P(ctypes.c_double)],
@@ -308,6 +310,19 @@ def mds_rw_sweep(ctx, rows, z, u, step, prior_sd):
     _check(lib.mds_rw_sweep(ctx, int(rows.size), _ptr(rows), _ptr(z), _ptr(u), float(step), float(prior_sd),
                             ctypes.byref(acc)), ctx)
     return acc.value
+
+
+def mds_set_tree_prior(ctx, parent, t, mu0=None, sigma_cov=None):
+    """parent: int64 (n_nodes,), t: float64 (n_nodes,); mu0 (d,), sigma_cov (d, d) or None.
+    An empty parent array removes the tree prior."""
+    _check(lib.mds_set_tree_prior(ctx, int(parent.size), _ptr(parent), _ptr(t), _ptr(mu0), _ptr(sigma_cov)), ctx)
+
+
+def mds_tree_prior(ctx, grad=None):
+    """Returns log p(X); fills grad (n x d float64) if given."""
+    v = ctypes.c_double()
+    _check(lib.mds_tree_prior(ctx, ctypes.byref(v), _ptr(grad)), ctx)
+    return v.value
 
 
 def mds_cv_set_heldout(ctx, i, j, y):

@@ -16,6 +16,7 @@
 #include "mds_kernels.cuh"
 #include "mds_row.cuh"
 #include "mds_cv.cuh"
+#include "mds_tree.cuh"
 
 using namespace mdsk;
 
@@ -106,6 +107,15 @@ struct mds_ctx_s {
     int64_t cv_m = -1;               // -1: no fold set
     int64_t cv_draws = 0;
 
+    // phylogenetic Brownian-diffusion prior (mds_set_tree_prior); replaces the
+    // iid prior of the HMC driver when set
+    bool tree = false;
+    TreeArgs ta{};                   // device pointers + parameters of the forest
+    int* d_tree_int = nullptr;       // CSR, levels, roots (one allocation)
+    double* d_tree_dbl = nullptr;    // t, messages, contributions (one allocation)
+    double* d_gprior = nullptr;      // [npad][d] d log prior / dX at the last evaluated point
+    double* d_logprior = nullptr;    // [2]: log prior there, saved copy
+
     void* d_rwbuf = nullptr;         // single-location sweeps: rows, z, u, outputs
     size_t rwbuf_bytes = 0;
 
@@ -171,7 +181,8 @@ void free_all(mds_ctx c) {
                   c->d_slab_pos, c->d_slabs, c->d_likpart, c->d_y, c->d_x, c->d_grad, c->d_lik, c->d_stage,
                   c->d_bad, c->d_count, c->d_partial, c->d_gathered, c->d_p, c->d_gl, c->d_xnext, c->d_xsave,
                   c->d_glsave, c->d_liksave, c->d_H, c->d_H0, c->d_prof, c->d_rwbuf,
-                  c->d_cv_ij, c->d_cv_y, c->d_cv_max, c->d_cv_sum, c->d_cv_out};
+                  c->d_cv_ij, c->d_cv_y, c->d_cv_max, c->d_cv_sum, c->d_cv_out,
+                  c->d_tree_int, c->d_tree_dbl, c->d_gprior, c->d_logprior};
     for (void* p : ps)
         if (p) cudaFree(p);
     for (auto& e : c->evpool)
@@ -256,6 +267,13 @@ mds_status run_pass(mds_ctx c, const double* xeval, double* grad_out, double* li
     a.p = c->d_p;
     a.gl = c->d_gl;
     a.xnext = c->d_xnext;
+    if (lf && c->tree) {
+        // d log prior / dX at the point this pass evaluates (consumed by the leapfrog update)
+        TreeArgs ta = c->ta;
+        ta.x = xeval;
+        tree_prior_launch(ta, c->d, s);
+        a.gprior = c->d_gprior;
+    }
     if (timed) CK(cudaEventRecord(next_event(c), s));
     mds_status st;
     if (c->world == 1) {
@@ -279,7 +297,8 @@ mds_status run_pass(mds_ctx c, const double* xeval, double* grad_out, double* li
                                                                          lik_out);
         if (lf)
             leapfrog_update_kernel<<<(unsigned)((nd + 255) / 256), 256, 0, s>>>(
-                grad_out, xeval, c->d_x, c->d_p, c->d_gl, c->d_xnext, nd, eps, 0.5 * eps, inv_tau2);
+                grad_out, xeval, c->d_x, c->d_p, c->d_gl, c->d_xnext, nd, eps, 0.5 * eps, inv_tau2,
+                c->tree ? c->d_gprior : nullptr);
     }
     if (timed) CK(cudaEventRecord(next_event(c), s));
     CK(cudaGetLastError());
@@ -907,6 +926,179 @@ mds_status mds_rw_sweep(mds_ctx c, int64_t k, const int64_t* rows, const double*
     CK(cudaStreamSynchronize(c->stream));
     if (accepted) *accepted = (int64_t)na;
     ++c->version;      // X moved (possibly)
+    return MDS_OK;
+}
+
+mds_status mds_set_tree_prior(mds_ctx c, int64_t n_nodes, const int64_t* parent, const double* t,
+                              const double* mu0, const double* sigma_cov) {
+    GUARD(c);
+    if (n_nodes == 0) {             // back to the iid prior
+        c->tree = false;
+        c->lf_version = 0;
+        return MDS_OK;
+    }
+    const int64_t n = c->n;
+    const int d = c->d;
+    if (n_nodes < n || n_nodes > INT_MAX / 2 || !parent || !t)
+        return fail(c, MDS_E_INVALID_ARG, "tree prior: need n_nodes >= n and parent/t arrays");
+    std::vector<int> nch((size_t)n_nodes, 0);
+    for (int64_t k = 0; k < n_nodes; ++k) {
+        if (parent[k] < -1 || parent[k] >= n_nodes || parent[k] == k)
+            return fail(c, MDS_E_INVALID_ARG, "tree prior: parent of node " + std::to_string(k) + " out of range");
+        if (parent[k] >= 0 && parent[k] < n)
+            return fail(c, MDS_E_INVALID_ARG, "tree prior: item " + std::to_string(parent[k]) + " has a child (items are tips)");
+        if (!(t[k] > 0.0) || !std::isfinite(t[k]))
+            return fail(c, MDS_E_INVALID_ARG, "tree prior: branch lengths / root variances must be finite and > 0");
+        if (parent[k] >= 0) ++nch[(size_t)parent[k]];
+    }
+    for (int64_t k = n; k < n_nodes; ++k)
+        if (nch[(size_t)k] == 0) return fail(c, MDS_E_INVALID_ARG, "tree prior: internal node without children");
+    // children CSR (ascending child index), depth from the roots, height from the tips
+    std::vector<int> ch_ptr((size_t)n_nodes + 1, 0), ch_idx((size_t)std::max<int64_t>(n_nodes, 1)), fill;
+    for (int64_t k = 0; k < n_nodes; ++k) ch_ptr[(size_t)k + 1] = ch_ptr[(size_t)k] + nch[(size_t)k];
+    fill.assign(ch_ptr.begin(), ch_ptr.end() - 1);
+    for (int64_t k = 0; k < n_nodes; ++k)
+        if (parent[k] >= 0) ch_idx[(size_t)fill[(size_t)parent[k]]++] = (int)k;
+    std::vector<int> roots, depth((size_t)n_nodes, -1), height((size_t)n_nodes, 0), order;
+    order.reserve((size_t)n_nodes);
+    for (int64_t k = 0; k < n_nodes; ++k)
+        if (parent[k] < 0) {
+            roots.push_back((int)k);
+            depth[(size_t)k] = 0;
+            order.push_back((int)k);
+        }
+    for (size_t q = 0; q < order.size(); ++q) {          // breadth-first from the roots
+        const int v = order[q];
+        for (int e = ch_ptr[(size_t)v]; e < ch_ptr[(size_t)v + 1]; ++e) {
+            depth[(size_t)ch_idx[(size_t)e]] = depth[(size_t)v] + 1;
+            order.push_back(ch_idx[(size_t)e]);
+        }
+    }
+    if ((int64_t)order.size() != n_nodes) return fail(c, MDS_E_INVALID_ARG, "tree prior: parent array has a cycle");
+    for (size_t q = order.size(); q-- > 0;) {             // reverse BFS: children before parents
+        const int v = order[q];
+        if (parent[v] >= 0) height[(size_t)parent[v]] = std::max(height[(size_t)parent[v]], height[(size_t)v] + 1);
+    }
+    int hmax = 0, dmax = 0;
+    for (int64_t k = 0; k < n_nodes; ++k) {
+        hmax = std::max(hmax, height[(size_t)k]);
+        if (nch[(size_t)k]) dmax = std::max(dmax, depth[(size_t)k]);
+    }
+    std::vector<int> up_ptr((size_t)hmax + 1, 0), up_nodes, dn_ptr((size_t)dmax + 2, 0), dn_nodes;
+    for (int h = 1; h <= hmax; ++h) {
+        for (int64_t k = n; k < n_nodes; ++k)
+            if (height[(size_t)k] == h) up_nodes.push_back((int)k);
+        up_ptr[(size_t)h] = (int)up_nodes.size();
+    }
+    for (int dd = 0; dd <= dmax; ++dd) {
+        for (int64_t k = 0; k < n_nodes; ++k)
+            if (nch[(size_t)k] && depth[(size_t)k] == dd) dn_nodes.push_back((int)k);
+        dn_ptr[(size_t)dd + 1] = (int)dn_nodes.size();
+    }
+    const int n_dn = dn_nodes.empty() ? 0 : dmax + 1;
+    // Sigma^-1 and log|Sigma| by Cholesky (d <= 8; parameter preprocessing, like SigmaParams)
+    double S[TREE_DMAX * TREE_DMAX], Lc[TREE_DMAX * TREE_DMAX] = {0}, Si[TREE_DMAX * TREE_DMAX] = {0};
+    for (int r = 0; r < d; ++r)
+        for (int q = 0; q < d; ++q) S[r * d + q] = sigma_cov ? sigma_cov[r * d + q] : (r == q ? 1.0 : 0.0);
+    double logdet = 0.0;
+    for (int r = 0; r < d; ++r) {
+        for (int q = 0; q <= r; ++q) {
+            if (!std::isfinite(S[r * d + q]) || S[r * d + q] != S[q * d + r])
+                return fail(c, MDS_E_INVALID_ARG, "tree prior: Sigma must be finite and symmetric");
+            double v = S[r * d + q];
+            for (int k = 0; k < q; ++k) v -= Lc[r * d + k] * Lc[q * d + k];
+            if (r == q) {
+                if (!(v > 0.0)) return fail(c, MDS_E_INVALID_ARG, "tree prior: Sigma is not positive definite");
+                Lc[r * d + r] = std::sqrt(v);
+                logdet += 2.0 * std::log(Lc[r * d + r]);
+            } else {
+                Lc[r * d + q] = v / Lc[q * d + q];
+            }
+        }
+    }
+    for (int col = 0; col < d; ++col) {                    // Sigma^-1 e_col by two triangular solves
+        double z[TREE_DMAX];
+        for (int r = 0; r < d; ++r) {
+            double v = (r == col) ? 1.0 : 0.0;
+            for (int k = 0; k < r; ++k) v -= Lc[r * d + k] * z[k];
+            z[r] = v / Lc[r * d + r];
+        }
+        for (int r = d - 1; r >= 0; --r) {
+            double v = z[r];
+            for (int k = r + 1; k < d; ++k) v -= Lc[k * d + r] * Si[k * d + col];
+            Si[r * d + col] = v / Lc[r * d + r];
+        }
+    }
+    for (int q = 0; q < d; ++q)
+        if (mu0 && !std::isfinite(mu0[q])) return fail(c, MDS_E_INVALID_ARG, "tree prior: non-finite mu0");
+    // device buffers
+    if (c->d_tree_int) cudaFree(c->d_tree_int);
+    if (c->d_tree_dbl) cudaFree(c->d_tree_dbl);
+    c->d_tree_int = nullptr;
+    c->d_tree_dbl = nullptr;
+    c->tree = false;
+    std::vector<int> ints;
+    auto put = [&](const std::vector<int>& v) {
+        const size_t off = ints.size();
+        ints.insert(ints.end(), v.begin(), v.end());
+        return off;
+    };
+    const size_t o_chp = put(ch_ptr), o_chi = put(ch_idx), o_upp = put(up_ptr), o_upn = put(up_nodes),
+                 o_dnp = put(dn_ptr), o_dnn = put(dn_nodes), o_rt = put(roots);
+    const size_t nn = (size_t)n_nodes;
+    mds_status st;
+    if ((st = dalloc(c, &c->d_tree_int, std::max<size_t>(ints.size(), 1))) ||
+        (st = dalloc(c, &c->d_tree_dbl, nn * (3 + 2 * (size_t)d) + nn)) ||
+        (!c->d_gprior && (st = dalloc(c, &c->d_gprior, (size_t)c->npad * d))) ||
+        (!c->d_logprior && (st = dalloc(c, &c->d_logprior, 2))))
+        return st;
+    CK(cudaMemcpy(c->d_tree_int, ints.data(), ints.size() * sizeof(int), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(c->d_tree_dbl, t, nn * sizeof(double), cudaMemcpyHostToDevice));
+    CK(cudaMemset(c->d_gprior, 0, (size_t)c->npad * d * sizeof(double)));
+    TreeArgs& A = c->ta;
+    A = TreeArgs{};
+    A.n_nodes = (int)n_nodes;
+    A.n_items = (int)n;
+    A.ch_ptr = c->d_tree_int + o_chp;
+    A.ch_idx = c->d_tree_int + o_chi;
+    A.up_lvl_ptr = c->d_tree_int + o_upp;
+    A.up_lvl_nodes = c->d_tree_int + o_upn;
+    A.n_up = hmax;
+    A.dn_lvl_ptr = c->d_tree_int + o_dnp;
+    A.dn_lvl_nodes = c->d_tree_int + o_dnn;
+    A.n_dn = n_dn;
+    A.roots = c->d_tree_int + o_rt;
+    A.n_roots = (int)roots.size();
+    for (int q = 0; q < d; ++q) A.mu0[q] = mu0 ? mu0[q] : 0.0;
+    for (int q = 0; q < d * d; ++q) A.sinv[q] = Si[q];
+    A.logdet = logdet;
+    A.t = c->d_tree_dbl;
+    A.up_v = c->d_tree_dbl + nn;
+    A.out_v = c->d_tree_dbl + 2 * nn;
+    A.contrib = c->d_tree_dbl + 3 * nn;
+    A.up_m = c->d_tree_dbl + 4 * nn;
+    A.out_m = c->d_tree_dbl + 4 * nn + nn * d;
+    A.grad = c->d_gprior;
+    A.logp = c->d_logprior;
+    c->tree = true;
+    c->lf_version = 0;               // leapfrog state must be re-primed under the new prior
+    return MDS_OK;
+}
+
+mds_status mds_tree_prior(mds_ctx c, double* logp, double* grad) {
+    GUARD(c);
+    if (!c->tree) return fail(c, MDS_E_STATE, "no tree prior set (mds_set_tree_prior)");
+    if (!c->x_set) return fail(c, MDS_E_STATE, "locations not set");
+    TreeArgs ta = c->ta;
+    ta.x = c->d_x;
+    tree_prior_launch(ta, c->d, c->stream);
+    CK(cudaGetLastError());
+    if (logp) CK(cudaMemcpyAsync(logp, c->d_logprior, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    if (grad)
+        CK(cudaMemcpyAsync(grad, c->d_gprior, (size_t)c->n * c->d * sizeof(double), cudaMemcpyDeviceToHost,
+                           c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    c->lf_version = 0;     // d_gprior / d_logprior now belong to X, not to the leapfrog state
     return MDS_OK;
 }
 

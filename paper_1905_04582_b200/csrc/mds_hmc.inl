@@ -45,7 +45,9 @@ mds_status check_hmc_cfg(mds_ctx c, const mds_hmc_config* cfg) {
     return MDS_OK;
 }
 
-inline double inv_tau2_of(const mds_hmc_config* cfg) {
+// iid prior precision; 0 (unused) when a tree prior is set
+inline double inv_tau2_of(mds_ctx c, const mds_hmc_config* cfg) {
+    if (c->tree) return 0.0;
     return cfg->prior_sd > 0.0 ? 1.0 / (cfg->prior_sd * cfg->prior_sd) : 0.0;
 }
 
@@ -53,9 +55,15 @@ inline double inv_tau2_of(const mds_hmc_config* cfg) {
 mds_status hmc_prime(mds_ctx c, double eps, double inv_tau2, cudaStream_t s) {
     mds_status st = run_pass(c, c->d_x, c->d_grad, c->d_lik, false, 0.0, 0.0, s, false);
     if (st) return st;
+    if (c->tree) {                   // log prior and its gradient at x (tree prior)
+        TreeArgs ta = c->ta;
+        ta.x = c->d_x;
+        tree_prior_launch(ta, c->d, s);
+    }
     const int64_t m = c->n * c->d;
     prime_kernel<<<(unsigned)((m + 255) / 256), 256, 0, s>>>(c->d_grad, c->d_x, c->d_p, c->d_gl, c->d_xnext, m,
-                                                              inv_tau2, eps, 0.5 * eps);
+                                                              inv_tau2, c->tree ? c->d_gprior : nullptr, eps,
+                                                              0.5 * eps);
     CK(cudaGetLastError());
     c->lf_eps = eps;
     c->lf_inv_tau2 = inv_tau2;
@@ -81,7 +89,8 @@ mds_status hmc_enqueue_steps(mds_ctx c, int L, double eps, double inv_tau2, cuda
 }
 
 mds_status hmc_energy(mds_ctx c, double* out, double inv_tau2, cudaStream_t s) {
-    hamiltonian_kernel<<<1, 1024, 0, s>>>(c->d_x, c->d_p, c->d_lik, c->n * c->d, inv_tau2, out);
+    hamiltonian_kernel<<<1, 1024, 0, s>>>(c->d_x, c->d_p, c->d_lik, c->n * c->d, inv_tau2,
+                                          c->tree ? c->d_logprior : nullptr, out);
     CK(cudaGetLastError());
     return MDS_OK;
 }
@@ -111,7 +120,7 @@ mds_status mds_hmc_trajectory(mds_ctx c, const mds_hmc_config* cfg, const double
     cudaStream_t s = c->stream;
     const int64_t m = c->n * c->d;
     const size_t mbytes = (size_t)c->npad * c->d * sizeof(double);
-    const double it2 = inv_tau2_of(cfg);
+    const double it2 = inv_tau2_of(c, cfg);
     CK(cudaMemcpyAsync(c->d_xsave, c->d_x, mbytes, cudaMemcpyDeviceToDevice, s));
     CK(cudaMemcpyAsync(c->d_p, p0, m * sizeof(double), cudaMemcpyHostToDevice, s));
     st = hmc_prime(c, cfg->step_size, it2, s);
@@ -144,7 +153,7 @@ mds_status mds_leapfrog_device(mds_ctx c, const mds_hmc_config* cfg, const doubl
     if (st) return st;
     cudaStream_t s = c->stream;
     const int64_t m = c->n * c->d;
-    const double it2 = inv_tau2_of(cfg);
+    const double it2 = inv_tau2_of(c, cfg);
     if (p0_dev) CK(cudaMemcpyAsync(c->d_p, p0_dev, m * sizeof(double), cudaMemcpyDeviceToDevice, s));
     if (p0_dev || c->lf_version != c->version || c->lf_inv_tau2 != it2) {
         st = hmc_prime(c, cfg->step_size, it2, s);      // gl, log L at x; first drift
@@ -183,7 +192,7 @@ mds_status mds_hmc_run(mds_ctx c, const mds_hmc_config* cfg, double* x_inout, md
     cudaStream_t s = sg.s;
     const int64_t m = c->n * c->d;
     const size_t mbytes = (size_t)c->npad * c->d * sizeof(double);
-    const double it2 = inv_tau2_of(cfg);
+    const double it2 = inv_tau2_of(c, cfg);
     const int L = cfg->n_leapfrog;
     const double eps = cfg->step_size;
 
@@ -232,6 +241,8 @@ mds_status mds_hmc_run(mds_ctx c, const mds_hmc_config* cfg, double* x_inout, md
         if (!ce) ce = cudaMemcpyAsync(c->d_xsave, c->d_x, mbytes, cudaMemcpyDeviceToDevice, s);
         if (!ce) ce = cudaMemcpyAsync(c->d_glsave, c->d_gl, m * sizeof(double), cudaMemcpyDeviceToDevice, s);
         if (!ce) ce = cudaMemcpyAsync(c->d_liksave, c->d_lik, sizeof(double), cudaMemcpyDeviceToDevice, s);
+        if (!ce && c->tree)
+            ce = cudaMemcpyAsync(c->d_logprior + 1, c->d_logprior, sizeof(double), cudaMemcpyDeviceToDevice, s);
         if (ce) break;
         st = hmc_redrift(c, eps, s);         // xnext for the new momentum
         if (st) break;
@@ -260,6 +271,8 @@ mds_status mds_hmc_run(mds_ctx c, const mds_hmc_config* cfg, double* x_inout, md
             ce = cudaMemcpyAsync(c->d_x, c->d_xsave, mbytes, cudaMemcpyDeviceToDevice, s);
             if (!ce) ce = cudaMemcpyAsync(c->d_gl, c->d_glsave, m * sizeof(double), cudaMemcpyDeviceToDevice, s);
             if (!ce) ce = cudaMemcpyAsync(c->d_lik, c->d_liksave, sizeof(double), cudaMemcpyDeviceToDevice, s);
+            if (!ce && c->tree)
+                ce = cudaMemcpyAsync(c->d_logprior, c->d_logprior + 1, sizeof(double), cudaMemcpyDeviceToDevice, s);
             if (ce) break;
         }
     }

@@ -98,10 +98,11 @@ __global__ void zero_pairs_kernel(const T* __restrict__ y, const double* __restr
 // gl = g - x / tau^2 (grad log pi) and the first drift xnext = x + eps (p + eps/2 gl)
 __global__ void prime_kernel(const double* __restrict__ g, const double* __restrict__ x, const double* __restrict__ p,
                              double* __restrict__ gl, double* __restrict__ xnext, int64_t m, double inv_tau2,
+                             const double* __restrict__ gprior,
                              double eps, double heps) {
     int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (k < m) {
-        const double v = g[k] - x[k] * inv_tau2;
+        const double v = gprior ? g[k] + gprior[k] : g[k] - x[k] * inv_tau2;
         gl[k] = v;
         xnext[k] = drift(x[k], p[k], v, eps, heps);
     }
@@ -119,12 +120,12 @@ __global__ void redrift_kernel(const double* __restrict__ x, const double* __res
 __global__ void leapfrog_update_kernel(const double* __restrict__ g, const double* __restrict__ xe,
                                        double* __restrict__ x, double* __restrict__ p, double* __restrict__ gl,
                                        double* __restrict__ xnext, int64_t m, double eps, double heps,
-                                       double inv_tau2) {
+                                       double inv_tau2, const double* __restrict__ gprior) {
     int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (k < m) {
         const double xv = xe[k];
         const double ph = __fma_rn(heps, gl[k], p[k]);
-        const double gn = g[k] - xv * inv_tau2;
+        const double gn = gprior ? g[k] + gprior[k] : g[k] - xv * inv_tau2;
         const double pn = __fma_rn(heps, gn, ph);
         x[k] = xv;
         p[k] = pn;
@@ -137,6 +138,7 @@ __global__ void leapfrog_update_kernel(const double* __restrict__ g, const doubl
 // out[0] = H, out[1] = loglik, out[2] = kinetic
 __global__ void hamiltonian_kernel(const double* __restrict__ x, const double* __restrict__ p,
                                    const double* __restrict__ loglik, int64_t m, double inv_tau2,
+                                   const double* __restrict__ logprior,
                                    double* __restrict__ out) {
     __shared__ double sp[1024], sk[1024];
     double a = 0.0, kin = 0.0;
@@ -155,7 +157,7 @@ __global__ void hamiltonian_kernel(const double* __restrict__ x, const double* _
         __syncthreads();
     }
     if (threadIdx.x == 0) {
-        const double prior = -0.5 * sp[0] * inv_tau2;
+        const double prior = logprior ? logprior[0] : -0.5 * sp[0] * inv_tau2;
         const double K = 0.5 * sk[0];
         out[0] = -(loglik[0] + prior) + K;
         out[1] = loglik[0];

@@ -157,6 +157,7 @@ struct PassArgs {
     double* gl;
     double* xnext;
     double eps, heps, inv_tau2;
+    const double* gprior;        // LEAPFROG: d log prior / dX at xeval (tree prior), or NULL = iid N(0, 1/inv_tau2)
     int vpw;                     // virtual unit ranges per warp (warp_seg has GW * vpw + 1 entries)
     int epl;                     // phase B: slab elements per lane (1, 2 or 4)
     SigmaParams P;
@@ -528,7 +529,7 @@ pass_kernel(PassArgs a) {
                         // leapfrog: the pass ran at xnext = x + eps (p + eps/2 gl)
                         const double xe = pre_xe;
                         const double ph = __fma_rn(a.heps, pre_gl, pre_p);    // first half-kick
-                        const double gn = g - xe * a.inv_tau2;                  // grad log pi at xnext
+                        const double gn = a.gprior ? g + a.gprior[e] : g - xe * a.inv_tau2;   // grad log pi at xnext
                         const double pn = __fma_rn(a.heps, gn, ph);             // second half-kick
                         a.grad[e] = g;
                         a.x[e] = xe;

@@ -1,0 +1,61 @@
+// mds_tree.cuh -- phylogenetic Brownian-diffusion prior of X (SURVEY 8(f)
+// NEXT-2; Eq. 3) and its gradient, in O(N D^2).
+//
+// X ~ MN(mu0, V_G, Sigma): tips of a forest evolve by Brownian motion with
+// covariance t_c Sigma along each branch; tree roots are N(mu0, tau0 Sigma),
+// unsequenced items are single-node trees N(mu0, tau_e Sigma).  Instead of
+// forming V_G^-1 (O(N^3)) the prior follows the dynamic program the paper
+// cites: a post-order pass absorbs the children's messages
+// (m, v) -- "the tips below are N(m; x_node, v Sigma)" -- contrast by contrast,
+//   delta = a_i - A, w = W + w_i:  log p += -1/2 delta' Sigma^-1 delta / w
+//                                          - D/2 log(2 pi w) - 1/2 log|Sigma|
+//   A <- (w_i A + W a_i)/w,  W <- W w_i / w,
+// and a root contrast against mu0 with variance v_root + tau_root (N contrasts
+// in all).  A pre-order pass forms each node's outside message (the law of
+// x_node given every tip NOT below it); for tip i that is the conditional law
+// N(m_i, v_i Sigma) of x_i given all other tips, so
+//   d log p / d x_i = - Sigma^-1 (x_i - m_i) / v_i        ([V^-1 (X - mu0) Sigma^-1]_i).
+// One CTA of 1024 threads walks the levels (nodes of equal height / depth in
+// parallel, __syncthreads between levels); the node contributions are summed
+// in a fixed order: deterministic, no atomics.
+#pragma once
+#include <cstdint>
+
+namespace mdsk {
+
+constexpr int TREE_DMAX = 8;
+
+struct TreeArgs {
+    // forest (device): node k < n is item k
+    int n_nodes;
+    int n_items;
+    const int* ch_ptr;        // [n_nodes + 1] children CSR (ascending child index)
+    const int* ch_idx;
+    const double* t;          // [n_nodes] branch length (roots: prior variance factor)
+    const int* up_lvl_ptr;    // [n_up + 1] post-order levels: internal nodes by height 1, 2, ...
+    const int* up_lvl_nodes;
+    int n_up;
+    const int* dn_lvl_ptr;    // [n_dn + 1] pre-order levels: nodes with children, by depth 0, 1, ...
+    const int* dn_lvl_nodes;
+    int n_dn;
+    const int* roots;         // [n_roots]
+    int n_roots;
+    // parameters
+    double mu0[TREE_DMAX];
+    double sinv[TREE_DMAX * TREE_DMAX];   // Sigma^-1 (row-major)
+    double logdet;                        // log |Sigma|
+    // state / scratch
+    const double* x;          // positions (n_pad x D)
+    double* up_m;             // [n_nodes][D]
+    double* up_v;             // [n_nodes]
+    double* out_m;            // [n_nodes][D]
+    double* out_v;            // [n_nodes]
+    double* contrib;          // [n_nodes] log-density contrasts absorbed at each node
+    // outputs
+    double* grad;             // [n_items][D]  d log p / d X
+    double* logp;             // [1]
+};
+
+void tree_prior_launch(const TreeArgs& a, int d, cudaStream_t s);
+
+}  // namespace mdsk

@@ -130,3 +130,42 @@ def unpack_lower(y_packed: np.ndarray, n: int) -> np.ndarray:
     full[il, jl] = y_packed
     full[jl, il] = y_packed
     return full
+
+
+def coalescent_forest(n: int, n_trees: int = 1, frac_unsequenced: float = 0.0, seed: int = BASE_SEED,
+                      tau0: float = 1.0, tau_e: float = 4.0, theta: float = 1.0):
+    """Synthetic phylogeny input for the Brownian-diffusion prior:
+    the n items are split into n_trees Kingman-coalescent trees plus a fraction of
+    unsequenced items.  Node k < n is item k (a tip); internal nodes are numbered
+    from n up.  Returns (parent, t): parent[k] = -1 for roots; t[k] = branch length
+    to the parent, or the root's prior variance factor for roots (tau0 for tree
+    roots, tau_e for unsequenced items).  Input generation only (no method
+    arithmetic); every tree is binary with strictly positive branch lengths."""
+    rng = np.random.default_rng(seed)
+    items = rng.permutation(n)
+    n_un = int(round(frac_unsequenced * n))
+    unseq, seq = items[:n_un], items[n_un:]
+    groups = [g for g in np.array_split(seq, n_trees) if g.size > 0]
+    parent = list(np.full(n, -1, dtype=np.int64))
+    t = list(np.zeros(n))
+    height = list(np.zeros(n))
+    for i in unseq:
+        t[i] = tau_e
+    for g in groups:
+        lineages = [int(v) for v in g]
+        time = 0.0
+        while len(lineages) > 1:
+            k = len(lineages)
+            time += rng.exponential(theta / (k * (k - 1) / 2.0)) + 1e-9
+            a, b = rng.choice(k, size=2, replace=False)
+            ca, cb = lineages[a], lineages[b]
+            node = len(parent)
+            parent.append(-1)
+            t.append(0.0)
+            height.append(time)
+            for c in (ca, cb):
+                parent[c] = node
+                t[c] = time - height[c]
+            lineages = [v for q, v in enumerate(lineages) if q not in (a, b)] + [node]
+        t[lineages[0]] = tau0
+    return np.array(parent, dtype=np.int64), np.array(t, dtype=np.float64)
