@@ -996,6 +996,11 @@ mds_status mds_set_tree_prior(mds_ctx c, int64_t n_nodes, const int64_t* parent,
         dn_ptr[(size_t)dd + 1] = (int)dn_nodes.size();
     }
     const int n_dn = dn_nodes.empty() ? 0 : dmax + 1;
+    // narrow levels (<= 32 nodes) near the roots run on one warp
+    int up_narrow = hmax;
+    while (up_narrow > 0 && up_ptr[(size_t)up_narrow] - up_ptr[(size_t)up_narrow - 1] <= 32) --up_narrow;
+    int dn_narrow = 0;
+    while (dn_narrow < n_dn && dn_ptr[(size_t)dn_narrow + 1] - dn_ptr[(size_t)dn_narrow] <= 32) ++dn_narrow;
     // Sigma^-1 and log|Sigma| by Cholesky (d <= 8; parameter preprocessing, like SigmaParams)
     double S[TREE_DMAX * TREE_DMAX], Lc[TREE_DMAX * TREE_DMAX] = {0}, Si[TREE_DMAX * TREE_DMAX] = {0};
     for (int r = 0; r < d; ++r)
@@ -1048,7 +1053,7 @@ mds_status mds_set_tree_prior(mds_ctx c, int64_t n_nodes, const int64_t* parent,
     const size_t nn = (size_t)n_nodes;
     mds_status st;
     if ((st = dalloc(c, &c->d_tree_int, std::max<size_t>(ints.size(), 1))) ||
-        (st = dalloc(c, &c->d_tree_dbl, nn * (3 + 2 * (size_t)d) + nn)) ||
+        (st = dalloc(c, &c->d_tree_dbl, nn * (4 + (size_t)d) + (nn - (size_t)n) * (d + 1))) ||
         (!c->d_gprior && (st = dalloc(c, &c->d_gprior, (size_t)c->npad * d))) ||
         (!c->d_logprior && (st = dalloc(c, &c->d_logprior, 2))))
         return st;
@@ -1072,17 +1077,42 @@ mds_status mds_set_tree_prior(mds_ctx c, int64_t n_nodes, const int64_t* parent,
     for (int q = 0; q < d; ++q) A.mu0[q] = mu0 ? mu0[q] : 0.0;
     for (int q = 0; q < d * d; ++q) A.sinv[q] = Si[q];
     A.logdet = logdet;
+    A.up_narrow = up_narrow;
+    A.dn_narrow = dn_narrow;
     A.t = c->d_tree_dbl;
-    A.up_v = c->d_tree_dbl + nn;
-    A.out_v = c->d_tree_dbl + 2 * nn;
-    A.contrib = c->d_tree_dbl + 3 * nn;
-    A.up_m = c->d_tree_dbl + 4 * nn;
-    A.out_m = c->d_tree_dbl + 4 * nn + nn * d;
+    A.pw = c->d_tree_dbl + nn;
+    A.cq = c->d_tree_dbl + 2 * nn;
+    A.cw = c->d_tree_dbl + 3 * nn;
+    A.up_m = c->d_tree_dbl + 4 * nn;                        // (nn - n) x d
+    A.msg = c->d_tree_dbl + 4 * nn + (nn - (size_t)n) * d;  // (nn - n) x (d + 1)
+    {
+        const size_t need = (nn - (size_t)n) * (d + 1) * sizeof(double);
+        A.smem = need <= TREE_SMEM_MAX ? std::max<size_t>(need, 16) : 0;
+    }
     A.grad = c->d_gprior;
     A.logp = c->d_logprior;
+    const char* pe = std::getenv("MDS_PROFILE_TREE");
+    if (pe && pe[0] == '1') {
+        static unsigned long long* prof = nullptr;
+        if (!prof) cudaMalloc(&prof, 256 * sizeof(unsigned long long));
+        cudaMemset(prof, 0, 256 * sizeof(unsigned long long));
+        A.prof = prof;
+        fprintf(stderr, "tree levels: up %d (narrow from %d), dn %d (narrow below %d)\n", hmax, up_narrow, n_dn,
+                dn_narrow);
+    }
     c->tree = true;
     c->lf_version = 0;               // leapfrog state must be re-primed under the new prior
     return MDS_OK;
+}
+
+void report_tree_profile(mds_ctx c) {
+    if (!c->ta.prof) return;
+    unsigned long long h[256];
+    cudaMemcpy(h, c->ta.prof, sizeof(h), cudaMemcpyDeviceToHost);
+    fprintf(stderr, "tree us:");
+    for (int k = 1; k < 256; ++k)
+        if (h[k]) fprintf(stderr, " %d:%.2f", k, (h[k] - h[0]) * 1e-3);
+    fprintf(stderr, "\n");
 }
 
 mds_status mds_tree_prior(mds_ctx c, double* logp, double* grad) {
@@ -1098,6 +1128,7 @@ mds_status mds_tree_prior(mds_ctx c, double* logp, double* grad) {
         CK(cudaMemcpyAsync(grad, c->d_gprior, (size_t)c->n * c->d * sizeof(double), cudaMemcpyDeviceToHost,
                            c->stream));
     CK(cudaStreamSynchronize(c->stream));
+    report_tree_profile(c);
     c->lf_version = 0;     // d_gprior / d_logprior now belong to X, not to the leapfrog state
     return MDS_OK;
 }

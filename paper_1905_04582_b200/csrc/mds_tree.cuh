@@ -15,18 +15,28 @@
 // x_node given every tip NOT below it); for tip i that is the conditional law
 // N(m_i, v_i Sigma) of x_i given all other tips, so
 //   d log p / d x_i = - Sigma^-1 (x_i - m_i) / v_i        ([V^-1 (X - mu0) Sigma^-1]_i).
-// One CTA of 1024 threads walks the levels (nodes of equal height / depth in
-// parallel, __syncthreads between levels); the node contributions are summed
-// in a fixed order: deterministic, no atomics.
+//
+// One CTA walks the levels (nodes of equal height / depth in parallel).  The
+// pass is latency-bound (26 + 26 levels at C2), so the level critical path is
+// kept on chip: the messages of INTERNAL nodes (the only dynamic state) live in
+// shared memory when they fit ((n_nodes - n) (D + 1) doubles; else a global
+// buffer), every static operand of a level (child ids, branch lengths, tip x,
+// the siblings' up messages in the pre-order) is fetched before the barrier
+// that publishes the previous level, the narrow levels near the roots run on
+// warp 0 alone with __syncwarp, one division per contrast, and the logs of the
+// contrast variances are deferred to the final parallel reduction.  Tip
+// gradients are written as the pre-order reaches them.  Node contributions are
+// summed in a fixed order: deterministic, no atomics.
 #pragma once
 #include <cstdint>
+#include <cstddef>
 
 namespace mdsk {
 
 constexpr int TREE_DMAX = 8;
 
 struct TreeArgs {
-    // forest (device): node k < n is item k
+    // forest (device): node k < n is item k; internal node k has slot k - n
     int n_nodes;
     int n_items;
     const int* ch_ptr;        // [n_nodes + 1] children CSR (ascending child index)
@@ -35,9 +45,11 @@ struct TreeArgs {
     const int* up_lvl_ptr;    // [n_up + 1] post-order levels: internal nodes by height 1, 2, ...
     const int* up_lvl_nodes;
     int n_up;
+    int up_narrow;            // first post-order level from which every level has <= 32 nodes
     const int* dn_lvl_ptr;    // [n_dn + 1] pre-order levels: nodes with children, by depth 0, 1, ...
     const int* dn_lvl_nodes;
     int n_dn;
+    int dn_narrow;            // pre-order levels [0, dn_narrow) all have <= 32 nodes
     const int* roots;         // [n_roots]
     int n_roots;
     // parameters
@@ -46,16 +58,19 @@ struct TreeArgs {
     double logdet;                        // log |Sigma|
     // state / scratch
     const double* x;          // positions (n_pad x D)
-    double* up_m;             // [n_nodes][D]
-    double* up_v;             // [n_nodes]
-    double* out_m;            // [n_nodes][D]
-    double* out_v;            // [n_nodes]
-    double* contrib;          // [n_nodes] log-density contrasts absorbed at each node
+    double* up_m;             // [n_nodes - n][D]  up message means of internal nodes (global copy)
+    double* pw;               // [n_nodes]         1 / (up_v + t): each up message's precision at its parent
+    double* msg;              // [(n_nodes - n) (D + 1)] internal-node messages when they do not fit smem
+    size_t smem;              // dynamic shared memory for the messages (0 = use msg)
+    double* cq;               // [n_nodes] -1/2 sum delta' Sigma^-1 delta / w - (#contrasts)(D log 2pi + log|Sigma|)/2
+    double* cw;               // [n_nodes] product of the node's contrast variances w (log taken at the end)
     // outputs
     double* grad;             // [n_items][D]  d log p / d X
     double* logp;             // [1]
+    unsigned long long* prof; // optional (MDS_PROFILE_TREE=1): globaltimer stamps per level
 };
 
+constexpr size_t TREE_SMEM_MAX = 200 * 1024;
 void tree_prior_launch(const TreeArgs& a, int d, cudaStream_t s);
 
 }  // namespace mdsk

@@ -94,6 +94,30 @@ def test_tree_prior_parity(mds, n, d, ntrees, fu, multi):
     assert lp == lp2 and np.array_equal(g, g2)        # deterministic
 
 
+def test_tree_prior_high_arity(mds):
+    """A star tree (one internal node with 400 children, short branches) and a
+    caterpillar (depth n - 1): extreme arity and depth."""
+    n, d = 400, 2
+    rng = np.random.default_rng(9)
+    star_p = np.array([n] * n + [-1])
+    star_t = np.concatenate([1e-3 + 1e-2 * rng.random(n), [2.0]])
+    cat_p = np.empty(2 * n - 1, np.int64)
+    cat_t = 0.05 + rng.random(2 * n - 1)
+    # internal node n + k joins item k + 1 and the subtree below n + k - 1 (n + 0 joins items 0, 1)
+    cat_p[0] = n
+    for k in range(n - 1):
+        cat_p[k + 1] = n + k
+        cat_p[n + k] = n + k + 1 if k < n - 2 else -1
+    for parent, t in ((star_p, star_t), (cat_p, cat_t)):
+        x = sample_prior(parent, t, n, d, np.zeros(d), np.eye(d), rng)
+        ref_lp, ref_g = tree.tree_prior(parent, t, x)
+        with mds.MDS(n, d) as c:
+            c.set_locations(x)
+            c.set_tree_prior(parent, t)
+            lp, g = c.tree_prior()
+        check(lp, g, ref_lp, ref_g)
+
+
 def test_tree_prior_c2_size(mds):
     n, d = 5392, 2
     parent, t = workload.coalescent_forest(n, 1, 0.0, seed=11)
