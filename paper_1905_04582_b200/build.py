@@ -43,27 +43,37 @@ def stale() -> bool:
     return any(os.path.getmtime(p) > t for p in deps())
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not stale():
+def build(force: bool = False, verbose: bool = False, extra=(), out: str | None = None) -> str:
+    """extra: additional nvcc flags (A/B variants, e.g. -DMDS_NO_FIRST_SPLIT) built to `out`."""
+    lib = out or LIB
+    if not force and not extra and out is None and not stale():
         return LIB
-    os.makedirs(OBJ, exist_ok=True)
+    objdir = OBJ if not extra else OBJ + "_" + "_".join(f.strip("-").replace("=", "") for f in extra)
+    os.makedirs(objdir, exist_ok=True)
     srcs = sources()
-    objs = [os.path.join(OBJ, os.path.basename(s)[:-3] + ".o") for s in srcs]
+    objs = [os.path.join(objdir, os.path.basename(s)[:-3] + ".o") for s in srcs]
 
     def compile_one(so):
         src, obj = so
-        cmd = [NVCC, *FLAGS, *(["-Xptxas", "-v"] if verbose else []), "-c", "-o", obj, src]
+        cmd = [NVCC, *FLAGS, *extra, *(["-Xptxas", "-v"] if verbose else []), "-c", "-o", obj, src]
         subprocess.check_call(cmd)
 
     with ThreadPoolExecutor(max_workers=max(1, min(len(srcs), os.cpu_count() or 1))) as ex:
         list(ex.map(compile_one, zip(srcs, objs)))
-    tmp = LIB + ".tmp%d" % os.getpid()
+    tmp = lib + ".tmp%d" % os.getpid()
     subprocess.check_call([NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-cudart", "static",
                            "-o", tmp, *objs])
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose="-v" in sys.argv)
-    print(LIB)
+    # python build.py [--force] [-v] [--variant NAME -DFLAG ...]  (variant -> libmds_ab_NAME.so)
+    args = sys.argv[1:]
+    if "--variant" in args:
+        k = args.index("--variant")
+        name, flags = args[k + 1], [a for a in args[k + 2:] if a.startswith("-D")]
+        print(build(force=True, extra=flags, out=os.path.join(HERE, "libmds_ab_%s.so" % name)))
+    else:
+        build(force="--force" in args, verbose="-v" in args)
+        print(LIB)

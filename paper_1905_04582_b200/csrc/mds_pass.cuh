@@ -549,8 +549,15 @@ pass_kernel(PassArgs a) {
         if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) *a.lik = __longlong_as_double(0x7ff8000000000000LL);
     } else if (blockIdx.x == gridDim.x - 1) {
         const int GW = gridDim.x * WPC;
+        // 4 partials per thread per round: the loads are in flight together
         A s = A(0);
-        for (int q = threadIdx.x; q < GW; q += WPC * 32) s += a.likpart[q];
+        for (int q0 = threadIdx.x; q0 < GW; q0 += 4 * WPC * 32) {
+            A v[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) v[u] = q0 + u * WPC * 32 < GW ? a.likpart[q0 + u * WPC * 32] : A(0);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) s += v[u];
+        }
         red[0][warp][lane] = s;
         __syncthreads();
         if (threadIdx.x < 32) {
