@@ -984,16 +984,21 @@ mds_status mds_set_tree_prior(mds_ctx c, int64_t n_nodes, const int64_t* parent,
         hmax = std::max(hmax, height[(size_t)k]);
         if (nch[(size_t)k]) dmax = std::max(dmax, depth[(size_t)k]);
     }
+    // levels by counting sort (ascending node index inside a level)
     std::vector<int> up_ptr((size_t)hmax + 1, 0), up_nodes, dn_ptr((size_t)dmax + 2, 0), dn_nodes;
-    for (int h = 1; h <= hmax; ++h) {
-        for (int64_t k = n; k < n_nodes; ++k)
-            if (height[(size_t)k] == h) up_nodes.push_back((int)k);
-        up_ptr[(size_t)h] = (int)up_nodes.size();
-    }
-    for (int dd = 0; dd <= dmax; ++dd) {
+    for (int64_t k = n; k < n_nodes; ++k) ++up_ptr[(size_t)height[(size_t)k]];       // height >= 1
+    for (int64_t k = 0; k < n_nodes; ++k)
+        if (nch[(size_t)k]) ++dn_ptr[(size_t)depth[(size_t)k] + 1];
+    up_ptr[0] = 0;
+    for (int h = 1; h <= hmax; ++h) up_ptr[(size_t)h] += up_ptr[(size_t)h - 1];
+    for (int dd = 1; dd <= dmax + 1; ++dd) dn_ptr[(size_t)dd] += dn_ptr[(size_t)dd - 1];
+    up_nodes.assign((size_t)up_ptr[(size_t)hmax], 0);
+    dn_nodes.assign((size_t)dn_ptr[(size_t)dmax + 1], 0);
+    {
+        std::vector<int> fu(up_ptr.begin(), up_ptr.end() - 1), fd(dn_ptr.begin(), dn_ptr.end() - 1);
+        for (int64_t k = n; k < n_nodes; ++k) up_nodes[(size_t)fu[(size_t)height[(size_t)k] - 1]++] = (int)k;
         for (int64_t k = 0; k < n_nodes; ++k)
-            if (nch[(size_t)k] && depth[(size_t)k] == dd) dn_nodes.push_back((int)k);
-        dn_ptr[(size_t)dd + 1] = (int)dn_nodes.size();
+            if (nch[(size_t)k]) dn_nodes[(size_t)fd[(size_t)depth[(size_t)k]]++] = (int)k;
     }
     const int n_dn = dn_nodes.empty() ? 0 : dmax + 1;
     // narrow levels (<= 32 nodes) near the roots run on one warp
@@ -1042,23 +1047,59 @@ mds_status mds_set_tree_prior(mds_ctx c, int64_t n_nodes, const int64_t* parent,
     c->d_tree_int = nullptr;
     c->d_tree_dbl = nullptr;
     c->tree = false;
+    // level-ordered entries: post-order (internal nodes by height), pre-order
+    // (nodes with children by depth), and each child's slot in its parent's
+    // pre-order entry
+    const size_t nn = (size_t)n_nodes;
+    const size_t E_up = up_nodes.size(), E_dn = dn_nodes.size();
+    std::vector<int> up_e(4 * E_up), dn_e(4 * E_dn), dn_pos(nn, -1);
+    std::vector<double> up_t(2 * E_up, 0.0), dn_t(2 * E_dn, 0.0);
+    for (size_t e = 0; e < E_up; ++e) {
+        const int v = up_nodes[e], c0 = ch_ptr[(size_t)v], k = ch_ptr[(size_t)v + 1] - c0;
+        up_e[4 * e] = v - (int)n;
+        for (int i = 0; i < 2; ++i) {
+            const int ch = i < k ? ch_idx[(size_t)c0 + i] : -1;
+            up_e[4 * e + 1 + i] = ch < 0 ? 0 : (ch < n ? -1 - ch : ch - (int)n);
+            up_t[2 * e + i] = ch < 0 ? 0.0 : t[ch];
+        }
+        up_e[4 * e + 3] = k;
+    }
+    for (size_t e = 0; e < E_dn; ++e) {
+        const int v = dn_nodes[e], c0 = ch_ptr[(size_t)v], k = ch_ptr[(size_t)v + 1] - c0;
+        dn_e[4 * e] = v - (int)n;
+        for (int i = 0; i < 2; ++i) {
+            const int ch = i < k ? ch_idx[(size_t)c0 + i] : -1;
+            dn_e[4 * e + 1 + i] = ch < 0 ? 0 : ch;
+            dn_t[2 * e + i] = ch < 0 ? 0.0 : t[ch];
+            if (ch >= 0) dn_pos[(size_t)ch] = (int)(2 * e + i);
+        }
+        dn_e[4 * e + 3] = k;
+    }
     std::vector<int> ints;
-    auto put = [&](const std::vector<int>& v) {
+    auto put = [&](const std::vector<int>& v) {     // 16-byte aligned offsets (int4 views)
+        while (ints.size() % 4) ints.push_back(0);
         const size_t off = ints.size();
         ints.insert(ints.end(), v.begin(), v.end());
         return off;
     };
-    const size_t o_chp = put(ch_ptr), o_chi = put(ch_idx), o_upp = put(up_ptr), o_upn = put(up_nodes),
-                 o_dnp = put(dn_ptr), o_dnn = put(dn_nodes), o_rt = put(roots);
-    const size_t nn = (size_t)n_nodes;
+    const size_t o_upe = put(up_e), o_dne = put(dn_e), o_chp = put(ch_ptr), o_chi = put(ch_idx), o_upp = put(up_ptr),
+                 o_dnp = put(dn_ptr), o_rt = put(roots), o_pos = put(dn_pos);
+    // doubles: t | pw | cq | cw | up_t | dn_t | up_m | dn_sib | msg   (16-byte aligned pieces)
+    auto al2 = [](size_t v) { return (v + 1) & ~(size_t)1; };
+    const size_t o_t = 0, o_pw = al2(o_t + nn), o_cq = al2(o_pw + nn), o_cw = al2(o_cq + nn), o_upt = al2(o_cw + nn),
+                 o_dnt = al2(o_upt + 2 * E_up), o_upm = al2(o_dnt + 2 * E_dn), o_sib = al2(o_upm + (nn - n) * d), o_msg = al2(o_sib + 2 * E_dn * (d + 1)),
+                 n_dbl = al2(o_msg + (nn - n) * (d + 1));
     mds_status st;
     if ((st = dalloc(c, &c->d_tree_int, std::max<size_t>(ints.size(), 1))) ||
-        (st = dalloc(c, &c->d_tree_dbl, nn * (4 + (size_t)d) + (nn - (size_t)n) * (d + 1))) ||
+        (st = dalloc(c, &c->d_tree_dbl, n_dbl)) ||
         (!c->d_gprior && (st = dalloc(c, &c->d_gprior, (size_t)c->npad * d))) ||
         (!c->d_logprior && (st = dalloc(c, &c->d_logprior, 2))))
         return st;
     CK(cudaMemcpy(c->d_tree_int, ints.data(), ints.size() * sizeof(int), cudaMemcpyHostToDevice));
-    CK(cudaMemcpy(c->d_tree_dbl, t, nn * sizeof(double), cudaMemcpyHostToDevice));
+    CK(cudaMemset(c->d_tree_dbl, 0, n_dbl * sizeof(double)));
+    CK(cudaMemcpy(c->d_tree_dbl + o_t, t, nn * sizeof(double), cudaMemcpyHostToDevice));
+    if (E_up) CK(cudaMemcpy(c->d_tree_dbl + o_upt, up_t.data(), up_t.size() * sizeof(double), cudaMemcpyHostToDevice));
+    if (E_dn) CK(cudaMemcpy(c->d_tree_dbl + o_dnt, dn_t.data(), dn_t.size() * sizeof(double), cudaMemcpyHostToDevice));
     CK(cudaMemset(c->d_gprior, 0, (size_t)c->npad * d * sizeof(double)));
     TreeArgs& A = c->ta;
     A = TreeArgs{};
@@ -1066,25 +1107,29 @@ mds_status mds_set_tree_prior(mds_ctx c, int64_t n_nodes, const int64_t* parent,
     A.n_items = (int)n;
     A.ch_ptr = c->d_tree_int + o_chp;
     A.ch_idx = c->d_tree_int + o_chi;
+    A.t = c->d_tree_dbl + o_t;
     A.up_lvl_ptr = c->d_tree_int + o_upp;
-    A.up_lvl_nodes = c->d_tree_int + o_upn;
+    A.up_e = reinterpret_cast<const int4*>(c->d_tree_int + o_upe);
+    A.up_t = reinterpret_cast<const double2*>(c->d_tree_dbl + o_upt);
     A.n_up = hmax;
+    A.up_narrow = up_narrow;
     A.dn_lvl_ptr = c->d_tree_int + o_dnp;
-    A.dn_lvl_nodes = c->d_tree_int + o_dnn;
+    A.dn_e = reinterpret_cast<const int4*>(c->d_tree_int + o_dne);
+    A.dn_t = reinterpret_cast<const double2*>(c->d_tree_dbl + o_dnt);
+    A.dn_sib = c->d_tree_dbl + o_sib;
+    A.dn_pos = c->d_tree_int + o_pos;
     A.n_dn = n_dn;
+    A.dn_narrow = dn_narrow;
     A.roots = c->d_tree_int + o_rt;
     A.n_roots = (int)roots.size();
     for (int q = 0; q < d; ++q) A.mu0[q] = mu0 ? mu0[q] : 0.0;
     for (int q = 0; q < d * d; ++q) A.sinv[q] = Si[q];
     A.logdet = logdet;
-    A.up_narrow = up_narrow;
-    A.dn_narrow = dn_narrow;
-    A.t = c->d_tree_dbl;
-    A.pw = c->d_tree_dbl + nn;
-    A.cq = c->d_tree_dbl + 2 * nn;
-    A.cw = c->d_tree_dbl + 3 * nn;
-    A.up_m = c->d_tree_dbl + 4 * nn;                        // (nn - n) x d
-    A.msg = c->d_tree_dbl + 4 * nn + (nn - (size_t)n) * d;  // (nn - n) x (d + 1)
+    A.pw = c->d_tree_dbl + o_pw;
+    A.cq = c->d_tree_dbl + o_cq;
+    A.cw = c->d_tree_dbl + o_cw;
+    A.up_m = c->d_tree_dbl + o_upm;
+    A.msg = c->d_tree_dbl + o_msg;
     {
         const size_t need = (nn - (size_t)n) * (d + 1) * sizeof(double);
         A.smem = need <= TREE_SMEM_MAX ? std::max<size_t>(need, 16) : 0;

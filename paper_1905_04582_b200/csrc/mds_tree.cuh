@@ -20,11 +20,14 @@
 // pass is latency-bound (26 + 26 levels at C2), so the level critical path is
 // kept on chip: the messages of INTERNAL nodes (the only dynamic state) live in
 // shared memory when they fit ((n_nodes - n) (D + 1) doubles; else a global
-// buffer), every static operand of a level (child ids, branch lengths, tip x,
-// the siblings' up messages in the pre-order) is fetched before the barrier
-// that publishes the previous level, the narrow levels near the roots run on
-// warp 0 alone with __syncwarp, one division per contrast, and the logs of the
-// contrast variances are deferred to the final parallel reduction.  Tip
+// buffer); the static operands of every level are laid out level by level
+// (one int4 + one double2 per node, the tip children's x and, for the
+// pre-order, the children's up messages gathered by wide parallel passes), so
+// a level's operands are one coalesced round of loads issued before the
+// barrier that publishes the previous level -- and one level ahead on the
+// narrow levels near the roots, which run on warp 0 alone with __syncwarp; one
+// division per contrast; the logs of the contrast variances are deferred to the
+// final parallel reduction.  Tip
 // gradients are written as the pre-order reaches them.  Node contributions are
 // summed in a fixed order: deterministic, no atomics.
 #pragma once
@@ -39,15 +42,21 @@ struct TreeArgs {
     // forest (device): node k < n is item k; internal node k has slot k - n
     int n_nodes;
     int n_items;
-    const int* ch_ptr;        // [n_nodes + 1] children CSR (ascending child index)
+    const int* ch_ptr;        // [n_nodes + 1] children CSR (ascending child index; arity > 2 only)
     const int* ch_idx;
     const double* t;          // [n_nodes] branch length (roots: prior variance factor)
-    const int* up_lvl_ptr;    // [n_up + 1] post-order levels: internal nodes by height 1, 2, ...
-    const int* up_lvl_nodes;
+    // post-order entries (internal nodes by height), level L = [up_lvl_ptr[L], up_lvl_ptr[L+1])
+    const int* up_lvl_ptr;    // [n_up + 1]
+    const int4* up_e;         // {slot, src0, src1, k}; src = internal slot, or -1 - item for a tip
+    const double2* up_t;      // {t(child 0), t(child 1)}
     int n_up;
     int up_narrow;            // first post-order level from which every level has <= 32 nodes
-    const int* dn_lvl_ptr;    // [n_dn + 1] pre-order levels: nodes with children, by depth 0, 1, ...
-    const int* dn_lvl_nodes;
+    // pre-order entries (nodes with children by depth)
+    const int* dn_lvl_ptr;    // [n_dn + 1]
+    const int4* dn_e;         // {slot, child 0, child 1, k} (children as node ids)
+    const double2* dn_t;      // {t(child 0), t(child 1)}
+    double* dn_sib;           // [E_dn][2][D + 1] up message (mean, precision at the parent) of children 0/1
+    const int* dn_pos;        // [n_nodes] 2 e + i for child i < 2 of pre-order entry e, else -1
     int n_dn;
     int dn_narrow;            // pre-order levels [0, dn_narrow) all have <= 32 nodes
     const int* roots;         // [n_roots]
