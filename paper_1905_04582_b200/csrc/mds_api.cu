@@ -42,6 +42,7 @@ struct mds_ctx_s {
 
     // persistent-pass schedule
     int grid = 0;                    // resident CTAs of the pass kernel
+    int pair_ctas = 0;               // of which run phase A (grid - 1 with a tree prior: the last walks the tree)
     int wpc = 0;                     // its warps per CTA
     size_t smem = 0;                 // its dynamic shared memory
     int nseg = 0;
@@ -200,7 +201,9 @@ PassKernel pass_fn_mode(int mode, int prec, int trunc, int d) {
         case MODE_EVAL_NOLIK: return f ? pass_m1_f64(trunc, d) : pass_m1_f32(trunc, d);
         case MODE_LEAPFROG: return f ? pass_m2_f64(trunc, d) : pass_m2_f32(trunc, d);
         case MODE_LEAPFROG_NOLIK: return f ? pass_m3_f64(trunc, d) : pass_m3_f32(trunc, d);
-        default: return f ? pass_m4_f64(trunc, d) : pass_m4_f32(trunc, d);
+        case MODE_LIK: return f ? pass_m4_f64(trunc, d) : pass_m4_f32(trunc, d);
+        case MODE_LEAPFROG_TREE: return f ? pass_m5_f64(trunc, d) : pass_m5_f32(trunc, d);
+        default: return f ? pass_m6_f64(trunc, d) : pass_m6_f32(trunc, d);
     }
 }
 
@@ -229,6 +232,7 @@ PassArgs base_args(mds_ctx c, const double* xeval) {
     a.n = c->n;
     a.slabs = c->d_slabs;
     a.likpart = c->d_likpart;
+    a.pair_ctas = c->pair_ctas;
     a.P = c->P;
     a.prof = c->d_prof;
     return a;
@@ -268,10 +272,13 @@ mds_status run_pass(mds_ctx c, const double* xeval, double* grad_out, double* li
     a.gl = c->d_gl;
     a.xnext = c->d_xnext;
     if (lf && c->tree) {
-        // d log prior / dX at the point this pass evaluates (consumed by the leapfrog update)
-        TreeArgs ta = c->ta;
-        ta.x = xeval;
-        tree_prior_launch(ta, c->d, s);
+        // d log prior / dX at the point this pass evaluates, walked by the pass
+        // kernel's last CTA during phase A (consumed by the leapfrog update)
+        a.tree = c->ta;
+        a.tree.x = xeval;
+        const size_t need = (size_t)(c->ta.n_nodes - c->n) * (c->d + 1) * sizeof(double);
+        a.tree.smem = need <= c->smem ? std::max<size_t>(need, 16) : 0;   // else the global message buffer
+        a.tree.prof = nullptr;
         a.gprior = c->d_gprior;
     }
     if (timed) CK(cudaEventRecord(next_event(c), s));
@@ -279,7 +286,8 @@ mds_status run_pass(mds_ctx c, const double* xeval, double* grad_out, double* li
     if (c->world == 1) {
         a.grad = grad_out;
         a.lik = lik_out;
-        const int mode = lf ? (want_lik ? MODE_LEAPFROG : MODE_LEAPFROG_NOLIK)
+        const int mode = lf ? (c->tree ? (want_lik ? MODE_LEAPFROG_TREE : MODE_LEAPFROG_NOLIK_TREE)
+                                       : (want_lik ? MODE_LEAPFROG : MODE_LEAPFROG_NOLIK))
                             : (want_lik ? MODE_EVAL : MODE_EVAL_NOLIK);
         st = launch_coop(c, pass_fn_mode(mode, c->prec, c->trunc, c->d), a, s);
         if (st) return st;
@@ -295,6 +303,12 @@ mds_status run_pass(mds_ctx c, const double* xeval, double* grad_out, double* li
             return fail(c, MDS_E_COMM, "all-gather callback failed");
         combine_kernel<<<(unsigned)((nd + 1 + 255) / 256), 256, 0, s>>>(c->d_gathered, c->world, nd + 1, grad_out,
                                                                          lik_out);
+        if (lf && c->tree) {
+            // sharded: the standalone tree walk (the EVAL-mode pass has no tree CTA)
+            TreeArgs ta = c->ta;
+            ta.x = xeval;
+            tree_prior_launch(ta, c->d, s);
+        }
         if (lf)
             leapfrog_update_kernel<<<(unsigned)((nd + 255) / 256), 256, 0, s>>>(
                 grad_out, xeval, c->d_x, c->d_p, c->d_gl, c->d_xnext, nd, eps, 0.5 * eps, inv_tau2,
@@ -481,8 +495,8 @@ mds_status build_schedule(mds_ctx c) {
     int dev = 0, sms = 0, occ = 1 << 30;
     CK(cudaGetDevice(&dev));
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    PassKernel ks[5];
-    for (int m = 0; m < 5; ++m) ks[m] = pass_fn_mode(m, c->prec, c->trunc, c->d);
+    PassKernel ks[N_MODES];
+    for (int m = 0; m < N_MODES; ++m) ks[m] = pass_fn_mode(m, c->prec, c->trunc, c->d);
     for (PassKernel k : ks) {
         CK(cudaFuncSetAttribute(k.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k.smem));
         int o = 0;
@@ -495,12 +509,29 @@ mds_status build_schedule(mds_ctx c) {
     const int64_t U = (int64_t)GROUPS_PER_TILE * c->ntl;
     int64_t G = (int64_t)sms * occ;
     G = std::max<int64_t>(std::min<int64_t>(G, (U + c->wpc - 1) / c->wpc), 1);
+    // with a tree prior one more CTA walks the tree during phase A
+    const int64_t Gp = G;
+    if (c->tree) G = Gp + 1 <= (int64_t)sms * occ ? Gp + 1 : Gp;
+    const int64_t GA = c->tree ? G - 1 : G;
+    if (GA < 1) return fail(c, MDS_E_UNSUPPORTED, "no CTA left for the pair phase");
     c->grid = (int)G;
+    c->pair_ctas = (int)GA;
     const int64_t GW = (int64_t)c->wpc * G;
+    {
+        void* old[] = {c->d_warp_seg, c->d_segs, c->d_blk_ptr, c->d_slab_pos, c->d_slabs, c->d_likpart};
+        for (void* p : old)
+            if (p) cudaFree(p);
+        c->d_warp_seg = nullptr;
+        c->d_segs = nullptr;
+        c->d_blk_ptr = nullptr;
+        c->d_slab_pos = nullptr;
+        c->d_slabs = nullptr;
+        c->d_likpart = nullptr;
+    }
 
     Plan P;
     std::string why;
-    if (!make_plan(c->n, c->rank, c->world, G, c->wpc, P, &why)) return fail(c, MDS_E_UNSUPPORTED, why);
+    if (!make_plan(c->n, c->rank, c->world, GA, c->wpc, P, &why)) return fail(c, MDS_E_UNSUPPORTED, why);
     const std::vector<int>& warp_seg = P.warp_seg;
     const std::vector<int4>& segs = P.segs;
     const std::vector<int>& ptr = P.ptr;
@@ -532,6 +563,8 @@ mds_status build_schedule(mds_ctx c) {
     CK(cudaMemset(c->d_slabs, 0, nslab * TB * c->d * sizeof(double)));
     const char* pe = std::getenv("MDS_PROFILE_PHASES");
     if (pe && pe[0] == '1') {
+        if (c->d_prof) cudaFree(c->d_prof);
+        c->d_prof = nullptr;
         if ((st = dalloc(c, &c->d_prof, (size_t)G * 7))) return st;
         CK(cudaMemset(c->d_prof, 0, (size_t)G * 7 * sizeof(unsigned long long)));
     }
@@ -933,9 +966,10 @@ mds_status mds_set_tree_prior(mds_ctx c, int64_t n_nodes, const int64_t* parent,
                               const double* mu0, const double* sigma_cov) {
     GUARD(c);
     if (n_nodes == 0) {             // back to the iid prior
+        const bool was = c->tree;
         c->tree = false;
         c->lf_version = 0;
-        return MDS_OK;
+        return was ? build_schedule(c) : MDS_OK;   // phase A gets the tree CTA back
     }
     const int64_t n = c->n;
     const int d = c->d;
@@ -1147,7 +1181,7 @@ mds_status mds_set_tree_prior(mds_ctx c, int64_t n_nodes, const int64_t* parent,
     }
     c->tree = true;
     c->lf_version = 0;               // leapfrog state must be re-primed under the new prior
-    return MDS_OK;
+    return build_schedule(c);        // one CTA of the pass kernel walks the tree during phase A
 }
 
 void report_tree_profile(mds_ctx c) {

@@ -35,6 +35,7 @@
 #include <cooperative_groups.h>
 #include <cstdint>
 #include "mds_math.cuh"
+#include "mds_tree_impl.cuh"
 
 namespace mdsk {
 namespace cg = cooperative_groups;
@@ -51,11 +52,20 @@ constexpr int PT = 128;             // threads per CTA of the small helper kerne
 //                   whose log L nobody reads
 //   LIK             log L only, at the SigmaParams passed (sigma-side sweep for
 //                   the MH update of sigma^2; no gradient, no slabs)
-enum Mode { MODE_EVAL = 0, MODE_EVAL_NOLIK = 1, MODE_LEAPFROG = 2, MODE_LEAPFROG_NOLIK = 3, MODE_LIK = 4 };
+//   LEAPFROG_TREE, LEAPFROG_NOLIK_TREE
+//                   the leapfrog modes under the phylogenetic prior: the grid's
+//                   last CTA walks the tree during phase A
+enum Mode {
+    MODE_EVAL = 0, MODE_EVAL_NOLIK = 1, MODE_LEAPFROG = 2, MODE_LEAPFROG_NOLIK = 3, MODE_LIK = 4,
+    MODE_LEAPFROG_TREE = 5, MODE_LEAPFROG_NOLIK_TREE = 6
+};
+constexpr int N_MODES = 7;
 template <int MODE> struct ModeTraits {
-    static constexpr bool LF = MODE == MODE_LEAPFROG || MODE == MODE_LEAPFROG_NOLIK;   // leapfrog update
-    static constexpr bool WL = !(MODE == MODE_EVAL_NOLIK || MODE == MODE_LEAPFROG_NOLIK);  // log L wanted
-    static constexpr bool WG = MODE != MODE_LIK;                                        // gradient wanted
+    static constexpr bool TREE = MODE == MODE_LEAPFROG_TREE || MODE == MODE_LEAPFROG_NOLIK_TREE;
+    static constexpr bool LF = MODE == MODE_LEAPFROG || MODE == MODE_LEAPFROG_NOLIK || TREE;   // leapfrog update
+    static constexpr bool WL = !(MODE == MODE_EVAL_NOLIK || MODE == MODE_LEAPFROG_NOLIK ||
+                                 MODE == MODE_LEAPFROG_NOLIK_TREE);                         // log L wanted
+    static constexpr bool WG = MODE != MODE_LIK;                                            // gradient wanted
 };
 
 template <typename T, bool TRUNC> struct Pair;
@@ -158,6 +168,9 @@ struct PassArgs {
     double* xnext;
     double eps, heps, inv_tau2;
     const double* gprior;        // LEAPFROG: d log prior / dX at xeval (tree prior), or NULL = iid N(0, 1/inv_tau2)
+    int pair_ctas;               // CTAs [0, pair_ctas) run phase A (the plan's CTA count)
+    TreeArgs tree;               // *_TREE modes: the tree prior walked by CTA gridDim.x - 1 during phase A
+                                 //   (its x = xeval, its grad = gprior)
     int vpw;                     // virtual unit ranges per warp (warp_seg has GW * vpw + 1 entries)
     int epl;                     // phase B: slab elements per lane (1, 2 or 4)
     SigmaParams P;
@@ -259,6 +272,7 @@ __global__ void __launch_bounds__(WarpsPerCTA<T, D>::value * 32, 1)
 pass_kernel(PassArgs a) {
     using A = double;
     constexpr bool LF = ModeTraits<MODE>::LF, WL = ModeTraits<MODE>::WL, WG = ModeTraits<MODE>::WG;
+    constexpr bool TREE = ModeTraits<MODE>::TREE;
     constexpr int WPC = WarpsPerCTA<T, D>::value;
     constexpr int UCOLS = KernelShape<T, D>::ucols;     // tile columns per unit
     constexpr int GPU = UCOLS / 4;                      // 4-column groups per unit
@@ -287,11 +301,17 @@ pass_kernel(PassArgs a) {
     __syncthreads();
     if (a.prof && threadIdx.x == 0) a.prof[blockIdx.x * 4 + 0] = gtimer();
     A lik_w = A(0);
+    // With a tree prior, the last CTA walks the tree (d log prior / dX at xeval,
+    // PAPER.md:243-246) while the others run phase A; the grid barrier below
+    // orders phase B's leapfrog update after both.
+    const bool skip_a = blockIdx.x >= a.pair_ctas;
+    if (TREE && blockIdx.x == gridDim.x - 1)
+        treek::tree_prior_block<D, WPC * 32>(a.tree, reinterpret_cast<double*>(dsm), exptab);
     unsigned not_ready = 0;                  // profiling: units whose data had not landed yet
     uint32_t phase = 0;                      // bit b: parity of stage b (persists across ranges)
     int cst = 0;                             // stage of the next unit to compute
 #pragma unroll 1
-    for (int vv = 0; vv < a.vpw; ++vv) {
+    for (int vv = 0; vv < (skip_a ? 0 : a.vpw); ++vv) {
     const int vw = gw * a.vpw + vv;
     const int ws0 = a.warp_seg[vw], ws1 = a.warp_seg[vw + 1];
     const int nsw = ws1 - ws0;
@@ -591,6 +611,8 @@ MDS_DECLARE_PASS(1)
 MDS_DECLARE_PASS(2)
 MDS_DECLARE_PASS(3)
 MDS_DECLARE_PASS(4)
+MDS_DECLARE_PASS(5)
+MDS_DECLARE_PASS(6)
 #undef MDS_DECLARE_PASS
 
 }  // namespace mdsk

@@ -144,9 +144,15 @@ def test_hmc_trajectory_with_tree_prior(mds):
         c.set_sigma(w.sigma)
         c.set_tree_prior(parent, t, None, S)
         out = c.hmc_trajectory(p0, 0.002, 12, prior_sd=123.0)     # prior_sd ignored under the tree prior
+        # with a tree prior the pass kernel's last CTA walks the tree: the pair
+        # schedule has one CTA less -- plain evaluations are unchanged
+        ll_t, g_t = c.log_likelihood_and_gradient()
         # back to the iid prior
         c.clear_tree_prior()
         out2 = c.hmc_trajectory(p0, 0.002, 12, prior_sd=10.0)
+    full = oracle.loglik_grad(y, x, w.sigma, 1)
+    assert ll_t == pytest.approx(full["loglik"], rel=1e-10)
+    np.testing.assert_allclose(g_t, full["grad"], rtol=1e-9, atol=1e-12)
     np.testing.assert_allclose(out["x"], ref["x"], rtol=1e-9, atol=1e-12)
     np.testing.assert_allclose(out["p"], ref["p"], rtol=1e-9, atol=1e-9)
     assert out["H0"] == pytest.approx(ref["H0"], rel=1e-10)

@@ -34,7 +34,7 @@ def main():
         lines = re.findall(r"/\*([0-9a-f]{4,})\*/\s+(.*?);", f)
         ins = [(int(a, 16), txt.strip()) for a, txt in lines]
         # backward branch of the group loop
-        # the pair loop is the backward-branch loop with the most MUFU (special-function) ops
+        # the pair loop is the backward-branch loop with the most MUFU.RSQ ops
         loop, best = None, None
         for addr, txt in ins:
             # a loop's back edge: predicated, not a warp-uniform retry (BRA.U.ANY) or an
@@ -42,7 +42,9 @@ def main():
             mm = re.match(r"@!?P\w+\s+BRA\s+(0x[0-9a-f]+)", txt)
             if mm and int(mm.group(1), 16) < addr:
                 cand = (int(mm.group(1), 16), addr)
-                nm = sum(1 for a2, t2 in ins if cand[0] <= a2 <= cand[1] and "MUFU" in t2)
+                # the pair loop: one reciprocal-sqrt seed per pair (the tree-prior walk
+                # fused into the leapfrog modes has MUFU.RCP64H loops but no RSQ)
+                nm = sum(1 for a2, t2 in ins if cand[0] <= a2 <= cand[1] and "MUFU.RSQ" in t2)
                 key = (nm, cand[1] - cand[0])
                 if best is None or key > best:
                     loop, best = cand, key
