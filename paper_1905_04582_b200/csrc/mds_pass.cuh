@@ -199,6 +199,20 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
                  "l"(src), "r"(bytes), "r"(smem_u32(b))
                  : "memory");
 }
+// the same with an L2 cache-policy hint (Y is streamed once per pass: evict-first
+// keeps X and the partial-sum slabs resident in L2 for phase B)
+__device__ __forceinline__ void bulk_g2s_hint(void* dst, const void* src, uint32_t bytes, uint64_t* b, uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(b)), "l"(pol)
+        : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
     asm volatile(
         "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}" ::"r"(
@@ -301,6 +315,9 @@ pass_kernel(PassArgs a) {
     __syncthreads();
     if (a.prof && threadIdx.x == 0) a.prof[blockIdx.x * 4 + 0] = gtimer();
     A lik_w = A(0);
+#ifndef MDS_Y_NO_EVICT_FIRST
+    const uint64_t ypol = policy_evict_first();
+#endif
     // With a tree prior, the last CTA walks the tree (d log prior / dX at xeval,
     // PAPER.md:243-246) while the others run phase A; the grid barrier below
     // orders phase B's leapfrog update after both.
@@ -344,7 +361,11 @@ pass_kernel(PassArgs a) {
                 // fence (it compiles to MEMBAR.ALL.CTA, which waits for this lane's
                 // outstanding column-slab stores)
                 mbar_arrive_tx(&W.bar[ist], YB + (nt ? XB : 0));
+#ifndef MDS_Y_NO_EVICT_FIRST
+                bulk_g2s_hint(W.y[ist], Y + (size_t)t * TB * TB + (size_t)jj0 * TB, YB, &W.bar[ist], ypol);
+#else
                 bulk_g2s(W.y[ist], Y + (size_t)t * TB * TB + (size_t)jj0 * TB, YB, &W.bar[ist]);
+#endif
                 if (nt) bulk_g2s(W.xcol[t & 1], X + (size_t)(t - itb) * TB * D, XB, &W.bar[ist]);
             }
             ++iu;
