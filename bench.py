@@ -51,6 +51,12 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=200)
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--graph", type=int, default=0,
+                    help="1: capture the K timed steps (flush + step, with external timing events) in one CUDA "
+                         "graph and replay it (N = 1 only)")
+    ap.add_argument("--flush", choices=["torch", "mds"], default="mds",
+                    help="L2 flush between timed steps: torch fill, or mds_l2_flush (same write, launched "
+                         "with the pass kernel's grid/block/smem shape)")
     return ap.parse_args()
 
 
@@ -196,7 +202,9 @@ def run_ours(args):
     w = workload.config(args.workload)
     n, d = w.n, w.d
     P_N = n * (n - 1) // 2
-    stream = torch.cuda.current_stream()
+    # a dedicated stream (graph capture needs a non-default stream)
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
     ctx = mds.MDS(n, d, args.precision, True, rank=rank, world=world, stream=stream)
     if world > 1:
         ctx.use_torch_allgather()
@@ -220,8 +228,28 @@ def run_ours(args):
     torch.cuda.synchronize()
 
     clocks = ClockSampler(torch.cuda.current_device())
-    ev0 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    ev1 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    use_graph = bool(args.graph) and world == 1
+    ev0 = [torch.cuda.Event(enable_timing=True, external=use_graph) for _ in range(args.steps)]
+    ev1 = [torch.cuda.Event(enable_timing=True, external=use_graph) for _ in range(args.steps)]
+
+    def timed_steps():
+        for k in range(args.steps):
+            if args.flush == "mds":        # untimed L2 flush before every timed step
+                ctx.l2_flush(flush)
+            else:
+                flush.zero_()
+            ev0[k].record(stream)
+            ctx.leapfrog_device(1, args.step_size, args.prior_sd)
+            ev1[k].record(stream)
+
+    graph = None
+    if use_graph:
+        # launch mechanics only: the same K (flush, step) pairs, captured once on
+        # the context's stream and replayed; events are external (timed) nodes
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=stream):
+            timed_steps()
+        torch.cuda.synchronize()
     # the library's timing mode (events around every launch) perturbs
     # back-to-back cooperative launches by ~8 us/step; unsharded, a step IS one
     # pass-kernel launch, so the per-step events below are the kernel's launch
@@ -232,11 +260,10 @@ def run_ours(args):
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    for k in range(args.steps):
-        flush.zero_()                      # untimed L2 flush before every timed step
-        ev0[k].record(stream)
-        ctx.leapfrog_device(1, args.step_size, args.prior_sd)
-        ev1[k].record(stream)
+    if graph is not None:
+        graph.replay()
+    else:
+        timed_steps()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -330,7 +357,10 @@ def run_ours(args):
                                "one leapfrog step (fused lik+grad pass) per step" % (args.workload, n, d,
                                                                                     args.precision, w.sigma),
                    "n": n, "d": d, "pairs_per_step": P_N, "observed_fraction": 1.0 - w.p_missing,
-                   "l2": "flushed between timed steps (256 MiB write, untimed)",
+                   "l2": "flushed between timed steps (256 MiB write, untimed, %s)" % (
+                       "torch fill" if args.flush == "torch" else "mds_l2_flush"),
+                   "launch": "one CUDA graph of the K (flush, step) pairs" if graph is not None
+                   else "stream launches",
                    "parallelism": "tile-row shards x %d" % world if world > 1 else "single GPU",
                    "setup_s": t_setup},
         "evals_per_s": 1e3 / ms_per_step,
