@@ -357,6 +357,24 @@ mds_status rw_scratch(mds_ctx c, size_t bytes) {
     return MDS_OK;
 }
 
+// one thread-block cluster of ROW_CLUSTER CTAs (mds_row.cuh)
+mds_status launch_row(mds_ctx c, RowArgs& a) {
+    cudaLaunchConfig_t cfg{};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = ROW_CLUSTER;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.gridDim = dim3(ROW_CLUSTER);
+    cfg.blockDim = dim3(ROW_THREADS);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = c->stream;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    CK(cudaLaunchKernelEx(&cfg, row_fn(c->prec == MDS_F64, c->trunc, c->d), a));
+    return MDS_OK;
+}
+
 RowArgs row_args(mds_ctx c) {
     RowArgs a{};
     a.y = c->d_y;
@@ -908,8 +926,7 @@ mds_status mds_row_loglik_delta(mds_ctx c, int64_t i, const double* x_new_i, dou
     a.xnew = dx;
     a.delta = dx + 8;
     a.K = 0;
-    row_fn(c->prec == MDS_F64, c->trunc, c->d)<<<1, ROW_THREADS, 0, c->stream>>>(a);
-    CK(cudaGetLastError());
+    if ((st = launch_row(c, a))) return st;
     CK(cudaMemcpyAsync(delta, dx + 8, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
     return MDS_OK;
@@ -952,8 +969,7 @@ mds_status mds_rw_sweep(mds_ctx c, int64_t k, const int64_t* rows, const double*
     a.step = step;
     a.inv_tau2 = prior_sd > 0.0 ? 1.0 / (prior_sd * prior_sd) : 0.0;
     a.accepted = dacc;
-    row_fn(c->prec == MDS_F64, c->trunc, c->d)<<<1, ROW_THREADS, 0, c->stream>>>(a);
-    CK(cudaGetLastError());
+    if ((st = launch_row(c, a))) return st;
     unsigned long long na = 0;
     CK(cudaMemcpyAsync(&na, dacc, sizeof(na), cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));

@@ -1,4 +1,5 @@
 // mds_row.cu -- single-location update kernels (see mds_row.cuh).
+#include <cooperative_groups.h>
 #include "mds_row.cuh"
 
 namespace mdsk {
@@ -46,12 +47,13 @@ __device__ __forceinline__ void ell2<float, false>(float s0, float s1, float y, 
     pair_f32<false, true, false>(s1, y, P, e1, u);
 }
 
-// Delta of row i between positions xn and xo (both [D] in shared memory),
-// returned to every thread.  Fixed order: per-thread sum over its columns in
-// ascending j, warp butterfly, then the 32 warp sums in order.
+// Row i's share of Delta owned by this CTA (columns j = rank*NT + tid, stride
+// CL*NT) between positions xn and xo (both [D] in shared memory).  Fixed
+// order: per-thread sum over its columns in ascending j, warp butterfly, then
+// the warp sums in order -> one partial per CTA.
 template <typename T, int D, bool TRUNC>
-__device__ double row_delta(const RowArgs& a, int64_t i, const double* xn, const double* xo, const double* exptab,
-                            double* red) {
+__device__ double row_partial(const RowArgs& a, int64_t i, const double* xn, const double* xo, const double* exptab,
+                              double* red, int rank) {
     const T* __restrict__ Y = static_cast<const T*>(a.y);
     const double* X = a.x;     // not __restrict__/nc: the sweep writes X between updates
     double acc = 0.0;
@@ -61,7 +63,7 @@ __device__ double row_delta(const RowArgs& a, int64_t i, const double* xn, const
         xnr[k] = (T)xn[k];
         xor_[k] = (T)xo[k];
     }
-    for (int64_t j = threadIdx.x; j < a.n; j += ROW_THREADS) {
+    for (int64_t j = (int64_t)rank * ROW_THREADS + threadIdx.x; j < a.n; j += (int64_t)ROW_CLUSTER * ROW_THREADS) {
         if (j == i) continue;
         const T y = j < i ? y_pair<T>(Y, a.row_local, i, j) : y_pair<T>(Y, a.row_local, j, i);
         if (is_missing(y)) continue;
@@ -84,63 +86,70 @@ __device__ double row_delta(const RowArgs& a, int64_t i, const double* xn, const
     __syncthreads();
     double t = 0.0;
     if (warp == 0) {
-        t = red[lane];
+        t = lane < ROW_THREADS / 32 ? red[lane] : 0.0;
 #pragma unroll
         for (int m = 16; m >= 1; m >>= 1) t += __shfl_xor_sync(0xffffffffu, t, m);
-        if (lane == 0) red[32] = t;
     }
-    __syncthreads();
-    t = red[32];
-    __syncthreads();   // red is reused by the next call
-    return t;
+    return t;   // valid on warp 0
 }
 
+// One cluster of ROW_CLUSTER CTAs per launch: every update's N - 1 column pairs
+// are split over the cluster's SMs; the CTA partials meet through distributed
+// shared memory (double-buffered by update parity, one cluster barrier per
+// update), and every CTA forms the same total in rank order, takes the same
+// decision and writes the same new x_i -- so no X traffic crosses CTAs.
 template <typename T, int D, bool TRUNC>
 __global__ void __launch_bounds__(ROW_THREADS, 1) row_kernel(RowArgs a) {
+    namespace cg = cooperative_groups;
+    cg::cluster_group cluster = cg::this_cluster();
+    const int rank = (int)cluster.block_rank();
     __shared__ double exptab[64];
-    __shared__ double red[33];
+    __shared__ double red[ROW_THREADS / 32];
+    __shared__ double part[2];
     __shared__ double xn[D], xo[D];
+    __shared__ int decide;
     if (threadIdx.x < 64) exptab[threadIdx.x] = EXPT64_TAB[threadIdx.x];
-    if (a.K == 0) {
-        if (threadIdx.x < D) {
-            xo[threadIdx.x] = a.x[a.i0 * D + threadIdx.x];
-            xn[threadIdx.x] = a.xnew[threadIdx.x];
-        }
-        __syncthreads();
-        const double dl = row_delta<T, D, TRUNC>(a, a.i0, xn, xo, exptab, red);
-        if (threadIdx.x == 0) *a.delta = dl;
-        return;
-    }
+    const int64_t K = a.K == 0 ? 1 : a.K;
     unsigned long long nacc = 0;
-    for (int64_t k = 0; k < a.K; ++k) {
-        const int64_t i = a.rows[k];
+    for (int64_t k = 0; k < K; ++k) {
+        const int64_t i = a.K == 0 ? a.i0 : a.rows[k];
         if (threadIdx.x < D) {
             const double v = a.x[i * D + threadIdx.x];
             xo[threadIdx.x] = v;
-            xn[threadIdx.x] = __fma_rn(a.step, a.z[k * D + threadIdx.x], v);
+            xn[threadIdx.x] = a.K == 0 ? a.xnew[threadIdx.x] : __fma_rn(a.step, a.z[k * D + threadIdx.x], v);
         }
         __syncthreads();
-        const double dl = row_delta<T, D, TRUNC>(a, i, xn, xo, exptab, red);
-        // log prior change (iid N(0, tau^2)); decision in fp64 on thread 0
+        const double p = row_partial<T, D, TRUNC>(a, i, xn, xo, exptab, red, rank);
+        const int par = (int)(k & 1);
+        if (threadIdx.x == 0) part[par] = p;
+        cluster.sync();                    // every CTA's partial of this update is published
         if (threadIdx.x == 0) {
-            double pn = 0.0, po = 0.0;
+            double dl = 0.0;
+            for (int r = 0; r < ROW_CLUSTER; ++r) dl += *cluster.map_shared_rank(&part[par], r);
+            if (a.K == 0) {
+                if (rank == 0) *a.delta = dl;
+                decide = 0;
+            } else {
+                // log prior change (iid N(0, tau^2)); the decision in fp64, identical on every CTA
+                double pn = 0.0, po = 0.0;
 #pragma unroll
-            for (int q = 0; q < D; ++q) {
-                pn = fma(xn[q], xn[q], pn);
-                po = fma(xo[q], xo[q], po);
-            }
-            const double lr = dl - 0.5 * (pn - po) * a.inv_tau2;
-            const bool ok = isfinite(lr) && log(a.u[k]) < lr;
-            if (ok) {
+                for (int q = 0; q < D; ++q) {
+                    pn = fma(xn[q], xn[q], pn);
+                    po = fma(xo[q], xo[q], po);
+                }
+                const double lr = dl - 0.5 * (pn - po) * a.inv_tau2;
+                decide = isfinite(lr) && log(a.u[k]) < lr;
+                if (decide) {
 #pragma unroll
-                for (int q = 0; q < D; ++q) a.x[i * D + q] = xn[q];
-                ++nacc;
+                    for (int q = 0; q < D; ++q) a.x[i * D + q] = xn[q];
+                    ++nacc;
+                }
             }
         }
-        __threadfence_block();
-        __syncthreads();   // X[i] (if accepted) is visible to the next update's column reads
+        __syncthreads();   // this CTA's copy of X[i] (if accepted) is visible to its next column reads
     }
-    if (threadIdx.x == 0) *a.accepted = nacc;
+    if (threadIdx.x == 0 && rank == 0 && a.K > 0) *a.accepted = nacc;
+    cluster.sync();        // no CTA exits while another may still read its partials
 }
 
 template <typename T, bool TR>

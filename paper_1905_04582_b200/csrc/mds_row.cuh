@@ -7,13 +7,15 @@
 // sampler of Bedford et al. that the paper compares against: update i, propose
 // x_i + step z, accept iff log u < Delta_i + Delta log prior.
 //
-// One CTA of 1024 threads evaluates one row: thread t takes columns
-// j = t, t + 1024, ... (y_ij gathered from the tiled triangle: for j > i the
-// 32 lanes of a warp read one contiguous 256 B run of a tile column), both
-// terms of a column in lock-step (pair_f64_n with NP = 2, likelihood only),
-// then a fixed-order block tree reduction: deterministic, no atomics.  A sweep
-// of K sequential updates is ONE launch (the updates are dependent: the CTA
-// loops, X stays in L2).
+// One thread-block cluster of 8 CTAs (8 SMs) evaluates one row: thread t of
+// CTA r takes columns j = 512 r + t, + 4096, ... (y_ij gathered from the tiled
+// triangle: for j > i the 32 lanes of a warp read one contiguous 256 B run of
+// a tile column), both terms of a column in lock-step (pair_f64_n with NP = 2,
+// likelihood only), a fixed-order block tree per CTA, and the 8 CTA partials
+// summed in rank order through distributed shared memory: deterministic, no
+// atomics.  A sweep of K sequential updates is ONE launch (the updates are
+// dependent: the cluster loops with one cluster barrier per update, X stays
+// in L2).
 #pragma once
 #include <cstdint>
 #include "mds_math.cuh"
@@ -41,7 +43,8 @@ struct RowArgs {
 };
 
 typedef void (*RowFn)(RowArgs);
-constexpr int ROW_THREADS = 1024;
+constexpr int ROW_THREADS = 512;    // per CTA
+constexpr int ROW_CLUSTER = 8;      // CTAs (SMs) per row: one thread-block cluster
 // row_kernel<T, D, TRUNC> for (precision, truncation, d); defined in mds_row.cu
 RowFn row_fn(int prec_is_f64, int trunc, int d);
 
