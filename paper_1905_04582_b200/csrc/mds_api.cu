@@ -1367,6 +1367,7 @@ SigmaParams sigma_params(double sigma) {
     P.half_inv_sigma2_f = (float)P.half_inv_sigma2;
     P.k0_f = (float)P.k0;
     P.cg_f = (float)P.cg;
+    for (int j = 0; j <= Q64_DEG; ++j) P.qc[j] = Q64_CH[j] / P.cg;
     return P;
 }
 }  // namespace

@@ -22,8 +22,8 @@ __device__ __forceinline__ double heldout_ell(const CvArgs& a, int64_t q, const 
 
 template <int D, bool TRUNC>
 __global__ void __launch_bounds__(256) cv_accumulate_kernel(CvArgs a) {
-    __shared__ double exptab[64];
-    if (threadIdx.x < 64) exptab[threadIdx.x] = EXPT64_TAB[threadIdx.x];
+    __shared__ double exptab[EXPT64_N];
+    build_exptab(exptab, a.P);
     __syncthreads();
     for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < a.m; q += (int64_t)gridDim.x * blockDim.x) {
         const double l = heldout_ell<D, TRUNC>(a, q, exptab);

@@ -8,13 +8,15 @@
 // +u (x_i - x_j) to g_j.  The pair's v = u (x_i - x_j) is formed by the caller.
 //
 // Device math, t >= 0 always on this path:
-//   E      = exp(-t^2/2) = exp(-s/(2 sigma^2))     -- one exp, argument from s directly:
-//            2^n 2^(j/64) p(r), 64-entry table in shared memory, degree-5 p
-//   Q      = 1 - Phi(t) = E q(w),  q = erfcx(t/sqrt2)/2 as a minimax polynomial in
-//            w = (t-K)/(t+K) (one reciprocal); absolute error of Q <= 3e-16
-//   1/Phi, 1/(1+Phi) from ONE reciprocal of Phi(1+Phi)
-//   log Phi = log1p(-Q) = -2 atanh(Q/(2-Q))        -- polynomial in z = (Q/(2-Q))^2 <= 1/9
-//   phi/Phi = E / (sqrt(2 pi) Phi)                 -- shares E with Q
+//   E'     = cg exp(-t^2/2), cg = 1/(sigma sqrt(2 pi)) -- one exp, argument from s
+//            directly: 2^n [cg 2^(j/256)] p(r), 256-entry table in shared memory
+//            (scaled by cg per launch), degree-4 p
+//   Q      = 1 - Phi(t) = E' q'(w),  q' = erfcx(t/sqrt2)/(2 cg) as a minimax polynomial
+//            in w = (t-K)/(t+K) (one reciprocal); absolute error of Q <= 3e-16
+//   1/Phi, 1/(2-Q) from ONE reciprocal of Phi(2-Q)
+//   log Phi = log1p(-Q) = -2 atanh(Q/(2-Q))        -- degree-7 polynomial in z = (Q/(2-Q))^2
+//            <= 1/9; absolute error <= 5e-14 (log Phi enters log L only: DESIGN.md R32)
+//   phi/(sigma Phi) = E' / Phi                     -- shares E' with Q
 // The reciprocal and rsqrt seeds come from MUFU (rcp/rsqrt.approx) refined by one
 // cubic Newton step.  About 65 FP64 instructions per pair of math (+ ~8 for the
 // distance and the sums, D = 2) instead of ~160 for libdevice erfc/log1p/exp/div.
@@ -33,6 +35,8 @@ struct SigmaParams {
     double cg;               // 1/(sigma sqrt(2 pi))
     double ks;               // KAPPA64 * sigma: w = (d - ks)/(d + ks) = (t - K)/(t + K)
     double two_ks;           // 2 KAPPA64 sigma
+    double qc[Q64_DEG + 1];  // Q64_C / cg: with the exp table scaled by cg (E' = cg E), Q = E' q'(w)
+                             // and phi/(sigma Phi) = E' / Phi -- one multiply less per pair
     float inv_sigma_f, inv_sigma2_f, half_inv_sigma2_f, k0_f, cg_f;
 };
 
@@ -131,6 +135,12 @@ __device__ __forceinline__ double horner4(const double* c, double x) {
     return fma(hi, x2, lo);
 }
 
+// the per-launch exp table of pair_f64_n: cg 2^(j/256), j < EXPT64_N (call with
+// every thread of the block, then __syncthreads)
+__device__ __forceinline__ void build_exptab(double* tab, const SigmaParams& P) {
+    for (int j = threadIdx.x; j < EXPT64_N; j += blockDim.x) tab[j] = EXPT64_TAB[j] * P.cg;
+}
+
 __device__ __forceinline__ bool is_missing(double y) {
     return (uint32_t)__double2hiint(y) == CANON_NAN_HI64;
 }
@@ -170,8 +180,9 @@ __device__ __forceinline__ void pair_f64_n(const double (&s)[NP], const double (
         if (WL) l[i] = fma(-(res[i] * P.half_inv_sigma2), res[i], P.k0);
     }
     if (TRUNC) {
-        // E = exp(-a), a = t^2/2 = s/(2 sigma^2): k = rint(-64 a / ln2), E = 2^(k>>6) 2^((k&63)/64) p(r),
-        // |r| <= ln2/128 (table in shared memory, degree-5 polynomial)
+        // E' = cg exp(-a), a = t^2/2 = s/(2 sigma^2): k = rint(-256 a / ln2),
+        // E' = 2^(k>>8) [cg 2^((k&255)/256)] p(r), |r| <= ln2/512 (cg-scaled table in
+        // shared memory, built per launch; degree-4 polynomial)
         double r[NP], E[NP], w[NP], den[NP], y0[NP];
         int k[NP];
         const double MAGIC = 6755399441055744.0;   // 1.5 * 2^52
@@ -179,11 +190,11 @@ __device__ __forceinline__ void pair_f64_n(const double (&s)[NP], const double (
         for (int i = 0; i < NP; ++i) {
             double a = s[i] * P.half_inv_sigma2;
             a = __hiloint2double(min(__double2hiint(a), 0x4085E000), __double2loint(a));   // a <= ~700
-            const double kd = fma(a, -92.33248261689366, MAGIC);                          // 64 / ln2
+            const double kd = fma(a, -EXPT64_INV_STEP, MAGIC);                           // 256 / ln2
             k[i] = __double2loint(kd);
             const double fk = kd - MAGIC;
-            r[i] = fma(fk, -0.010830424696249145, -a);                                    // ln2/64 hi
-            r[i] = fma(fk, -3.6235106466348432e-19, r[i]);                                // ln2/64 lo
+            r[i] = fma(fk, -EXPT64_STEP_HI, -a);                                          // ln2/256 hi
+            r[i] = fma(fk, -EXPT64_STEP_LO, r[i]);                                        // ln2/256 lo
             // w = (t - K)/(t + K) = (d - K sigma)/(d + K sigma): MUFU seed issued early
             den[i] = d[i] + P.ks;
             y0[i] = rcp_seed(den[i]);
@@ -197,8 +208,8 @@ __device__ __forceinline__ void pair_f64_n(const double (&s)[NP], const double (
             for (int i = 0; i < NP; ++i) p[i] = fma(p[i], r[i], EXPT64_C[j]);
 #pragma unroll
         for (int i = 0; i < NP; ++i) {
-            const double pt = p[i] * exptab[k[i] & 63];
-            E[i] = __hiloint2double(__double2hiint(pt) + (int)((unsigned)(k[i] >> 6) << 20), __double2loint(pt));
+            const double pt = p[i] * exptab[k[i] & (EXPT64_N - 1)];
+            E[i] = __hiloint2double(__double2hiint(pt) + (int)((unsigned)(k[i] >> 8) << 20), __double2loint(pt));
             const double e1 = fma(-den[i], y0[i], 1.0);
             const double ee = fma(e1, e1, e1);
             const double rden = fma(ee, y0[i], y0[i]);
@@ -206,11 +217,11 @@ __device__ __forceinline__ void pair_f64_n(const double (&s)[NP], const double (
         }
         double q[NP];
 #pragma unroll
-        for (int i = 0; i < NP; ++i) q[i] = Q64_C[Q64_DEG];
+        for (int i = 0; i < NP; ++i) q[i] = P.qc[Q64_DEG];
 #pragma unroll
         for (int j = Q64_DEG - 1; j >= 0; --j)
 #pragma unroll
-            for (int i = 0; i < NP; ++i) q[i] = fma(q[i], w[i], Q64_C[j]);
+            for (int i = 0; i < NP; ++i) q[i] = fma(q[i], w[i], P.qc[j]);
         double Q[NP], Phi[NP], opp[NP], prod[NP], z0[NP];
 #pragma unroll
         for (int i = 0; i < NP; ++i) {
@@ -228,7 +239,7 @@ __device__ __forceinline__ void pair_f64_n(const double (&s)[NP], const double (
             const double rp = fma(f2, z0[i], z0[i]);
             if (WG) {
                 const double invPhi = WL ? opp[i] * rp : rp;
-                G[i] = (E[i] * P.cg) * invPhi;
+                G[i] = E[i] * invPhi;             // E already carries cg
             }
             if (WL) {
                 const double invOpp = WG ? Phi[i] * rp : rp;

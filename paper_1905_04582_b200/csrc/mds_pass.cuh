@@ -270,15 +270,15 @@ template <typename T, int D>
 constexpr size_t pass_smem_bytes() { return WarpsPerCTA<T, D>::value * sizeof(WarpStage<T, D>); }
 // dynamic staging + the static reduction buffers must fit the 227 KB of one CTA
 // (phase B reuses the staging area for its 4 x warps x 32 partial sums)
-static_assert(pass_smem_bytes<double, 8>() + 512 <= 227 * 1024, "smem");
-static_assert(pass_smem_bytes<double, 4>() + 512 <= 227 * 1024, "smem");
-static_assert(pass_smem_bytes<float, 8>() + 512 <= 227 * 1024, "smem");
-static_assert(pass_smem_bytes<float, 6>() + 512 <= 227 * 1024, "smem");
-static_assert(pass_smem_bytes<float, 2>() + 512 <= 227 * 1024, "smem");
-static_assert(pass_smem_bytes<double, 3>() + 512 <= 227 * 1024, "smem");
-static_assert(pass_smem_bytes<double, 2>() + 512 <= 227 * 1024, "smem");
-static_assert(pass_smem_bytes<double, 1>() + 512 <= 227 * 1024, "smem");
-static_assert(pass_smem_bytes<float, 1>() + 512 <= 227 * 1024, "smem");
+static_assert(pass_smem_bytes<double, 8>() + EXPT64_N * 8 + 512 <= 227 * 1024, "smem");
+static_assert(pass_smem_bytes<double, 4>() + EXPT64_N * 8 + 512 <= 227 * 1024, "smem");
+static_assert(pass_smem_bytes<float, 8>() + EXPT64_N * 8 + 512 <= 227 * 1024, "smem");
+static_assert(pass_smem_bytes<float, 6>() + EXPT64_N * 8 + 512 <= 227 * 1024, "smem");
+static_assert(pass_smem_bytes<float, 2>() + EXPT64_N * 8 + 512 <= 227 * 1024, "smem");
+static_assert(pass_smem_bytes<double, 3>() + EXPT64_N * 8 + 512 <= 227 * 1024, "smem");
+static_assert(pass_smem_bytes<double, 2>() + EXPT64_N * 8 + 512 <= 227 * 1024, "smem");
+static_assert(pass_smem_bytes<double, 1>() + EXPT64_N * 8 + 512 <= 227 * 1024, "smem");
+static_assert(pass_smem_bytes<float, 1>() + EXPT64_N * 8 + 512 <= 227 * 1024, "smem");
 static_assert(sizeof(WarpStage<float, 1>) >= 4 * 32 * sizeof(double), "phase B buffer");
 
 template <typename T, int D, bool TRUNC, int MODE>
@@ -292,7 +292,7 @@ pass_kernel(PassArgs a) {
     constexpr int GPU = UCOLS / 4;                      // 4-column groups per unit
     constexpr int UNITS_PER_TILE = TB / UCOLS;
     extern __shared__ __align__(128) unsigned char dsm[];
-    __shared__ double exptab[64];
+    __shared__ double exptab[EXPT64_N];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int gw = blockIdx.x * WPC + warp;
     WarpStage<T, D>& W = reinterpret_cast<WarpStage<T, D>*>(dsm)[warp];
@@ -311,7 +311,7 @@ pass_kernel(PassArgs a) {
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         fence_async_smem();
     }
-    if (threadIdx.x < 64) exptab[threadIdx.x] = EXPT64_TAB[threadIdx.x];
+    build_exptab(exptab, a.P);
     __syncthreads();
     if (a.prof && threadIdx.x == 0) a.prof[blockIdx.x * 4 + 0] = gtimer();
     A lik_w = A(0);

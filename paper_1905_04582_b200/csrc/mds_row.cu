@@ -103,12 +103,12 @@ __global__ void __launch_bounds__(ROW_THREADS, 1) row_kernel(RowArgs a) {
     namespace cg = cooperative_groups;
     cg::cluster_group cluster = cg::this_cluster();
     const int rank = (int)cluster.block_rank();
-    __shared__ double exptab[64];
+    __shared__ double exptab[EXPT64_N];
     __shared__ double red[ROW_THREADS / 32];
     __shared__ double part[2];
     __shared__ double xn[D], xo[D];
     __shared__ int decide;
-    if (threadIdx.x < 64) exptab[threadIdx.x] = EXPT64_TAB[threadIdx.x];
+    build_exptab(exptab, a.P);
     const int64_t K = a.K == 0 ? 1 : a.K;
     unsigned long long nacc = 0;
     for (int64_t k = 0; k < K; ++k) {
