@@ -375,3 +375,24 @@ def test_virtual_ranges_and_wide_d(mds):
         x32 = x.astype(np.float32).astype(np.float64)
         ll, g = run_gpu(mds, w.n, d, y, x, w.sigma, prec="f32")
         fp32_check(ll, g, oracle.loglik_grad(y32, x32, w.sigma, 1))
+
+
+@pytest.mark.skipif(not __import__("os").environ.get("MDS_TEST_C5"), reason="C5 (40 GB of Y) only with MDS_TEST_C5=1")
+def test_c5_full_size_sampled_rows(mds):
+    """C5 at full size on one GPU (N = 100000, D = 2, fp64, 5.0e9 pairs, 40 GB of
+    tiled Y streamed from the generator in row chunks): sampled gradient rows
+    against the per-row oracle; the gradient rows sum to zero."""
+    import torch
+    w = workload.config("C5")
+    with mds.MDS(w.n, w.d, "f64", True) as c:
+        for i0 in range(0, w.n, 1000):
+            c.set_dissimilarity_rows(i0, min(w.n, i0 + 1000), w.y_rows(i0, min(w.n, i0 + 1000)))
+        c.set_locations(w.x0)
+        c.set_sigma(w.sigma)
+        ll, g = c.log_likelihood_and_gradient()
+    rows = np.array([0, 1, 64, 4095, 50000, 77777, 99999])
+    ref = oracle.grad_rows(rows, w.y_full_rows(rows), w.x0, w.sigma, 1)
+    err = np.abs(g[rows] - ref["grad"])
+    assert np.all(err <= np.maximum(1e-9 * np.abs(ref["grad"]), 1e-12)), err.max()
+    assert np.all(np.abs(g.sum(0)) <= 1e-12 * np.abs(g).sum(0))
+    assert np.isfinite(ll)

@@ -90,12 +90,40 @@ def run_c3(n_iter, L):
             "paper_context": "PAPER.md:672 -- 2e6 HMC states in ~48 h on a GP100 (86.4 ms/state) for the flu data"}
 
 
+def run_c5(steps=5):
+    """C5 at P = 1: N = 100000, D = 2, fp64 -- 5.0e9 pairs, 40 GB of tiled Y on one
+    B200.  Y is streamed to the context in row chunks straight from the seeded
+    generator (no host N x N matrix); the timed steps are device-resident
+    leapfrog steps as in bench.py (Y is far larger than L2: no flush needed)."""
+    import torch
+    import workload
+    import paper_1905_04582_b200 as mds
+    w = workload.config("C5")
+    t0 = time.time()
+    ctx = mds.MDS(w.n, w.d, "f64", True, stream=torch.cuda.current_stream())
+    step = 1000
+    for i0 in range(0, w.n, step):
+        i1 = min(w.n, i0 + step)
+        ctx.set_dissimilarity_rows(i0, i1, w.y_rows(i0, i1))
+    ctx.set_locations(w.x0)
+    ctx.set_sigma(w.sigma)
+    torch.cuda.synchronize()
+    setup = time.time() - t0
+    mean_ms, med_ms = step_rate(ctx, w.n, w.d, steps, 1)
+    P = w.n * (w.n - 1) // 2
+    ll = ctx.log_likelihood()
+    ctx.close()
+    return {"config": "C5", "precision": "f64", "n": w.n, "d": w.d, "gpus": 1, "ms_per_step": mean_ms,
+            "ms_p50": med_ms, "pair_evals_per_s": P / (mean_ms * 1e-3), "setup_s": setup, "loglik": ll}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--c3-iter", type=int, default=1000)
     ap.add_argument("--leapfrog", type=int, default=20)
     ap.add_argument("--skip-c3", action="store_true")
     ap.add_argument("--skip-c4", action="store_true")
+    ap.add_argument("--c5", action="store_true")
     a = ap.parse_args()
     import torch
     torch.cuda.set_device(0)
@@ -104,6 +132,8 @@ def main():
             print(json.dumps(run_c4(prec)), flush=True)
     if not a.skip_c3:
         print(json.dumps(run_c3(a.c3_iter, a.leapfrog)), flush=True)
+    if a.c5:
+        print(json.dumps(run_c5()), flush=True)
 
 
 if __name__ == "__main__":
