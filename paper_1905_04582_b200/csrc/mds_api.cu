@@ -1102,8 +1102,8 @@ mds_status mds_set_tree_prior(mds_ctx c, int64_t n_nodes, const int64_t* parent,
     // pre-order entry
     const size_t nn = (size_t)n_nodes;
     const size_t E_up = up_nodes.size(), E_dn = dn_nodes.size();
-    std::vector<int> up_e(4 * E_up), dn_e(4 * E_dn), dn_pos(nn, -1);
-    std::vector<double> up_t(2 * E_up, 0.0), dn_t(2 * E_dn, 0.0);
+    std::vector<int> up_e(4 * E_up), dn_e(4 * E_dn), dn_pos(nn, -1), up_dpos(E_up, -1), tip_upos((size_t)n, -1);
+    std::vector<double> up_t(2 * E_up, 0.0), dn_t(2 * E_dn, 0.0), up_tn(E_up, 0.0);
     for (size_t e = 0; e < E_up; ++e) {
         const int v = up_nodes[e], c0 = ch_ptr[(size_t)v], k = ch_ptr[(size_t)v + 1] - c0;
         up_e[4 * e] = v - (int)n;
@@ -1111,8 +1111,10 @@ mds_status mds_set_tree_prior(mds_ctx c, int64_t n_nodes, const int64_t* parent,
             const int ch = i < k ? ch_idx[(size_t)c0 + i] : -1;
             up_e[4 * e + 1 + i] = ch < 0 ? 0 : (ch < n ? -1 - ch : ch - (int)n);
             up_t[2 * e + i] = ch < 0 ? 0.0 : t[ch];
+            if (ch >= 0 && ch < n) tip_upos[(size_t)ch] = (int)(2 * e + i);
         }
         up_e[4 * e + 3] = k;
+        up_tn[e] = t[v];
     }
     for (size_t e = 0; e < E_dn; ++e) {
         const int v = dn_nodes[e], c0 = ch_ptr[(size_t)v], k = ch_ptr[(size_t)v + 1] - c0;
@@ -1125,6 +1127,7 @@ mds_status mds_set_tree_prior(mds_ctx c, int64_t n_nodes, const int64_t* parent,
         }
         dn_e[4 * e + 3] = k;
     }
+    for (size_t e = 0; e < E_up; ++e) up_dpos[e] = dn_pos[(size_t)up_nodes[e]];
     std::vector<int> ints;
     auto put = [&](const std::vector<int>& v) {     // 16-byte aligned offsets (int4 views)
         while (ints.size() % 4) ints.push_back(0);
@@ -1133,11 +1136,13 @@ mds_status mds_set_tree_prior(mds_ctx c, int64_t n_nodes, const int64_t* parent,
         return off;
     };
     const size_t o_upe = put(up_e), o_dne = put(dn_e), o_chp = put(ch_ptr), o_chi = put(ch_idx), o_upp = put(up_ptr),
-                 o_dnp = put(dn_ptr), o_rt = put(roots), o_pos = put(dn_pos);
+                 o_dnp = put(dn_ptr), o_rt = put(roots), o_pos = put(dn_pos), o_udp = put(up_dpos),
+                 o_tup = put(tip_upos);
     // doubles: t | pw | cq | cw | up_t | dn_t | up_m | dn_sib | msg   (16-byte aligned pieces)
     auto al2 = [](size_t v) { return (v + 1) & ~(size_t)1; };
     const size_t o_t = 0, o_pw = al2(o_t + nn), o_cq = al2(o_pw + nn), o_cw = al2(o_cq + nn), o_upt = al2(o_cw + nn),
-                 o_dnt = al2(o_upt + 2 * E_up), o_upm = al2(o_dnt + 2 * E_dn), o_sib = al2(o_upm + (nn - n) * d), o_msg = al2(o_sib + 2 * E_dn * (d + 1)),
+                 o_dnt = al2(o_upt + 2 * E_up), o_utn = al2(o_dnt + 2 * E_dn), o_upx = al2(o_utn + E_up),
+                 o_upm = al2(o_upx + 2 * E_up * d), o_sib = al2(o_upm + (nn - n) * d), o_msg = al2(o_sib + 2 * E_dn * (d + 1)),
                  n_dbl = al2(o_msg + (nn - n) * (d + 1));
     mds_status st;
     if ((st = dalloc(c, &c->d_tree_int, std::max<size_t>(ints.size(), 1))) ||
@@ -1150,6 +1155,7 @@ mds_status mds_set_tree_prior(mds_ctx c, int64_t n_nodes, const int64_t* parent,
     CK(cudaMemcpy(c->d_tree_dbl + o_t, t, nn * sizeof(double), cudaMemcpyHostToDevice));
     if (E_up) CK(cudaMemcpy(c->d_tree_dbl + o_upt, up_t.data(), up_t.size() * sizeof(double), cudaMemcpyHostToDevice));
     if (E_dn) CK(cudaMemcpy(c->d_tree_dbl + o_dnt, dn_t.data(), dn_t.size() * sizeof(double), cudaMemcpyHostToDevice));
+    if (E_up) CK(cudaMemcpy(c->d_tree_dbl + o_utn, up_tn.data(), up_tn.size() * sizeof(double), cudaMemcpyHostToDevice));
     CK(cudaMemset(c->d_gprior, 0, (size_t)c->npad * d * sizeof(double)));
     TreeArgs& A = c->ta;
     A = TreeArgs{};
@@ -1161,6 +1167,10 @@ mds_status mds_set_tree_prior(mds_ctx c, int64_t n_nodes, const int64_t* parent,
     A.up_lvl_ptr = c->d_tree_int + o_upp;
     A.up_e = reinterpret_cast<const int4*>(c->d_tree_int + o_upe);
     A.up_t = reinterpret_cast<const double2*>(c->d_tree_dbl + o_upt);
+    A.up_tn = c->d_tree_dbl + o_utn;
+    A.up_dpos = c->d_tree_int + o_udp;
+    A.tip_upos = c->d_tree_int + o_tup;
+    A.up_x = c->d_tree_dbl + o_upx;
     A.n_up = hmax;
     A.up_narrow = up_narrow;
     A.dn_lvl_ptr = c->d_tree_int + o_dnp;
@@ -1191,6 +1201,10 @@ mds_status mds_set_tree_prior(mds_ctx c, int64_t n_nodes, const int64_t* parent,
         static unsigned long long* prof = nullptr;
         if (!prof) cudaMalloc(&prof, 256 * sizeof(unsigned long long));
         cudaMemset(prof, 0, 256 * sizeof(unsigned long long));
+        if (std::getenv("MDS_TREE_NO_PREFETCH")) {
+            const unsigned long long one = 1;
+            cudaMemcpy(prof + 255, &one, sizeof(one), cudaMemcpyHostToDevice);
+        }
         A.prof = prof;
         fprintf(stderr, "tree levels: up %d (narrow from %d), dn %d (narrow below %d)\n", hmax, up_narrow, n_dn,
                 dn_narrow);
@@ -1205,7 +1219,7 @@ void report_tree_profile(mds_ctx c) {
     unsigned long long h[256];
     cudaMemcpy(h, c->ta.prof, sizeof(h), cudaMemcpyDeviceToHost);
     fprintf(stderr, "tree us:");
-    for (int k = 1; k < 256; ++k)
+    for (int k = 1; k < 255; ++k)
         if (h[k]) fprintf(stderr, " %d:%.2f", k, (h[k] - h[0]) * 1e-3);
     fprintf(stderr, "\n");
 }

@@ -25,8 +25,9 @@
 // pre-order, the children's up messages gathered by wide parallel passes), so
 // a level's operands are one coalesced round of loads issued before the
 // barrier that publishes the previous level -- and one level ahead on the
-// narrow levels near the roots, which run on warp 0 alone with __syncwarp; one
-// division per contrast; the logs of the contrast variances are deferred to the
+// narrow levels near the roots, which run on warp 0 alone with __syncwarp;
+// reciprocals from the MUFU seed + one cubic Newton step (no IEEE division
+// subroutine on the level chain); the logs of the contrast variances are deferred to the
 // final parallel reduction.  Tip
 // gradients are written as the pre-order reaches them.  Node contributions are
 // summed in a fixed order: deterministic, no atomics.
@@ -49,6 +50,10 @@ struct TreeArgs {
     const int* up_lvl_ptr;    // [n_up + 1]
     const int4* up_e;         // {slot, src0, src1, k}; src = internal slot, or -1 - item for a tip
     const double2* up_t;      // {t(child 0), t(child 1)}
+    const double* up_tn;      // [E_up] the node's own branch length (root: prior variance)
+    const int* up_dpos;       // [E_up] the node's slot in its parent's pre-order entry (dn_pos of the node)
+    const int* tip_upos;      // [n] 2 e + i if item i is child i < 2 of post-order entry e, else -1
+    double* up_x;             // [E_up][2][D] x of tip children 0/1, scattered from X at the start of a walk
     int n_up;
     int up_narrow;            // first post-order level from which every level has <= 32 nodes
     // pre-order entries (nodes with children by depth)

@@ -4,6 +4,7 @@
 #pragma once
 #include <cuda_runtime.h>
 #include "mds_tree.cuh"
+#include "mds_math.cuh"
 
 namespace mdsk {
 namespace treek {
@@ -44,16 +45,16 @@ struct UpEnt {
 };
 template <int D>
 __device__ __forceinline__ void load_up(const TreeArgs& a, int e, UpEnt<D>& u) {
-    const int n = a.n_items;
+    // every operand indexed by the entry: one round of independent, coalesced loads
     u.e = a.up_e[e];
     u.t = a.up_t[e];
-    u.tn = a.t[n + u.e.x];
-    u.pos = a.dn_pos[n + u.e.x];
-    const int s0 = u.e.y, s1 = u.e.z;
+    u.tn = a.up_tn[e];
+    u.pos = a.up_dpos[e];
+    const double* xp = a.up_x + (size_t)e * 2 * D;
 #pragma unroll
     for (int r = 0; r < D; ++r) {
-        u.x0[r] = s0 < 0 ? a.x[(int64_t)(-1 - s0) * D + r] : 0.0;
-        u.x1[r] = (s1 < 0 && u.e.w >= 2) ? a.x[(int64_t)(-1 - s1) * D + r] : 0.0;
+        u.x0[r] = xp[r];
+        u.x1[r] = xp[D + r];
     }
 }
 
@@ -111,7 +112,7 @@ __device__ __forceinline__ void absorb(const TreeArgs& a, double* M, const UpEnt
         }
         const double wi = av + tc;
         const double w = W + wi;
-        const double rw = 1.0 / w;
+        const double rw = rcp_refined(w);
         double dl[D];
 #pragma unroll
         for (int r = 0; r < D; ++r) dl[r] = am[r] - A[r];
@@ -132,7 +133,7 @@ __device__ __forceinline__ void absorb(const TreeArgs& a, double* M, const UpEnt
     a.cq[n + slot] = -0.5 * q - 0.5 * (k - 1) * (D * LOG_2PI + a.logdet) - 0.5 * D * lw;
     a.cw[n + slot] = wp;
     // the node's up message as its parent's pre-order entry will read it
-    const double p = 1.0 / (W + u.tn);
+    const double p = rcp_refined(W + u.tn);
     a.pw[n + slot] = p;
 #pragma unroll
     for (int r = 0; r < D; ++r) a.up_m[(size_t)slot * D + r] = A[r];
@@ -149,8 +150,8 @@ __device__ __forceinline__ void absorb(const TreeArgs& a, double* M, const UpEnt
 template <int D>
 __device__ __forceinline__ void emit(const TreeArgs& a, double* M, int c, double tc, double P, const double (&Mm)[D]) {
     const int n = a.n_items;
-    const double iv = 1.0 / P;
-    const double ovc = 1.0 / (iv + tc);
+    const double iv = rcp_refined(P);
+    const double ovc = rcp_refined(iv + tc);
     if (c < n) {
         // d log p / d x_c = -Sigma^-1 (x_c - m_c) / v_c
         double rr[D];
@@ -225,7 +226,7 @@ __device__ __forceinline__ void tree_prior_block(const TreeArgs& a, double* dyn,
     stamp(a, 0);
     // The level walk is a chain of dependent loads: pull every static array into
     // L2 up front (one TMA bulk prefetch each), so the chain runs at L2 latency.
-    if (tid == 0) {
+    if (tid == 0 && !(a.prof && a.prof[255] == 1)) {   // (profiling switch: prof[255] = 1 skips the prefetch)
         auto pf = [](const void* p, size_t bytes) {
             bytes &= ~(size_t)15;
             if (bytes)
@@ -236,10 +237,36 @@ __device__ __forceinline__ void tree_prior_block(const TreeArgs& a, double* dyn,
         pf(a.up_t, (size_t)eu * sizeof(double2));
         pf(a.dn_e, (size_t)ed * sizeof(int4));
         pf(a.dn_t, (size_t)ed * sizeof(double2));
+        pf(a.up_tn, (size_t)eu * sizeof(double));
+        pf(a.up_dpos, (size_t)eu * sizeof(int));
+        pf(a.tip_upos, (size_t)n * sizeof(int));
         pf(a.t, (size_t)a.n_nodes * sizeof(double));
         pf(a.dn_pos, (size_t)a.n_nodes * sizeof(int));
         pf(a.x, (size_t)n * D * sizeof(double));
     }
+    stamp(a, 98);
+    // tips' x into their parents' post-order entries (coalesced reads, scattered
+    // stores that nothing waits on)
+    // (8 tips per thread per round: all loads in flight before the stores)
+    for (int i0 = tid; i0 < n; i0 += 8 * NT) {
+        int pos[8];
+        double xv[8][D];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int i = i0 + u * NT;
+            pos[u] = i < n ? a.tip_upos[i] : -1;
+#pragma unroll
+            for (int r = 0; r < D; ++r) xv[u][r] = i < n ? a.x[(int64_t)i * D + r] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+            if (pos[u] >= 0) {
+#pragma unroll
+                for (int r = 0; r < D; ++r) a.up_x[(size_t)pos[u] * D + r] = xv[u][r];
+            }
+    }
+    __syncthreads();
+    stamp(a, 99);
     // Level loop with a one-ahead pipeline: the static operands of the next chunk
     // (same level, or the next level's first chunk) are loaded before working on
     // the current one; `sync` publishes the previous level's writes.
@@ -293,7 +320,7 @@ __device__ __forceinline__ void tree_prior_block(const TreeArgs& a, double* dyn,
             for (int u = 0; u < 4; ++u) {
                 const int i = i0 + u * (NT - 32);
                 if (i >= n) break;
-                const double p = 1.0 / tv[u];
+                const double p = rcp_refined(tv[u]);
                 a.pw[i] = p;
                 a.cq[i] = 0.0;
                 a.cw[i] = 1.0;
@@ -321,7 +348,7 @@ __device__ __forceinline__ void tree_prior_block(const TreeArgs& a, double* dyn,
         a.cq[r] += -0.5 * quad<D>(a.sinv, dl) / w - 0.5 * (D * LOG_2PI + a.logdet);
         a.cw[r] *= w;
         if (r < n) {
-            const double iv = 1.0 / a.t[r];
+            const double iv = rcp_refined(a.t[r]);
 #pragma unroll
             for (int q = 0; q < D; ++q) {
                 double g = 0.0;
@@ -338,7 +365,7 @@ __device__ __forceinline__ void tree_prior_block(const TreeArgs& a, double* dyn,
         double* mr = M + (size_t)(r - n) * (D + 1);
 #pragma unroll
         for (int q = 0; q < D; ++q) mr[q] = a.mu0[q];
-        mr[D] = 1.0 / a.t[r];
+        mr[D] = rcp_refined(a.t[r]);
     }
     __syncthreads();
     stamp(a, 101);
