@@ -116,6 +116,7 @@ struct mds_ctx_s {
     double* d_tree_dbl = nullptr;    // t, messages, contributions (one allocation)
     double* d_gprior = nullptr;      // [npad][d] d log prior / dX at the last evaluated point
     double* d_logprior = nullptr;    // [2]: log prior there, saved copy
+    unsigned int* d_tips_done = nullptr;   // pass kernel: pair CTAs that finished their tips slice
 
     void* d_rwbuf = nullptr;         // single-location sweeps: rows, z, u, outputs
     size_t rwbuf_bytes = 0;
@@ -183,7 +184,7 @@ void free_all(mds_ctx c) {
                   c->d_bad, c->d_count, c->d_partial, c->d_gathered, c->d_p, c->d_gl, c->d_xnext, c->d_xsave,
                   c->d_glsave, c->d_liksave, c->d_H, c->d_H0, c->d_prof, c->d_rwbuf,
                   c->d_cv_ij, c->d_cv_y, c->d_cv_max, c->d_cv_sum, c->d_cv_out,
-                  c->d_tree_int, c->d_tree_dbl, c->d_gprior, c->d_logprior};
+                  c->d_tree_int, c->d_tree_dbl, c->d_gprior, c->d_logprior, c->d_tips_done};
     for (void* p : ps)
         if (p) cudaFree(p);
     for (auto& e : c->evpool)
@@ -279,6 +280,8 @@ mds_status run_pass(mds_ctx c, const double* xeval, double* grad_out, double* li
         const size_t need = (size_t)(c->ta.n_nodes - c->n) * (c->d + 1) * sizeof(double);
         a.tree.smem = need <= c->smem ? std::max<size_t>(need, 16) : 0;   // else the global message buffer
         a.tree.prof = nullptr;
+        a.tree.ext_tips = c->pair_ctas;          // the pair CTAs run the tips pass
+        a.tree.tips_done = c->d_tips_done;
         a.gprior = c->d_gprior;
     }
     if (timed) CK(cudaEventRecord(next_event(c), s));
@@ -1148,8 +1151,10 @@ mds_status mds_set_tree_prior(mds_ctx c, int64_t n_nodes, const int64_t* parent,
     if ((st = dalloc(c, &c->d_tree_int, std::max<size_t>(ints.size(), 1))) ||
         (st = dalloc(c, &c->d_tree_dbl, n_dbl)) ||
         (!c->d_gprior && (st = dalloc(c, &c->d_gprior, (size_t)c->npad * d))) ||
-        (!c->d_logprior && (st = dalloc(c, &c->d_logprior, 2))))
+        (!c->d_logprior && (st = dalloc(c, &c->d_logprior, 2))) ||
+        (!c->d_tips_done && (st = dalloc(c, &c->d_tips_done, 1))))
         return st;
+    CK(cudaMemset(c->d_tips_done, 0, sizeof(unsigned int)));
     CK(cudaMemcpy(c->d_tree_int, ints.data(), ints.size() * sizeof(int), cudaMemcpyHostToDevice));
     CK(cudaMemset(c->d_tree_dbl, 0, n_dbl * sizeof(double)));
     CK(cudaMemcpy(c->d_tree_dbl + o_t, t, nn * sizeof(double), cudaMemcpyHostToDevice));

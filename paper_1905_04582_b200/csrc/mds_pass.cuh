@@ -322,6 +322,17 @@ pass_kernel(PassArgs a) {
     // PAPER.md:243-246) while the others run phase A; the grid barrier below
     // orders phase B's leapfrog update after both.
     const bool skip_a = blockIdx.x >= a.pair_ctas;
+    if (TREE && !skip_a) {
+        // this CTA's slice of the tree walk's tips pass (a few tips per CTA), then check in
+        const int per = (a.tree.n_items + a.pair_ctas - 1) / a.pair_ctas;
+        const int lo = min(a.tree.n_items, (int)blockIdx.x * per), hi = min(a.tree.n_items, lo + per);
+        treek::tips_pass<D>(a.tree, lo, hi, threadIdx.x, WPC * 32);
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            __threadfence();
+            atomicAdd(a.tree.tips_done, 1u);
+        }
+    }
     if (TREE && blockIdx.x == gridDim.x - 1)
         treek::tree_prior_block<D, WPC * 32>(a.tree, reinterpret_cast<double*>(dsm), exptab);
     unsigned not_ready = 0;                  // profiling: units whose data had not landed yet

@@ -82,6 +82,11 @@ struct TreeArgs {
     double* grad;             // [n_items][D]  d log p / d X
     double* logp;             // [1]
     unsigned long long* prof; // optional (MDS_PROFILE_TREE=1): globaltimer stamps per level
+    // inside the pass kernel: the tips pass is split over the pair CTAs, which
+    // count themselves in tips_done; the walk waits for ext_tips arrivals (0 = the
+    // walk does the tips pass itself)
+    int ext_tips;
+    unsigned int* tips_done;
 };
 
 constexpr size_t TREE_SMEM_MAX = 200 * 1024;

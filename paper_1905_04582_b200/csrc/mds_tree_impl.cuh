@@ -215,6 +215,46 @@ __device__ __forceinline__ void spread(const TreeArgs& a, double* M, const DnEnt
 }
 
 
+// Every tip-side operand, for items [i_lo, i_hi) (coalesced reads, scattered
+// stores nothing waits on): x into the parent's post-order entry; (x, 1/t) into
+// the parent's pre-order entry; the tip's precision and its (empty)
+// contributions.  8 tips per thread per round: loads in flight first.
+template <int D>
+__device__ __forceinline__ void tips_pass(const TreeArgs& a, int i_lo, int i_hi, int tid, int nt) {
+    for (int i0 = i_lo + tid; i0 < i_hi; i0 += 8 * nt) {
+        int pos[8], dps[8];
+        double xv[8][D], tv[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int i = i0 + u * nt;
+            pos[u] = i < i_hi ? a.tip_upos[i] : -1;
+            dps[u] = i < i_hi ? a.dn_pos[i] : -1;
+            tv[u] = i < i_hi ? a.t[i] : 1.0;
+#pragma unroll
+            for (int r = 0; r < D; ++r) xv[u][r] = i < i_hi ? a.x[(int64_t)i * D + r] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int i = i0 + u * nt;
+            if (i >= i_hi) break;
+            const double p = rcp_refined(tv[u]);
+            a.pw[i] = p;
+            a.cq[i] = 0.0;
+            a.cw[i] = 1.0;
+            if (pos[u] >= 0) {
+#pragma unroll
+                for (int r = 0; r < D; ++r) a.up_x[(size_t)pos[u] * D + r] = xv[u][r];
+            }
+            if (dps[u] >= 0) {
+                double* sp = a.dn_sib + (size_t)dps[u] * (D + 1);
+#pragma unroll
+                for (int r = 0; r < D; ++r) sp[r] = xv[u][r];
+                sp[D] = p;
+            }
+        }
+    }
+}
+
 // The whole walk on one CTA of NT threads.  dyn: the internal-node messages
 // when a.smem != 0 (else a.msg is used); red: NT / 32 + 1 doubles of scratch.
 template <int D, int NT>
@@ -245,25 +285,16 @@ __device__ __forceinline__ void tree_prior_block(const TreeArgs& a, double* dyn,
         pf(a.x, (size_t)n * D * sizeof(double));
     }
     stamp(a, 98);
-    // tips' x into their parents' post-order entries (coalesced reads, scattered
-    // stores that nothing waits on)
-    // (8 tips per thread per round: all loads in flight before the stores)
-    for (int i0 = tid; i0 < n; i0 += 8 * NT) {
-        int pos[8];
-        double xv[8][D];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-            const int i = i0 + u * NT;
-            pos[u] = i < n ? a.tip_upos[i] : -1;
-#pragma unroll
-            for (int r = 0; r < D; ++r) xv[u][r] = i < n ? a.x[(int64_t)i * D + r] : 0.0;
+    if (!a.ext_tips) tips_pass<D>(a, 0, n, tid, NT);
+    else {
+        // the pass kernel's pair CTAs did the tips pass (one slice each) at launch:
+        // wait until all have published theirs, then re-arm the counter
+        if (tid == 0) {
+            const unsigned want = (unsigned)a.ext_tips;
+            while (atomicAdd(a.tips_done, 0u) < want) __nanosleep(200);
+            __threadfence();
+            atomicExch(a.tips_done, 0u);
         }
-#pragma unroll
-        for (int u = 0; u < 8; ++u)
-            if (pos[u] >= 0) {
-#pragma unroll
-                for (int r = 0; r < D; ++r) a.up_x[(size_t)pos[u] * D + r] = xv[u][r];
-            }
     }
     __syncthreads();
     stamp(a, 99);
@@ -300,39 +331,10 @@ __device__ __forceinline__ void tree_prior_block(const TreeArgs& a, double* dyn,
     auto bar_warp = [] { __syncwarp(); };
 
     // ---- post-order (by height): wide levels on the CTA, narrow ones on warp 0
-    // while the other warps set up the tips (precision, pre-order entry, contributions)
     run_levels(UpEnt<D>{}, ld_up, wk_up, a.up_lvl_ptr, 0, a.up_narrow, NT, tid, bar_cta, 3);
     __syncthreads();
     stamp(a, 2);
-    if (tid < 32) {
-        run_levels(UpEnt<D>{}, ld_up, wk_up, a.up_lvl_ptr, a.up_narrow, a.n_up, 32, tid, bar_warp, 3);
-    } else {
-        for (int i0 = tid - 32; i0 < n; i0 += 4 * (NT - 32)) {
-            double tv[4];
-            int pv[4];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const int i = i0 + u * (NT - 32);
-                tv[u] = i < n ? a.t[i] : 1.0;
-                pv[u] = i < n ? a.dn_pos[i] : -1;
-            }
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const int i = i0 + u * (NT - 32);
-                if (i >= n) break;
-                const double p = rcp_refined(tv[u]);
-                a.pw[i] = p;
-                a.cq[i] = 0.0;
-                a.cw[i] = 1.0;
-                if (pv[u] >= 0) {
-                    double* sp = a.dn_sib + (size_t)pv[u] * (D + 1);
-#pragma unroll
-                    for (int r = 0; r < D; ++r) sp[r] = a.x[(int64_t)i * D + r];
-                    sp[D] = p;
-                }
-            }
-        }
-    }
+    if (tid < 32) run_levels(UpEnt<D>{}, ld_up, wk_up, a.up_lvl_ptr, a.up_narrow, a.n_up, 32, tid, bar_warp, 3);
     __syncthreads();
     stamp(a, 100);
     // roots: contrast against mu0 (variance v_root + tau_root); an unsequenced item
