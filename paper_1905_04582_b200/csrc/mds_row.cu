@@ -47,13 +47,37 @@ __device__ __forceinline__ void ell2<float, false>(float s0, float s1, float y, 
     pair_f32<false, true, false>(s1, y, P, e1, u);
 }
 
+// The first RPF columns of a thread (j = rank*NT + tid + c*CL*NT) are staged in
+// registers one update ahead: y_ij (static) and x_j (patched if the update in
+// between moved row j), so an update's gathers are already in flight while the
+// previous one reduces and decides.
+constexpr int RPF = 4;
+template <typename T, int D>
+struct RowCols {
+    T y[RPF];
+    T x[RPF][D];
+};
+
+template <typename T, int D>
+__device__ __forceinline__ void row_stage(const RowArgs& a, int64_t i, int rank, RowCols<T, D>& c) {
+    const T* __restrict__ Y = static_cast<const T*>(a.y);
+#pragma unroll
+    for (int q = 0; q < RPF; ++q) {
+        const int64_t j = (int64_t)rank * ROW_THREADS + threadIdx.x + (int64_t)q * ROW_CLUSTER * ROW_THREADS;
+        const bool ok = j < a.n && j != i;
+        c.y[q] = ok ? (j < i ? y_pair<T>(Y, a.row_local, i, j) : y_pair<T>(Y, a.row_local, j, i)) : T(NAN);
+#pragma unroll
+        for (int k = 0; k < D; ++k) c.x[q][k] = ok ? (T)a.x[j * D + k] : T(0);
+    }
+}
+
 // Row i's share of Delta owned by this CTA (columns j = rank*NT + tid, stride
-// CL*NT) between positions xn and xo (both [D] in shared memory).  Fixed
-// order: per-thread sum over its columns in ascending j, warp butterfly, then
-// the warp sums in order -> one partial per CTA.
+// CL*NT) between positions xn and xo (both [D] in shared memory); the first
+// RPF columns come staged in c.  Fixed order: per-thread sum over its columns in
+// ascending j, warp butterfly, then the warp sums in order -> one partial per CTA.
 template <typename T, int D, bool TRUNC>
 __device__ double row_partial(const RowArgs& a, int64_t i, const double* xn, const double* xo, const double* exptab,
-                              double* red, int rank) {
+                              double* red, int rank, const RowCols<T, D>& c) {
     const T* __restrict__ Y = static_cast<const T*>(a.y);
     const double* X = a.x;     // not __restrict__/nc: the sweep writes X between updates
     double acc = 0.0;
@@ -63,21 +87,29 @@ __device__ double row_partial(const RowArgs& a, int64_t i, const double* xn, con
         xnr[k] = (T)xn[k];
         xor_[k] = (T)xo[k];
     }
-    for (int64_t j = (int64_t)rank * ROW_THREADS + threadIdx.x; j < a.n; j += (int64_t)ROW_CLUSTER * ROW_THREADS) {
-        if (j == i) continue;
-        const T y = j < i ? y_pair<T>(Y, a.row_local, i, j) : y_pair<T>(Y, a.row_local, j, i);
-        if (is_missing(y)) continue;
+    auto term = [&](T y, const T* xj) {
+        if (is_missing(y) || y != y) return;     // missing, or not a column of this thread
         T sn = T(0), so = T(0);
 #pragma unroll
         for (int k = 0; k < D; ++k) {
-            const T xj = (T)X[j * D + k];
-            const T dn = xnr[k] - xj, dl = xor_[k] - xj;
+            const T dn = xnr[k] - xj[k], dl = xor_[k] - xj[k];
             sn = fma(dn, dn, sn);
             so = fma(dl, dl, so);
         }
         T en, eo;
         ell2<T, TRUNC>(sn, so, y, a.P, exptab, en, eo);
         acc += double(en) - double(eo);
+    };
+#pragma unroll
+    for (int q = 0; q < RPF; ++q) term(c.y[q], c.x[q]);
+    for (int64_t j = (int64_t)rank * ROW_THREADS + threadIdx.x + (int64_t)RPF * ROW_CLUSTER * ROW_THREADS; j < a.n;
+         j += (int64_t)ROW_CLUSTER * ROW_THREADS) {
+        if (j == i) continue;
+        const T y = j < i ? y_pair<T>(Y, a.row_local, i, j) : y_pair<T>(Y, a.row_local, j, i);
+        T xj[D];
+#pragma unroll
+        for (int k = 0; k < D; ++k) xj[k] = (T)X[j * D + k];
+        term(y, xj);
     }
 #pragma unroll
     for (int m = 16; m >= 1; m >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, m);
@@ -111,21 +143,40 @@ __global__ void __launch_bounds__(ROW_THREADS, 1) row_kernel(RowArgs a) {
     build_exptab(exptab, a.P);
     const int64_t K = a.K == 0 ? 1 : a.K;
     unsigned long long nacc = 0;
+    RowCols<T, D> cur, nxt;
+    // everything an update needs that does not depend on the previous decision is
+    // loaded one update ahead: its row, the staged columns, x_i (patched if the
+    // previous update moved the same row), z and u
+    int64_t i_nx = a.K == 0 ? a.i0 : a.rows[0];
+    row_stage<T, D>(a, i_nx, rank, nxt);
+    double xi_nx = threadIdx.x < D ? a.x[i_nx * D + threadIdx.x] : 0.0;
     for (int64_t k = 0; k < K; ++k) {
-        const int64_t i = a.K == 0 ? a.i0 : a.rows[k];
+        const int64_t i = i_nx;
+        const double xi = xi_nx;
+        cur = nxt;
+        const double zk = (a.K > 0 && threadIdx.x < D) ? a.z[k * D + threadIdx.x] : 0.0;
+        const double uk = (a.K > 0 && threadIdx.x == 0) ? a.u[k] : 1.0;
+        if (k + 1 < K) {                       // in flight during this update
+            i_nx = a.rows[k + 1];
+            row_stage<T, D>(a, i_nx, rank, nxt);
+            if (threadIdx.x < D) xi_nx = a.x[i_nx * D + threadIdx.x];
+        }
         if (threadIdx.x < D) {
-            const double v = a.x[i * D + threadIdx.x];
-            xo[threadIdx.x] = v;
-            xn[threadIdx.x] = a.K == 0 ? a.xnew[threadIdx.x] : __fma_rn(a.step, a.z[k * D + threadIdx.x], v);
+            xo[threadIdx.x] = xi;
+            xn[threadIdx.x] = a.K == 0 ? a.xnew[threadIdx.x] : __fma_rn(a.step, zk, xi);
         }
         __syncthreads();
-        const double p = row_partial<T, D, TRUNC>(a, i, xn, xo, exptab, red, rank);
+        const double p = row_partial<T, D, TRUNC>(a, i, xn, xo, exptab, red, rank, cur);
         const int par = (int)(k & 1);
         if (threadIdx.x == 0) part[par] = p;
         cluster.sync();                    // every CTA's partial of this update is published
         if (threadIdx.x == 0) {
+            double pr[ROW_CLUSTER];
+#pragma unroll
+            for (int r = 0; r < ROW_CLUSTER; ++r) pr[r] = *cluster.map_shared_rank(&part[par], r);
             double dl = 0.0;
-            for (int r = 0; r < ROW_CLUSTER; ++r) dl += *cluster.map_shared_rank(&part[par], r);
+#pragma unroll
+            for (int r = 0; r < ROW_CLUSTER; ++r) dl += pr[r];
             if (a.K == 0) {
                 if (rank == 0) *a.delta = dl;
                 decide = 0;
@@ -138,7 +189,7 @@ __global__ void __launch_bounds__(ROW_THREADS, 1) row_kernel(RowArgs a) {
                     po = fma(xo[q], xo[q], po);
                 }
                 const double lr = dl - 0.5 * (pn - po) * a.inv_tau2;
-                decide = isfinite(lr) && log(a.u[k]) < lr;
+                decide = isfinite(lr) && log(uk) < lr;
                 if (decide) {
 #pragma unroll
                     for (int q = 0; q < D; ++q) a.x[i * D + q] = xn[q];
@@ -147,6 +198,18 @@ __global__ void __launch_bounds__(ROW_THREADS, 1) row_kernel(RowArgs a) {
             }
         }
         __syncthreads();   // this CTA's copy of X[i] (if accepted) is visible to its next column reads
+        if (decide && k + 1 < K) {
+            // values staged for the next update that predate this move of row i
+            if (i_nx == i && threadIdx.x < D) xi_nx = xn[threadIdx.x];
+#pragma unroll
+            for (int q = 0; q < RPF; ++q) {
+                const int64_t j = (int64_t)rank * ROW_THREADS + threadIdx.x + (int64_t)q * ROW_CLUSTER * ROW_THREADS;
+                if (j == i) {
+#pragma unroll
+                    for (int kk = 0; kk < D; ++kk) nxt.x[q][kk] = (T)xn[kk];
+                }
+            }
+        }
     }
     if (threadIdx.x == 0 && rank == 0 && a.K > 0) *a.accepted = nacc;
     cluster.sync();        // no CTA exits while another may still read its partials
