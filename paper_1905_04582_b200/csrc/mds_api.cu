@@ -586,8 +586,8 @@ mds_status build_schedule(mds_ctx c) {
     if (pe && pe[0] == '1') {
         if (c->d_prof) cudaFree(c->d_prof);
         c->d_prof = nullptr;
-        if ((st = dalloc(c, &c->d_prof, (size_t)G * 7))) return st;
-        CK(cudaMemset(c->d_prof, 0, (size_t)G * 7 * sizeof(unsigned long long)));
+        if ((st = dalloc(c, &c->d_prof, (size_t)G * 9))) return st;
+        CK(cudaMemset(c->d_prof, 0, (size_t)G * 9 * sizeof(unsigned long long)));
     }
     return MDS_OK;
 }
@@ -595,7 +595,7 @@ mds_status build_schedule(mds_ctx c) {
 // MDS_PROFILE_PHASES=1: per-CTA phase times of the last pass, printed to stderr
 void report_phases(mds_ctx c) {
     if (!c->d_prof) return;
-    std::vector<unsigned long long> h((size_t)c->grid * 7);
+    std::vector<unsigned long long> h((size_t)c->grid * 9);
     if (cudaMemcpy(h.data(), c->d_prof, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost)) return;
     unsigned long long t0 = ~0ull, t3 = 0;
     std::vector<double> a, w, b, s0, f0;
@@ -618,6 +618,19 @@ void report_phases(mds_ctx c) {
     };
     std::fprintf(stderr, "[mds phases us] span %.2f | A end: %s | sync wait: %s | B: %s\n", (t3 - t0) * 1e-3,
                  st(a).c_str(), st(w).c_str(), st(b).c_str());
+    {   // phase B of the job CTAs: slab loads, CTA reduction, final (update + stores)
+        std::vector<double> l1, l2, l3;
+        for (int g = 0; g < c->grid; ++g) {
+            const unsigned long long s7 = h[(size_t)c->grid * 7 + g], s8 = h[(size_t)c->grid * 8 + g];
+            if (!s7 || !s8 || s7 < h[4 * g + 2]) continue;
+            l1.push_back((s7 - h[4 * g + 2]) * 1e-3);
+            l2.push_back((s8 - s7) * 1e-3);
+            l3.push_back((h[4 * g + 3] - s8) * 1e-3);
+        }
+        if (!l1.empty())
+            std::fprintf(stderr, "[mds phases us] B jobs: slab loads %s | CTA sum %s | update+stores %s\n",
+                         st(l1).c_str(), st(l2).c_str(), st(l3).c_str());
+    }
     if (!f0.empty())
         std::fprintf(stderr, "[mds phases us] CTA start: %s | warp 0 first unit landed: %s\n", st(s0).c_str(),
                      st(f0).c_str());

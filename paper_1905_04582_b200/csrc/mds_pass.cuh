@@ -548,24 +548,29 @@ pass_kernel(PassArgs a) {
         // 8 rows in flight (rows past the end add exact zeros)
         const double* __restrict__ sb = a.slabs + (size_t)q0 * TB * D;
         for (int k0 = warp; k0 < nq; k0 += 8 * WPC) {
+            // all (element, slab) loads of the round first, then the adds in order:
+            // one L2 round trip per round instead of one per element
+            A x[EPLMAX][8];
 #pragma unroll
             for (int ee = 0; ee < EPLMAX; ++ee) {
-                if (ee < epl && el[ee] < TB * D) {
-                    A x[8];
+                const bool on = ee < epl && el[ee] < TB * D;
 #pragma unroll
-                    for (int r = 0; r < 8; ++r) {
-                        const int k = k0 + r * WPC;
-                        x[r] = k < nq ? sb[(size_t)k * TB * D + el[ee]] : A(0);
-                    }
-#pragma unroll
-                    for (int r = 0; r < 8; ++r) acc[ee] += x[r];
+                for (int r = 0; r < 8; ++r) {
+                    const int k = k0 + r * WPC;
+                    x[ee][r] = (on && k < nq) ? sb[(size_t)k * TB * D + el[ee]] : A(0);
                 }
             }
+#pragma unroll
+            for (int ee = 0; ee < EPLMAX; ++ee)
+#pragma unroll
+                for (int r = 0; r < 8; ++r) acc[ee] += x[ee][r];
         }
+        if (a.prof && threadIdx.x == 0) a.prof[gridDim.x * 7 + blockIdx.x] = gtimer();   // slab sums loaded
 #pragma unroll
         for (int ee = 0; ee < EPLMAX; ++ee)
             if (ee < epl) red[ee][warp][lane] = acc[ee];
         __syncthreads();
+        if (a.prof && threadIdx.x == 0) a.prof[gridDim.x * 8 + blockIdx.x] = gtimer();   // CTA partials in smem
         if (warp < epl) {
             const int ee = warp;
             const int e_in = ch * CH + ee * 32 + lane;
