@@ -196,3 +196,27 @@ def test_tree_prior_errors(mds):
         lp, g = c.tree_prior()
     ref_lp, _ = tree.tree_prior(good_p, good_t, np.zeros((4, 2)))
     assert lp == pytest.approx(ref_lp, rel=1e-12)
+
+
+def test_fp32_leapfrog_with_tree_prior(mds):
+    """fp32 storage/pair math (reading R15) with the tree walk fused into the
+    leapfrog pass (pass_kernel<float, D, T, LEAPFROG_TREE>): trajectory vs the
+    oracle on fp32-rounded inputs, fp32 tolerance."""
+    import torch
+    n, d = 350, 3
+    w = workload.Workload(n, d, p_missing=0.05, seed=91)
+    y = w.y_packed().astype(np.float32).astype(np.float64)
+    x = w.x0.astype(np.float32).astype(np.float64)
+    parent, t = workload.coalescent_forest(n, 2, 0.05, seed=4, tau0=4.0)
+    p0 = w.normals(4, (n, d))
+    ref = tree.leapfrog_tree(y, x, p0, w.sigma, 0.002, 6, parent, t)
+    with mds.MDS(n, d, "f32") as c:
+        c.set_dissimilarities_packed(y)
+        c.set_locations(x)
+        c.set_sigma(w.sigma)
+        c.set_tree_prior(parent, t)
+        c.leapfrog_device(6, 0.002, 0.0, p0_dev=torch.from_numpy(p0).cuda())
+        xs = c.get_locations()
+        ll = c.log_likelihood()
+    np.testing.assert_allclose(xs, ref["x"], rtol=1e-5, atol=1e-7)
+    assert ll == pytest.approx(ref["loglik"], rel=1e-4)
