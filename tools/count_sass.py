@@ -45,7 +45,9 @@ def main():
                 # the pair loop: one reciprocal-sqrt seed per pair (the tree-prior walk
                 # fused into the leapfrog modes has MUFU.RCP64H loops but no RSQ)
                 nm = sum(1 for a2, t2 in ins if cand[0] <= a2 <= cand[1] and "MUFU.RSQ" in t2)
-                key = (nm, cand[1] - cand[0])
+                # innermost loop among those with the most RSQ: the 4-column group loop
+                # (8 pairs per lane per trip), not the unit / segment / step loops around it
+                key = (nm, -(cand[1] - cand[0]))
                 if best is None or key > best:
                     loop, best = cand, key
         if loop is None:
