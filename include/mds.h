@@ -88,7 +88,8 @@ mds_status mds_create_sharded(int64_t n, int32_t d, int32_t precision, int32_t t
 void mds_destroy(mds_ctx ctx);
 
 /* Use the given cudaStream_t (e.g. torch.cuda.current_stream().cuda_stream)
- * for all later work.  NULL selects the legacy default stream. */
+ * for all later work.  NULL selects the legacy default stream.  Work queued on
+ * the previous stream is waited for first. */
 mds_status mds_set_stream(mds_ctx ctx, void *cuda_stream);
 
 /* ---- inputs ------------------------------------------------------------ */
@@ -112,7 +113,10 @@ mds_status mds_set_dissimilarity_rows(mds_ctx ctx, int64_t i0, int64_t i1, const
 mds_status mds_set_dissimilarity_rows_device(mds_ctx ctx, int64_t i0, int64_t i1,
                                              const double *y_lower_dev);
 
-/* Latent locations X (host, n x d row-major).  Non-finite -> INVALID_ARG. */
+/* Latent locations X (host, n x d row-major).  Non-finite -> INVALID_ARG (X
+ * unchanged).  The values are copied into a context-owned pinned buffer and
+ * uploaded stream-ordered on the context's stream, so x is free when the call
+ * returns and a following evaluation queues right behind the upload. */
 mds_status mds_set_locations(mds_ctx ctx, const double *x);
 
 /* Latent locations from device memory (fp64, n x d), stream-ordered.  Not

@@ -118,6 +118,9 @@ struct mds_ctx_s {
     double* d_logprior = nullptr;    // [2]: log prior there, saved copy
     unsigned int* d_tips_done = nullptr;   // pass kernel: pair CTAs that finished their tips slice
 
+    double* h_xstage = nullptr;      // pinned staging of mds_set_locations (asynchronous upload)
+    cudaEvent_t xstage_done = nullptr;
+
     void* d_rwbuf = nullptr;         // single-location sweeps: rows, z, u, outputs
     size_t rwbuf_bytes = 0;
 
@@ -189,6 +192,8 @@ void free_all(mds_ctx c) {
         if (p) cudaFree(p);
     for (auto& e : c->evpool)
         if (e) cudaEventDestroy(e);
+    if (c->h_xstage) cudaFreeHost(c->h_xstage);
+    if (c->xstage_done) cudaEventDestroy(c->xstage_done);
 }
 
 inline int64_t packed_off(int64_t i) { return i * (i - 1) / 2; }
@@ -839,6 +844,9 @@ void mds_destroy(mds_ctx c) {
 
 mds_status mds_set_stream(mds_ctx c, void* s) {
     GUARD(c);
+    // work already queued on the old stream (e.g. an asynchronous X upload) must
+    // not race with what the new stream runs next
+    if ((cudaStream_t)s != c->stream) CK(cudaStreamSynchronize(c->stream));
     c->stream = (cudaStream_t)s;
     return MDS_OK;
 }
@@ -884,10 +892,33 @@ mds_status mds_set_locations(mds_ctx c, const double* x) {
     GUARD(c);
     if (!x) return fail(c, MDS_E_INVALID_ARG, "NULL locations");
     const int64_t m = c->n * c->d;
-    for (int64_t q = 0; q < m; ++q)
-        if (!std::isfinite(x[q])) return fail(c, MDS_E_INVALID_ARG, "locations must be finite");
-    CK(cudaMemcpyAsync(c->d_x, x, m * sizeof(double), cudaMemcpyHostToDevice, c->stream));
-    CK(cudaStreamSynchronize(c->stream));
+    // validate while copying into a pinned staging buffer owned by the context, so
+    // the upload is asynchronous (the caller's array is free when we return) and
+    // the next evaluation queues right behind it with no host round trip
+    if (!c->h_xstage) {
+        if (cudaMallocHost(&c->h_xstage, (size_t)m * sizeof(double)) != cudaSuccess) {
+            cudaGetLastError();
+            c->h_xstage = nullptr;
+        }
+        if (c->h_xstage) CK(cudaEventCreateWithFlags(&c->xstage_done, cudaEventDisableTiming));
+    }
+    if (!c->h_xstage) {    // no pinned memory: synchronous upload from the caller's array
+        for (int64_t q = 0; q < m; ++q)
+            if (!std::isfinite(x[q])) return fail(c, MDS_E_INVALID_ARG, "locations must be finite");
+        CK(cudaMemcpyAsync(c->d_x, x, m * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+    } else {
+        CK(cudaEventSynchronize(c->xstage_done));      // the previous upload has left the buffer
+        bool ok = true;
+        for (int64_t q = 0; q < m; ++q) {
+            const double v = x[q];
+            ok &= std::isfinite(v);
+            c->h_xstage[q] = v;
+        }
+        if (!ok) return fail(c, MDS_E_INVALID_ARG, "locations must be finite");
+        CK(cudaMemcpyAsync(c->d_x, c->h_xstage, m * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+        CK(cudaEventRecord(c->xstage_done, c->stream));
+    }
     c->x_set = true;
     ++c->version;
     return MDS_OK;
