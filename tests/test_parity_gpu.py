@@ -396,3 +396,25 @@ def test_c5_full_size_sampled_rows(mds):
     assert np.all(err <= np.maximum(1e-9 * np.abs(ref["grad"]), 1e-12)), err.max()
     assert np.all(np.abs(g.sum(0)) <= 1e-12 * np.abs(g).sum(0))
     assert np.isfinite(ll)
+
+
+def test_create_argument_errors(mds):
+    """Degenerate shapes and options are refused at creation (n < 2, d outside
+    1..MDS_D_MAX, unknown precision or truncation flag)."""
+    import ctypes
+    for n, d, prec, trunc in [(1, 2, 0, 1), (0, 2, 0, 1), (10, 0, 0, 1), (10, 9, 0, 1), (10, 2, 7, 1), (10, 2, 0, 2)]:
+        h = ctypes.c_void_p()
+        st = mds._abi.lib.mds_create(n, d, prec, trunc, ctypes.byref(h))
+        assert st == 1, (n, d, prec, trunc, st)          # MDS_E_INVALID_ARG
+    for rank, world in [(2, 2), (-1, 2), (0, 0)]:
+        h = ctypes.c_void_p()
+        assert mds._abi.lib.mds_create_sharded(10, 2, 0, 1, rank, world, ctypes.byref(h)) == 1
+    # the smallest problem: one pair
+    with mds.MDS(2, 1) as c:
+        c.set_dissimilarities_packed(np.array([1.5]))
+        c.set_locations(np.array([[0.0], [2.0]]))
+        c.set_sigma(0.8)
+        ll, g = c.log_likelihood_and_gradient()
+    ref = oracle.loglik_grad(np.array([1.5]), np.array([[0.0], [2.0]]), 0.8, 1)
+    assert ll == pytest.approx(ref["loglik"], rel=1e-12)
+    np.testing.assert_allclose(g, ref["grad"], rtol=1e-12)
