@@ -54,7 +54,7 @@ def parse():
     ap.add_argument("--graph", type=int, default=0,
                     help="1: capture the K timed steps (flush + step, with external timing events) in one CUDA "
                          "graph and replay it (N = 1 only)")
-    ap.add_argument("--flush", choices=["torch", "mds"], default="mds",
+    ap.add_argument("--flush", choices=["torch", "mds", "mds-clean"], default="mds",
                     help="L2 flush between timed steps: torch fill, or mds_l2_flush (same write, launched "
                          "with the pass kernel's grid/block/smem shape)")
     return ap.parse_args()
@@ -220,7 +220,8 @@ def run_ours(args):
     # phase B reduction/leapfrog update); sharded: + combine + update kernels
     launches_per_step = 1 if world == 1 else 3
 
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")   # > 126 MB L2
+    # > 126 MB L2 (mds-clean: two halves of 256 MiB, written then read)
+    flush = torch.empty((512 if args.flush == "mds-clean" else 256) << 20, dtype=torch.uint8, device="cuda")
     # warm-up (also primes grad log pi)
     ctx.leapfrog_device(1, args.step_size, args.prior_sd, p0_dev=p0)
     for _ in range(max(0, args.warmup - 1)):
@@ -236,6 +237,8 @@ def run_ours(args):
         for k in range(args.steps):
             if args.flush == "mds":        # untimed L2 flush before every timed step
                 ctx.l2_flush(flush)
+            elif args.flush == "mds-clean":
+                ctx.l2_flush_clean(flush)
             else:
                 flush.zero_()
             ev0[k].record(stream)
@@ -357,8 +360,9 @@ def run_ours(args):
                                "one leapfrog step (fused lik+grad pass) per step" % (args.workload, n, d,
                                                                                     args.precision, w.sigma),
                    "n": n, "d": d, "pairs_per_step": P_N, "observed_fraction": 1.0 - w.p_missing,
-                   "l2": "flushed between timed steps (256 MiB write, untimed, %s)" % (
-                       "torch fill" if args.flush == "torch" else "mds_l2_flush"),
+                   "l2": "flushed between timed steps (untimed, %s)" % (
+                       {"torch": "256 MiB torch fill", "mds": "256 MiB write, mds_l2_flush",
+                        "mds-clean": "256 MiB write + 256 MiB read, mds_l2_flush_clean"}[args.flush]),
                    "launch": "one CUDA graph of the K (flush, step) pairs" if graph is not None
                    else "stream launches",
                    "parallelism": "tile-row shards x %d" % world if world > 1 else "single GPU",

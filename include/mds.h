@@ -388,6 +388,12 @@ mds_status mds_device_info(int32_t *sm_count, int32_t *cc_major, int32_t *cc_min
  * MDS_E_CUDA. */
 mds_status mds_l2_flush(mds_ctx ctx, void *dev_buf, size_t bytes);
 
+/* As mds_l2_flush on the first half of dev_buf, then a read of the second half
+ * (each half should exceed the 126 MB L2): the dirty lines the write leaves are
+ * written back inside the flush, so a following timed kernel starts from a cold
+ * AND clean L2.  Same launch shape as mds_l2_flush.  Errors as mds_l2_flush. */
+mds_status mds_l2_flush_clean(mds_ctx ctx, void *dev_buf, size_t bytes);
+
 /* Measure this device's FP64 (dfma) and FP32 (ffma) lane throughput with a
  * register-resident dependent-chain microbenchmark; results in lane-FMA/s.
  * Used for the ALU roofline denominator. */

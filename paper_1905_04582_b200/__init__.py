@@ -133,6 +133,11 @@ class MDS:
         shape (timing utility, mds_l2_flush)."""
         _abi.mds_l2_flush(self.ctx, buf.data_ptr(), buf.numel() * buf.element_size())
 
+    def l2_flush_clean(self, buf):
+        """Write the first half of `buf`, read the second half (each > L2): a cold and
+        clean L2 for the next kernel (timing utility, mds_l2_flush_clean)."""
+        _abi.mds_l2_flush_clean(self.ctx, buf.data_ptr(), buf.numel() * buf.element_size())
+
     def last_timing(self):
         return _abi.mds_last_timing(self.ctx)
 

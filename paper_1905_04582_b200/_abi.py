@@ -30,7 +30,7 @@ EXPORTS = [
     "mds_set_allgather", "mds_plan",
     "mds_log_likelihood_at_sigma", "mds_sigma_mh_step", "mds_row_loglik_delta", "mds_rw_sweep",
     "mds_cv_set_heldout", "mds_cv_accumulate", "mds_cv_lpd", "mds_set_tree_prior", "mds_tree_prior",
-    "mds_last_error", "mds_status_string", "mds_version", "mds_device_info", "mds_measure_fma_peaks", "mds_l2_flush",
+    "mds_last_error", "mds_status_string", "mds_version", "mds_device_info", "mds_measure_fma_peaks", "mds_l2_flush", "mds_l2_flush_clean",
 ]
 
 
@@ -102,6 +102,7 @@ def _load():
         "mds_device_info": [P(i32), P(i32), P(i32)],
         "mds_measure_fma_peaks": [P(ctypes.c_double), P(ctypes.c_double)],
         "mds_l2_flush": [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t],
+        "mds_l2_flush_clean": [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t],
         "mds_log_likelihood_at_sigma": [vp, ctypes.c_double, P(ctypes.c_double)],
         "mds_cv_set_heldout": [vp, i64, dp, dp, dp],
         "mds_set_tree_prior": [vp, i64, dp, dp, dp, dp],
@@ -237,6 +238,10 @@ def mds_set_timing(ctx, enable):
 
 def mds_l2_flush(ctx, dev_ptr, nbytes):
     _check(lib.mds_l2_flush(ctx, ctypes.c_void_p(dev_ptr), ctypes.c_size_t(nbytes)), ctx)
+
+
+def mds_l2_flush_clean(ctx, dev_ptr, nbytes):
+    _check(lib.mds_l2_flush_clean(ctx, ctypes.c_void_p(dev_ptr), ctypes.c_size_t(nbytes)), ctx)
 
 
 def mds_last_timing(ctx):

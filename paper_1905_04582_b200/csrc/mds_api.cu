@@ -1666,6 +1666,23 @@ mds_status mds_l2_flush(mds_ctx c, void* dev_buf, size_t bytes) {
     return e == cudaSuccess ? MDS_OK : fail(c, MDS_E_CUDA, cudaGetErrorString(e));
 }
 
+mds_status mds_l2_flush_clean(mds_ctx c, void* dev_buf, size_t bytes) {
+    if (!c || !dev_buf || bytes < 32) return MDS_E_INVALID_ARG;
+    const size_t half = (bytes / 2) & ~(size_t)15;
+    mds_status st = mds_l2_flush(c, dev_buf, half);
+    if (st) return st;
+    static bool attr_set = false;
+    if (!attr_set) {
+        if (cudaFuncSetAttribute(l2_read_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem))
+            return fail(c, MDS_E_CUDA, "l2_flush attribute");
+        attr_set = true;
+    }
+    l2_read_kernel<<<c->grid, 32 * c->wpc, c->smem, c->stream>>>((const uint4*)((char*)dev_buf + half), half / 16,
+                                                                   (unsigned*)dev_buf);
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? MDS_OK : fail(c, MDS_E_CUDA, cudaGetErrorString(e));
+}
+
 mds_status mds_measure_fma_peaks(double* fp64, double* fp32) {
     int dev = 0, sms = 0;
     if (cudaGetDevice(&dev) != cudaSuccess) {

@@ -53,6 +53,19 @@ __global__ void fill_nan_kernel(T* p, size_t count) {
 // L2 flush for timing loops: overwrite a buffer larger than L2 with 16-byte
 // stores.  Launched with the pass kernel's block size and dynamic shared memory
 // so the SMs keep the same L1/shared-memory split between timed passes.
+// read pass of mds_l2_flush_clean: stream a buffer larger than L2 through it
+// so the dirty lines the write pass left are written back inside the flush
+__global__ void l2_read_kernel(const uint4* __restrict__ p, size_t count16, unsigned* sink) {
+    size_t k = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const size_t stride = (size_t)gridDim.x * blockDim.x;
+    unsigned acc = 0;
+    for (; k < count16; k += stride) {
+        const uint4 w = __ldcg(p + k);
+        acc ^= w.x ^ w.y ^ w.z ^ w.w;
+    }
+    if (acc == 0x12345678u) *sink = acc;    // keep the loads alive
+}
+
 __global__ void l2_flush_kernel(uint4* p, size_t count16, unsigned v) {
     size_t k = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
     const size_t stride = (size_t)gridDim.x * blockDim.x;
