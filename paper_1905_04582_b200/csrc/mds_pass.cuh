@@ -260,6 +260,7 @@ template <typename T, int D>
 struct alignas(16) WarpStage {
     static constexpr int UC = KernelShape<T, D>::ucols;
     uint64_t bar[NSTAGE];
+    uint64_t bar0[4];                       // the kernel's first unit: one barrier per 4-column group
     alignas(16) double xcol[2][TB * D];     // bulk-copy destinations: 16-byte aligned
     alignas(16) T y[NSTAGE][UC * TB];
     int4 seg[MAXSEG_W];
@@ -308,6 +309,8 @@ pass_kernel(PassArgs a) {
     if (lane == 0) {
 #pragma unroll
         for (int b = 0; b < NSTAGE; ++b) mbar_init(&W.bar[b], 1);
+#pragma unroll
+        for (int b = 0; b < 4; ++b) mbar_init(&W.bar0[b], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         fence_async_smem();
     }
@@ -382,8 +385,37 @@ pass_kernel(PassArgs a) {
             ++iu;
             ist = (ist + 1 == NSTAGE) ? 0 : ist + 1;
         };
+        // Staggered start: at launch every warp's first copy competes for HBM, so the
+        // kernel's first unit is fetched group by group -- the first 4-column group
+        // alone (2 KB + the tile's x), the rest once it has landed -- and compute
+        // starts on ~1/4 of the start-up traffic.
+#ifdef MDS_NO_STAGGER
+        bool first_pending = false;
+#else
+        bool first_pending = vv == 0;
+#endif
+        const int fc4b = max(W.seg[0].y - GPU * ub, 0), fc4e = min(W.seg[0].z - GPU * ub, GPU);
+        const int fst = ist;                     // the first unit's stage
+        auto issue_group = [&](int g, bool with_x) {
+            const int t = ub / UNITS_PER_TILE, jj0 = (ub % UNITS_PER_TILE) * UCOLS;
+            constexpr uint32_t GB = 4 * TB * sizeof(T);
+            mbar_arrive_tx(&W.bar0[g], GB + (with_x ? XB : 0));
+#ifndef MDS_Y_NO_EVICT_FIRST
+            bulk_g2s_hint(W.y[fst] + 4 * g * TB, Y + (size_t)t * TB * TB + (size_t)(jj0 + 4 * g) * TB, GB,
+                          &W.bar0[g], ypol);
+#else
+            bulk_g2s(W.y[fst] + 4 * g * TB, Y + (size_t)t * TB * TB + (size_t)(jj0 + 4 * g) * TB, GB, &W.bar0[g]);
+#endif
+            if (with_x) bulk_g2s(W.xcol[t & 1], X + (size_t)(t - itb) * TB * D, XB, &W.bar0[g]);
+        };
 #ifndef MDS_EXP_NO_TMA
-        issue_one();
+        if (first_pending) {
+            if (lane == 0) issue_group(fc4b, true);
+            ++iu;
+            ist = (ist + 1 == NSTAGE) ? 0 : ist + 1;
+        } else {
+            issue_one();
+        }
         if (NSTAGE > 2 && iu < ue) issue_one();
 #endif
 #pragma unroll 1
@@ -401,21 +433,41 @@ pass_kernel(PassArgs a) {
             for (int u = sg.y / GPU; u < (sg.z + GPU - 1) / GPU; ++u) {
                 // the unit's 4-column groups inside this segment: [c4b, c4e)
                 const int c4b = max(sg.y - GPU * u, 0), c4e = min(sg.z - GPU * u, GPU);
+                const bool fu = first_pending;        // the staggered first unit (per-group barriers)
+                first_pending = false;
 #ifndef MDS_EXP_NO_TMA
-                if (a.prof && lane == 0 && !mbar_ready(&W.bar[cst], (phase >> cst) & 1)) ++not_ready;
-                mbar_wait(&W.bar[cst], (phase >> cst) & 1);
-                if (a.prof && threadIdx.x == 0 && not_ready < 0x80000000u) {   // first unit of warp 0 landed
-                    a.prof[gridDim.x * 6 + blockIdx.x] = gtimer();
-                    not_ready |= 0x80000000u;
+                if (!fu) {
+                    if (a.prof && lane == 0 && !mbar_ready(&W.bar[cst], (phase >> cst) & 1)) ++not_ready;
+                    mbar_wait(&W.bar[cst], (phase >> cst) & 1);
+                    if (a.prof && threadIdx.x == 0 && not_ready < 0x80000000u) {   // first unit of warp 0 landed
+                        a.prof[gridDim.x * 6 + blockIdx.x] = gtimer();
+                        not_ready |= 0x80000000u;
+                    }
+                    phase ^= 1u << cst;
+                    __syncwarp();                     // all lanes are done with the stage being refilled
+                    if (iu < ue) issue_one();
                 }
-                phase ^= 1u << cst;
-                __syncwarp();                         // all lanes are done with the stage being refilled
-                if (iu < ue) issue_one();
 #endif
                 const int t = u / UNITS_PER_TILE, jb = (u % UNITS_PER_TILE) * UCOLS;
                 const int cpos = __ldg(a.slab_pos + a.nseg + t);    // used after the groups' math
 #pragma unroll 1
                 for (int c4 = c4b; c4 < c4e; ++c4) {       // 4-column reduce groups of the unit
+#ifndef MDS_EXP_NO_TMA
+                if (fu) {
+                    mbar_wait(&W.bar0[c4], 0);
+                    if (c4 == c4b) {
+                        if (a.prof && threadIdx.x == 0) {
+                            a.prof[gridDim.x * 6 + blockIdx.x] = gtimer();
+                            not_ready |= 0x80000000u;
+                        }
+                        __syncwarp();
+                        // the first group has landed: fetch the rest of the unit and the next unit
+                        if (lane == 0)
+                            for (int g = c4b + 1; g < c4e; ++g) issue_group(g, false);
+                        if (iu < ue) issue_one();
+                    }
+                }
+#endif
                 const int jj0 = jb + 4 * c4;
                 const T* __restrict__ yst = W.y[cst] + 4 * c4 * TB;
                 const double* __restrict__ xc = W.xcol[t & 1] + jj0 * D;
