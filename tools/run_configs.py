@@ -117,6 +117,32 @@ def run_c5(steps=5):
             "ms_p50": med_ms, "pair_evals_per_s": P / (mean_ms * 1e-3), "setup_s": setup, "loglik": ll}
 
 
+def run_sweep(ns=(5392, 10000, 20000, 30000, 50000, 100000), kinds=("clustered", "gaussian"), steps=5):
+    """SURVEY 8(d) roofline N sweep (fig:time_by_N): D = 2, fp64,
+    P = 1, both workloads; device-resident leapfrog steps as bench.py (no flush:
+    Y exceeds L2 from N = 10000 on)."""
+    import torch
+    import workload
+    import paper_1905_04582_b200 as mds
+    out = []
+    for kind in kinds:
+        for n in ns:
+            w = workload.Workload(n, 2, kind=kind, seed=workload.BASE_SEED + 40 + n)
+            ctx = mds.MDS(n, 2, "f64", True, stream=torch.cuda.current_stream())
+            step = 2000
+            for i0 in range(0, n, step):
+                i1 = min(n, i0 + step)
+                ctx.set_dissimilarity_rows(i0, i1, w.y_rows(i0, i1))
+            ctx.set_locations(w.x0)
+            ctx.set_sigma(w.sigma)
+            mean_ms, med_ms = step_rate(ctx, n, 2, steps if n > 30000 else 20, 2)
+            ctx.close()
+            P = n * (n - 1) // 2
+            out.append({"sweep": kind, "n": n, "d": 2, "ms_per_step": mean_ms, "pair_evals_per_s": P / (mean_ms * 1e-3)})
+            print(json.dumps(out[-1]), flush=True)
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--c3-iter", type=int, default=1000)
@@ -124,6 +150,7 @@ def main():
     ap.add_argument("--skip-c3", action="store_true")
     ap.add_argument("--skip-c4", action="store_true")
     ap.add_argument("--c5", action="store_true")
+    ap.add_argument("--sweep", action="store_true", help="SURVEY 8(d) N sweep (D = 2, fp64, both workloads)")
     a = ap.parse_args()
     import torch
     torch.cuda.set_device(0)
@@ -134,6 +161,8 @@ def main():
         print(json.dumps(run_c3(a.c3_iter, a.leapfrog)), flush=True)
     if a.c5:
         print(json.dumps(run_c5()), flush=True)
+    if a.sweep:
+        run_sweep()
 
 
 if __name__ == "__main__":
