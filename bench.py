@@ -135,7 +135,21 @@ def cpu_baseline(w, budget_s: float):
     pairs = ns * (ns - 1) // 2
     return {"value": pairs * evals / tot, "unit": UNIT, "cores": 1, "kind": "oracle",
             "sample": "%d full %s evaluations (N=%d, %d pairs each), serial C oracle, %.1f s" % (
-                evals, "C2" if n == 5392 else "workload", ns, pairs, tot)}
+                evals, "C2" if n == 5392 else "workload", ns, pairs, tot),
+            "host_cpu": host_cpu()}
+
+
+def host_cpu() -> str:
+    """CPU model and logical core count of the host running the oracle."""
+    model = "unknown"
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return "%s, %d logical cores" % (model, os.cpu_count() or 0)
 
 
 def sass_fp64_per_pair(prec: str, d: int) -> float | None:
@@ -183,7 +197,8 @@ def run_reference(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": el / args.steps * 1e3,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "config": {"workload": "%s (oracle sample)" % args.workload, "n": ns, "d": w.d},
-        "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample,
+                         "host_cpu": host_cpu()},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }))
 
