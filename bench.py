@@ -287,7 +287,7 @@ def run_ours(args):
         dist.barrier()
     clk = clocks.stop()
     step_ms = np.array([a.elapsed_time(b) for a, b in zip(ev0, ev1)])
-    if os.environ.get("MDS_PROFILE_PHASES") == "1":
+    if os.environ.get("MDS_PROFILE_PHASES") in ("1", "2"):
         ctx.last_timing()                  # prints the last pass's phase split to stderr
     if world > 1:
         pair_ms, red_ms = ctx.last_timing()

@@ -588,7 +588,7 @@ mds_status build_schedule(mds_ctx c) {
     if (!pos.empty()) CK(cudaMemcpy(c->d_slab_pos, pos.data(), pos.size() * sizeof(int), cudaMemcpyHostToDevice));
     CK(cudaMemset(c->d_slabs, 0, nslab * TB * c->d * sizeof(double)));
     const char* pe = std::getenv("MDS_PROFILE_PHASES");
-    if (pe && pe[0] == '1') {
+    if (pe && (pe[0] == '1' || pe[0] == '2')) {
         if (c->d_prof) cudaFree(c->d_prof);
         c->d_prof = nullptr;
         if ((st = dalloc(c, &c->d_prof, (size_t)G * 9))) return st;
@@ -652,6 +652,12 @@ void report_phases(mds_ctx c) {
         std::fprintf(stderr, " (%d %llu %.1f %llu)", idx[q], h[(size_t)c->grid * 5 + idx[q]], a[idx[q]],
                      h[(size_t)c->grid * 4 + idx[q]]);
     std::fprintf(stderr, "\n");
+    const char* pe = std::getenv("MDS_PROFILE_PHASES");
+    if (pe && pe[0] == '2') {      // every CTA's phase-A end, in CTA order
+        std::fprintf(stderr, "[mds phases] A end by cta:");
+        for (int g = 0; g < c->grid; ++g) std::fprintf(stderr, " %.1f", a[g]);
+        std::fprintf(stderr, "\n");
+    }
 }
 
 mds_status create_impl(int64_t n, int32_t d, int32_t precision, int32_t truncation, int32_t rank, int32_t world,
