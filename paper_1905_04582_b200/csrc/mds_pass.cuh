@@ -330,6 +330,11 @@ pass_kernel(PassArgs a) {
         const int per = (a.tree.n_items + a.pair_ctas - 1) / a.pair_ctas;
         const int lo = min(a.tree.n_items, (int)blockIdx.x * per), hi = min(a.tree.n_items, lo + per);
         treek::tips_pass<D>(a.tree, lo, hi, threadIdx.x, WPC * 32);
+        // ... and this CTA's slice of the walk's first level (cherries: tip children only)
+        const int e_all = a.tree.n_up > 0 ? __ldg(a.tree.up_lvl_ptr + 1) : 0;
+        const int pe = (e_all + a.pair_ctas - 1) / a.pair_ctas;
+        const int elo = min(e_all, (int)blockIdx.x * pe), ehi = min(e_all, elo + pe);
+        treek::level0_slice<D>(a.tree, elo, ehi, threadIdx.x, WPC * 32);
         __syncthreads();
         if (threadIdx.x == 0) {
             __threadfence();

@@ -255,6 +255,28 @@ __device__ __forceinline__ void tips_pass(const TreeArgs& a, int i_lo, int i_hi,
     }
 }
 
+// The first post-order level (height 1: every child a tip) for entries
+// [e_lo, e_hi), with the tips' x gathered straight from X, messages into the
+// global buffer a.msg.  Inside the pass kernel the pair CTAs run one slice each
+// at launch, so the walk starts at level 2.
+template <int D>
+__device__ __forceinline__ void level0_slice(const TreeArgs& a, int e_lo, int e_hi, int tid, int nt) {
+    for (int e = e_lo + tid; e < e_hi; e += nt) {
+        UpEnt<D> u;
+        u.e = a.up_e[e];
+        u.t = a.up_t[e];
+        u.tn = a.up_tn[e];
+        u.pos = a.up_dpos[e];
+        const int s0 = u.e.y, s1 = u.e.z;
+#pragma unroll
+        for (int r = 0; r < D; ++r) {
+            u.x0[r] = a.x[(int64_t)(-1 - s0) * D + r];
+            u.x1[r] = u.e.w >= 2 ? a.x[(int64_t)(-1 - s1) * D + r] : 0.0;
+        }
+        absorb<D>(a, a.msg, u);
+    }
+}
+
 // The whole walk on one CTA of NT threads.  dyn: the internal-node messages
 // when a.smem != 0 (else a.msg is used); red: NT / 32 + 1 doubles of scratch.
 template <int D, int NT>
@@ -295,6 +317,16 @@ __device__ __forceinline__ void tree_prior_block(const TreeArgs& a, double* dyn,
             __threadfence();
             atomicExch(a.tips_done, 0u);
         }
+        __syncthreads();
+        // ... and the first level (into a.msg): bring those messages into M
+        if (M != a.msg && a.n_up > 0) {
+            const int e0 = a.up_lvl_ptr[1];
+            for (int e = tid; e < e0; e += NT) {
+                const int sl = a.up_e[e].x;
+#pragma unroll
+                for (int r = 0; r <= D; ++r) M[(size_t)sl * (D + 1) + r] = __ldcg(a.msg + (size_t)sl * (D + 1) + r);
+            }
+        }
     }
     __syncthreads();
     stamp(a, 99);
@@ -331,10 +363,12 @@ __device__ __forceinline__ void tree_prior_block(const TreeArgs& a, double* dyn,
     auto bar_warp = [] { __syncwarp(); };
 
     // ---- post-order (by height): wide levels on the CTA, narrow ones on warp 0
-    run_levels(UpEnt<D>{}, ld_up, wk_up, a.up_lvl_ptr, 0, a.up_narrow, NT, tid, bar_cta, 3);
+    const int L0 = a.ext_tips ? 1 : 0;      // level 0 came from the pair CTAs
+    run_levels(UpEnt<D>{}, ld_up, wk_up, a.up_lvl_ptr, L0, a.up_narrow, NT, tid, bar_cta, 3);
     __syncthreads();
     stamp(a, 2);
-    if (tid < 32) run_levels(UpEnt<D>{}, ld_up, wk_up, a.up_lvl_ptr, a.up_narrow, a.n_up, 32, tid, bar_warp, 3);
+    if (tid < 32)
+        run_levels(UpEnt<D>{}, ld_up, wk_up, a.up_lvl_ptr, max(L0, a.up_narrow), a.n_up, 32, tid, bar_warp, 3);
     __syncthreads();
     stamp(a, 100);
     // roots: contrast against mu0 (variance v_root + tau_root); an unsequenced item
