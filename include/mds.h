@@ -342,6 +342,27 @@ mds_status mds_get_momentum(mds_ctx ctx, double *p);
  * the final state. */
 mds_status mds_hmc_run(mds_ctx ctx, const mds_hmc_config *cfg, double *x_inout, mds_hmc_stats *stats);
 
+/* The sampler of PAPER.md:672 on this library's pieces: cfg->n_iter
+ * iterations of { one HMC transition of X (as mds_hmc_run with n_iter = 1:
+ * cfg->n_leapfrog fused leapfrog steps, Metropolis accept), then one
+ * Metropolis-Hastings update of sigma^2 (as mds_sigma_mh_step with prior and
+ * random-walk scale sigma_step on log sigma^2) }.  Momenta and the sigma
+ * proposals / uniforms come from the counter-based generator seeded by
+ * cfg->seed.  x_inout (host, n x d, may be NULL = current X) is the start and
+ * receives the final state; the context's X and sigma are left at the final
+ * state.  Errors: as mds_hmc_run and mds_sigma_mh_step. */
+typedef struct {
+    int64_t accepted_x;      /* HMC transitions accepted */
+    int64_t accepted_sigma;  /* sigma^2 updates accepted */
+    int64_t grad_evals;
+    double seconds;          /* device time (CUDA events) */
+    double final_loglik;     /* log L at the final X and sigma */
+    double final_sigma;
+} mds_mcmc_stats;
+mds_status mds_mcmc_run(mds_ctx ctx, const mds_hmc_config *cfg, const mds_sigma_prior *prior, double sigma_step,
+                        double *x_inout, mds_mcmc_stats *stats);
+
+
 /* ---- misc -------------------------------------------------------------- */
 
 /* Text of the last error on ctx (never NULL; "" when none). */

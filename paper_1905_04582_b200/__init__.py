@@ -187,6 +187,16 @@ class MDS:
         Returns (accepted, log_ratio); the context's sigma moves on acceptance."""
         return _abi.mds_sigma_mh_step(self.ctx, shape, rate, step, z, u)
 
+    def mcmc_run(self, n_iter: int, n_leapfrog: int, step_size: float, prior_sd: float, seed: int,
+                 shape: float, rate: float, sigma_step: float, x0: np.ndarray | None = None):
+        """PAPER.md:672's sampler: per iteration one HMC transition of X, then one MH
+        update of sigma^2 (prior sigma^-2 ~ Gamma(shape, rate)).  Returns (x, stats)."""
+        cfg = HmcConfig(int(n_iter), int(n_leapfrog), float(step_size), float(prior_sd), int(seed))
+        x = None if x0 is None else np.ascontiguousarray(x0, dtype=np.float64).copy()
+        st = _abi.mds_mcmc_run(self.ctx, cfg, shape, rate, sigma_step, x)
+        return x, dict(accepted_x=st.accepted_x, accepted_sigma=st.accepted_sigma, grad_evals=st.grad_evals,
+                       seconds=st.seconds, final_loglik=st.final_loglik, final_sigma=st.final_sigma)
+
     # phylogenetic prior (SURVEY 8(f) NEXT-2)
     def set_tree_prior(self, parent, t, mu0=None, sigma_cov=None):
         f = lambda a: None if a is None else np.ascontiguousarray(a, dtype=np.float64)

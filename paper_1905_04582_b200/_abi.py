@@ -28,7 +28,7 @@ EXPORTS = [
     "mds_observed_pairs", "mds_zero_distance_pairs", "mds_set_timing", "mds_last_timing",
     "mds_hmc_trajectory", "mds_hmc_run", "mds_leapfrog_device", "mds_get_locations", "mds_get_momentum",
     "mds_set_allgather", "mds_plan",
-    "mds_log_likelihood_at_sigma", "mds_sigma_mh_step", "mds_row_loglik_delta", "mds_rw_sweep",
+    "mds_log_likelihood_at_sigma", "mds_sigma_mh_step", "mds_mcmc_run", "mds_row_loglik_delta", "mds_rw_sweep",
     "mds_cv_set_heldout", "mds_cv_accumulate", "mds_cv_lpd", "mds_set_tree_prior", "mds_tree_prior",
     "mds_last_error", "mds_status_string", "mds_version", "mds_device_info", "mds_measure_fma_peaks", "mds_l2_flush", "mds_l2_flush_clean",
 ]
@@ -58,6 +58,11 @@ class HmcStats(ctypes.Structure):
 
 class SigmaPrior(ctypes.Structure):
     _fields_ = [("shape", ctypes.c_double), ("rate", ctypes.c_double)]
+
+
+class McmcStats(ctypes.Structure):
+    _fields_ = [("accepted_x", ctypes.c_int64), ("accepted_sigma", ctypes.c_int64), ("grad_evals", ctypes.c_int64),
+                ("seconds", ctypes.c_double), ("final_loglik", ctypes.c_double), ("final_sigma", ctypes.c_double)]
 
 
 # int (*)(void* user, const double* send_dev, double* recv_dev, int64_t count, void* stream)
@@ -111,6 +116,7 @@ def _load():
         "mds_cv_lpd": [vp, P(ctypes.c_double), P(i64)],
         "mds_row_loglik_delta": [vp, i64, dp, P(ctypes.c_double)],
         "mds_rw_sweep": [vp, i64, dp, dp, dp, ctypes.c_double, ctypes.c_double, P(i64)],
+        "mds_mcmc_run": [vp, P(HmcConfig), P(SigmaPrior), ctypes.c_double, dp, P(McmcStats)],
         "mds_sigma_mh_step": [vp, P(SigmaPrior), ctypes.c_double, ctypes.c_double, ctypes.c_double, P(i32),
                               P(ctypes.c_double)],
     }
@@ -344,6 +350,14 @@ def mds_cv_lpd(ctx):
     v, s = ctypes.c_double(), ctypes.c_int64()
     _check(lib.mds_cv_lpd(ctx, ctypes.byref(v), ctypes.byref(s)), ctx)
     return v.value, s.value
+
+
+def mds_mcmc_run(ctx, cfg: HmcConfig, shape, rate, sigma_step, x_inout=None):
+    pr = SigmaPrior(float(shape), float(rate))
+    st = McmcStats()
+    _check(lib.mds_mcmc_run(ctx, ctypes.byref(cfg), ctypes.byref(pr), float(sigma_step), _ptr(x_inout),
+                            ctypes.byref(st)), ctx)
+    return st
 
 
 def mds_last_error(ctx):

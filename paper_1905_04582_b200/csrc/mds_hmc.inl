@@ -303,3 +303,62 @@ mds_status mds_hmc_run(mds_ctx c, const mds_hmc_config* cfg, double* x_inout, md
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------- MCMC driver
+// The sampler structure of PAPER.md:672 on the path's pieces: each iteration one
+// HMC transition of X (mds_hmc_run, L fused leapfrog steps) followed by one
+// Metropolis-Hastings update of sigma^2 (mds_sigma_mh_step, reading R27).  The
+// random numbers come from the same counter-based generator as mds_hmc_run,
+// on streams distinct per iteration and per use.
+extern "C" mds_status mds_mcmc_run(mds_ctx c, const mds_hmc_config* cfg, const mds_sigma_prior* prior,
+                                   double sigma_step, double* x_inout, mds_mcmc_stats* stats) {
+    GUARD(c);
+    mds_status st = check_hmc_cfg(c, cfg);
+    if (st) return st;
+    if (!prior || !(prior->shape > 0.0) || !(prior->rate > 0.0) || !(sigma_step > 0.0) || !std::isfinite(sigma_step))
+        return fail(c, MDS_E_INVALID_ARG, "mcmc: need a sigma prior with shape, rate > 0 and sigma_step > 0");
+    if (x_inout) {
+        st = mds_set_locations(c, x_inout);
+        if (st) return st;
+    }
+    st = ready(c);
+    if (st) return st;
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    CK(cudaEventRecord(e0, c->stream));
+    int64_t acc_x = 0, acc_s = 0, evals = 0;
+    double ll = 0.0;
+    for (int it = 0; it < cfg->n_iter; ++it) {
+        mds_hmc_config one = *cfg;
+        one.n_iter = 1;
+        one.seed = hmc_mix(cfg->seed ^ hmc_mix(0x3C3Cull + (uint64_t)it));
+        mds_hmc_stats hs{};
+        if ((st = mds_hmc_run(c, &one, nullptr, &hs))) break;
+        acc_x += hs.accepted;
+        evals += hs.grad_evals;
+        const double z = hmc_normal(cfg->seed ^ 0x5167A5ull, (uint64_t)it, 0);
+        const double u = hmc_u01(hmc_mix(cfg->seed ^ hmc_mix(0x5167A6ull ^ hmc_mix((uint64_t)it))));
+        int32_t a = 0;
+        if ((st = mds_sigma_mh_step(c, prior, sigma_step, z, u, &a, nullptr))) break;
+        acc_s += a;
+        ll = c->mh_ll;     // log L at the current X and sigma (from the MH step's likelihood pass)
+    }
+    CK(cudaEventRecord(e1, c->stream));
+    CK(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    if (st) return st;
+    if (x_inout) CK(cudaMemcpy(x_inout, c->d_x, (size_t)c->n * c->d * sizeof(double), cudaMemcpyDeviceToHost));
+    if (stats) {
+        stats->accepted_x = acc_x;
+        stats->accepted_sigma = acc_s;
+        stats->grad_evals = evals;
+        stats->seconds = ms * 1e-3;
+        stats->final_loglik = ll;
+        stats->final_sigma = c->sigma;
+    }
+    return MDS_OK;
+}

@@ -127,3 +127,40 @@ def test_leapfrog_device_gradient_only_steps(mds, prec):
     else:
         np.testing.assert_allclose(xs, ref["x"], rtol=1e-5, atol=1e-7)
         assert ll == pytest.approx(ref["loglik"], rel=1e-4)
+
+
+def test_mcmc_run_c1_chain(mds):
+    """PAPER.md:672's sampler (HMC on X, then MH on sigma^2): the final state is
+    consistent with the oracle (log L at the final X and sigma)."""
+    w = workload.config("C1")
+    y = w.y_packed()
+    with mds.MDS(w.n, w.d) as c:
+        c.set_dissimilarities_packed(y)
+        c.set_sigma(w.sigma)
+        x, st = c.mcmc_run(40, 10, 0.01, 10.0, 7, 2.0, 0.5, 0.1, x0=w.x0)
+        ll = c.log_likelihood()
+    assert st["grad_evals"] == 400
+    assert 0 < st["accepted_x"] <= 40 and 0 < st["accepted_sigma"] < 40
+    ref = oracle.loglik_grad(y, x, st["final_sigma"], 1)["loglik"]
+    assert st["final_loglik"] == pytest.approx(ref, rel=1e-10)
+    assert ll == pytest.approx(ref, rel=1e-10)
+
+
+def test_mcmc_run_prior_only_sigma(mds):
+    """All pairs missing: log L = 0, so sigma^-2 must follow its Gamma(shape, rate) prior."""
+    n, d = 20, 2
+    shape, rate = 3.0, 2.0
+    y = np.full(n * (n - 1) // 2, np.nan)
+    taus = []
+    with mds.MDS(n, d) as c:
+        c.set_dissimilarities_packed(y)
+        c.set_sigma(1.0)
+        x = np.random.default_rng(0).normal(size=(n, d))
+        for k in range(60):
+            x, st = c.mcmc_run(25, 3, 0.5, 2.0, 100 + k, shape, rate, 1.0, x0=x)
+            if k >= 5:
+                taus.append(1.0 / st["final_sigma"] ** 2)
+    t = np.array(taus)
+    mean, var = shape / rate, shape / rate ** 2
+    assert abs(t.mean() - mean) < 4 * math.sqrt(var / t.size), (t.mean(), mean)
+    assert 0.6 < t.var() / var < 1.5
