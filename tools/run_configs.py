@@ -117,6 +117,28 @@ def run_c5(steps=5):
             "ms_p50": med_ms, "pair_evals_per_s": P / (mean_ms * 1e-3), "setup_s": setup, "loglik": ll}
 
 
+def run_mcmc(n_iter=200, L=20):
+    """The PAPER.md:672 sampler on the C3 data: per iteration one HMC transition of
+    X (L = 20) and one MH update of sigma^2 (mds_mcmc_run)."""
+    import torch
+    import workload
+    import paper_1905_04582_b200 as mds
+    w = workload.config("C3")
+    ctx = mds.MDS(w.n, w.d, "f64", True, stream=torch.cuda.current_stream())
+    ctx.set_dissimilarities_packed(w.y_packed())
+    ctx.set_sigma(w.sigma)
+    x, st = ctx.mcmc_run(20, L, 0.00235, 10.0, 5, 2.0, 0.5, 0.002, x0=w.x0)    # warm-up
+    t0 = time.time()
+    x, st = ctx.mcmc_run(n_iter, L, 0.00235, 10.0, 6, 2.0, 0.5, 0.002, x0=x)
+    wall = time.time() - t0
+    P = w.n * (w.n - 1) // 2
+    ctx.close()
+    return {"config": "C3 + sigma^2 MH (mds_mcmc_run)", "iterations": n_iter, "leapfrog": L,
+            "device_seconds": st["seconds"], "wall_seconds": wall, "ms_per_iteration": st["seconds"] * 1e3 / n_iter,
+            "accepted_x": st["accepted_x"], "accepted_sigma": st["accepted_sigma"], "final_sigma": st["final_sigma"],
+            "grad_evals_per_s": st["grad_evals"] / st["seconds"]}
+
+
 def run_sweep(ns=(5392, 10000, 20000, 30000, 50000, 100000), kinds=("clustered", "gaussian"), steps=5):
     """SURVEY 8(d) roofline N sweep (fig:time_by_N): D = 2, fp64,
     P = 1, both workloads; device-resident leapfrog steps as bench.py (no flush:
@@ -151,6 +173,7 @@ def main():
     ap.add_argument("--skip-c4", action="store_true")
     ap.add_argument("--c5", action="store_true")
     ap.add_argument("--sweep", action="store_true", help="SURVEY 8(d) N sweep (D = 2, fp64, both workloads)")
+    ap.add_argument("--mcmc", action="store_true", help="C3 data with the sigma^2 update (mds_mcmc_run)")
     a = ap.parse_args()
     import torch
     torch.cuda.set_device(0)
@@ -163,6 +186,8 @@ def main():
         print(json.dumps(run_c5()), flush=True)
     if a.sweep:
         run_sweep()
+    if a.mcmc:
+        print(json.dumps(run_mcmc()), flush=True)
 
 
 if __name__ == "__main__":
