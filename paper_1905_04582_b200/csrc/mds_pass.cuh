@@ -294,6 +294,7 @@ pass_kernel(PassArgs a) {
     constexpr int UNITS_PER_TILE = TB / UCOLS;
     extern __shared__ __align__(128) unsigned char dsm[];
     __shared__ double exptab[EXPT64_N];
+    __shared__ uint64_t pb_bar;              // phase B: one bulk copy of a block's slabs
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int gw = blockIdx.x * WPC + warp;
     WarpStage<T, D>& W = reinterpret_cast<WarpStage<T, D>*>(dsm)[warp];
@@ -311,6 +312,7 @@ pass_kernel(PassArgs a) {
         for (int b = 0; b < NSTAGE; ++b) mbar_init(&W.bar[b], 1);
 #pragma unroll
         for (int b = 0; b < 4; ++b) mbar_init(&W.bar0[b], 1);
+        if (warp == 0) mbar_init(&pb_bar, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         fence_async_smem();
     }
@@ -582,6 +584,7 @@ pass_kernel(PassArgs a) {
     // sums slabs w, w + WPC, ... in order with 8 slab indices in flight
     // the staging area is free after the grid barrier: reuse it for the sums
     A (*red)[WPC][32] = reinterpret_cast<A (*)[WPC][32]>(dsm);
+    uint32_t pb_phase = 0;
     for (int job = blockIdx.x; WG && job < jobs; job += gridDim.x) {
         const int b = job / chunks, ch = job % chunks;
         const int q0 = a.blk_ptr[b], nq = a.blk_ptr[b + 1] - q0;
@@ -602,8 +605,25 @@ pass_kernel(PassArgs a) {
             pre_gl = a.gl[e_glb];
         }
         // block b's slabs are contiguous: warp w sums rows w, w + WPC, ... in order,
-        // 8 rows in flight (rows past the end add exact zeros)
+        // 8 rows in flight (rows past the end add exact zeros).  When the job covers
+        // whole slabs and they fit the (now free) staging area, ONE bulk copy brings
+        // them into shared memory first: the sums then read shared memory, same order.
         const double* __restrict__ sb = a.slabs + (size_t)q0 * TB * D;
+#ifndef MDS_NO_PHASEB_TMA
+        constexpr size_t PB_OFF = ((sizeof(A) * EPLMAX * WPC * 32) + 127) & ~(size_t)127;   // past red[][][]
+        const uint32_t pb_bytes = (uint32_t)nq * TB * D * sizeof(A);
+        if (chunks == 1 && PB_OFF + pb_bytes <= (size_t)WPC * sizeof(WarpStage<T, D>) && nq > 0) {
+            double* sm = reinterpret_cast<double*>(dsm + PB_OFF);
+            if (threadIdx.x == 0) {
+                fence_async_smem();
+                mbar_arrive_tx(&pb_bar, pb_bytes);
+                bulk_g2s(sm, sb, pb_bytes, &pb_bar);
+            }
+            mbar_wait(&pb_bar, pb_phase);
+            pb_phase ^= 1u;
+            sb = sm;
+        }
+#endif
         for (int k0 = warp; k0 < nq; k0 += 8 * WPC) {
             // all (element, slab) loads of the round first, then the adds in order:
             // one L2 round trip per round instead of one per element
