@@ -1661,11 +1661,11 @@ mds_status mds_device_info(int32_t* sm_count, int32_t* cc_major, int32_t* cc_min
 
 mds_status mds_l2_flush(mds_ctx c, void* dev_buf, size_t bytes) {
     if (!c || !dev_buf || bytes < 16) return MDS_E_INVALID_ARG;
-    static bool attr_set = false;
-    if (!attr_set) {
+    static size_t attr_set = 0;      // largest dynamic shared memory enabled so far (contexts differ)
+    if (c->smem > attr_set) {
         if (cudaFuncSetAttribute(l2_flush_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem))
             return fail(c, MDS_E_CUDA, "l2_flush attribute");
-        attr_set = true;
+        attr_set = c->smem;
     }
     l2_flush_kernel<<<c->grid, 32 * c->wpc, c->smem, c->stream>>>((uint4*)dev_buf, bytes / 16, 0x3c3c3c3cu);
     cudaError_t e = cudaGetLastError();
@@ -1677,11 +1677,11 @@ mds_status mds_l2_flush_clean(mds_ctx c, void* dev_buf, size_t bytes) {
     const size_t half = (bytes / 2) & ~(size_t)15;
     mds_status st = mds_l2_flush(c, dev_buf, half);
     if (st) return st;
-    static bool attr_set = false;
-    if (!attr_set) {
+    static size_t attr_set = 0;
+    if (c->smem > attr_set) {
         if (cudaFuncSetAttribute(l2_read_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem))
             return fail(c, MDS_E_CUDA, "l2_flush attribute");
-        attr_set = true;
+        attr_set = c->smem;
     }
     l2_read_kernel<<<c->grid, 32 * c->wpc, c->smem, c->stream>>>((const uint4*)((char*)dev_buf + half), half / 16,
                                                                    (unsigned*)dev_buf);
