@@ -32,6 +32,16 @@ def test_shards_partition_the_triangle(n, world):
     assert np.all(cover == 1)
 
 
+@pytest.mark.parametrize("ctas,wpc", [(147, 12), (147, 8), (147, 24), (1, 12), (73, 16)])
+def test_plan_for_any_pair_cta_count(ctas, wpc):
+    """With a tree prior the pass kernel plans its pairs on G - 1 CTAs (the last
+    walks the tree); any CTA count must still tile the triangle, balanced."""
+    for n in (65, 5392):
+        info = mds.mds_plan(n, 0, 1, ctas, wpc)
+        assert info["pairs"] == n * (n - 1) // 2
+        assert info["max_units_per_warp"] - info["min_units_per_warp"] <= 1
+
+
 def test_plan_scales_to_c5():
     info = mds.mds_plan(100000, 0, 1, 148, 12)
     assert info["pairs"] == 100000 * 99999 // 2
