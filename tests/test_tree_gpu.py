@@ -220,3 +220,25 @@ def test_fp32_leapfrog_with_tree_prior(mds):
         ll = c.log_likelihood()
     np.testing.assert_allclose(xs, ref["x"], rtol=1e-5, atol=1e-7)
     assert ll == pytest.approx(ref["loglik"], rel=1e-4)
+
+
+def test_tree_leapfrog_bitwise_deterministic(mds):
+    """The fused walk (tips pass and first level on the pair CTAs, a device counter
+    between them) keeps the pass deterministic: two runs from the same state are
+    bitwise identical."""
+    import torch
+    n, d = 2000, 2
+    w = workload.Workload(n, d, p_missing=0.05, seed=5)
+    parent, t = workload.coalescent_forest(n, 3, 0.05, seed=6, tau0=3.0)
+    p0 = torch.from_numpy(w.normals(7, (n, d))).cuda()
+    outs = []
+    for _ in range(2):
+        with mds.MDS(n, d) as c:
+            c.set_dissimilarities_packed(w.y_packed())
+            c.set_locations(w.x0)
+            c.set_sigma(w.sigma)
+            c.set_tree_prior(parent, t)
+            c.leapfrog_device(9, 0.001, 0.0, p0_dev=p0)
+            outs.append((c.get_locations(), c.get_momentum(), c.log_likelihood()))
+    assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])
+    assert outs[0][2] == outs[1][2]
