@@ -57,6 +57,7 @@ def _load():
         lib.oracle_log_phi.restype = ctypes.c_double
         lib.oracle_loglik_grad.argtypes = [i64, i32, d_p, d_p, ctypes.c_double, i32,
                                            d_p, d_p, d_p, P(i64), P(i64)]
+        lib.oracle_loglik_rows.argtypes = [i64, i32, i64, i64, d_p, d_p, ctypes.c_double, i32, d_p, P(i64)]
         lib.oracle_grad_rows.argtypes = [i64, i32, i64, P(i64), d_p, d_p, ctypes.c_double, i32,
                                          d_p, d_p, d_p]
         lib.oracle_leapfrog.argtypes = [i64, i32, d_p, d_p, d_p, ctypes.c_double, i32,
@@ -125,6 +126,25 @@ def loglik_grad(y_packed: np.ndarray, x: np.ndarray, sigma: float, truncation: i
     if rc:
         raise ValueError("invalid oracle arguments")
     return dict(loglik=ll.value, grad=g, absscale=s, n_obs=nobs.value, zero_pairs=nz.value)
+
+
+def loglik_rows(i0: int, i1: int, y_rows: np.ndarray, x: np.ndarray, sigma: float, truncation: int = 1):
+    """(log L over the pairs (i, j < i), i0 <= i < i1, n_obs of the range) from the
+    packed rows i0..i1-1 (streaming form of loglik_grad's Eq. 2 sum for sizes whose
+    packed triangle does not fit host memory; add chunk results in row order)."""
+    lib = _load()
+    x = _f64(x)
+    n, d = x.shape
+    y_rows = _f64(y_rows)
+    lo = i0 * (i0 - 1) // 2 if i0 > 0 else 0
+    if y_rows.size != i1 * (i1 - 1) // 2 - lo:
+        raise ValueError("y_rows must hold rows i0..i1-1 of the packed triangle")
+    ll = ctypes.c_double()
+    nobs = ctypes.c_int64()
+    if lib.oracle_loglik_rows(n, d, int(i0), int(i1), _dp(y_rows), _dp(x), float(sigma), int(truncation),
+                              ctypes.byref(ll), ctypes.byref(nobs)):
+        raise ValueError("invalid oracle arguments")
+    return ll.value, nobs.value
 
 
 def grad_rows(rows, yrows: np.ndarray, x: np.ndarray, sigma: float, truncation: int = 1):

@@ -88,6 +88,43 @@ int oracle_pair_term(double y, double d, double sigma, int truncation,
 /* log Phi(t) for t >= 0 exactly as the oracle forms it (exposed for pins). */
 double oracle_log_phi(double t) { return log1p(-0.5 * erfc(t / sqrt(2.0))); }
 
+/* ---- log L over a range of rows (streaming; full-size configs) ----------- */
+/* The Eq. 2 sum restricted to the pairs (i, j), i0 <= i < i1,
+ * j < i: the same terms, order (i ascending, j ascending) and compensated sum
+ * as oracle_loglik_grad, without the gradient.  y_rows holds rows i0..i1-1 of
+ * the packed strict lower triangle back to back (row i: y_i0 .. y_i,i-1), so a
+ * caller can stream an n too large for one packed array in row chunks and add
+ * the chunk results in order.  Outputs: *loglik (this range's sum), *n_obs. */
+int oracle_loglik_rows(int64_t n, int32_t d, int64_t i0, int64_t i1, const double *y_rows, const double *x,
+                       double sigma, int32_t truncation, double *loglik, int64_t *n_obs)
+{
+    if (n < 2 || d < 1 || i0 < 0 || i1 > n || i0 > i1 || !x || !(sigma > 0.0) || !isfinite(sigma)) return -1;
+    if (i1 > i0 && i1 > 1 && !y_rows) return -1;
+    acc_t L = {0.0, 0.0};
+    int64_t nobs = 0;
+    const int64_t r0 = i0 > 1 ? i0 : 1;
+    const int64_t base = (r0 * (r0 - 1)) / 2;
+    for (int64_t i = r0; i < i1; ++i) {
+        const double *yrow = y_rows + ((i * (i - 1)) / 2 - base);
+        for (int64_t j = 0; j < i; ++j) {
+            double y = yrow[j];
+            if (isnan(y)) continue;                       /* missing (R7) */
+            double s = 0.0;
+            for (int k = 0; k < d; ++k) {
+                double t = x[i * d + k] - x[j * d + k];
+                s += t * t;
+            }
+            double ell;
+            oracle_pair_term(y, sqrt(s), sigma, truncation, &ell, NULL);
+            acc_add(&L, ell);
+            ++nobs;
+        }
+    }
+    if (loglik) *loglik = acc_val(&L);
+    if (n_obs) *n_obs = nobs;
+    return 0;
+}
+
 /* ---- full evaluation over the packed strict lower triangle -------------- */
 /* y_packed: row i (i = 1..n-1) holds y_i0 .. y_i,i-1 at offset i(i-1)/2.
  * x: n*d row-major.  Outputs: *loglik, grad[n*d], absscale[n*d] (may be NULL:

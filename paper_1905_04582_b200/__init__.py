@@ -27,6 +27,21 @@ def _wrap_dev(ptr: int, count: int, dev):
     return torch.as_tensor(_CAI(), device=dev)
 
 
+def _device_f64(t, numel: int, what: str):
+    """A torch tensor handed to a *_device entry point must be CUDA fp64,
+    contiguous and of the expected size (the C side reads raw doubles)."""
+    if not getattr(t, "is_cuda", False):
+        raise TypeError("%s: expected a CUDA tensor (got device %s)" % (what, getattr(t, "device", "?")))
+    import torch
+    if t.dtype != torch.float64:
+        raise TypeError("%s: expected torch.float64 (got %s)" % (what, t.dtype))
+    if not t.is_contiguous():
+        raise ValueError("%s: expected a contiguous tensor" % what)
+    if t.numel() != numel:
+        raise ValueError("%s: expected %d values (got %d)" % (what, numel, t.numel()))
+    return t
+
+
 _PREC = {"f64": MDS_F64, "fp64": MDS_F64, "float64": MDS_F64, MDS_F64: MDS_F64,
          "f32": MDS_F32, "fp32": MDS_F32, "float32": MDS_F32, MDS_F32: MDS_F32}
 
@@ -76,6 +91,8 @@ class MDS:
 
     def set_dissimilarity_rows(self, i0: int, i1: int, y_lower):
         if hasattr(y_lower, "data_ptr"):
+            lo = i0 * (i0 - 1) // 2 if i0 > 0 else 0
+            _device_f64(y_lower, i1 * (i1 - 1) // 2 - lo, "set_dissimilarity_rows")
             _abi.mds_set_dissimilarity_rows_device(self.ctx, i0, i1, y_lower)
         else:
             _abi.mds_set_dissimilarity_rows(self.ctx, i0, i1, np.ascontiguousarray(y_lower, dtype=np.float64))
@@ -85,7 +102,7 @@ class MDS:
 
     def set_locations(self, x):
         if hasattr(x, "data_ptr"):
-            _abi.mds_set_locations_device(self.ctx, x)
+            _abi.mds_set_locations_device(self.ctx, _device_f64(x, self.n * self.d, "set_locations"))
         else:
             _abi.mds_set_locations(self.ctx, np.ascontiguousarray(x, dtype=np.float64))
 
@@ -110,12 +127,21 @@ class MDS:
         return g
 
     def evaluate_device(self, loglik_dev, grad_dev):
+        if loglik_dev is not None:
+            _device_f64(loglik_dev, 1, "evaluate_device(loglik)")
+        if grad_dev is not None:
+            _device_f64(grad_dev, self.n * self.d, "evaluate_device(grad)")
         _abi.mds_evaluate_device(self.ctx, loglik_dev, grad_dev)
 
     def evaluate_partial_device(self, part_dev):
-        _abi.mds_evaluate_partial_device(self.ctx, part_dev)
+        _abi.mds_evaluate_partial_device(self.ctx, _device_f64(part_dev, self.n * self.d + 1, "evaluate_partial"))
 
     def combine_partials_device(self, gathered_dev, world, loglik_dev, grad_dev):
+        _device_f64(gathered_dev, int(world) * (self.n * self.d + 1), "combine_partials(gathered)")
+        if loglik_dev is not None:
+            _device_f64(loglik_dev, 1, "combine_partials(loglik)")
+        if grad_dev is not None:
+            _device_f64(grad_dev, self.n * self.d, "combine_partials(grad)")
         _abi.mds_combine_partials_device(self.ctx, gathered_dev, world, loglik_dev, grad_dev)
 
     # diagnostics / timing
@@ -176,6 +202,8 @@ class MDS:
 
     def leapfrog_device(self, n_steps: int, step_size: float, prior_sd: float = 0.0, p0_dev=None):
         cfg = HmcConfig(0, int(n_steps), float(step_size), float(prior_sd), 0)
+        if p0_dev is not None:
+            _device_f64(p0_dev, self.n * self.d, "leapfrog_device(p0)")
         _abi.mds_leapfrog_device(self.ctx, cfg, p0_dev)
 
     # sigma side

@@ -328,6 +328,12 @@ mds_status run_pass(mds_ctx c, const double* xeval, double* grad_out, double* li
 }
 
 SigmaParams sigma_params(double sigma);
+mds_status sigma_mh_impl(mds_ctx c, cudaStream_t s, const mds_sigma_prior* prior, double step, double z, double u,
+                         int32_t* accepted, double* log_ratio, const double* cur_ll_dev);
+
+// a pass sequence can be captured in a CUDA graph unless the exchange runs on
+// the host (the mds_set_allgather callback of a sharded context)
+bool graph_capturable(mds_ctx c) { return c->world == 1; }
 
 // log L only (MODE_LIK) at the context's X for the SigmaParams given, into the
 // device double lik_out; sharded: local partial -> exchange -> rank-ordered sum
@@ -582,18 +588,21 @@ mds_status build_schedule(mds_ctx c) {
     if ((st = dalloc(c, &c->d_slab_pos, std::max<size_t>(pos.size(), 1)))) return st;
     if ((st = dalloc(c, &c->d_slabs, nslab * TB * c->d))) return st;
     if ((st = dalloc(c, &c->d_likpart, (size_t)GW))) return st;
-    CK(cudaMemcpy(c->d_warp_seg, warp_seg.data(), warp_seg.size() * sizeof(int), cudaMemcpyHostToDevice));
-    if (!segs.empty()) CK(cudaMemcpy(c->d_segs, segs.data(), segs.size() * sizeof(int4), cudaMemcpyHostToDevice));
-    CK(cudaMemcpy(c->d_blk_ptr, ptr.data(), ptr.size() * sizeof(int), cudaMemcpyHostToDevice));
-    if (!pos.empty()) CK(cudaMemcpy(c->d_slab_pos, pos.data(), pos.size() * sizeof(int), cudaMemcpyHostToDevice));
-    CK(cudaMemset(c->d_slabs, 0, nslab * TB * c->d * sizeof(double)));
+    CK(cudaMemcpyAsync(c->d_warp_seg, warp_seg.data(), warp_seg.size() * sizeof(int), cudaMemcpyHostToDevice, c->stream));
+    if (!segs.empty()) CK(cudaMemcpyAsync(c->d_segs, segs.data(), segs.size() * sizeof(int4), cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(c->d_blk_ptr, ptr.data(), ptr.size() * sizeof(int), cudaMemcpyHostToDevice, c->stream));
+    if (!pos.empty()) CK(cudaMemcpyAsync(c->d_slab_pos, pos.data(), pos.size() * sizeof(int), cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemsetAsync(c->d_slabs, 0, nslab * TB * c->d * sizeof(double), c->stream));
     const char* pe = std::getenv("MDS_PROFILE_PHASES");
     if (pe && (pe[0] == '1' || pe[0] == '2')) {
         if (c->d_prof) cudaFree(c->d_prof);
         c->d_prof = nullptr;
         if ((st = dalloc(c, &c->d_prof, (size_t)G * 9))) return st;
-        CK(cudaMemset(c->d_prof, 0, (size_t)G * 9 * sizeof(unsigned long long)));
+        CK(cudaMemsetAsync(c->d_prof, 0, (size_t)G * 9 * sizeof(unsigned long long), c->stream));
     }
+    // the host vectors above die on return and the uploads are stream-ordered on
+    // the context's stream (possibly a non-blocking one): complete them here
+    CK(cudaStreamSynchronize(c->stream));
     return MDS_OK;
 }
 
@@ -1204,14 +1213,14 @@ mds_status mds_set_tree_prior(mds_ctx c, int64_t n_nodes, const int64_t* parent,
         (!c->d_logprior && (st = dalloc(c, &c->d_logprior, 2))) ||
         (!c->d_tips_done && (st = dalloc(c, &c->d_tips_done, 1))))
         return st;
-    CK(cudaMemset(c->d_tips_done, 0, sizeof(unsigned int)));
-    CK(cudaMemcpy(c->d_tree_int, ints.data(), ints.size() * sizeof(int), cudaMemcpyHostToDevice));
-    CK(cudaMemset(c->d_tree_dbl, 0, n_dbl * sizeof(double)));
-    CK(cudaMemcpy(c->d_tree_dbl + o_t, t, nn * sizeof(double), cudaMemcpyHostToDevice));
-    if (E_up) CK(cudaMemcpy(c->d_tree_dbl + o_upt, up_t.data(), up_t.size() * sizeof(double), cudaMemcpyHostToDevice));
-    if (E_dn) CK(cudaMemcpy(c->d_tree_dbl + o_dnt, dn_t.data(), dn_t.size() * sizeof(double), cudaMemcpyHostToDevice));
-    if (E_up) CK(cudaMemcpy(c->d_tree_dbl + o_utn, up_tn.data(), up_tn.size() * sizeof(double), cudaMemcpyHostToDevice));
-    CK(cudaMemset(c->d_gprior, 0, (size_t)c->npad * d * sizeof(double)));
+    CK(cudaMemsetAsync(c->d_tips_done, 0, sizeof(unsigned int), c->stream));
+    CK(cudaMemcpyAsync(c->d_tree_int, ints.data(), ints.size() * sizeof(int), cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemsetAsync(c->d_tree_dbl, 0, n_dbl * sizeof(double), c->stream));
+    CK(cudaMemcpyAsync(c->d_tree_dbl + o_t, t, nn * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    if (E_up) CK(cudaMemcpyAsync(c->d_tree_dbl + o_upt, up_t.data(), up_t.size() * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    if (E_dn) CK(cudaMemcpyAsync(c->d_tree_dbl + o_dnt, dn_t.data(), dn_t.size() * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    if (E_up) CK(cudaMemcpyAsync(c->d_tree_dbl + o_utn, up_tn.data(), up_tn.size() * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemsetAsync(c->d_gprior, 0, (size_t)c->npad * d * sizeof(double), c->stream));
     TreeArgs& A = c->ta;
     A = TreeArgs{};
     A.n_nodes = (int)n_nodes;
@@ -1251,6 +1260,7 @@ mds_status mds_set_tree_prior(mds_ctx c, int64_t n_nodes, const int64_t* parent,
     }
     A.grad = c->d_gprior;
     A.logp = c->d_logprior;
+    CK(cudaStreamSynchronize(c->stream));   // the uploads above read host vectors that die on return
     const char* pe = std::getenv("MDS_PROFILE_TREE");
     if (pe && pe[0] == '1') {
         static unsigned long long* prof = nullptr;
@@ -1322,8 +1332,9 @@ mds_status mds_cv_set_heldout(mds_ctx c, int64_t m, const int64_t* i, const int6
         (!c->d_cv_out && (st = dalloc(c, &c->d_cv_out, 1))))
         return st;
     if (m > 0) {
-        CK(cudaMemcpy(c->d_cv_ij, ij.data(), (size_t)m * sizeof(int2), cudaMemcpyHostToDevice));
-        CK(cudaMemcpy(c->d_cv_y, y, (size_t)m * sizeof(double), cudaMemcpyHostToDevice));
+        CK(cudaMemcpyAsync(c->d_cv_ij, ij.data(), (size_t)m * sizeof(int2), cudaMemcpyHostToDevice, c->stream));
+        CK(cudaMemcpyAsync(c->d_cv_y, y, (size_t)m * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+        CK(cudaStreamSynchronize(c->stream));   // ij dies on return; y belongs to the caller
     }
     c->cv_m = m;
     return MDS_OK;
@@ -1378,6 +1389,17 @@ mds_status mds_cv_lpd(mds_ctx c, double* lpd, int64_t* draws) {
 mds_status mds_sigma_mh_step(mds_ctx c, const mds_sigma_prior* prior, double step, double z, double u,
                              int32_t* accepted, double* log_ratio) {
     GUARD(c);
+    return sigma_mh_impl(c, c->stream, prior, step, z, u, accepted, log_ratio, nullptr);
+}
+
+}  // extern "C"
+
+namespace {
+// One MH update of sigma^2 on stream s.  cur_ll_dev (nullable): a device double
+// holding log L at the current X and sigma (the HMC driver's d_lik), which then
+// replaces the likelihood-only pass at the current sigma.
+mds_status sigma_mh_impl(mds_ctx c, cudaStream_t s, const mds_sigma_prior* prior, double step, double z, double u,
+                         int32_t* accepted, double* log_ratio, const double* cur_ll_dev) {
     if (!prior || !(prior->shape > 0.0) || !(prior->rate > 0.0) || !std::isfinite(prior->shape) ||
         !std::isfinite(prior->rate))
         return fail(c, MDS_E_INVALID_ARG, "sigma prior needs shape > 0 and rate > 0");
@@ -1389,18 +1411,20 @@ mds_status mds_sigma_mh_step(mds_ctx c, const mds_sigma_prior* prior, double ste
     const double phi1 = phi0 + step * z;
     const double sigma1 = std::exp(0.5 * phi1);
     if (!(sigma1 > 0.0) || !std::isfinite(sigma1)) return fail(c, MDS_E_INVALID_ARG, "proposal sigma out of range");
-    // log L at the current sigma: cached from the previous step when nothing changed
-    if (c->mh_version != c->version) {
-        st = run_lik_pass(c, c->P, c->d_lik + 2, c->stream);
+    // log L at the current sigma: cached from the previous step when nothing changed,
+    // or handed in by the HMC driver
+    const bool need_cur = !cur_ll_dev && c->mh_version != c->version;
+    if (need_cur) {
+        st = run_lik_pass(c, c->P, c->d_lik + 2, s);
         if (st) return st;
     }
-    st = run_lik_pass(c, sigma_params(sigma1), c->d_lik + 3, c->stream);
+    st = run_lik_pass(c, sigma_params(sigma1), c->d_lik + 3, s);
     if (st) return st;
     double ll[2] = {c->mh_ll, 0.0};
-    if (c->mh_version != c->version)
-        CK(cudaMemcpyAsync(&ll[0], c->d_lik + 2, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-    CK(cudaMemcpyAsync(&ll[1], c->d_lik + 3, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-    CK(cudaStreamSynchronize(c->stream));
+    if (cur_ll_dev) CK(cudaMemcpyAsync(&ll[0], cur_ll_dev, sizeof(double), cudaMemcpyDeviceToHost, s));
+    else if (need_cur) CK(cudaMemcpyAsync(&ll[0], c->d_lik + 2, sizeof(double), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(&ll[1], c->d_lik + 3, sizeof(double), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
     // log prior of phi: tau = 1/sigma^2 = e^-phi ~ Gamma(shape, rate), Jacobian |dtau/dphi| = tau
     auto lp = [&](double phi) { return -prior->shape * phi - prior->rate * std::exp(-phi); };
     const double lr = (ll[1] - ll[0]) + (lp(phi1) - lp(phi0));
@@ -1418,9 +1442,6 @@ mds_status mds_sigma_mh_step(mds_ctx c, const mds_sigma_prior* prior, double ste
     return MDS_OK;
 }
 
-}  // extern "C"
-
-namespace {
 SigmaParams sigma_params(double sigma) {
     const double pi = 3.14159265358979323846;
     SigmaParams P{};

@@ -95,13 +95,148 @@ mds_status hmc_energy(mds_ctx c, double* out, double inv_tau2, cudaStream_t s) {
     return MDS_OK;
 }
 
-struct StreamGuard {
+// One HMC chain's launch state, kept across transitions (mds_hmc_run and the
+// PAPER.md:672 sampler mds_mcmc_run): the CUDA graph of the L fused leapfrog
+// steps (captured once; updated in place when sigma moves, since the sigma
+// constants are kernel parameters), the pinned momentum buffer and the timing
+// events.  Per transition: momentum upload, save, redrift, H0, graph, H1, one
+// host sync for the accept/reject.
+struct HmcSession {
     cudaStream_t s = nullptr;
-    bool owned = false;
-    ~StreamGuard() {
-        if (owned && s) cudaStreamDestroy(s);
+    bool owned = false;                 // stream created here (the context had the legacy stream)
+    cudaGraphExec_t exec = nullptr;
+    double* pbuf = nullptr;             // pinned momentum staging (or the vector below)
+    bool pinned = false;
+    std::vector<double> pvec;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    int L = 1;
+    double eps = 0.0, it2 = 0.0;
+    int64_t accepted = 0;
+    double sum_abs_dh = 0.0;
+    float elapsed_ms() const {
+        float ms = 0.f;
+        if (e0 && e1) cudaEventElapsedTime(&ms, e0, e1);
+        return ms;
     }
 };
+
+void hmc_session_end(HmcSession& S) {
+    if (S.exec) cudaGraphExecDestroy(S.exec);
+    if (S.pinned && S.pbuf) cudaFreeHost(S.pbuf);
+    if (S.e0) cudaEventDestroy(S.e0);
+    if (S.e1) cudaEventDestroy(S.e1);
+    if (S.owned && S.s) cudaStreamDestroy(S.s);
+    S = HmcSession();
+}
+
+// (re)capture the L-step trajectory at the context's current sigma constants;
+// an existing executable graph is updated in place (same topology)
+mds_status hmc_session_capture(mds_ctx c, HmcSession& S) {
+    if (!graph_capturable(c)) return MDS_OK;      // host-callback exchange: direct launches
+    cudaGraph_t graph = nullptr;
+    CK(cudaStreamBeginCapture(S.s, cudaStreamCaptureModeThreadLocal));
+    mds_status st = hmc_enqueue_steps(c, S.L, S.eps, S.it2, S.s, false);
+    cudaError_t ce = cudaStreamEndCapture(S.s, &graph);
+    if (st) {
+        if (graph) cudaGraphDestroy(graph);
+        return st;
+    }
+    if (ce) return fail(c, MDS_E_CUDA, std::string("graph capture: ") + cudaGetErrorString(ce));
+    if (S.exec) {
+        cudaGraphExecUpdateResultInfo info{};
+        ce = cudaGraphExecUpdate(S.exec, graph, &info);
+        if (ce) {                                  // topology changed: instantiate anew
+            cudaGetLastError();
+            cudaGraphExecDestroy(S.exec);
+            S.exec = nullptr;
+        }
+    }
+    if (!S.exec) ce = cudaGraphInstantiate(&S.exec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (ce) return fail(c, MDS_E_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(ce));
+    return MDS_OK;
+}
+
+mds_status hmc_session_begin(mds_ctx c, const mds_hmc_config* cfg, HmcSession& S) {
+    mds_status st = hmc_alloc(c);
+    if (st) return st;
+    S.s = c->stream;
+    if (!S.s) {                                    // graph capture needs a non-legacy stream
+        CK(cudaStreamCreateWithFlags(&S.s, cudaStreamNonBlocking));
+        S.owned = true;
+        CK(cudaDeviceSynchronize());
+    }
+    S.L = cfg->n_leapfrog;
+    S.eps = cfg->step_size;
+    S.it2 = inv_tau2_of(c, cfg);
+    const size_t m = (size_t)(c->n * c->d);
+    if (cudaMallocHost(&S.pbuf, m * sizeof(double)) == cudaSuccess) {
+        S.pinned = true;
+    } else {
+        cudaGetLastError();
+        S.pvec.assign(m, 0.0);
+        S.pbuf = S.pvec.data();
+    }
+    CK(cudaEventCreate(&S.e0));
+    CK(cudaEventCreate(&S.e1));
+    return hmc_session_capture(c, S);
+}
+
+// gl and log L at the current X (after a start or a sigma move)
+mds_status hmc_session_prime(mds_ctx c, HmcSession& S) { return hmc_prime(c, S.eps, S.it2, S.s); }
+
+mds_status hmc_session_mark(mds_ctx c, HmcSession& S, cudaEvent_t e) {
+    CK(cudaEventRecord(e, S.s));
+    return MDS_OK;
+}
+
+// one HMC transition with momentum stream (seed, it): Metropolis accept on dH
+mds_status hmc_session_transition(mds_ctx c, HmcSession& S, uint64_t seed, uint64_t it) {
+    cudaStream_t s = S.s;
+    const int64_t m = c->n * c->d;
+    const size_t mbytes = (size_t)c->npad * c->d * sizeof(double);
+    CK(cudaStreamSynchronize(s));                  // pbuf is reused: the previous upload must be done
+    for (int64_t q = 0; q < m; ++q) S.pbuf[q] = hmc_normal(seed, it, (uint64_t)q);
+    CK(cudaMemcpyAsync(c->d_p, S.pbuf, m * sizeof(double), cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(c->d_xsave, c->d_x, mbytes, cudaMemcpyDeviceToDevice, s));
+    CK(cudaMemcpyAsync(c->d_glsave, c->d_gl, m * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    CK(cudaMemcpyAsync(c->d_liksave, c->d_lik, sizeof(double), cudaMemcpyDeviceToDevice, s));
+    if (c->tree) CK(cudaMemcpyAsync(c->d_logprior + 1, c->d_logprior, sizeof(double), cudaMemcpyDeviceToDevice, s));
+    mds_status st = hmc_redrift(c, S.eps, s);     // xnext for the new momentum
+    if (st) return st;
+    if ((st = hmc_energy(c, c->d_H0, S.it2, s))) return st;
+    if (S.exec) {
+        CK(cudaGraphLaunch(S.exec, s));
+    } else if ((st = hmc_enqueue_steps(c, S.L, S.eps, S.it2, s, false))) {
+        return st;
+    }
+    if ((st = hmc_energy(c, c->d_H, S.it2, s))) return st;
+    double hh[2] = {0, 0};
+    CK(cudaMemcpyAsync(&hh[0], c->d_H0, sizeof(double), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(&hh[1], c->d_H, sizeof(double), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    const double dH = hh[1] - hh[0];
+    const double u = hmc_u01(hmc_mix(seed ^ hmc_mix(0xACCE97ull ^ hmc_mix(it))));
+    const bool ok = std::isfinite(dH) && std::log(u) < -dH;
+    S.sum_abs_dh += std::isfinite(dH) ? std::fabs(dH) : 0.0;
+    if (ok) {
+        ++S.accepted;
+    } else {
+        CK(cudaMemcpyAsync(c->d_x, c->d_xsave, mbytes, cudaMemcpyDeviceToDevice, s));
+        CK(cudaMemcpyAsync(c->d_gl, c->d_glsave, m * sizeof(double), cudaMemcpyDeviceToDevice, s));
+        CK(cudaMemcpyAsync(c->d_lik, c->d_liksave, sizeof(double), cudaMemcpyDeviceToDevice, s));
+        if (c->tree) CK(cudaMemcpyAsync(c->d_logprior, c->d_logprior + 1, sizeof(double), cudaMemcpyDeviceToDevice, s));
+    }
+    return MDS_OK;
+}
+
+// final log L (d_lik: the accepted state's) and X to the host
+mds_status hmc_session_finish(mds_ctx c, HmcSession& S, double* x_out, double* final_ll) {
+    CK(cudaMemcpyAsync(final_ll, c->d_lik, sizeof(double), cudaMemcpyDeviceToHost, S.s));
+    if (x_out) CK(cudaMemcpyAsync(x_out, c->d_x, (size_t)(c->n * c->d) * sizeof(double), cudaMemcpyDeviceToHost, S.s));
+    CK(cudaStreamSynchronize(S.s));
+    return MDS_OK;
+}
 
 }  // namespace
 
@@ -180,122 +315,24 @@ mds_status mds_hmc_run(mds_ctx c, const mds_hmc_config* cfg, double* x_inout, md
     }
     st = ready(c);
     if (st) return st;
-    st = hmc_alloc(c);
-    if (st) return st;
-    StreamGuard sg;   // graph capture needs a non-legacy stream
-    sg.s = c->stream;
-    if (!sg.s) {
-        CK(cudaStreamCreateWithFlags(&sg.s, cudaStreamNonBlocking));
-        sg.owned = true;
-        CK(cudaDeviceSynchronize());
-    }
-    cudaStream_t s = sg.s;
-    const int64_t m = c->n * c->d;
-    const size_t mbytes = (size_t)c->npad * c->d * sizeof(double);
-    const double it2 = inv_tau2_of(c, cfg);
-    const int L = cfg->n_leapfrog;
-    const double eps = cfg->step_size;
-
-    // capture the L-step trajectory once (unsharded: the exchange callback of a
-    // sharded context runs on the host, so those launch directly)
-    cudaGraph_t graph = nullptr;
-    cudaGraphExec_t exec = nullptr;
-    cudaError_t ce = cudaSuccess;
-    if (c->world == 1) {
-        CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
-        st = hmc_enqueue_steps(c, L, eps, it2, s, false);
-        ce = cudaStreamEndCapture(s, &graph);
-        if (st) {
-            if (graph) cudaGraphDestroy(graph);
-            return st;
-        }
-        if (ce) return fail(c, MDS_E_CUDA, std::string("graph capture: ") + cudaGetErrorString(ce));
-        ce = cudaGraphInstantiate(&exec, graph, 0);
-        cudaGraphDestroy(graph);
-        if (ce) return fail(c, MDS_E_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(ce));
-    }
-
-    std::vector<double> ph((size_t)m);
-    double* ph_pinned = nullptr;
-    if (cudaMallocHost(&ph_pinned, m * sizeof(double)) != cudaSuccess) {
-        cudaGetLastError();
-        ph_pinned = nullptr;
-    }
-    double* pbuf = ph_pinned ? ph_pinned : ph.data();
-    cudaEvent_t e0, e1;
-    cudaEventCreate(&e0);
-    cudaEventCreate(&e1);
-
-    int64_t accepted = 0;
-    double sum_abs_dh = 0.0;
-    double hh[2] = {0, 0};
-    st = hmc_prime(c, eps, it2, s);      // gl, log L at the start (p is redrawn below)
-    if (!st) ce = cudaEventRecord(e0, s);
-    for (int it = 0; it < cfg->n_iter && !st && !ce; ++it) {
-        if (it > 0) {
-            ce = cudaStreamSynchronize(s);   // pbuf is reused: the previous upload must be done
-            if (ce) break;
-        }
-        for (int64_t q = 0; q < m; ++q) pbuf[q] = hmc_normal(cfg->seed, (uint64_t)it, (uint64_t)q);
-        ce = cudaMemcpyAsync(c->d_p, pbuf, m * sizeof(double), cudaMemcpyHostToDevice, s);
-        if (!ce) ce = cudaMemcpyAsync(c->d_xsave, c->d_x, mbytes, cudaMemcpyDeviceToDevice, s);
-        if (!ce) ce = cudaMemcpyAsync(c->d_glsave, c->d_gl, m * sizeof(double), cudaMemcpyDeviceToDevice, s);
-        if (!ce) ce = cudaMemcpyAsync(c->d_liksave, c->d_lik, sizeof(double), cudaMemcpyDeviceToDevice, s);
-        if (!ce && c->tree)
-            ce = cudaMemcpyAsync(c->d_logprior + 1, c->d_logprior, sizeof(double), cudaMemcpyDeviceToDevice, s);
-        if (ce) break;
-        st = hmc_redrift(c, eps, s);         // xnext for the new momentum
-        if (st) break;
-        st = hmc_energy(c, c->d_H0, it2, s);
-        if (st) break;
-        if (exec) {
-            ce = cudaGraphLaunch(exec, s);
-            if (ce) break;
-        } else {
-            st = hmc_enqueue_steps(c, L, eps, it2, s, false);
-            if (st) break;
-        }
-        st = hmc_energy(c, c->d_H, it2, s);
-        if (st) break;
-        ce = cudaMemcpyAsync(&hh[0], c->d_H0, sizeof(double), cudaMemcpyDeviceToHost, s);
-        if (!ce) ce = cudaMemcpyAsync(&hh[1], c->d_H, sizeof(double), cudaMemcpyDeviceToHost, s);
-        if (!ce) ce = cudaStreamSynchronize(s);
-        if (ce) break;
-        const double dH = hh[1] - hh[0];
-        const double u = hmc_u01(hmc_mix(cfg->seed ^ hmc_mix(0xACCE97ull ^ hmc_mix((uint64_t)it))));
-        const bool ok = std::isfinite(dH) && std::log(u) < -dH;
-        sum_abs_dh += std::isfinite(dH) ? std::fabs(dH) : 0.0;
-        if (ok) {
-            ++accepted;
-        } else {
-            ce = cudaMemcpyAsync(c->d_x, c->d_xsave, mbytes, cudaMemcpyDeviceToDevice, s);
-            if (!ce) ce = cudaMemcpyAsync(c->d_gl, c->d_glsave, m * sizeof(double), cudaMemcpyDeviceToDevice, s);
-            if (!ce) ce = cudaMemcpyAsync(c->d_lik, c->d_liksave, sizeof(double), cudaMemcpyDeviceToDevice, s);
-            if (!ce && c->tree)
-                ce = cudaMemcpyAsync(c->d_logprior, c->d_logprior + 1, sizeof(double), cudaMemcpyDeviceToDevice, s);
-            if (ce) break;
-        }
-    }
-    if (!ce && !st) ce = cudaEventRecord(e1, s);
+    HmcSession S;
+    st = hmc_session_begin(c, cfg, S);
+    if (!st) st = hmc_session_prime(c, S);
+    if (!st) st = hmc_session_mark(c, S, S.e0);
+    for (int it = 0; it < cfg->n_iter && !st; ++it) st = hmc_session_transition(c, S, cfg->seed, (uint64_t)it);
+    if (!st) st = hmc_session_mark(c, S, S.e1);
     double final_ll = 0.0;
-    if (!ce && !st) ce = cudaMemcpyAsync(&final_ll, c->d_lik, sizeof(double), cudaMemcpyDeviceToHost, s);
-    if (!ce && !st && x_inout) ce = cudaMemcpyAsync(x_inout, c->d_x, m * sizeof(double), cudaMemcpyDeviceToHost, s);
-    if (!ce && !st) ce = cudaStreamSynchronize(s);
-    float ms = 0.f;
-    if (!ce && !st) cudaEventElapsedTime(&ms, e0, e1);
-    cudaEventDestroy(e0);
-    cudaEventDestroy(e1);
-    if (exec) cudaGraphExecDestroy(exec);
-    if (ph_pinned) cudaFreeHost(ph_pinned);
+    if (!st) st = hmc_session_finish(c, S, x_inout, &final_ll);
+    const float ms = st ? 0.f : S.elapsed_ms();
+    hmc_session_end(S);
     if (st) return st;
-    if (ce) return fail(c, MDS_E_CUDA, std::string("hmc: ") + cudaGetErrorString(ce));
     ++c->version;          // X moved
     c->eval_version = 0;
     c->lf_version = 0;
     if (stats) {
-        stats->accepted = accepted;
-        stats->grad_evals = (int64_t)cfg->n_iter * L;
-        stats->mean_abs_dH = cfg->n_iter ? sum_abs_dh / cfg->n_iter : 0.0;
+        stats->accepted = S.accepted;
+        stats->grad_evals = (int64_t)cfg->n_iter * cfg->n_leapfrog;
+        stats->mean_abs_dH = cfg->n_iter ? S.sum_abs_dh / cfg->n_iter : 0.0;
         stats->seconds = ms * 1e-3;
         stats->final_loglik = final_ll;
     }
@@ -323,39 +360,42 @@ extern "C" mds_status mds_mcmc_run(mds_ctx c, const mds_hmc_config* cfg, const m
     }
     st = ready(c);
     if (st) return st;
-    cudaEvent_t e0, e1;
-    CK(cudaEventCreate(&e0));
-    CK(cudaEventCreate(&e1));
-    CK(cudaEventRecord(e0, c->stream));
-    int64_t acc_x = 0, acc_s = 0, evals = 0;
-    double ll = 0.0;
-    for (int it = 0; it < cfg->n_iter; ++it) {
-        mds_hmc_config one = *cfg;
-        one.n_iter = 1;
-        one.seed = hmc_mix(cfg->seed ^ hmc_mix(0x3C3Cull + (uint64_t)it));
-        mds_hmc_stats hs{};
-        if ((st = mds_hmc_run(c, &one, nullptr, &hs))) break;
-        acc_x += hs.accepted;
-        evals += hs.grad_evals;
+    // one session for the whole chain: the trajectory graph is captured once and
+    // updated in place only when sigma moves; the sigma proposal's likelihood-only
+    // pass reuses the transition's log L at the current sigma (d_lik), so an
+    // iteration costs L passes + 1 (+ 1 re-prime of grad log pi when sigma moved)
+    HmcSession S;
+    st = hmc_session_begin(c, cfg, S);
+    if (!st) st = hmc_session_prime(c, S);
+    if (!st) st = hmc_session_mark(c, S, S.e0);
+    int64_t acc_s = 0;
+    const uint64_t xseed = hmc_mix(cfg->seed ^ 0x3C3Cull);
+    for (int it = 0; it < cfg->n_iter && !st; ++it) {
+        if ((st = hmc_session_transition(c, S, xseed, (uint64_t)it))) break;
         const double z = hmc_normal(cfg->seed ^ 0x5167A5ull, (uint64_t)it, 0);
         const double u = hmc_u01(hmc_mix(cfg->seed ^ hmc_mix(0x5167A6ull ^ hmc_mix((uint64_t)it))));
         int32_t a = 0;
-        if ((st = mds_sigma_mh_step(c, prior, sigma_step, z, u, &a, nullptr))) break;
+        if ((st = sigma_mh_impl(c, S.s, prior, sigma_step, z, u, &a, nullptr, c->d_lik))) break;
         acc_s += a;
-        ll = c->mh_ll;     // log L at the current X and sigma (from the MH step's likelihood pass)
+        if (a) {         // the sigma constants are kernel parameters; grad log pi depends on sigma
+            if ((st = hmc_session_capture(c, S))) break;
+            if ((st = hmc_session_prime(c, S))) break;
+        }
     }
-    CK(cudaEventRecord(e1, c->stream));
-    CK(cudaEventSynchronize(e1));
-    float ms = 0.f;
-    cudaEventElapsedTime(&ms, e0, e1);
-    cudaEventDestroy(e0);
-    cudaEventDestroy(e1);
+    if (!st) st = hmc_session_mark(c, S, S.e1);
+    double ll = 0.0;
+    if (!st) st = hmc_session_finish(c, S, x_inout, &ll);
+    const float ms = st ? 0.f : S.elapsed_ms();
+    const int64_t acc_x = S.accepted;
+    hmc_session_end(S);
     if (st) return st;
-    if (x_inout) CK(cudaMemcpy(x_inout, c->d_x, (size_t)c->n * c->d * sizeof(double), cudaMemcpyDeviceToHost));
+    ++c->version;          // X moved
+    c->eval_version = 0;
+    c->lf_version = 0;
     if (stats) {
         stats->accepted_x = acc_x;
         stats->accepted_sigma = acc_s;
-        stats->grad_evals = evals;
+        stats->grad_evals = (int64_t)cfg->n_iter * cfg->n_leapfrog;
         stats->seconds = ms * 1e-3;
         stats->final_loglik = ll;
         stats->final_sigma = c->sigma;

@@ -209,7 +209,14 @@ __device__ __forceinline__ void pair_f64_n(const double (&s)[NP], const double (
 #pragma unroll
         for (int i = 0; i < NP; ++i) {
             const double pt = p[i] * exptab[k[i] & (EXPT64_N - 1)];
-            E[i] = __hiloint2double(__double2hiint(pt) + (int)((unsigned)(k[i] >> 8) << 20), __double2loint(pt));
+            // 2^(k>>8) spliced into the exponent field.  pt carries cg, so for large
+            // sigma (cg < 2^-13, sigma > ~3.3e3) and a near the clamp the biased
+            // exponent would go <= 0 and wrap into the sign bit: clamp the high word
+            // at 0 instead (one IMNMX), i.e. E' < 2^-1022 where the true E' is below
+            // the normal range (reading R33: absolute error < 2^-1022 in E', and
+            // < 2^-1023 sigma sqrt(2 pi) in Q, both far inside the tolerances)
+            const int ehi = __double2hiint(pt) + (int)((unsigned)(k[i] >> 8) << 20);
+            E[i] = __hiloint2double(max(ehi, 0), __double2loint(pt));
             const double e1 = fma(-den[i], y0[i], 1.0);
             const double ee = fma(e1, e1, e1);
             const double rden = fma(ee, y0[i], y0[i]);

@@ -166,6 +166,11 @@ __global__ void __launch_bounds__(ROW_THREADS, 1) row_kernel(RowArgs a) {
             xn[threadIdx.x] = a.K == 0 ? a.xnew[threadIdx.x] : __fma_rn(a.step, zk, xi);
         }
         __syncthreads();
+        // this update's proposal in registers: the patch below must not read xn after
+        // the decision barrier (threads 0..D-1 overwrite it for the next update)
+        double xn_r[D];
+#pragma unroll
+        for (int q = 0; q < D; ++q) xn_r[q] = xn[q];
         const double p = row_partial<T, D, TRUNC>(a, i, xn, xo, exptab, red, rank, cur);
         const int par = (int)(k & 1);
         if (threadIdx.x == 0) part[par] = p;
@@ -200,13 +205,13 @@ __global__ void __launch_bounds__(ROW_THREADS, 1) row_kernel(RowArgs a) {
         __syncthreads();   // this CTA's copy of X[i] (if accepted) is visible to its next column reads
         if (decide && k + 1 < K) {
             // values staged for the next update that predate this move of row i
-            if (i_nx == i && threadIdx.x < D) xi_nx = xn[threadIdx.x];
+            if (i_nx == i && threadIdx.x < D) xi_nx = xn_r[threadIdx.x];
 #pragma unroll
             for (int q = 0; q < RPF; ++q) {
                 const int64_t j = (int64_t)rank * ROW_THREADS + threadIdx.x + (int64_t)q * ROW_CLUSTER * ROW_THREADS;
                 if (j == i) {
 #pragma unroll
-                    for (int kk = 0; kk < D; ++kk) nxt.x[q][kk] = (T)xn[kk];
+                    for (int kk = 0; kk < D; ++kk) nxt.x[q][kk] = (T)xn_r[kk];
                 }
             }
         }

@@ -65,3 +65,22 @@ def test_product_does_not_import_oracle():
             if f.endswith((".py", ".cu", ".cuh", ".h", ".inl")):
                 txt = open(os.path.join(dirpath, f)).read()
                 assert "import oracle" not in txt and "from oracle" not in txt and "mds_oracle" not in txt, f
+
+
+def test_device_tensor_arguments_are_checked():
+    """The binding refuses tensors the C side would misread as fp64 device memory
+    (CPU tensors, float32, non-contiguous views, wrong sizes)."""
+    import torch
+    from paper_1905_04582_b200 import _device_f64
+    with pytest.raises(TypeError):
+        _device_f64(torch.zeros(6, dtype=torch.float64), 6, "x")          # CPU tensor
+    cuda_like = type("T", (), {"is_cuda": True, "dtype": torch.float32,
+                               "is_contiguous": lambda self: True, "numel": lambda self: 6})()
+    with pytest.raises(TypeError):
+        _device_f64(cuda_like, 6, "x")                                      # float32
+    cuda_like.dtype = torch.float64
+    with pytest.raises(ValueError):
+        _device_f64(cuda_like, 5, "x")                                      # wrong size
+    cuda_like.is_contiguous = lambda: False
+    with pytest.raises(ValueError):
+        _device_f64(cuda_like, 6, "x")                                      # strided view

@@ -290,6 +290,27 @@ def test_grad_rows_agree_with_full():
     assert allrows["rowlik"].sum() == pytest.approx(full["loglik"], rel=1e-13)
 
 
+def test_loglik_rows_streaming_pins():
+    """The streaming row-range log L (used at C5, whose packed triangle is 40 GB):
+    its chunks, added in row order, equal the scipy truncnorm/norm sum of Eq. 1
+    densities over the same pairs, and each chunk is the scipy sum over its rows."""
+    rng = np.random.default_rng(12)
+    x, y = rand_instance(rng, 23, 3, sigma=0.7, missing=0.15)
+    yp = oracle.pack_lower(y)
+    for trunc in (0, 1):
+        tot, nobs = 0.0, 0
+        for i0, i1 in [(0, 1), (1, 5), (5, 6), (6, 17), (17, 23)]:
+            lo, hi = i0 * (i0 - 1) // 2 if i0 else 0, i1 * (i1 - 1) // 2
+            ll, no = oracle.loglik_rows(i0, i1, yp[lo:hi], x, 0.7, trunc)
+            ych = np.full_like(y, np.nan)
+            ych[i0:i1] = y[i0:i1]
+            assert ll == pytest.approx(scipy_loglik(ych, x, 0.7, trunc), rel=1e-13, abs=1e-300)
+            tot += ll
+            nobs += no
+        assert tot == pytest.approx(scipy_loglik(y, x, 0.7, trunc), rel=1e-13)
+        assert nobs == int((~np.isnan(yp)).sum())
+
+
 # ---------------------------------------------------------------- leapfrog
 def test_leapfrog_gaussian_closed_form():
     """All-missing Y: target is the N(0, tau^2) prior; one leapfrog step is the
