@@ -324,15 +324,17 @@ mds_status mds_hmc_run(mds_ctx c, const mds_hmc_config* cfg, double* x_inout, md
     double final_ll = 0.0;
     if (!st) st = hmc_session_finish(c, S, x_inout, &final_ll);
     const float ms = st ? 0.f : S.elapsed_ms();
+    const int64_t accepted = S.accepted;
+    const double sum_abs_dh = S.sum_abs_dh;
     hmc_session_end(S);
     if (st) return st;
     ++c->version;          // X moved
     c->eval_version = 0;
     c->lf_version = 0;
     if (stats) {
-        stats->accepted = S.accepted;
+        stats->accepted = accepted;
         stats->grad_evals = (int64_t)cfg->n_iter * cfg->n_leapfrog;
-        stats->mean_abs_dH = cfg->n_iter ? S.sum_abs_dh / cfg->n_iter : 0.0;
+        stats->mean_abs_dH = cfg->n_iter ? sum_abs_dh / cfg->n_iter : 0.0;
         stats->seconds = ms * 1e-3;
         stats->final_loglik = final_ll;
     }
