@@ -75,14 +75,38 @@ typedef enum {
 mds_status mds_create(int64_t n, int32_t d, int32_t precision, int32_t truncation, mds_ctx *out);
 
 /* As mds_create, but this rank owns only the tile-rows r with
- * r mod world == rank of the tiled triangle: it stores and
- * evaluates only its share of the pairs.  Evaluations then produce this
- * rank's PARTIAL log L and gradient (mds_evaluate_partial_device); the caller
- * gathers the world partials (e.g. NCCL all-gather through torch.distributed)
- * and combines them with mds_combine_partials_device.  world == 1 is the
- * unsharded case.  Errors as mds_create, plus rank/world out of range. */
+ * r mod world == rank of the tiled triangle (the row-sharding
+ * of the paper's multi-device cost model c0/S + c1): it
+ * stores and evaluates only its share of the pairs, and each evaluation ends
+ * with ONE exchange of this rank's partial (n*d gradient values + log L)
+ * followed by a rank-ordered combine, so every rank holds the FULL result,
+ * bitwise identical across ranks.
+ *
+ * nccl_unique_id: MDS_NCCL_ID_BYTES bytes from mds_nccl_unique_id() on one
+ * rank, shared with all ranks (e.g. torch.distributed.broadcast_object_list).
+ * Then this call is COLLECTIVE (every rank calls it with the same id, on its
+ * own GPU): the context creates and owns an NCCL communicator, and the
+ * exchange is ncclAllGather on the context's stream (NVLink/NVSwitch within a
+ * node), so sharded leapfrog steps and HMC transitions are captured in CUDA
+ * graphs like unsharded ones.  A world == 1 context with an id runs the same
+ * partial -> all-gather -> combine sequence (plumbing check on one GPU).
+ * nccl_unique_id == NULL: no communicator; register the exchange with
+ * mds_set_allgather, or drive mds_evaluate_partial_device /
+ * mds_combine_partials_device yourself.
+ * Errors as mds_create, plus rank/world out of range (MDS_E_INVALID_ARG) and
+ * NCCL load/initialisation failures (MDS_E_COMM). */
+#define MDS_NCCL_ID_BYTES 128
 mds_status mds_create_sharded(int64_t n, int32_t d, int32_t precision, int32_t truncation,
-                              int32_t rank, int32_t world, mds_ctx *out);
+                              int32_t rank, int32_t world, const void *nccl_unique_id, mds_ctx *out);
+
+/* A fresh NCCL unique id (MDS_NCCL_ID_BYTES bytes into id_out) for
+ * mds_create_sharded; call on one rank only.  NCCL is loaded on first use
+ * (the copy already in the process, e.g. torch's, else libnccl.so.2).
+ * Errors: MDS_E_INVALID_ARG (NULL), MDS_E_COMM (NCCL unavailable). */
+mds_status mds_nccl_unique_id(void *id_out);
+
+/* *has = 1 if ctx owns an NCCL communicator (created with a unique id). */
+mds_status mds_has_communicator(mds_ctx ctx, int32_t *has);
 
 /* Free every device and host resource of ctx (NULL is ignored). */
 void mds_destroy(mds_ctx ctx);
@@ -146,7 +170,8 @@ mds_status mds_evaluate_device(mds_ctx ctx, double *loglik_dev, double *grad_dev
  * n*d gradient values followed by 1 log L value (n*d + 1 doubles). */
 mds_status mds_evaluate_partial_device(mds_ctx ctx, double *part_dev);
 
-/* Exchange used by sharded contexts.  fn must all-gather `count` doubles
+/* Exchange used by sharded contexts WITHOUT a communicator (created with a
+ * NULL unique id; a context that owns one ignores fn).  fn must all-gather `count` doubles
  * from every rank's send_dev into recv_dev[world][count] in rank order,
  * stream-ordered on cuda_stream (e.g. NCCL all-gather over NVLink through
  * torch.distributed), and return 0 on success.  Once registered, sharded
@@ -400,25 +425,8 @@ const char *mds_version(void);
  * if there is no device). */
 mds_status mds_device_info(int32_t *sm_count, int32_t *cc_major, int32_t *cc_minor);
 
-/* Timing utility (not part of the method): overwrite `bytes` of the device
- * buffer `dev_buf` (caller-owned, >= 16 bytes; use more than the 126 MB L2)
- * on the context's stream, launched with the pass kernel's grid, block size and
- * dynamic shared memory so the SMs keep the pass kernel's L1/shared split
- * between timed passes (a flush with another split makes the next pass
- * reconfigure the SMs inside the timed region).  Errors: MDS_E_INVALID_ARG,
- * MDS_E_CUDA. */
-mds_status mds_l2_flush(mds_ctx ctx, void *dev_buf, size_t bytes);
-
-/* As mds_l2_flush on the first half of dev_buf, then a read of the second half
- * (each half should exceed the 126 MB L2): the dirty lines the write leaves are
- * written back inside the flush, so a following timed kernel starts from a cold
- * AND clean L2.  Same launch shape as mds_l2_flush.  Errors as mds_l2_flush. */
-mds_status mds_l2_flush_clean(mds_ctx ctx, void *dev_buf, size_t bytes);
-
-/* Measure this device's FP64 (dfma) and FP32 (ffma) lane throughput with a
- * register-resident dependent-chain microbenchmark; results in lane-FMA/s.
- * Used for the ALU roofline denominator. */
-mds_status mds_measure_fma_peaks(double *fp64_fma_per_s, double *fp32_fma_per_s);
+/* Measurement utilities (L2 flush, FMA peak probe) are declared in
+ * include/mds_bench.h: they are not part of the method. */
 
 #ifdef __cplusplus
 }

@@ -8,6 +8,8 @@ is no CPU path.
 """
 from __future__ import annotations
 
+import ctypes
+
 import numpy as np
 
 from . import _abi
@@ -42,6 +44,50 @@ def _device_f64(t, numel: int, what: str):
     return t
 
 
+def allgather_callback(world: int, group=None, host_staged: bool = False, owner=None, device=None):
+    """The mds_allgather_fn of a torch.distributed exchange: gather `count` doubles
+    at send from every rank into recv[world][count], rank order, stream-ordered
+    on the stream libmds passes (marshalling only).
+
+    host_staged=False: send/recv are device pointers, all_gather_into_tensor on
+    the passed stream (NCCL).  host_staged=True: device -> host copy, all_gather
+    through the (gloo) group, host -> device copy, all on that stream; with
+    device="cpu" the pointers are host memory (CPU tests of the exchange logic)."""
+    import torch
+    import torch.distributed as dist
+
+    def _host(ptr, count):
+        buf = (ctypes.c_double * int(count)).from_address(int(ptr))
+        return torch.frombuffer(buf, dtype=torch.float64)
+
+    def _ag(user, send, recv, count, stream):
+        try:
+            if device == "cpu":
+                s, r = _host(send, count), _host(recv, count * world)
+                parts = list(r.view(world, count).unbind(0))
+                dist.all_gather(parts, s, group=group)
+                return 0
+            dev = torch.device("cuda", torch.cuda.current_device())
+            st = torch.cuda.ExternalStream(stream) if stream else torch.cuda.current_stream()
+            with torch.cuda.stream(st):
+                s = _wrap_dev(send, count, dev)
+                r = _wrap_dev(recv, count * world, dev)
+                if not host_staged:
+                    dist.all_gather_into_tensor(r, s, group=group)
+                else:
+                    hs = s.cpu()                       # synchronises the passed stream
+                    parts = [torch.empty_like(hs) for _ in range(world)]
+                    dist.all_gather(parts, hs, group=group)
+                    r.copy_(torch.cat(parts).to(dev, non_blocking=False))
+            return 0
+        except Exception as e:  # reported as MDS_E_COMM
+            if owner is not None:
+                owner.last_exchange_error = repr(e)
+            return 1
+
+    return _ag
+
+
 _PREC = {"f64": MDS_F64, "fp64": MDS_F64, "float64": MDS_F64, MDS_F64: MDS_F64,
          "f32": MDS_F32, "fp32": MDS_F32, "float32": MDS_F32, MDS_F32: MDS_F32}
 
@@ -50,14 +96,19 @@ class MDS:
     """One libmds context (marshalling only)."""
 
     def __init__(self, n: int, d: int, precision="f64", truncation: bool = True,
-                 rank: int = 0, world: int = 1, stream=None):
+                 rank: int = 0, world: int = 1, stream=None, nccl_unique_id: bytes | None = None):
+        """world > 1 (or a unique id): a row-sharded context owning tile-rows r mod world == rank.
+        With nccl_unique_id (mds_nccl_unique_id() on one rank, the same bytes on all) creation is
+        collective and the context owns its NCCL communicator; without, register an exchange
+        (use_torch_allgather / mds_set_allgather)."""
         self.n, self.d = int(n), int(d)
         self.precision = _PREC[precision]
         self.rank, self.world = int(rank), int(world)
-        if world == 1:
+        if world == 1 and nccl_unique_id is None:
             self.ctx = _abi.mds_create(n, d, self.precision, int(bool(truncation)))
         else:
-            self.ctx = _abi.mds_create_sharded(n, d, self.precision, int(bool(truncation)), rank, world)
+            self.ctx = _abi.mds_create_sharded(n, d, self.precision, int(bool(truncation)), rank, world,
+                                               nccl_unique_id)
         if stream is not None:
             self.set_stream(stream)
 
@@ -167,27 +218,24 @@ class MDS:
     def last_timing(self):
         return _abi.mds_last_timing(self.ctx)
 
-    def use_torch_allgather(self, group=None):
-        """Register torch.distributed all_gather_into_tensor (NCCL on GPU) as
-        the exchange of this sharded context (mds_set_allgather)."""
-        import torch
+    @staticmethod
+    def shared_nccl_id(group=None) -> bytes:
+        """A fresh NCCL unique id made on rank 0 of torch.distributed and broadcast to every
+        rank (for MDS(..., nccl_unique_id=...))."""
         import torch.distributed as dist
+        obj = [_abi.mds_nccl_unique_id() if dist.get_rank() == 0 else None]
+        dist.broadcast_object_list(obj, src=0, group=group)
+        return obj[0]
 
-        dev = torch.device("cuda", torch.cuda.current_device())
+    def has_communicator(self) -> bool:
+        return _abi.mds_has_communicator(self.ctx)
 
-        def _ag(user, send, recv, count, stream):
-            try:
-                st = torch.cuda.ExternalStream(stream) if stream else torch.cuda.current_stream()
-                with torch.cuda.stream(st):
-                    s = _wrap_dev(send, count, dev)
-                    r = _wrap_dev(recv, count * self.world, dev)
-                    dist.all_gather_into_tensor(r, s, group=group)
-                return 0
-            except Exception as e:  # reported as MDS_E_COMM
-                self.last_exchange_error = repr(e)
-                return 1
-
-        self._ag_cb = _abi.ALLGATHER_FN(_ag)
+    def use_torch_allgather(self, group=None, host_staged: bool = False):
+        """Register a torch.distributed all-gather as the exchange of this sharded
+        context (mds_set_allgather; only for contexts created without an NCCL id).
+        host_staged: stage through host memory (gloo process groups, e.g. several
+        ranks sharing one GPU in tests); else all_gather_into_tensor on device (NCCL)."""
+        self._ag_cb = _abi.ALLGATHER_FN(allgather_callback(self.world, group, host_staged, owner=self))
         _abi.mds_set_allgather(self.ctx, self._ag_cb, None)
 
     def get_locations(self) -> np.ndarray:

@@ -20,7 +20,8 @@ STATUS = {0: "MDS_OK", 1: "MDS_E_INVALID_ARG", 2: "MDS_E_STATE", 3: "MDS_E_OOM",
 
 # every symbol include/mds.h declares (checked by tests/test_abi.py)
 EXPORTS = [
-    "mds_create", "mds_create_sharded", "mds_destroy", "mds_set_stream",
+    "mds_create", "mds_create_sharded", "mds_nccl_unique_id", "mds_has_communicator", "mds_destroy",
+    "mds_set_stream",
     "mds_set_dissimilarities", "mds_set_dissimilarity_rows", "mds_set_dissimilarity_rows_device",
     "mds_set_locations", "mds_set_locations_device", "mds_set_sigma",
     "mds_log_likelihood", "mds_gradient", "mds_log_likelihood_and_gradient", "mds_evaluate_device",
@@ -79,7 +80,9 @@ def _load():
     P = ctypes.POINTER
     sig = {
         "mds_create": [i64, i32, i32, i32, P(vp)],
-        "mds_create_sharded": [i64, i32, i32, i32, i32, i32, P(vp)],
+        "mds_create_sharded": [i64, i32, i32, i32, i32, i32, vp, P(vp)],
+        "mds_nccl_unique_id": [vp],
+        "mds_has_communicator": [vp, P(i32)],
         "mds_set_stream": [vp, vp],
         "mds_set_dissimilarities": [vp, dp, i64],
         "mds_set_dissimilarity_rows": [vp, i64, i64, dp],
@@ -162,11 +165,33 @@ def mds_create(n, d, precision=MDS_F64, truncation=1):
     return h
 
 
-def mds_create_sharded(n, d, precision, truncation, rank, world):
+MDS_NCCL_ID_BYTES = 128
+
+
+def mds_create_sharded(n, d, precision, truncation, rank, world, nccl_unique_id: bytes | None = None):
+    """nccl_unique_id: the MDS_NCCL_ID_BYTES bytes of mds_nccl_unique_id() (same on every rank; the call is
+    then collective and the context owns an NCCL communicator), or None (exchange via mds_set_allgather)."""
     h = ctypes.c_void_p()
+    idbuf = None
+    if nccl_unique_id is not None:
+        if len(nccl_unique_id) != MDS_NCCL_ID_BYTES:
+            raise ValueError("nccl_unique_id must be %d bytes" % MDS_NCCL_ID_BYTES)
+        idbuf = ctypes.create_string_buffer(bytes(nccl_unique_id), MDS_NCCL_ID_BYTES)
     _check(lib.mds_create_sharded(int(n), int(d), int(precision), int(truncation), int(rank), int(world),
-                                  ctypes.byref(h)))
+                                  idbuf, ctypes.byref(h)))
     return h
+
+
+def mds_nccl_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(MDS_NCCL_ID_BYTES)
+    _check(lib.mds_nccl_unique_id(buf))
+    return buf.raw
+
+
+def mds_has_communicator(ctx) -> bool:
+    v = ctypes.c_int32()
+    _check(lib.mds_has_communicator(ctx, ctypes.byref(v)), ctx)
+    return bool(v.value)
 
 
 def mds_destroy(ctx):

@@ -33,7 +33,7 @@ def sources():
 
 def deps():
     return sources() + glob.glob(os.path.join(CSRC, "*.cuh")) + glob.glob(os.path.join(CSRC, "*.inl")) + \
-        glob.glob(os.path.join(CSRC, "*.h")) + [os.path.join(ROOT, "include", "mds.h"), __file__]
+        glob.glob(os.path.join(CSRC, "*.h")) + glob.glob(os.path.join(ROOT, "include", "*.h")) + [__file__]
 
 
 def stale() -> bool:
@@ -62,7 +62,7 @@ def build(force: bool = False, verbose: bool = False, extra=(), out: str | None 
         list(ex.map(compile_one, zip(srcs, objs)))
     tmp = lib + ".tmp%d" % os.getpid()
     subprocess.check_call([NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-cudart", "static",
-                           "-o", tmp, *objs])
+                           "-o", tmp, *objs, "-ldl"])
     os.replace(tmp, lib)
     return lib
 

@@ -12,7 +12,11 @@
 #include <string>
 #include <vector>
 
+#include <dlfcn.h>
+#include <nccl.h>   // types and enum values only: the entry points are resolved at run time (nccl_api)
+
 #include "../../include/mds.h"
+#include "../../include/mds_bench.h"
 #include "mds_kernels.cuh"
 #include "mds_row.cuh"
 #include "mds_cv.cuh"
@@ -21,7 +25,43 @@
 using namespace mdsk;
 
 namespace {
-const char* kVersion = "0.2.0";
+const char* kVersion = "0.3.0";
+
+// NCCL, loaded on first use.  In a process that already holds libnccl.so.2
+// (torch's bundled copy), RTLD_NOLOAD reuses that one, so the library and
+// torch.distributed share one NCCL; otherwise the system libnccl.so.2 is opened.
+// Only sharded contexts created with a unique id need it.
+struct NcclApi {
+    bool tried = false, ok = false;
+    std::string err;
+    ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+NcclApi& nccl_api() {
+    static NcclApi a;
+    if (a.tried) return a;
+    a.tried = true;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_LOCAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_LOCAL);
+    if (!h) {
+        const char* e = dlerror();
+        a.err = std::string("cannot load libnccl.so.2: ") + (e ? e : "?");
+        return a;
+    }
+    a.GetUniqueId = (decltype(a.GetUniqueId))dlsym(h, "ncclGetUniqueId");
+    a.CommInitRank = (decltype(a.CommInitRank))dlsym(h, "ncclCommInitRank");
+    a.AllGather = (decltype(a.AllGather))dlsym(h, "ncclAllGather");
+    a.CommDestroy = (decltype(a.CommDestroy))dlsym(h, "ncclCommDestroy");
+    a.GetErrorString = (decltype(a.GetErrorString))dlsym(h, "ncclGetErrorString");
+    a.ok = a.GetUniqueId && a.CommInitRank && a.AllGather && a.CommDestroy && a.GetErrorString;
+    if (!a.ok) a.err = "libnccl.so.2 lacks an entry point";
+    return a;
+}
 }  // namespace
 
 struct mds_ctx_s {
@@ -64,7 +104,9 @@ struct mds_ctx_s {
     int* d_bad = nullptr;
     unsigned long long* d_count = nullptr;
 
-    // sharded exchange
+    // sharded exchange: the library's own NCCL communicator (mds_create_sharded
+    // with a unique id; graph-capturable) or the caller's callback (mds_set_allgather)
+    ncclComm_t comm = nullptr;
     mds_allgather_fn ag_fn = nullptr;
     void* ag_user = nullptr;
     double* d_partial = nullptr;     // n*d + 1
@@ -194,6 +236,8 @@ void free_all(mds_ctx c) {
         if (e) cudaEventDestroy(e);
     if (c->h_xstage) cudaFreeHost(c->h_xstage);
     if (c->xstage_done) cudaEventDestroy(c->xstage_done);
+    if (c->comm) nccl_api().CommDestroy(c->comm);
+    c->comm = nullptr;
 }
 
 inline int64_t packed_off(int64_t i) { return i * (i - 1) / 2; }
@@ -209,7 +253,9 @@ PassKernel pass_fn_mode(int mode, int prec, int trunc, int d) {
         case MODE_LEAPFROG_NOLIK: return f ? pass_m3_f64(trunc, d) : pass_m3_f32(trunc, d);
         case MODE_LIK: return f ? pass_m4_f64(trunc, d) : pass_m4_f32(trunc, d);
         case MODE_LEAPFROG_TREE: return f ? pass_m5_f64(trunc, d) : pass_m5_f32(trunc, d);
-        default: return f ? pass_m6_f64(trunc, d) : pass_m6_f32(trunc, d);
+        case MODE_LEAPFROG_NOLIK_TREE: return f ? pass_m6_f64(trunc, d) : pass_m6_f32(trunc, d);
+        case MODE_EVAL_TREE: return f ? pass_m7_f64(trunc, d) : pass_m7_f32(trunc, d);
+        default: return f ? pass_m8_f64(trunc, d) : pass_m8_f32(trunc, d);
     }
 }
 
@@ -259,6 +305,26 @@ mds_status launch_coop(mds_ctx c, PassKernel k, PassArgs& a, cudaStream_t s) {
     return MDS_OK;
 }
 
+// The sharded exchange: every rank's count doubles at send into recv[world][count]
+// in rank order, stream-ordered on s (NCCL all-gather over NVLink, or the caller's
+// callback)
+mds_status exchange(mds_ctx c, const double* send, double* recv, int64_t count, cudaStream_t s) {
+    if (c->comm) {
+        const ncclResult_t r = nccl_api().AllGather(send, recv, (size_t)count, ncclFloat64, c->comm, s);
+        if (r != ncclSuccess)
+            return fail(c, MDS_E_COMM, std::string("ncclAllGather: ") + nccl_api().GetErrorString(r));
+        return MDS_OK;
+    }
+    if (!c->ag_fn)
+        return fail(c, MDS_E_STATE, "sharded context: create it with an NCCL unique id or register mds_set_allgather");
+    if (c->ag_fn(c->ag_user, send, recv, count, (void*)s) != 0) return fail(c, MDS_E_COMM, "all-gather callback failed");
+    return MDS_OK;
+}
+
+// unsharded: one pass kernel does everything; sharded (or a world-1 context with
+// a communicator): local partial -> exchange -> rank-ordered combine
+inline bool direct(mds_ctx c) { return c->world == 1 && !c->comm; }
+
 // A fused pass at xeval.  EVAL: (grad_out, lik_out) <- full result.  With a
 // leapfrog state (lf = true): the pass runs at xnext and applies the leapfrog
 // update (x, p, gl, xnext, grad, lik).  want_lik = false skips log L (the
@@ -291,7 +357,7 @@ mds_status run_pass(mds_ctx c, const double* xeval, double* grad_out, double* li
     }
     if (timed) CK(cudaEventRecord(next_event(c), s));
     mds_status st;
-    if (c->world == 1) {
+    if (direct(c)) {
         a.grad = grad_out;
         a.lik = lik_out;
         const int mode = lf ? (c->tree ? (want_lik ? MODE_LEAPFROG_TREE : MODE_LEAPFROG_NOLIK_TREE)
@@ -301,26 +367,23 @@ mds_status run_pass(mds_ctx c, const double* xeval, double* grad_out, double* li
         if (st) return st;
         if (timed) CK(cudaEventRecord(next_event(c), s));
     } else {
-        if (!c->ag_fn) return fail(c, MDS_E_STATE, "sharded context: register the exchange with mds_set_allgather");
+        // local partial; with a tree prior the pass kernel's last CTA walks the tree
+        // at xeval during phase A (EVAL_TREE modes: d log prior / dX into gprior)
         a.grad = c->d_partial;
         a.lik = c->d_partial + nd;
-        st = launch_coop(c, pass_fn_mode(want_lik ? MODE_EVAL : MODE_EVAL_NOLIK, c->prec, c->trunc, c->d), a, s);
+        const int mode = (lf && c->tree) ? (want_lik ? MODE_EVAL_TREE : MODE_EVAL_NOLIK_TREE)
+                                         : (want_lik ? MODE_EVAL : MODE_EVAL_NOLIK);
+        st = launch_coop(c, pass_fn_mode(mode, c->prec, c->trunc, c->d), a, s);
         if (st) return st;
         if (timed) CK(cudaEventRecord(next_event(c), s));
-        if (c->ag_fn(c->ag_user, c->d_partial, c->d_gathered, nd + 1, (void*)s) != 0)
-            return fail(c, MDS_E_COMM, "all-gather callback failed");
-        combine_kernel<<<(unsigned)((nd + 1 + 255) / 256), 256, 0, s>>>(c->d_gathered, c->world, nd + 1, grad_out,
-                                                                         lik_out);
-        if (lf && c->tree) {
-            // sharded: the standalone tree walk (the EVAL-mode pass has no tree CTA)
-            TreeArgs ta = c->ta;
-            ta.x = xeval;
-            tree_prior_launch(ta, c->d, s);
-        }
-        if (lf)
-            leapfrog_update_kernel<<<(unsigned)((nd + 255) / 256), 256, 0, s>>>(
-                grad_out, xeval, c->d_x, c->d_p, c->d_gl, c->d_xnext, nd, eps, 0.5 * eps, inv_tau2,
-                c->tree ? c->d_gprior : nullptr);
+        if ((st = exchange(c, c->d_partial, c->d_gathered, nd + 1, s))) return st;
+        const unsigned blocks = (unsigned)((nd + 1 + 255) / 256);
+        if (lf)      // rank-ordered combine fused with the leapfrog update
+            combine_update_kernel<<<blocks, 256, 0, s>>>(c->d_gathered, c->world, nd, grad_out, lik_out, xeval, c->d_x,
+                                                         c->d_p, c->d_gl, c->d_xnext, eps, 0.5 * eps, inv_tau2,
+                                                         c->tree ? c->d_gprior : nullptr);
+        else
+            combine_kernel<<<blocks, 256, 0, s>>>(c->d_gathered, c->world, nd + 1, grad_out, lik_out);
     }
     if (timed) CK(cudaEventRecord(next_event(c), s));
     CK(cudaGetLastError());
@@ -333,7 +396,7 @@ mds_status sigma_mh_impl(mds_ctx c, cudaStream_t s, const mds_sigma_prior* prior
 
 // a pass sequence can be captured in a CUDA graph unless the exchange runs on
 // the host (the mds_set_allgather callback of a sharded context)
-bool graph_capturable(mds_ctx c) { return c->world == 1; }
+bool graph_capturable(mds_ctx c) { return c->world == 1 || c->comm; }
 
 // log L only (MODE_LIK) at the context's X for the SigmaParams given, into the
 // device double lik_out; sharded: local partial -> exchange -> rank-ordered sum
@@ -341,17 +404,15 @@ mds_status run_lik_pass(mds_ctx c, const SigmaParams& P, double* lik_out, cudaSt
     PassArgs a = base_args(c, c->d_x);
     a.P = P;
     const PassKernel k = pass_fn_mode(MODE_LIK, c->prec, c->trunc, c->d);
-    if (c->world == 1) {
+    if (direct(c)) {
         a.lik = lik_out;
         return launch_coop(c, k, a, s);
     }
-    if (!c->ag_fn) return fail(c, MDS_E_STATE, "sharded context: register the exchange with mds_set_allgather");
     double* part = c->d_partial + c->n * c->d;
     a.lik = part;
     mds_status st = launch_coop(c, k, a, s);
     if (st) return st;
-    if (c->ag_fn(c->ag_user, part, c->d_gathered, 1, (void*)s) != 0)
-        return fail(c, MDS_E_COMM, "all-gather callback failed");
+    if ((st = exchange(c, part, c->d_gathered, 1, s))) return st;
     combine_kernel<<<1, 32, 0, s>>>(c->d_gathered, c->world, 1, nullptr, lik_out);
     CK(cudaGetLastError());
     return MDS_OK;
@@ -670,7 +731,7 @@ void report_phases(mds_ctx c) {
 }
 
 mds_status create_impl(int64_t n, int32_t d, int32_t precision, int32_t truncation, int32_t rank, int32_t world,
-                       mds_ctx* out) {
+                       const void* nccl_id, mds_ctx* out) {
     if (!out) return MDS_E_INVALID_ARG;
     *out = nullptr;
     if (n < 2 || d < 1 || d > MDS_D_MAX || (precision != MDS_F64 && precision != MDS_F32) ||
@@ -718,7 +779,7 @@ mds_status create_impl(int64_t n, int32_t d, int32_t precision, int32_t truncati
         (st = dalloc(c, &c->d_xnext, m)))
         goto fail_alloc;
     c->d_y = yb;
-    if (world > 1 && ((st = dalloc(c, &c->d_partial, (size_t)n * d + 1)) ||
+    if ((world > 1 || nccl_id) && ((st = dalloc(c, &c->d_partial, (size_t)n * d + 1)) ||
                       (st = dalloc(c, &c->d_gathered, ((size_t)n * d + 1) * world))))
         goto fail_alloc;
     {
@@ -742,6 +803,24 @@ mds_status create_impl(int64_t n, int32_t d, int32_t precision, int32_t truncati
     }
     st = build_schedule(c);
     if (st) goto fail_alloc;
+    if (nccl_id) {
+        // the context's own communicator (collective: every rank of the world calls
+        // this with the same id); the exchange is then ncclAllGather on the context's
+        // stream, so sharded passes can be captured in CUDA graphs
+        NcclApi& api = nccl_api();
+        if (!api.ok) {
+            st = fail(c, MDS_E_COMM, api.err);
+            goto fail_alloc;
+        }
+        ncclUniqueId id;
+        std::memcpy(&id, nccl_id, sizeof(id));
+        const ncclResult_t r = api.CommInitRank(&c->comm, world, id, rank);
+        if (r != ncclSuccess) {
+            c->comm = nullptr;
+            st = fail(c, MDS_E_COMM, std::string("ncclCommInitRank: ") + api.GetErrorString(r));
+            goto fail_alloc;
+        }
+    }
     *out = c;
     return MDS_OK;
 fail_alloc:
@@ -841,12 +920,29 @@ mds_status set_rows_host(mds_ctx c, int64_t i0, int64_t i1, const double* y_lowe
 extern "C" {
 
 mds_status mds_create(int64_t n, int32_t d, int32_t precision, int32_t truncation, mds_ctx* out) {
-    return create_impl(n, d, precision, truncation, 0, 1, out);
+    return create_impl(n, d, precision, truncation, 0, 1, nullptr, out);
 }
 
 mds_status mds_create_sharded(int64_t n, int32_t d, int32_t precision, int32_t truncation, int32_t rank,
-                              int32_t world, mds_ctx* out) {
-    return create_impl(n, d, precision, truncation, rank, world, out);
+                              int32_t world, const void* nccl_unique_id, mds_ctx* out) {
+    return create_impl(n, d, precision, truncation, rank, world, nccl_unique_id, out);
+}
+
+mds_status mds_nccl_unique_id(void* id_out) {
+    if (!id_out) return MDS_E_INVALID_ARG;
+    NcclApi& api = nccl_api();
+    if (!api.ok) return MDS_E_COMM;
+    ncclUniqueId id;
+    if (api.GetUniqueId(&id) != ncclSuccess) return MDS_E_COMM;
+    std::memcpy(id_out, &id, sizeof(id));
+    return MDS_OK;
+}
+
+mds_status mds_has_communicator(mds_ctx c, int32_t* has) {
+    GUARD(c);
+    if (!has) return fail(c, MDS_E_INVALID_ARG, "NULL output");
+    *has = c->comm ? 1 : 0;
+    return MDS_OK;
 }
 
 void mds_destroy(mds_ctx c) {

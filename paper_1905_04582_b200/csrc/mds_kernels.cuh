@@ -178,6 +178,34 @@ __global__ void hamiltonian_kernel(const double* __restrict__ x, const double* _
     }
 }
 
+// Sharded leapfrog step after the exchange: the rank-ordered sum of the gathered
+// partials (gathered[r][0..m) = gradient partials, gathered[r][m] = log L partial)
+// fused with the leapfrog update of leapfrog_update_kernel.  Bitwise identical on
+// every rank (same inputs, same order).
+__global__ void combine_update_kernel(const double* __restrict__ gathered, int world, int64_t m,
+                                      double* __restrict__ grad_out, double* __restrict__ lik_out,
+                                      const double* __restrict__ xe, double* __restrict__ x, double* __restrict__ p,
+                                      double* __restrict__ gl, double* __restrict__ xnext, double eps, double heps,
+                                      double inv_tau2, const double* __restrict__ gprior) {
+    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k > m) return;
+    double g = 0.0;
+    for (int r = 0; r < world; ++r) g += gathered[(size_t)r * (m + 1) + k];
+    if (k == m) {
+        if (lik_out) *lik_out = g;
+        return;
+    }
+    grad_out[k] = g;
+    const double xv = xe[k];
+    const double ph = __fma_rn(heps, gl[k], p[k]);
+    const double gn = gprior ? g + gprior[k] : g - xv * inv_tau2;
+    const double pn = __fma_rn(heps, gn, ph);
+    x[k] = xv;
+    p[k] = pn;
+    gl[k] = gn;
+    xnext[k] = drift(xv, pn, gn, eps, heps);
+}
+
 // rank-ordered sum of gathered partials: out[e] = sum_r gathered[r][e]
 __global__ void combine_kernel(const double* __restrict__ gathered, int world, int64_t len,
                                double* __restrict__ grad_out, double* __restrict__ lik_out) {

@@ -55,16 +55,22 @@ constexpr int PT = 128;             // threads per CTA of the small helper kerne
 //   LEAPFROG_TREE, LEAPFROG_NOLIK_TREE
 //                   the leapfrog modes under the phylogenetic prior: the grid's
 //                   last CTA walks the tree during phase A
+//   EVAL_TREE, EVAL_NOLIK_TREE
+//                   sharded leapfrog steps under the phylogenetic prior: the rank's
+//                   partial (EVAL) while the last CTA walks the tree into gprior; the
+//                   leapfrog update follows the exchange (combine_update_kernel)
 enum Mode {
     MODE_EVAL = 0, MODE_EVAL_NOLIK = 1, MODE_LEAPFROG = 2, MODE_LEAPFROG_NOLIK = 3, MODE_LIK = 4,
-    MODE_LEAPFROG_TREE = 5, MODE_LEAPFROG_NOLIK_TREE = 6
+    MODE_LEAPFROG_TREE = 5, MODE_LEAPFROG_NOLIK_TREE = 6, MODE_EVAL_TREE = 7, MODE_EVAL_NOLIK_TREE = 8
 };
-constexpr int N_MODES = 7;
+constexpr int N_MODES = 9;
 template <int MODE> struct ModeTraits {
-    static constexpr bool TREE = MODE == MODE_LEAPFROG_TREE || MODE == MODE_LEAPFROG_NOLIK_TREE;
-    static constexpr bool LF = MODE == MODE_LEAPFROG || MODE == MODE_LEAPFROG_NOLIK || TREE;   // leapfrog update
+    static constexpr bool TREE = MODE == MODE_LEAPFROG_TREE || MODE == MODE_LEAPFROG_NOLIK_TREE ||
+                                 MODE == MODE_EVAL_TREE || MODE == MODE_EVAL_NOLIK_TREE;
+    static constexpr bool LF = MODE == MODE_LEAPFROG || MODE == MODE_LEAPFROG_NOLIK ||
+                               MODE == MODE_LEAPFROG_TREE || MODE == MODE_LEAPFROG_NOLIK_TREE;   // leapfrog update
     static constexpr bool WL = !(MODE == MODE_EVAL_NOLIK || MODE == MODE_LEAPFROG_NOLIK ||
-                                 MODE == MODE_LEAPFROG_NOLIK_TREE);                         // log L wanted
+                                 MODE == MODE_LEAPFROG_NOLIK_TREE || MODE == MODE_EVAL_NOLIK_TREE);   // log L wanted
     static constexpr bool WG = MODE != MODE_LIK;                                            // gradient wanted
 };
 
@@ -727,6 +733,8 @@ MDS_DECLARE_PASS(3)
 MDS_DECLARE_PASS(4)
 MDS_DECLARE_PASS(5)
 MDS_DECLARE_PASS(6)
+MDS_DECLARE_PASS(7)
+MDS_DECLARE_PASS(8)
 #undef MDS_DECLARE_PASS
 
 }  // namespace mdsk

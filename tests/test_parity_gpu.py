@@ -428,7 +428,7 @@ def test_create_argument_errors(mds):
         assert st == 1, (n, d, prec, trunc, st)          # MDS_E_INVALID_ARG
     for rank, world in [(2, 2), (-1, 2), (0, 0)]:
         h = ctypes.c_void_p()
-        assert mds._abi.lib.mds_create_sharded(10, 2, 0, 1, rank, world, ctypes.byref(h)) == 1
+        assert mds._abi.lib.mds_create_sharded(10, 2, 0, 1, rank, world, None, ctypes.byref(h)) == 1
     # the smallest problem: one pair
     with mds.MDS(2, 1) as c:
         c.set_dissimilarities_packed(np.array([1.5]))

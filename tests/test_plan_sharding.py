@@ -111,3 +111,67 @@ def test_gloo_world2_partition_and_combine(n):
         p.join(timeout=60)
     assert sorted(r for r, _ in res) == [0, 1]
     assert all(ok for _, ok in res)
+
+
+def _oracle_worker(rank, world, port, n, d, q):
+    """One rank of the N > 1 path's host logic with libmds replaced by the oracle:
+    this rank's partial = the Eq. 2 / Eq. 6 sums over the pairs of ITS tile-rows
+    (mds_plan's ownership; the oracle on Y with every other row missing), gathered
+    through the binding's exchange callback (allgather_callback, the function
+    libmds calls through mds_set_allgather) over gloo in host memory, then the
+    rank-ordered combine -- equal to the full oracle and identical on every rank."""
+    import torch
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import oracle
+        import workload
+        import paper_1905_04582_b200 as m
+        w = workload.Workload(n, d, p_missing=0.1, seed=n + world)
+        y = w.y_packed()
+        own = np.zeros(n, dtype=np.uint8)
+        m.mds_plan(n, rank, world, 148, 12, own)
+        rows = np.repeat(np.arange(n), np.arange(n))          # row i of each packed entry
+        ymine = np.where(own[rows] == 1, y, np.nan)
+        r = oracle.loglik_grad(ymine, w.x0, w.sigma, 1, want_absscale=False)
+        cnt = n * d + 1
+        send = np.empty(cnt)
+        send[:-1] = r["grad"].ravel()
+        send[-1] = r["loglik"]
+        recv = np.empty(world * cnt)
+        cb = m.allgather_callback(world, device="cpu")
+        assert cb(None, send.ctypes.data, recv.ctypes.data, cnt, None) == 0
+        g = recv.reshape(world, cnt)
+        comb = g[0].copy()
+        for k in range(1, world):                              # rank order, as combine_kernel
+            comb += g[k]
+        full = oracle.loglik_grad(y, w.x0, w.sigma, 1, want_absscale=False)
+        ok = abs(comb[-1] - full["loglik"]) <= 1e-10 * abs(full["loglik"])
+        G = full["grad"].ravel()
+        ok = ok and bool(np.all(np.abs(comb[:-1] - G) <= np.maximum(1e-9 * np.abs(G), 1e-12)))
+        digest = torch.tensor([float(np.frombuffer(comb.tobytes(), dtype=np.uint64).sum() % (1 << 52))])
+        allv = [torch.zeros(1, dtype=torch.float64) for _ in range(world)]
+        dist.all_gather(allv, digest.double())
+        q.put((rank, ok and all(v.item() == allv[0].item() for v in allv)))
+    except Exception as e:
+        q.put((rank, repr(e)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("n,d,world", [(300, 2, 2), (517, 3, 3)])
+def test_gloo_oracle_partials_exchange_and_combine(n, d, world):
+    import torch.multiprocessing as tmp
+    ctx = tmp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_oracle_worker, args=(r, world, port, n, d, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=180) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+    assert sorted(r for r, _ in res) == list(range(world))
+    assert all(ok is True for _, ok in res), res
