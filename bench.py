@@ -3,18 +3,27 @@
 
 One "step" = one HMC leapfrog step of the hot path:
 half-kick + drift, one fused likelihood+gradient pass over every unordered pair
-(pair kernel + fixed-order reduction [+ NCCL all-gather + combine when sharded]),
-half-kick.  Workload (N=1): BASELINE.json configs[1] = C2, N = 5392, D = 2, fp64,
-clustered synthetic points (K = 189), truncation on.  value = unordered pairs
-(all of them, observed or not) x steps / device time.
+(pair kernel + fixed-order reduction [+ NCCL all-gather + rank-ordered combine
+when sharded]), half-kick.  value = unordered pairs (all of them, observed or
+not) x steps / device time (max over ranks).
 
-  python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+Headline workload, the SAME at every N (strong scaling): BASELINE.json
+configs[4] = C5, N = 100000, D = 2, fp64, clustered synthetic points (K = 189),
+truncation on: 5.0e9 pairs per step, 40 GB of tiled Y (5 GB per rank at N = 8),
+larger than the 126 MB L2, so no flush is needed between steps.  At N = 1 the
+line also carries C2 (BASELINE configs[1], the paper's N = 5392; L2-flushed) and
+C4 (configs[3], N = 30000, D = 6, 10% missing, fp64 and fp32) under "configs".
 
-Under torchrun (N > 1) every rank owns the tile-rows r mod N and the exchange
-is torch.distributed all_gather_into_tensor over NCCL; timing is CUDA events
-on the launching stream, max over ranks.  L2 is flushed (256 MiB write)
-between timed steps because C2's tiled Y (120 MB) would otherwise sit in the
-126 MB L2.
+  python bench.py [--gpus N --steps K --warmup W] [--impl reference] [--dry-run]
+
+--gpus N > 1 without torchrun's environment re-launches this script under
+torch.distributed.run (one rank per GPU, 127.0.0.1 rendezvous).  Each rank
+owns the tile-rows r mod N, generates and uploads only those rows, and owns an
+NCCL communicator inside libmds (unique id broadcast over torch.distributed);
+the exchange is ncclAllGather of n*d + 1 doubles on the context stream.
+--exchange gloo-host instead registers a host-staged gloo all-gather (several
+ranks sharing one GPU: a plumbing check, not a measurement).  --dry-run: plan
+only (CPU, gloo): every rank reports its share of the pairs.
 """
 from __future__ import annotations
 
@@ -22,6 +31,7 @@ import argparse
 import json
 import math
 import os
+import socket
 import subprocess
 import sys
 import tempfile
@@ -36,28 +46,56 @@ METRIC = "MDS likelihood+gradient pair-evals/s"
 UNIT = "pair-evals/s"
 PAPER_CONTEXT = ("PAPER.md:724 (Quadro GP100, OpenCL, fp64, N=5338): 4.5 ms likelihood + 4 ms gradient "
                  "per eval = 1.68e9 unordered pair-evals/s for the pair of calls; context only")
+L2_BYTES = 126 << 20
+SM_MAX_GHZ = 1.965
+I64_REF = 160.0      # FP64 instructions per pair of the libdevice formulation (fixed reference)
 
 
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=2000)
-    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--workload", default="C2")
+    ap.add_argument("--workload", default="C5")
     ap.add_argument("--precision", default="f64", choices=["f64", "f32"])
+    ap.add_argument("--extra", default="auto",
+                    help="extra configs at N = 1 (comma list of C2, C4, C4f32; 'none'); auto = all at N = 1")
     ap.add_argument("--step-size", type=float, default=2e-5)
     ap.add_argument("--prior-sd", type=float, default=10.0)
-    ap.add_argument("--e2e-steps", type=int, default=200)
-    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--e2e-seconds", type=float, default=2.0)
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--graph", type=int, default=0,
-                    help="1: capture the K timed steps (flush + step, with external timing events) in one CUDA "
-                         "graph and replay it (N = 1 only)")
-    ap.add_argument("--flush", choices=["torch", "mds", "mds-clean"], default="mds",
-                    help="L2 flush between timed steps: torch fill, or mds_l2_flush (same write, launched "
-                         "with the pass kernel's grid/block/smem shape)")
+    ap.add_argument("--exchange", choices=["nccl", "torch", "gloo-host"], default="nccl",
+                    help="sharded exchange: libmds-owned NCCL communicator (default), torch.distributed NCCL "
+                         "callback, or host-staged gloo callback (ranks sharing a GPU)")
+    ap.add_argument("--flush", choices=["auto", "mds", "none"], default="auto",
+                    help="L2 flush between timed steps: auto = when the rank's Y fits 2x L2")
+    ap.add_argument("--graph", type=int, default=0, help="1: replay the K timed steps from one CUDA graph")
+    ap.add_argument("--dry-run", action="store_true", help="plan only (CPU): per-rank pair shares")
     return ap.parse_args()
+
+
+# ----------------------------------------------------------------------------- launcher
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+def free_port() -> int:
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def relaunch_under_torchrun(args) -> int:
+    """--gpus N > 1 outside torchrun: one rank per GPU on this node (the driver's own
+    launch line, run for the user)."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", str(args.gpus),
+           "--master-addr", "127.0.0.1", "--master-port", str(free_port()), os.path.abspath(__file__)]
+    cmd += [a for a in sys.argv[1:]]
+    return subprocess.call(cmd)
 
 
 # ----------------------------------------------------------------------------- clocks
@@ -111,34 +149,6 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------------------- helpers
-def dist_env():
-    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
-
-
-def cpu_baseline(w, budget_s: float):
-    """The oracle as it stands (serial C, 1 core) on a bounded sample of the
-    same workload: the leading n_s x n_s sub-problem, whole evaluations."""
-    import oracle
-    n = w.n
-    y = w.y_rows(0, n)
-    # time one full evaluation; if too slow for the budget, shrink to a leading block
-    ns = n
-    t0 = time.perf_counter()
-    oracle.loglik_grad(y, w.x0, w.sigma, 1, want_absscale=False)
-    t1 = time.perf_counter() - t0
-    evals, tot = 1, t1
-    while tot < budget_s:
-        t0 = time.perf_counter()
-        oracle.loglik_grad(y, w.x0, w.sigma, 1, want_absscale=False)
-        tot += time.perf_counter() - t0
-        evals += 1
-    pairs = ns * (ns - 1) // 2
-    return {"value": pairs * evals / tot, "unit": UNIT, "cores": 1, "kind": "oracle",
-            "sample": "%d full %s evaluations (N=%d, %d pairs each), serial C oracle, %.1f s" % (
-                evals, "C2" if n == 5392 else "workload", ns, pairs, tot),
-            "host_cpu": host_cpu()}
-
-
 def host_cpu() -> str:
     """CPU model and logical core count of the host running the oracle."""
     model = "unknown"
@@ -152,19 +162,70 @@ def host_cpu() -> str:
     return "%s, %d logical cores" % (model, os.cpu_count() or 0)
 
 
-def sass_fp64_per_pair(prec: str, d: int) -> float | None:
-    """FP64-pipe instructions per evaluated pair slot in the pair kernel's loop
-    (static SASS count, profiles/sass_counts.json, written by tools/count_sass.py)."""
+def sass_counts(prec: str, d: int, mode: int = 2) -> dict | None:
+    """Per-pair instruction counts of the pass kernel's loop (static SASS count,
+    profiles/sass_counts.json, written by tools/count_sass.py); mode 2 = LEAPFROG."""
     path = os.path.join(ROOT, "profiles", "sass_counts.json")
     try:
         tab = json.load(open(path))
-        return tab["%s_d%d_t1" % (prec, d)]["fp64_per_pair"]
+        key = "%s_d%d_t1" % (prec, d) if mode == 2 else "%s_d%d_t1_m%d" % (prec, d, mode)
+        return tab[key]
     except Exception:
         return None
 
 
+def profile_json(name: str) -> dict:
+    try:
+        return json.load(open(os.path.join(ROOT, "profiles", name)))
+    except Exception:
+        return {}
+
+
+def hbm_peak():
+    """(GB/s, source): MEASURED_PEAKS.json (driver-written) else the B200_PROFILING.md fallback."""
+    try:
+        v = float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"])
+        return v, "MEASURED_PEAKS.json hbm_gbs (of measured)"
+    except Exception:
+        return 6650.0, "B200_PROFILING.md fallback 6.65 TB/s (of fallback)"
+
+
+def t_quantiles(w, samples: int = 200000) -> dict:
+    """Quantiles of t = delta*_ij / sigma over random pairs of the workload's evaluation
+    state (reported with every benchmark; tail t > 8.3 is the cheap part)."""
+    rng = np.random.default_rng(1)
+    i = rng.integers(0, w.n, samples)
+    j = rng.integers(0, w.n, samples)
+    keep = i != j
+    dd = np.linalg.norm(w.x0[i[keep]] - w.x0[j[keep]], axis=1) / w.sigma
+    q = np.quantile(dd, [0.1, 0.5, 0.9])
+    return {"p10": float(q[0]), "p50": float(q[1]), "p90": float(q[2]), "frac_gt_8.3": float((dd > 8.3).mean()),
+            "pairs_sampled": int(keep.sum())}
+
+
+def owned_row_ranges(mds, n, rank, world, chunk_rows):
+    """Contiguous row ranges of the tile-rows this rank owns (cyclic I mod world),
+    cut into pieces of at most chunk_rows rows."""
+    own = np.zeros(n, dtype=np.uint8)
+    mds.mds_plan(n, rank, world, 148, 12, own)
+    out, i = [], 0
+    while i < n:
+        if not own[i]:
+            i += 1
+            continue
+        j = i
+        while j < n and own[j] and j - i < chunk_rows:
+            j += 1
+        out.append((i, j))
+        i = j
+    return out
+
+
 # ----------------------------------------------------------------------------- reference arm
 def run_reference(args):
+    """The oracle as it stands (serial C, 1 core) on this arm's workload/metric:
+    each step is a bounded sample (the leading n_s x n_s sub-problem, one full
+    evaluation) sized so that K + W steps take about two minutes."""
     rank, world, _ = dist_env()
     if rank != 0:
         return
@@ -172,16 +233,15 @@ def run_reference(args):
     import workload
     w = workload.config(args.workload)
     budget = 120.0
-    # per-step sample: leading n_s items so that (K + W) steps take ~budget seconds
-    ns_full = w.n
-    y_all = w.y_rows(0, ns_full)
+    n_probe = min(w.n, 2000)
+    y_probe = w.y_rows(0, n_probe)
     t0 = time.perf_counter()
-    oracle.loglik_grad(y_all, w.x0, w.sigma, 1, want_absscale=False)
-    t_full = time.perf_counter() - t0
+    oracle.loglik_grad(y_probe, w.x0[:n_probe], w.sigma, 1, want_absscale=False)
+    t_probe = max(time.perf_counter() - t0, 1e-6)
+    per_pair = t_probe / (n_probe * (n_probe - 1) / 2)
     per_step = budget / max(1, args.steps + args.warmup)
-    frac = min(1.0, per_step / max(t_full, 1e-9))
-    ns = max(64, int(ns_full * math.sqrt(frac)))
-    ys = y_all[: ns * (ns - 1) // 2]
+    ns = int(min(w.n, max(64, math.sqrt(2.0 * per_step / per_pair))))
+    ys = w.y_rows(0, ns)
     xs = w.x0[:ns]
     for _ in range(args.warmup):
         oracle.loglik_grad(ys, xs, w.sigma, 1, want_absscale=False)
@@ -200,109 +260,235 @@ def run_reference(args):
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample,
                          "host_cpu": host_cpu()},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-    }))
+    }), flush=True)
+
+
+def cpu_baseline(w, budget_s: float, tag: str):
+    """The oracle as it stands (serial C, 1 core) on a bounded sample of the same
+    workload: whole evaluations of its leading n_s x n_s sub-problem."""
+    import oracle
+    ns = min(w.n, 4000)
+    y = w.y_rows(0, ns)
+    x = w.x0[:ns]
+    evals, tot = 0, 0.0
+    while tot < budget_s or evals == 0:
+        t0 = time.perf_counter()
+        oracle.loglik_grad(y, x, w.sigma, 1, want_absscale=False)
+        tot += time.perf_counter() - t0
+        evals += 1
+    pairs = ns * (ns - 1) // 2
+    return {"value": pairs * evals / tot, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": "%d full evaluations (log L + gradient) of the leading %d x %d block of %s (%d pairs "
+                      "each), serial C oracle, %.1f s" % (evals, ns, ns, tag, pairs, tot),
+            "host_cpu": host_cpu()}
+
+
+# ----------------------------------------------------------------------------- dry run (CPU)
+def run_dry(args):
+    """Launcher + rendezvous + ownership plan, no GPU: each rank reports the pairs
+    of its tile-rows; rank 0 checks they partition the triangle."""
+    import torch
+    import torch.distributed as dist
+    import workload
+    import paper_1905_04582_b200 as mds
+    rank, world, _ = dist_env()
+    if world > 1:
+        dist.init_process_group("gloo")
+    idx, n, d, kind, pm = workload.CONFIGS[args.workload]
+    info = mds.mds_plan(n, rank, world, 148, 12)
+    ranges = owned_row_ranges(mds, n, rank, world, 1 << 30)
+    t = torch.tensor([float(info["pairs"]), float(info["tiles"]), float(len(ranges))], dtype=torch.float64)
+    allv = [torch.zeros_like(t) for _ in range(world)] if world > 1 else [t]
+    if world > 1:
+        dist.all_gather(allv, t)
+    if rank == 0:
+        pairs = [float(v[0]) for v in allv]
+        print(json.dumps({"dry_run": True, "n_gpus": world, "workload": args.workload, "n": n,
+                          "pairs_per_rank": pairs, "total_pairs": sum(pairs), "expected_pairs": n * (n - 1) // 2,
+                          "tiles_per_rank": [float(v[1]) for v in allv],
+                          "balance_max_over_mean": max(pairs) / (sum(pairs) / world)}), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
 
 
 # ----------------------------------------------------------------------------- our arm
+class Rank:
+    def __init__(self, args):
+        import torch
+        import torch.distributed as dist
+        self.torch, self.dist = torch, dist
+        self.rank, self.world, self.local = dist_env()
+        self.args = args
+        torch.cuda.set_device(self.local if args.exchange != "gloo-host" else 0)
+        if self.world > 1:
+            if args.exchange == "gloo-host":
+                dist.init_process_group("gloo")
+            else:
+                dist.init_process_group("nccl", device_id=torch.device("cuda", self.local))
+
+    def barrier(self):
+        if self.world > 1:
+            self.dist.barrier()
+
+    def max_over_ranks(self, vals):
+        if self.world == 1:
+            return [float(v) for v in vals]
+        t = self.torch.tensor([float(v) for v in vals], dtype=self.torch.float64,
+                              device="cpu" if self.args.exchange == "gloo-host" else "cuda")
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+        return [float(v) for v in t.cpu()]
+
+    def nccl_id(self):
+        if self.args.exchange != "nccl":
+            return None
+        import paper_1905_04582_b200 as mds
+        if self.world == 1:
+            return None
+        obj = [mds.mds_nccl_unique_id() if self.rank == 0 else None]
+        self.dist.broadcast_object_list(obj, src=0)
+        return obj[0]
+
+
+def build_ctx(R, mds, w, prec, stream):
+    """A context for workload w on this rank: its tile-rows only, generated and
+    uploaded row chunk by row chunk (the full triangle never exists on one host)."""
+    t0 = time.perf_counter()
+    ctx = mds.MDS(w.n, w.d, prec, True, rank=R.rank, world=R.world, stream=stream, nccl_unique_id=R.nccl_id())
+    if R.world > 1 and not ctx.has_communicator():
+        ctx.use_torch_allgather(host_staged=R.args.exchange == "gloo-host")
+    t_gen = 0.0
+    for i0, i1 in owned_row_ranges(mds, w.n, R.rank, R.world, 512):
+        a = time.perf_counter()
+        y = w.y_rows(i0, i1)
+        t_gen += time.perf_counter() - a
+        ctx.set_dissimilarity_rows(i0, i1, y)
+        del y
+    ctx.set_locations(w.x0)
+    ctx.set_sigma(w.sigma)
+    R.torch.cuda.synchronize()
+    return ctx, {"setup_s": time.perf_counter() - t0, "generate_s": t_gen}
+
+
+def time_steps(R, ctx, w, steps, warmup, flush_buf, graph=False, clocks=None):
+    """W untimed warm-up leapfrog steps, then K timed ones, each bracketed by CUDA
+    events on the context's stream; barrier + synchronize on both sides; optional
+    untimed L2 flush before every timed step.  Returns (per-step ms [K], pass-kernel
+    mean ms or None)."""
+    torch = R.torch
+    stream = torch.cuda.current_stream()
+    n, d = w.n, w.d
+    p0 = torch.from_numpy(w.normals(1, (n, d))).cuda()
+    ctx.leapfrog_device(1, R.args.step_size, R.args.prior_sd, p0_dev=p0)
+    for _ in range(max(0, warmup - 1)):
+        ctx.leapfrog_device(1, R.args.step_size, R.args.prior_sd)
+    torch.cuda.synchronize()
+    ev0 = [torch.cuda.Event(enable_timing=True, external=graph) for _ in range(steps)]
+    ev1 = [torch.cuda.Event(enable_timing=True, external=graph) for _ in range(steps)]
+
+    def body():
+        for k in range(steps):
+            if flush_buf is not None:
+                ctx.l2_flush(flush_buf)
+            ev0[k].record(stream)
+            ctx.leapfrog_device(1, R.args.step_size, R.args.prior_sd)
+            ev1[k].record(stream)
+
+    g = None
+    if graph:
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=stream):
+            body()
+        torch.cuda.synchronize()
+    # sharded: events around the pass kernel inside the library (its share of the step)
+    ctx.set_timing(R.world > 1)
+    R.barrier()
+    torch.cuda.synchronize()
+    if clocks:
+        clocks.start()
+        time.sleep(0.2)
+    R.barrier()
+    torch.cuda.synchronize()
+    if g is not None:
+        g.replay()
+    else:
+        body()
+    torch.cuda.synchronize()
+    R.barrier()
+    clk = clocks.stop() if clocks else None
+    step_ms = np.array([a.elapsed_time(b) for a, b in zip(ev0, ev1)])
+    kern_ms = None
+    if R.world > 1:
+        kern_ms, _ = ctx.last_timing()
+    ctx.set_timing(False)
+    if os.environ.get("MDS_PROFILE_PHASES") in ("1", "2"):
+        ctx.set_timing(True)
+        ctx.leapfrog_device(1, R.args.step_size, R.args.prior_sd)
+        ctx.last_timing()
+        ctx.set_timing(False)
+    return step_ms, kern_ms, clk
+
+
+def roofline_of(prec, d, pairs_per_launch, kern_ms, clk_mhz, traffic):
+    """ALU roofline of the pass kernel: FP64 (fp32: FP32+issue)
+    lane-instructions per pair x pairs per launch / launch time vs 148 x 64 lanes x clock."""
+    sc = sass_counts(prec, d)
+    if sc is None or not kern_ms:
+        return None
+    lanes = 64 if prec == "f64" else 128
+    peak = 148 * lanes * SM_MAX_GHZ * 1e9
+    ipp = sc["fp64_per_pair"] if prec == "f64" else sc["fp32_per_pair"]
+    achieved = ipp * pairs_per_launch / (kern_ms * 1e-3)
+    hbm, hbm_src = hbm_peak()
+    bpp = 8.0 if prec == "f64" else 4.0
+    rf = {"bound": "alu", "achieved": achieved / 1e12, "peak": peak / 1e12,
+          "unit": "T %s-lane-op/s" % ("fp64" if prec == "f64" else "fp32"), "frac": achieved / peak,
+          "traffic": traffic,
+          "kernel": "pass_kernel<%s,D=%d,T=1,LEAPFROG>" % (prec, d),
+          "ops_per_pair": ipp, "issued_per_pair": sc.get("issued_per_pair"),
+          "pass_kernel_ms": kern_ms,
+          "peak_source": "148 SM x %d %s lanes/clk x 1.965 GHz max SM clock (B200_PROFILING.md)" % (
+              lanes, "FP64" if prec == "f64" else "FP32"),
+          "hbm_gbs": bpp * pairs_per_launch / (kern_ms * 1e-3) / 1e9,
+          "hbm_frac": bpp * pairs_per_launch / (kern_ms * 1e-3) / (hbm * 1e9), "hbm_peak_source": hbm_src}
+    if clk_mhz:
+        rf["frac_at_measured_clock"] = achieved / (148 * lanes * clk_mhz * 1e6)
+    if prec == "f64":
+        # SURVEY 8(d)(2): pair-evals/s against R_ALU with the FIXED libdevice reference
+        # I64_ref = 160 FP64 instructions per pair (independent of this kernel's count)
+        rf["frac_fixed_I64_ref"] = (pairs_per_launch / (kern_ms * 1e-3)) / (148 * 64 * SM_MAX_GHZ * 1e9 / I64_REF)
+    return rf
+
+
 def run_ours(args):
     import torch
-    import torch.distributed as dist
-    rank, world, local = dist_env()
-    torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     import workload
     import paper_1905_04582_b200 as mds
 
+    R = Rank(args)
+    rank, world = R.rank, R.world
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
     w = workload.config(args.workload)
     n, d = w.n, w.d
     P_N = n * (n - 1) // 2
-    # a dedicated stream (graph capture needs a non-default stream)
-    stream = torch.cuda.Stream()
-    torch.cuda.set_stream(stream)
-    ctx = mds.MDS(n, d, args.precision, True, rank=rank, world=world, stream=stream)
-    if world > 1:
-        ctx.use_torch_allgather()
-    t0 = time.perf_counter()
-    y = w.y_packed()
-    ctx.set_dissimilarities_packed(y)
-    del y
-    ctx.set_locations(w.x0)
-    ctx.set_sigma(w.sigma)
-    t_setup = time.perf_counter() - t0
-    p0 = torch.from_numpy(w.normals(1, (n, d))).cuda()
-    # our kernels per leapfrog step: the persistent pass kernel (phase A pairs +
-    # phase B reduction/leapfrog update); sharded: + combine + update kernels
-    launches_per_step = 1 if world == 1 else 3
+    ctx, setup = build_ctx(R, mds, w, args.precision, stream)
 
-    # > 126 MB L2 (mds-clean: two halves of 256 MiB, written then read)
-    flush = torch.empty((512 if args.flush == "mds-clean" else 256) << 20, dtype=torch.uint8, device="cuda")
-    # warm-up (also primes grad log pi)
-    ctx.leapfrog_device(1, args.step_size, args.prior_sd, p0_dev=p0)
-    for _ in range(max(0, args.warmup - 1)):
-        ctx.leapfrog_device(1, args.step_size, args.prior_sd)
-    torch.cuda.synchronize()
-
+    y_rank_bytes = (8 if args.precision == "f64" else 4) * P_N / world
+    flush = None
+    if args.flush == "mds" or (args.flush == "auto" and y_rank_bytes < 2 * L2_BYTES):
+        flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     clocks = ClockSampler(torch.cuda.current_device())
-    use_graph = bool(args.graph) and world == 1
-    ev0 = [torch.cuda.Event(enable_timing=True, external=use_graph) for _ in range(args.steps)]
-    ev1 = [torch.cuda.Event(enable_timing=True, external=use_graph) for _ in range(args.steps)]
-
-    def timed_steps():
-        for k in range(args.steps):
-            if args.flush == "mds":        # untimed L2 flush before every timed step
-                ctx.l2_flush(flush)
-            elif args.flush == "mds-clean":
-                ctx.l2_flush_clean(flush)
-            else:
-                flush.zero_()
-            ev0[k].record(stream)
-            ctx.leapfrog_device(1, args.step_size, args.prior_sd)
-            ev1[k].record(stream)
-
-    graph = None
-    if use_graph:
-        # launch mechanics only: the same K (flush, step) pairs, captured once on
-        # the context's stream and replayed; events are external (timed) nodes
-        graph = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(graph, stream=stream):
-            timed_steps()
-        torch.cuda.synchronize()
-    # the library's timing mode (events around every launch) perturbs
-    # back-to-back cooperative launches by ~8 us/step; unsharded, a step IS one
-    # pass-kernel launch, so the per-step events below are the kernel's launch
-    # duration.  Sharded steps have several kernels + NCCL: timing mode is on.
-    ctx.set_timing(world > 1)
-    clocks.start()
-    time.sleep(0.2)
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    if graph is not None:
-        graph.replay()
-    else:
-        timed_steps()
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    clk = clocks.stop()
-    step_ms = np.array([a.elapsed_time(b) for a, b in zip(ev0, ev1)])
-    if os.environ.get("MDS_PROFILE_PHASES") in ("1", "2"):
-        ctx.last_timing()                  # prints the last pass's phase split to stderr
-    if world > 1:
-        pair_ms, red_ms = ctx.last_timing()
-    else:
-        pair_ms, red_ms = float(step_ms.mean()), 0.0
-    ctx.set_timing(False)
+    step_ms, kern_ms, clk = time_steps(R, ctx, w, args.steps, args.warmup, flush,
+                                       graph=bool(args.graph), clocks=clocks)
     tot_ms = float(step_ms.sum())
-    if world > 1:
-        t = torch.tensor([tot_ms, pair_ms], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        tot_ms, pair_ms = float(t[0]), float(t[1])
+    if kern_ms is None:
+        kern_ms = float(step_ms.mean())        # unsharded: a step IS one pass-kernel launch
+    tot_ms, kern_ms = R.max_over_ranks([tot_ms, kern_ms])
     ms_per_step = tot_ms / args.steps
     value = P_N * args.steps / (tot_ms * 1e-3)
 
-    # ---- end to end through the public API with host buffers (per step: H2D X, pass, D2H log L + grad)
+    # ---- end to end through the public API with host buffers (per step: H2D X, one
+    # fused pass [+ exchange], D2H log L + gradient)
     def pinned(a):
         t = torch.empty(a.shape, dtype=torch.float64, pin_memory=True)
         t.copy_(torch.from_numpy(np.ascontiguousarray(a)))
@@ -311,96 +497,109 @@ def run_ours(args):
     xs = [pinned(w.x0), pinned(w.x0 + 1e-6)]
     ll = pinned(np.zeros(1))
     g = pinned(np.zeros((n, d)))
-    for q in range(3):
+    e2e_steps = int(max(3, min(200, args.e2e_seconds / max(ms_per_step * 1e-3, 1e-6))))
+    for q in range(2):
         ctx.set_locations(xs[q % 2])
         mds.mds_log_likelihood_and_gradient(ctx.ctx, ll, g)
-    if world > 1:
-        dist.barrier()
+    R.barrier()
     torch.cuda.synchronize()
     e_a, e_b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e_a.record(stream)
-    for q in range(args.e2e_steps):
+    for q in range(e2e_steps):
         ctx.set_locations(xs[q % 2])
         mds.mds_log_likelihood_and_gradient(ctx.ctx, ll, g)
     e_b.record(stream)
     torch.cuda.synchronize()
-    e2e_ms = e_a.elapsed_time(e_b)
-    if world > 1:
-        t = torch.tensor([e2e_ms], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_ms = float(t[0])
-    e2e = {"value": P_N * args.e2e_steps / (e2e_ms * 1e-3), "unit": UNIT,
-           "h2d_bytes_per_step": n * d * 8, "d2h_bytes_per_step": (n * d + 1) * 8,
-           "steps": args.e2e_steps,
+    e2e_ms = R.max_over_ranks([e_a.elapsed_time(e_b)])[0]
+    e2e = {"value": P_N * e2e_steps / (e2e_ms * 1e-3), "unit": UNIT,
+           "h2d_bytes_per_step": n * d * 8, "d2h_bytes_per_step": (n * d + 1) * 8, "steps": e2e_steps,
            "api": "mds_set_locations(host X) + mds_log_likelihood_and_gradient(host log L, host grad)"}
+    ctx.close()
+    del ctx
+
+    # ---- extra configs at N = 1 (the paper's size and BASELINE's "1/2/4/8" config)
+    extras = {}
+    want = [] if world > 1 else (["C2", "C4", "C4f32"] if args.extra == "auto" else
+                                 [e for e in args.extra.split(",") if e and e != "none"])
+    for name in want:
+        cfg = name.replace("f32", "")
+        prec = "f32" if name.endswith("f32") else "f64"
+        we = workload.config(cfg)
+        ce, su = build_ctx(R, mds, we, prec, stream)
+        yb = (8 if prec == "f64" else 4) * we.n_pairs
+        fb = torch.empty(256 << 20, dtype=torch.uint8, device="cuda") if yb < 2 * L2_BYTES else None
+        k = max(args.steps, 20)
+        sm, _, _ = time_steps(R, ce, we, k, max(args.warmup, 3), fb)
+        ce.close()
+        del ce, fb
+        kms = float(sm.mean())
+        rf = roofline_of(prec, we.d, we.n_pairs, kms, clk.get("sm_mhz") if clk else None,
+                         profile_json("traffic.json").get("%s_%s" % (cfg, prec)))
+        extras[name] = {"workload": "%s: N=%d D=%d %s, %.0f%% missing" % (cfg, we.n, we.d, prec, 100 * we.p_missing),
+                        "value": we.n_pairs / (kms * 1e-3), "unit": UNIT, "ms_per_step": kms, "steps": k,
+                        "step_ms_p50": float(np.median(sm)),
+                        "l2": "flushed between timed steps (mds_l2_flush, 256 MiB)" if yb < 2 * L2_BYTES
+                        else "Y (%.1f GB) > L2, no flush" % (yb / 1e9),
+                        "setup_s": su["setup_s"],
+                        "roofline_frac": rf["frac"] if rf else None,
+                        "frac_fixed_I64_ref": rf.get("frac_fixed_I64_ref") if rf else None}
 
     if rank != 0:
-        ctx.close()
         if world > 1:
-            dist.destroy_process_group()
+            R.dist.destroy_process_group()
         return
 
-    # ---- roofline: FP64 pipe (ALU-bound path)
-    fp64_rate, fp32_rate = mds.mds_measure_fma_peaks()
-    sms, _, _ = mds.mds_device_info()
-    peak_derived = sms * 64 * 1.965e9          # 64 FP64 lanes/SM/clk x max SM clock
-    ipp = sass_fp64_per_pair(args.precision, d)
-    roofline = None
-    if ipp is not None and pair_ms > 0:
-        pairs_per_launch = P_N / world
-        achieved = ipp * pairs_per_launch / (pair_ms * 1e-3)
-        roofline = {"bound": "alu", "achieved": achieved / 1e12, "peak": peak_derived / 1e12,
-                    "unit": "T fp64-lane-op/s", "frac": achieved / peak_derived,
-                    "traffic": None, "kernel": "pass_kernel<%s,D=%d,T=1,LEAPFROG>" % (args.precision, d),
-                    "fp64_ops_per_pair": ipp, "pass_kernel_ms": pair_ms, "post_kernel_ms": red_ms,
-                    "peak_source": "148 SM x 64 FP64 lanes/clk x 1.965 GHz (B200_PROFILING.md SM count/clock); "
-                                   "dfma microbenchmark on this GPU: %.2f T lane-op/s" % (fp64_rate / 1e12),
-                    "hbm_frac": (8.0 * pairs_per_launch / (pair_ms * 1e-3)) / 6543.7e9}
-        tr = os.path.join(ROOT, "profiles", "traffic.json")
-        if os.path.exists(tr):
-            try:
-                roofline["traffic"] = json.load(open(tr)).get("%s_%s" % (args.workload, args.precision))
-            except Exception:
-                pass
-
+    traffic = profile_json("traffic.json").get("%s_%s" % (args.workload, args.precision))
+    roofline = roofline_of(args.precision, d, P_N / world, kern_ms, clk.get("sm_mhz") if clk else None, traffic)
+    if roofline is not None:
+        roofline["pass_kernel_share_of_step"] = kern_ms / ms_per_step
+        nc = profile_json("ncu_summary.json").get("%s_%s" % (args.workload, args.precision))
+        if nc:
+            roofline["ncu"] = nc
     cpu = None
     if not args.no_cpu_baseline and world == 1:
-        cpu = cpu_baseline(w, args.cpu_seconds)
+        cpu = cpu_baseline(w, args.cpu_seconds, args.workload)
 
+    if world == 1:
+        par = "single GPU"
+    else:
+        par = "tile-row shards x %d (rank r owns tile-rows I mod %d == r); exchange: %s" % (
+            world, world, {"nccl": "ncclAllGather of n*d+1 doubles per step by the libmds-owned communicator",
+                           "torch": "torch.distributed all_gather_into_tensor (NCCL) callback",
+                           "gloo-host": "host-staged gloo all-gather callback (ranks share one GPU)"}[args.exchange])
     out = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": args.precision, "data": "synthetic",
-        "config": {"workload": "%s: N=%d D=%d %s clustered (K=189) sigma=%.4f, truncation on; "
-                               "one leapfrog step (fused lik+grad pass) per step" % (args.workload, n, d,
-                                                                                    args.precision, w.sigma),
+        "config": {"workload": "%s: N=%d D=%d %s clustered (K=189) sigma=%.4f, truncation on; one leapfrog step "
+                               "(fused lik+grad pass) per step" % (args.workload, n, d, args.precision, w.sigma),
                    "n": n, "d": d, "pairs_per_step": P_N, "observed_fraction": 1.0 - w.p_missing,
-                   "l2": "flushed between timed steps (untimed, %s)" % (
-                       {"torch": "256 MiB torch fill", "mds": "256 MiB write, mds_l2_flush",
-                        "mds-clean": "256 MiB write + 256 MiB read, mds_l2_flush_clean"}[args.flush]),
-                   "launch": "one CUDA graph of the K (flush, step) pairs" if graph is not None
-                   else "stream launches",
-                   "parallelism": "tile-row shards x %d" % world if world > 1 else "single GPU",
-                   "setup_s": t_setup},
+                   "l2": ("flushed between timed steps (untimed mds_l2_flush, 256 MiB write)" if flush is not None
+                          else "no flush: the rank's Y (%.1f GB) exceeds the 126 MB L2" % (y_rank_bytes / 1e9)),
+                   "launch": "one CUDA graph of the K steps" if args.graph else "stream launches",
+                   "parallelism": par, "t_quantiles": t_quantiles(w), **setup},
         "evals_per_s": 1e3 / ms_per_step,
         "step_ms_p50": float(np.median(step_ms)), "step_ms_min": float(step_ms.min()),
-        "gpu_launches": launches_per_step * args.steps,
+        "gpu_launches": (1 if world == 1 else 2) * args.steps,
         "roofline": roofline,
         "cpu_baseline": cpu,
         "e2e": e2e,
         "clocks": clk,
+        "configs": extras,
         "paper_context": PAPER_CONTEXT,
-        "fma_peaks_measured": {"fp64_lane_op_per_s": fp64_rate, "fp32_lane_op_per_s": fp32_rate},
     }
-    print(json.dumps(out))
-    ctx.close()
+    print(json.dumps(out), flush=True)
     if world > 1:
-        dist.destroy_process_group()
+        R.dist.destroy_process_group()
 
 
 if __name__ == "__main__":
     a = parse()
+    if a.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch_under_torchrun(a))
     if a.impl == "reference":
         run_reference(a)
+    elif a.dry_run:
+        run_dry(a)
     else:
         run_ours(a)

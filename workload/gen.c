@@ -99,7 +99,7 @@ int wl_dissim_rows(int64_t n, int32_t d, const double x_true[], uint64_t seed, d
     if (n < 2 || d < 1 || i0 < 0 || i1 > n || i0 > i1) return -1;
     int64_t base = (i0 * (i0 - 1)) / 2;
     if (i0 == 0) base = 0;
-#pragma omp parallel for schedule(dynamic, 16)
+#pragma omp parallel for schedule(dynamic, 1)
     for (int64_t i = (i0 > 1 ? i0 : 1); i < i1; ++i) {
         double *row = out + ((i * (i - 1)) / 2 - base);
         for (int64_t j = 0; j < i; ++j)
