@@ -466,6 +466,10 @@ def run_ours(args):
 
     R = Rank(args)
     rank, world = R.rank, R.world
+    # torch.distributed.run sets OMP_NUM_THREADS=1 per rank: give the input generator
+    # this rank's share of the host cores instead
+    local_world = int(os.environ.get("LOCAL_WORLD_SIZE", world))
+    workload.set_threads(max(1, (os.cpu_count() or 1) // max(1, local_world)))
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
     w = workload.config(args.workload)

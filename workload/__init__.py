@@ -56,8 +56,14 @@ def _load():
         lib.wl_dissim_full_rows.argtypes = [i64, i32, d_p, u64, ctypes.c_double, ctypes.c_double, i64,
                                             P(i64), d_p]
         lib.wl_normals.argtypes = [u64, u64, i64, d_p]
+        lib.wl_set_threads.argtypes = [i32]
         _lib = lib
     return _lib
+
+
+def set_threads(n: int) -> None:
+    """Threads of the row generators (0 = OpenMP default)."""
+    _load().wl_set_threads(int(n))
 
 
 def _dp(a):

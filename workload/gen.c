@@ -20,6 +20,7 @@
  *   probability p_missing the pair is NaN (missing).
  */
 #include <math.h>
+#include <omp.h>
 #include <stdint.h>
 #include <stddef.h>
 
@@ -48,6 +49,11 @@ static double normal(uint64_t seed, uint64_t tag, uint64_t a, uint64_t b, uint64
     uint64_t h2 = key4(seed, tag, a, b, 2 * c + 1);
     return sqrt(-2.0 * log(u01(h1))) * cos(WL_TWO_PI * u01(h2));
 }
+
+/* threads for the row generators (0 = the OpenMP default); a launcher that
+ * sets OMP_NUM_THREADS=1 per rank (torch.distributed.run) can raise it */
+static int wl_threads = 0;
+int wl_set_threads(int32_t n) { wl_threads = n > 0 ? n : 0; return 0; }
 
 enum { TAG_CENTRE = 1, TAG_LABEL = 2, TAG_SPREAD = 3, TAG_X0 = 4, TAG_Y = 5, TAG_MISS = 6, TAG_GAUSS = 7 };
 
@@ -99,7 +105,7 @@ int wl_dissim_rows(int64_t n, int32_t d, const double x_true[], uint64_t seed, d
     if (n < 2 || d < 1 || i0 < 0 || i1 > n || i0 > i1) return -1;
     int64_t base = (i0 * (i0 - 1)) / 2;
     if (i0 == 0) base = 0;
-#pragma omp parallel for schedule(dynamic, 1)
+#pragma omp parallel for schedule(dynamic, 1) num_threads(wl_threads > 0 ? wl_threads : omp_get_max_threads())
     for (int64_t i = (i0 > 1 ? i0 : 1); i < i1; ++i) {
         double *row = out + ((i * (i - 1)) / 2 - base);
         for (int64_t j = 0; j < i; ++j)
@@ -113,7 +119,7 @@ int wl_dissim_full_rows(int64_t n, int32_t d, const double x_true[], uint64_t se
                         double p_missing, int64_t nrows, const int64_t rows[], double out[])
 {
     if (n < 2 || d < 1 || nrows < 0) return -1;
-#pragma omp parallel for schedule(static)
+#pragma omp parallel for schedule(static) num_threads(wl_threads > 0 ? wl_threads : omp_get_max_threads())
     for (int64_t r = 0; r < nrows; ++r) {
         int64_t i = rows[r];
         for (int64_t j = 0; j < n; ++j)
