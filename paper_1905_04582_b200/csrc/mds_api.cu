@@ -291,6 +291,9 @@ PassArgs base_args(mds_ctx c, const double* xeval) {
 }
 
 mds_status launch_coop(mds_ctx c, PassKernel k, PassArgs& a, cudaStream_t s) {
+    // the fp64 pass leaves the per-pair constant of Eq. 2 out of its sums (n_obs is
+    // counted by ready() whenever Y changed)
+    a.lik_const = c->prec == MDS_F64 ? (double)c->n_obs * a.P.k0 : 0.0;
     cudaLaunchConfig_t cfg{};
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeCooperative;
@@ -460,13 +463,32 @@ RowArgs row_args(mds_ctx c) {
     return a;
 }
 
+// observed pairs stored by this context (cached until Y changes; one count kernel)
+mds_status count_obs(mds_ctx c) {
+    if (c->n_obs >= 0) return MDS_OK;
+    CK(cudaMemsetAsync(c->d_count, 0, sizeof(unsigned long long), c->stream));
+    const size_t cnt = (size_t)c->ntl * TB * TB;
+    if (cnt) {
+        if (c->prec == MDS_F64)
+            count_obs_kernel<double><<<1184, 256, 0, c->stream>>>((const double*)c->d_y, cnt, c->d_count);
+        else
+            count_obs_kernel<float><<<1184, 256, 0, c->stream>>>((const float*)c->d_y, cnt, c->d_count);
+        CK(cudaGetLastError());
+    }
+    unsigned long long h = 0;
+    CK(cudaMemcpyAsync(&h, c->d_count, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    c->n_obs = (int64_t)h;
+    return MDS_OK;
+}
+
 mds_status ready(mds_ctx c) {
     if (c->rows_supplied < c->rows_needed)
         return fail(c, MDS_E_STATE, "dissimilarities not set (" + std::to_string(c->rows_supplied) + " of " +
                                         std::to_string(c->rows_needed) + " rows supplied)");
     if (!c->x_set) return fail(c, MDS_E_STATE, "locations not set");
     if (!c->sigma_set) return fail(c, MDS_E_STATE, "sigma not set");
-    return MDS_OK;
+    return count_obs(c);     // the fp64 pass adds n_obs x (-1/2 log(2 pi sigma^2)) once
 }
 
 // evaluate into the internal buffers if stale
@@ -1639,21 +1661,8 @@ mds_status mds_combine_partials_device(mds_ctx c, const double* gathered_dev, in
 mds_status mds_observed_pairs(mds_ctx c, int64_t* count) {
     GUARD(c);
     if (!count) return fail(c, MDS_E_INVALID_ARG, "NULL output");
-    if (c->n_obs < 0) {
-        CK(cudaMemsetAsync(c->d_count, 0, sizeof(unsigned long long), c->stream));
-        const size_t cnt = (size_t)c->ntl * TB * TB;
-        if (cnt) {
-            if (c->prec == MDS_F64)
-                count_obs_kernel<double><<<1184, 256, 0, c->stream>>>((const double*)c->d_y, cnt, c->d_count);
-            else
-                count_obs_kernel<float><<<1184, 256, 0, c->stream>>>((const float*)c->d_y, cnt, c->d_count);
-            CK(cudaGetLastError());
-        }
-        unsigned long long h = 0;
-        CK(cudaMemcpyAsync(&h, c->d_count, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
-        CK(cudaStreamSynchronize(c->stream));
-        c->n_obs = (int64_t)h;
-    }
+    mds_status st = count_obs(c);
+    if (st) return st;
     *count = c->n_obs;
     return MDS_OK;
 }

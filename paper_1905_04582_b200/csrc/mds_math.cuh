@@ -159,7 +159,10 @@ __device__ __forceinline__ bool is_missing(float y) {
 //   WL && WG : one reciprocal of Phi (2 - Q) gives 1/Phi and 1/(2 - Q)
 //   WG only  : 1/Phi alone (no atanh series)
 //   WL only  : 1/(2 - Q) alone (no phi/Phi)
-template <bool TRUNC, int NP, bool WL = true, bool WG = true>
+// ACC: ell is in/out -- the term WITHOUT the constant -1/2 log(2 pi sigma^2) is
+// added to the incoming value (the caller's running sum), the constant being
+// added once per observed pair count at the end (one FP64 add per pair less).
+template <bool TRUNC, int NP, bool WL = true, bool WG = true, bool ACC = false>
 __device__ __forceinline__ void pair_f64_n(const double (&s)[NP], const double (&y)[NP], const SigmaParams& P,
                                            const double* __restrict__ exptab, double (&ell)[NP], double (&u)[NP]) {
     double rs[NP], d[NP], res[NP], l[NP];
@@ -177,7 +180,7 @@ __device__ __forceinline__ void pair_f64_n(const double (&s)[NP], const double (
     for (int i = 0; i < NP; ++i) {
         d[i] = s[i] * rs[i];
         res[i] = y[i] - d[i];
-        if (WL) l[i] = fma(-(res[i] * P.half_inv_sigma2), res[i], P.k0);
+        if (WL) l[i] = fma(-(res[i] * P.half_inv_sigma2), res[i], ACC ? ell[i] : P.k0);
     }
     if (TRUNC) {
         // E' = cg exp(-a), a = t^2/2 = s/(2 sigma^2): k = rint(-256 a / ln2),

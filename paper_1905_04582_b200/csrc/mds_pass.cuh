@@ -76,10 +76,12 @@ template <int MODE> struct ModeTraits {
 
 template <typename T, bool TRUNC> struct Pair;
 template <bool TRUNC> struct Pair<double, TRUNC> {
+    // l is in/out: the caller's running sums; each gets its pair's Eq. 2 term
+    // without the constant -1/2 log(2 pi sigma^2) (added as n_obs k0 at the end)
     template <bool WL, bool WG>
     __device__ __forceinline__ static void eval4(const double (&s)[4], const double (&y)[4], const SigmaParams& P,
                                                  const double* exptab, double (&l)[4], double (&u)[4]) {
-        pair_f64_n<TRUNC, 4, WL, WG>(s, y, P, exptab, l, u);
+        pair_f64_n<TRUNC, 4, WL, WG, true>(s, y, P, exptab, l, u);
     }
 };
 template <bool TRUNC> struct Pair<float, TRUNC> {
@@ -180,6 +182,7 @@ struct PassArgs {
     int vpw;                     // virtual unit ranges per warp (warp_seg has GW * vpw + 1 entries)
     int epl;                     // phase B: slab elements per lane (1, 2 or 4)
     SigmaParams P;
+    double lik_const;            // added to log L: n_obs x P.k0 (fp64 pass), 0 (fp32 pass)
     unsigned long long* prof;    // optional [G][4] globaltimer stamps (start, end A, after sync, end)
 };
 
@@ -326,6 +329,7 @@ pass_kernel(PassArgs a) {
     __syncthreads();
     if (a.prof && threadIdx.x == 0) a.prof[blockIdx.x * 4 + 0] = gtimer();
     A lik_w = A(0);
+    A lacc[4] = {A(0), A(0), A(0), A(0)};   // fp64: running log L sums by lock-step position
 #ifndef MDS_Y_NO_EVICT_FIRST
     const uint64_t ypol = policy_evict_first();
 #endif
@@ -506,26 +510,53 @@ pass_kernel(PassArgs a) {
                         ss[2 * qq + 1] = sb;
                     }
                     T ll[4], uu[4];
-                    Pair<T, TRUNC>::template eval4<WL, WG>(ss, ys, a.P, exptab, ll, uu);
-                    T lsum = T(0);
+                    if constexpr (sizeof(T) == 8) {
+                        // fp64: the log L terms go straight into the 4 running sums
+                        // (missing pairs keep the old sum: a select, not an FP64 add)
 #pragma unroll
-                    for (int i = 0; i < 4; ++i) {
-                        const bool mi = is_missing(ys[i]);
-                        if (WL && !mi) lsum += ll[i];         // predicated, no select
-                        if (WG) uu[i] = mi ? T(0) : uu[i];
-                    }
-                    if (WG) {
+                        for (int i = 0; i < 4; ++i) ll[i] = lacc[i];
+                        Pair<T, TRUNC>::template eval4<WL, WG>(ss, ys, a.P, exptab, ll, uu);
 #pragma unroll
-                        for (int k = 0; k < D; ++k) {
-                            const T va0 = uu[0] * dd[0][k], vb0 = uu[1] * dd[1][k];
-                            const T va1 = uu[2] * dd[2][k], vb1 = uu[3] * dd[3][k];
-                            g0[k] -= A(va0 + va1);
-                            g1[k] -= A(vb0 + vb1);
-                            cv[2 * h][k] = va0 + vb0;
-                            cv[2 * h + 1][k] = va1 + vb1;
+                        for (int i = 0; i < 4; ++i) {
+                            const bool mi = is_missing(ys[i]);
+                            if (WL) lacc[i] = mi ? lacc[i] : ll[i];
+                            if (WG) uu[i] = mi ? T(0) : uu[i];
                         }
+                        if (WG) {
+                            // pair (row r, column c) adds -u (x_r - x_c) to row r and +u (x_r - x_c)
+                            // to column c: rows by fused multiply-adds, columns as one product + one fma
+#pragma unroll
+                            for (int k = 0; k < D; ++k) {
+                                g0[k] = fma(-uu[0], dd[0][k], g0[k]);
+                                g0[k] = fma(-uu[2], dd[2][k], g0[k]);
+                                g1[k] = fma(-uu[1], dd[1][k], g1[k]);
+                                g1[k] = fma(-uu[3], dd[3][k], g1[k]);
+                                cv[2 * h][k] = fma(uu[0], dd[0][k], uu[1] * dd[1][k]);
+                                cv[2 * h + 1][k] = fma(uu[2], dd[2][k], uu[3] * dd[3][k]);
+                            }
+                        }
+                    } else {
+                        Pair<T, TRUNC>::template eval4<WL, WG>(ss, ys, a.P, exptab, ll, uu);
+                        T lsum = T(0);
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) {
+                            const bool mi = is_missing(ys[i]);
+                            if (WL && !mi) lsum += ll[i];         // predicated, no select
+                            if (WG) uu[i] = mi ? T(0) : uu[i];
+                        }
+                        if (WG) {
+#pragma unroll
+                            for (int k = 0; k < D; ++k) {
+                                const T va0 = uu[0] * dd[0][k], vb0 = uu[1] * dd[1][k];
+                                const T va1 = uu[2] * dd[2][k], vb1 = uu[3] * dd[3][k];
+                                g0[k] -= A(va0 + va1);
+                                g1[k] -= A(vb0 + vb1);
+                                cv[2 * h][k] = va0 + vb0;
+                                cv[2 * h + 1][k] = va1 + vb1;
+                            }
+                        }
+                        if (WL) lik_w += A(lsum);
                     }
-                    if (WL) lik_w += A(lsum);
                 }
                 double* __restrict__ cslab = a.slabs + (size_t)cpos * TB * D + (size_t)jj0 * D;
 #ifndef MDS_EXP_NO_COLRED
@@ -558,6 +589,7 @@ pass_kernel(PassArgs a) {
         }
     }
     }   // virtual ranges
+    lik_w += (lacc[0] + lacc[1]) + (lacc[2] + lacc[3]);
 #pragma unroll
     for (int m = 16; m >= 1; m >>= 1) lik_w += __shfl_xor_sync(0xffffffffu, lik_w, m);
     if (lane == 0) a.likpart[gw] = lik_w;
@@ -705,7 +737,9 @@ pass_kernel(PassArgs a) {
             for (int w = 0; w < WPC; ++w) t += red[0][w][threadIdx.x];
 #pragma unroll
             for (int m = 16; m >= 1; m >>= 1) t += __shfl_xor_sync(0xffffffffu, t, m);
-            if (threadIdx.x == 0) *a.lik = t;
+            // the per-pair constant -1/2 log(2 pi sigma^2) of the fp64 path, once:
+            // n_obs (this context's observed pairs) x k0
+            if (threadIdx.x == 0) *a.lik = t + a.lik_const;
         }
     }
     if (a.prof) {
