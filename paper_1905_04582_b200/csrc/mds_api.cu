@@ -13,6 +13,7 @@
 #include <vector>
 
 #include <dlfcn.h>
+#include <nvtx3/nvToolsExt.h>   // header-only NVTX v3: ranges cost nothing unless a profiler attaches
 #include <nccl.h>   // types and enum values only: the entry points are resolved at run time (nccl_api)
 
 #include "../../include/mds.h"
@@ -26,6 +27,13 @@ using namespace mdsk;
 
 namespace {
 const char* kVersion = "0.3.0";
+
+// NVTX range for the lifetime of a scope (nsys / ncu --nvtx timelines of the host
+// orchestration: passes, exchanges, HMC transitions, sigma updates, uploads)
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
 
 // NCCL, loaded on first use.  In a process that already holds libnccl.so.2
 // (torch's bundled copy), RTLD_NOLOAD reuses that one, so the library and
@@ -312,6 +320,7 @@ mds_status launch_coop(mds_ctx c, PassKernel k, PassArgs& a, cudaStream_t s) {
 // in rank order, stream-ordered on s (NCCL all-gather over NVLink, or the caller's
 // callback)
 mds_status exchange(mds_ctx c, const double* send, double* recv, int64_t count, cudaStream_t s) {
+    NvtxRange nv("mds_exchange");
     if (c->comm) {
         const ncclResult_t r = nccl_api().AllGather(send, recv, (size_t)count, ncclFloat64, c->comm, s);
         if (r != ncclSuccess)
@@ -336,6 +345,7 @@ inline bool direct(mds_ctx c) { return c->world == 1 && !c->comm; }
 // timing mode three events bracket the pass kernel and the post-kernel work.
 mds_status run_pass(mds_ctx c, const double* xeval, double* grad_out, double* lik_out, bool lf, double eps,
                     double inv_tau2, cudaStream_t s, bool timed, bool want_lik = true) {
+    NvtxRange nv(lf ? "mds_leapfrog_step" : "mds_pass");
     timed = timed && c->timing;
     const int64_t nd = c->n * c->d;
     PassArgs a = base_args(c, xeval);
@@ -404,6 +414,7 @@ bool graph_capturable(mds_ctx c) { return c->world == 1 || c->comm; }
 // log L only (MODE_LIK) at the context's X for the SigmaParams given, into the
 // device double lik_out; sharded: local partial -> exchange -> rank-ordered sum
 mds_status run_lik_pass(mds_ctx c, const SigmaParams& P, double* lik_out, cudaStream_t s) {
+    NvtxRange nv("mds_lik_pass");
     PassArgs a = base_args(c, c->d_x);
     a.P = P;
     const PassKernel k = pass_fn_mode(MODE_LIK, c->prec, c->trunc, c->d);
@@ -853,6 +864,7 @@ fail_alloc:
 
 // pack rows [i0, i1) from fp64 packed rows in device memory into the tiles
 mds_status pack_rows_device(mds_ctx c, int64_t i0, int64_t i1, const double* src_dev, int64_t src_base) {
+    NvtxRange nv("mds_pack_rows");
     CK(cudaMemsetAsync(c->d_bad, 0, sizeof(int), c->stream));
     PackArgs a;
     a.src = src_dev;
@@ -1518,6 +1530,7 @@ namespace {
 // replaces the likelihood-only pass at the current sigma.
 mds_status sigma_mh_impl(mds_ctx c, cudaStream_t s, const mds_sigma_prior* prior, double step, double z, double u,
                          int32_t* accepted, double* log_ratio, const double* cur_ll_dev) {
+    NvtxRange nv("mds_sigma_mh_step");
     if (!prior || !(prior->shape > 0.0) || !(prior->rate > 0.0) || !std::isfinite(prior->shape) ||
         !std::isfinite(prior->rate))
         return fail(c, MDS_E_INVALID_ARG, "sigma prior needs shape > 0 and rate > 0");

@@ -132,6 +132,7 @@ void hmc_session_end(HmcSession& S) {
 // (re)capture the L-step trajectory at the context's current sigma constants;
 // an existing executable graph is updated in place (same topology)
 mds_status hmc_session_capture(mds_ctx c, HmcSession& S) {
+    NvtxRange nv("mds_hmc_capture");
     if (!graph_capturable(c)) return MDS_OK;      // host-callback exchange: direct launches
     cudaGraph_t graph = nullptr;
     CK(cudaStreamBeginCapture(S.s, cudaStreamCaptureModeThreadLocal));
@@ -192,6 +193,7 @@ mds_status hmc_session_mark(mds_ctx c, HmcSession& S, cudaEvent_t e) {
 
 // one HMC transition with momentum stream (seed, it): Metropolis accept on dH
 mds_status hmc_session_transition(mds_ctx c, HmcSession& S, uint64_t seed, uint64_t it) {
+    NvtxRange nv("mds_hmc_transition");
     cudaStream_t s = S.s;
     const int64_t m = c->n * c->d;
     const size_t mbytes = (size_t)c->npad * c->d * sizeof(double);
