@@ -147,7 +147,9 @@ mds_status mds_set_locations(mds_ctx ctx, const double *x);
  * validated (the caller owns finiteness of device data). */
 mds_status mds_set_locations_device(mds_ctx ctx, const double *x_dev);
 
-/* sigma > 0 and finite (the standard deviation, not sigma^2; R13). */
+/* The standard deviation sigma (not sigma^2; R13), 1e-30 <= sigma <= 1e30
+ * (the per-sigma device constants hold sigma^-7 .. sigma^2; reading R33).
+ * Outside -> MDS_E_INVALID_ARG. */
 mds_status mds_set_sigma(mds_ctx ctx, double sigma);
 
 /* ---- evaluation (one fused pass computes both) ------------------------- */
@@ -194,7 +196,7 @@ mds_status mds_combine_partials_device(mds_ctx ctx, const double *gathered_dev, 
 /* ---- sigma side ------------------------------------ */
 
 /* log L (Eq. 2) at the context's X and Y for another sigma
- * (> 0, finite), into *loglik (host).  The context's sigma and cached results
+ * (in [1e-30, 1e30]), into *loglik (host).  The context's sigma and cached results
  * are unchanged.  One likelihood-only pass: the per-pair Eq. 2 term without
  * the Eq. 6 coefficient, no gradient reduction.  Synchronises.  Errors:
  * MDS_E_INVALID_ARG, MDS_E_STATE (inputs not set), MDS_E_CUDA, MDS_E_COMM. */

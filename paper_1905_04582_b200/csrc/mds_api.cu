@@ -404,6 +404,8 @@ mds_status run_pass(mds_ctx c, const double* xeval, double* grad_out, double* li
 }
 
 SigmaParams sigma_params(double sigma);
+// the sigma range of the device constants (sigma^+-7 normal, sigma^2 finite)
+inline bool sigma_ok(double sigma) { return sigma >= 1e-30 && sigma <= 1e30; }
 mds_status sigma_mh_impl(mds_ctx c, cudaStream_t s, const mds_sigma_prior* prior, double step, double z, double u,
                          int32_t* accepted, double* log_ratio, const double* cur_ll_dev);
 
@@ -1080,7 +1082,7 @@ mds_status mds_set_locations_device(mds_ctx c, const double* x_dev) {
 
 mds_status mds_set_sigma(mds_ctx c, double sigma) {
     GUARD(c);
-    if (!(sigma > 0.0) || !std::isfinite(sigma)) return fail(c, MDS_E_INVALID_ARG, "sigma must be > 0 and finite");
+    if (!sigma_ok(sigma)) return fail(c, MDS_E_INVALID_ARG, "sigma must lie in [1e-30, 1e30]");
     c->sigma = sigma;
     c->P = sigma_params(sigma);
     c->sigma_set = true;
@@ -1091,7 +1093,7 @@ mds_status mds_set_sigma(mds_ctx c, double sigma) {
 mds_status mds_log_likelihood_at_sigma(mds_ctx c, double sigma, double* loglik) {
     GUARD(c);
     if (!loglik) return fail(c, MDS_E_INVALID_ARG, "NULL output");
-    if (!(sigma > 0.0) || !std::isfinite(sigma)) return fail(c, MDS_E_INVALID_ARG, "sigma must be > 0 and finite");
+    if (!sigma_ok(sigma)) return fail(c, MDS_E_INVALID_ARG, "sigma must lie in [1e-30, 1e30]");
     mds_status st = ready(c);
     if (st) return st;
     st = run_lik_pass(c, sigma_params(sigma), c->d_lik + 2, c->stream);
@@ -1541,7 +1543,7 @@ mds_status sigma_mh_impl(mds_ctx c, cudaStream_t s, const mds_sigma_prior* prior
     const double phi0 = 2.0 * std::log(c->sigma);          // phi = log sigma^2
     const double phi1 = phi0 + step * z;
     const double sigma1 = std::exp(0.5 * phi1);
-    if (!(sigma1 > 0.0) || !std::isfinite(sigma1)) return fail(c, MDS_E_INVALID_ARG, "proposal sigma out of range");
+    if (!sigma_ok(sigma1)) return fail(c, MDS_E_INVALID_ARG, "proposal sigma outside [1e-30, 1e30]");
     // log L at the current sigma: cached from the previous step when nothing changed,
     // or handed in by the HMC driver
     const bool need_cur = !cur_ll_dev && c->mh_version != c->version;
@@ -1581,14 +1583,25 @@ SigmaParams sigma_params(double sigma) {
     P.half_inv_sigma2 = 0.5 / (sigma * sigma);
     P.k0 = -0.5 * std::log(2.0 * pi * sigma * sigma);
     P.cg = 1.0 / (sigma * std::sqrt(2.0 * pi));
-    P.ks = KAPPA64 * sigma;
-    P.two_ks = 2.0 * KAPPA64 * sigma;
+    // the rational q = P/R in d: P_j / (cg sigma^j), R_j / sigma^j (sigma in [1e-30, 1e30]:
+    // sigma^-7 stays normal); d clamped at TCLAMP64 sigma (high word, rounded up)
+    {
+        double sj = 1.0;
+        for (int j = 0; j <= QR64_DEG; ++j) {
+            if (j <= QP64_DEG) P.qp[j] = QP64_CH[j] / (P.cg * sj);
+            P.qr[j] = QR64_CH[j] / sj;
+            sj *= sigma;
+        }
+        const double dcl = TCLAMP64 * sigma;
+        uint64_t bits;
+        std::memcpy(&bits, &dcl, sizeof(bits));
+        P.dclamp_hi = (int)(bits >> 32) + 1;
+    }
     P.inv_sigma_f = (float)P.inv_sigma;
     P.inv_sigma2_f = (float)P.inv_sigma2;
     P.half_inv_sigma2_f = (float)P.half_inv_sigma2;
     P.k0_f = (float)P.k0;
     P.cg_f = (float)P.cg;
-    for (int j = 0; j <= Q64_DEG; ++j) P.qc[j] = Q64_CH[j] / P.cg;
     return P;
 }
 }  // namespace

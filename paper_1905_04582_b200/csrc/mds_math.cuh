@@ -11,9 +11,9 @@
 //   E'     = cg exp(-t^2/2), cg = 1/(sigma sqrt(2 pi)) -- one exp, argument from s
 //            directly: 2^n [cg 2^(j/256)] p(r), 256-entry table in shared memory
 //            (scaled by cg per launch), degree-4 p
-//   Q      = 1 - Phi(t) = E' q'(w),  q' = erfcx(t/sqrt2)/(2 cg) as a minimax polynomial
-//            in w = (t-K)/(t+K) (one reciprocal); absolute error of Q <= 3e-16
-//   1/Phi, 1/(2-Q) from ONE reciprocal of Phi(2-Q)
+//   Q      = 1 - Phi(t) = E' P'(d)/R'(d): erfcx(t/sqrt2)/2 as a weighted-minimax rational
+//            of degree (6, 7) (positive coefficients; absolute error of Q <= 2e-17 + rounding)
+//   1/Phi, Q/(2-Q) from ONE reciprocal of (R - EP)(2R - EP), EP = E' P' = Q R
 //   log Phi = log1p(-Q) = -2 atanh(Q/(2-Q))        -- degree-7 polynomial in z = (Q/(2-Q))^2
 //            <= 1/9; absolute error <= 5e-14 (log Phi enters log L only: DESIGN.md R32)
 //   phi/(sigma Phi) = E' / Phi                     -- shares E' with Q
@@ -33,10 +33,10 @@ struct SigmaParams {
     double half_inv_sigma2;  // 1/(2 sigma^2)
     double k0;               // -1/2 log(2 pi sigma^2)
     double cg;               // 1/(sigma sqrt(2 pi))
-    double ks;               // KAPPA64 * sigma: w = (d - ks)/(d + ks) = (t - K)/(t + K)
-    double two_ks;           // 2 KAPPA64 sigma
-    double qc[Q64_DEG + 1];  // Q64_C / cg: with the exp table scaled by cg (E' = cg E), Q = E' q'(w)
-                             // and phi/(sigma Phi) = E' / Phi -- one multiply less per pair
+    double qp[QP64_DEG + 1]; // P_j / (cg sigma^j): Q = E' P'(d) / R'(d) with E' = cg E (exp table scaled
+    double qr[QR64_DEG + 1]; // R_j / sigma^j      by cg), in d directly: no t = d/sigma multiply
+    int dclamp_hi;           // high word of TCLAMP64 sigma: d clamped there before P', R'
+    int pad_;
     float inv_sigma_f, inv_sigma2_f, half_inv_sigma2_f, k0_f, cg_f;
 };
 
@@ -186,7 +186,7 @@ __device__ __forceinline__ void pair_f64_n(const double (&s)[NP], const double (
         // E' = cg exp(-a), a = t^2/2 = s/(2 sigma^2): k = rint(-256 a / ln2),
         // E' = 2^(k>>8) [cg 2^((k&255)/256)] p(r), |r| <= ln2/512 (cg-scaled table in
         // shared memory, built per launch; degree-4 polynomial)
-        double r[NP], E[NP], w[NP], den[NP], y0[NP];
+        double r[NP], E[NP];
         int k[NP];
         const double MAGIC = 6755399441055744.0;   // 1.5 * 2^52
 #pragma unroll
@@ -198,10 +198,25 @@ __device__ __forceinline__ void pair_f64_n(const double (&s)[NP], const double (
             const double fk = kd - MAGIC;
             r[i] = fma(fk, -EXPT64_STEP_HI, -a);                                          // ln2/256 hi
             r[i] = fma(fk, -EXPT64_STEP_LO, r[i]);                                        // ln2/256 lo
-            // w = (t - K)/(t + K) = (d - K sigma)/(d + K sigma): MUFU seed issued early
-            den[i] = d[i] + P.ks;
-            y0[i] = rcp_seed(den[i]);
         }
+        // Q = 1 - Phi(t) = E q(t), q = P/R a rational of degree (6, 7) in t with positive
+        // coefficients (tools/gen_coeffs.py), evaluated in d with the 1/sigma^j folded
+        // into the coefficients; d clamped at 38 sigma (beyond, E' underflows).  Two
+        // independent Horner chains, no reciprocal for a transformed variable.
+        double pp[NP], rr[NP], dc[NP];
+#pragma unroll
+        for (int i = 0; i < NP; ++i) {
+            dc[i] = __hiloint2double(min(__double2hiint(d[i]), P.dclamp_hi), __double2loint(d[i]));
+            pp[i] = fma(P.qp[QP64_DEG], dc[i], P.qp[QP64_DEG - 1]);
+            rr[i] = fma(P.qr[QR64_DEG], dc[i], P.qr[QR64_DEG - 1]);
+        }
+#pragma unroll
+        for (int j = QR64_DEG - 2; j >= 0; --j)
+#pragma unroll
+            for (int i = 0; i < NP; ++i) {
+                rr[i] = fma(rr[i], dc[i], P.qr[j]);
+                if (j <= QP64_DEG - 2) pp[i] = fma(pp[i], dc[i], P.qp[j]);
+            }
         double p[NP];
 #pragma unroll
         for (int i = 0; i < NP; ++i) p[i] = EXPT64_C[EXPT64_DEG];
@@ -220,26 +235,22 @@ __device__ __forceinline__ void pair_f64_n(const double (&s)[NP], const double (
             // < 2^-1023 sigma sqrt(2 pi) in Q, both far inside the tolerances)
             const int ehi = __double2hiint(pt) + (int)((unsigned)(k[i] >> 8) << 20);
             E[i] = __hiloint2double(max(ehi, 0), __double2loint(pt));
-            const double e1 = fma(-den[i], y0[i], 1.0);
-            const double ee = fma(e1, e1, e1);
-            const double rden = fma(ee, y0[i], y0[i]);
-            w[i] = fma(-P.two_ks, rden, 1.0);
         }
-        double q[NP];
-#pragma unroll
-        for (int i = 0; i < NP; ++i) q[i] = P.qc[Q64_DEG];
-#pragma unroll
-        for (int j = Q64_DEG - 1; j >= 0; --j)
-#pragma unroll
-            for (int i = 0; i < NP; ++i) q[i] = fma(q[i], w[i], P.qc[j]);
-        double Q[NP], Phi[NP], opp[NP], prod[NP], z0[NP];
+        // With EP = E' P' = Q R:  1 - Q = (R - EP)/R,  2 - Q = (2R - EP)/R, so
+        //   1/Phi = R / (R - EP),   Q/(2 - Q) = EP / (2R - EP)
+        // and one refined reciprocal of their product gives both (no cancellation:
+        // R - EP = R Phi >= R/2).  phi/(sigma Phi) = E'/Phi = E' R / (R - EP).
+        double EP[NP], D1[NP], D2[NP], prod[NP], z0[NP], nG[NP], nS[NP];
 #pragma unroll
         for (int i = 0; i < NP; ++i) {
-            Q[i] = E[i] * q[i];
-            Phi[i] = 1.0 - Q[i];
-            opp[i] = 2.0 - Q[i];
-            prod[i] = (WL && WG) ? Phi[i] * opp[i] : (WG ? Phi[i] : opp[i]);
+            EP[i] = E[i] * pp[i];
+            D1[i] = rr[i] - EP[i];
+            D2[i] = fma(2.0, rr[i], -EP[i]);
+            prod[i] = (WL && WG) ? D1[i] * D2[i] : (WG ? D1[i] : D2[i]);
             z0[i] = rcp_seed(prod[i]);
+            // numerators, formed while the reciprocal is in flight
+            if (WG) nG[i] = WL ? (E[i] * rr[i]) * D2[i] : E[i] * rr[i];
+            if (WL) nS[i] = WG ? EP[i] * D1[i] : EP[i];
         }
         double sa[NP], zz[NP], G[NP];
 #pragma unroll
@@ -247,13 +258,9 @@ __device__ __forceinline__ void pair_f64_n(const double (&s)[NP], const double (
             const double f1 = fma(-prod[i], z0[i], 1.0);
             const double f2 = fma(f1, f1, f1);
             const double rp = fma(f2, z0[i], z0[i]);
-            if (WG) {
-                const double invPhi = WL ? opp[i] * rp : rp;
-                G[i] = E[i] * invPhi;             // E already carries cg
-            }
+            if (WG) G[i] = nG[i] * rp;            // E'/Phi (E' carries cg)
             if (WL) {
-                const double invOpp = WG ? Phi[i] * rp : rp;
-                sa[i] = Q[i] * invOpp;
+                sa[i] = nS[i] * rp;               // Q/(2 - Q)
                 zz[i] = sa[i] * sa[i];
             }
         }

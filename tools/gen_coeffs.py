@@ -101,6 +101,54 @@ def fit_q(deg, kappa, tmax=12):
     return lawson(xs, fs, wts, deg)
 
 
+def fit_q_rational(m, n, tmax=14, npts=300, iters=40):
+    """q(t) = erfcx(t/sqrt2)/2 = P(t)/R(t), deg P = m, deg R = n, R(0) = 1, on t in
+    [0, tmax] (Chebyshev nodes in w = (t-4)/(t+4)), weighted by E(t) = e^{-t^2/2} so
+    the fitted quantity is the ABSOLUTE error of Q(t) = E P/R.  Sanathanan-Koerner
+    iteration (linearised P - q R, reweighted by 1/R_prev) with Lawson weights for
+    the minimax.  Beyond tmax E < 1e-42: the rational only has to stay positive
+    and bounded there (every coefficient of this fit is positive)."""
+    K = mp.mpf(4)
+    wmax = (tmax - K) / (tmax + K)
+    ts = [K * (1 + w) / (1 - w) for w in cheb_nodes(mp.mpf(-1), wmax, npts)]
+    fs = [Qf(t) * mp.exp(t * t / 2) for t in ts]
+    W = [mp.exp(-t * t / 2) for t in ts]
+    Rprev = [mp.mpf(1)] * npts
+    lam = [mp.mpf(1)] * npts
+    best = None
+
+    def ev(cs, t):
+        acc = mp.mpf(0)
+        for a in reversed(cs):
+            acc = acc * t + a
+        return acc
+
+    for it in range(iters):
+        nu = m + 1 + n
+        A = mp.matrix(nu, nu)
+        b = mp.matrix(nu, 1)
+        for k, t in enumerate(ts):
+            wk = lam[k] * (W[k] / Rprev[k]) ** 2
+            row = [t ** j for j in range(m + 1)] + [-fs[k] * t ** j for j in range(1, n + 1)]
+            for i in range(nu):
+                b[i] += wk * row[i] * fs[k]
+                for j in range(nu):
+                    A[i, j] += wk * row[i] * row[j]
+        c = mp.lu_solve(A, b)
+        P = [c[j] for j in range(m + 1)]
+        R = [mp.mpf(1)] + [c[m + 1 + j] for j in range(n)]
+        Rv = [ev(R, t) for t in ts]
+        errs = [abs(W[k] * (fs[k] - ev(P, t) / Rv[k])) for k, t in enumerate(ts)]
+        mx = max(errs) if min(Rv) > 0 else mp.inf
+        if best is None or mx < best[0]:
+            best = (mx, P, R)
+        Rprev = Rv
+        if it >= 8:
+            s = sum(lam[k] * errs[k] for k in range(npts))
+            lam = [lam[k] * errs[k] / s * npts for k in range(npts)]
+    return best
+
+
 def fit_atanh(deg):
     xs = cheb_nodes(mp.mpf(0), mp.mpf(1) / 9, 120)
     fs = []
@@ -128,10 +176,13 @@ def main():
     hi = mp.floor(l256 / mp.power(2, e - 31)) * mp.power(2, e - 31)
     lo = l256 - hi
     q64 = fit_q(13, kappa64)
+    qr64 = fit_q_rational(6, 7)
+    assert all(x > 0 for x in qr64[1]) and all(x > 0 for x in qr64[2]), "rational q: coefficient sign"
     at64 = fit_atanh(7)
     exp32 = fit_exp(5)
     q32 = fit_q(6, kappa32, tmax=7)
     at32 = fit_atanh(3)
+    print("qr64     deg (6,7)  weighted max err %.3e" % float(qr64[0]), file=sys.stderr)
     for name, r in [("exp64", exp64), ("expt64", expt64), ("q64", q64), ("atanh64", at64),
                     ("exp32", exp32), ("q32", q32), ("atanh32", at32)]:
         print("%-8s deg %2d  weighted max err %.3e" % (name, len(r[1]) - 1, float(r[0])), file=sys.stderr)
@@ -158,6 +209,15 @@ def main():
         "constexpr int Q64_DEG = %d;" % (len(q64[1]) - 1),
         "static __constant__ double Q64_C[] = {%s};" % fmt(q64[1]),
         "constexpr double Q64_CH[] = {%s};" % fmt(q64[1]),
+        "// q(t) = erfcx(t/sqrt2)/2 = P(t)/R(t), deg (6, 7), R(0) = 1, all coefficients > 0 (no pole on t >= 0);",
+        "// max |E(t)(q - P/R)| = %.2e on [0, 14] (E = e^{-t^2/2}: the absolute error of Q = 1 - Phi)." % float(qr64[0]),
+        "// One reciprocal of R(1-Q) R(2-Q) then gives 1/Phi and Q/(2-Q) (no reciprocal for a variable).",
+        "// Host copies: the kernels take P / (cg sigma^j) and R / sigma^j per sigma (SigmaParams::qp, qr)",
+        "constexpr int QP64_DEG = %d;" % (len(qr64[1]) - 1),
+        "constexpr int QR64_DEG = %d;" % (len(qr64[2]) - 1),
+        "constexpr double QP64_CH[] = {%s};" % fmt(qr64[1]),
+        "constexpr double QR64_CH[] = {%s};" % fmt(qr64[2]),
+        "constexpr double TCLAMP64 = 38.0;   // t = d/sigma clamped here (E' < 1e-313 cg beyond)",
         "// 2 atanh(sqrt z)/sqrt z, z in [0,1/9]; max rel err %.2e (log Phi only enters log L: DESIGN.md R32)" % float(at64[0]),
         "constexpr int ATANH64_DEG = %d;" % (len(at64[1]) - 1),
         "static __constant__ double ATANH64_C[] = {%s};" % fmt(at64[1]),
