@@ -14,8 +14,8 @@
 //   Q      = 1 - Phi(t) = E' P'(d)/R'(d): erfcx(t/sqrt2)/2 as a weighted-minimax rational
 //            of degree (6, 7) (positive coefficients; absolute error of Q <= 2e-17 + rounding)
 //   1/Phi, Q/(2-Q) from ONE reciprocal of (R - EP)(2R - EP), EP = E' P' = Q R
-//   log Phi = log1p(-Q) = -2 atanh(Q/(2-Q))        -- degree-7 polynomial in z = (Q/(2-Q))^2
-//            <= 1/9; absolute error <= 5e-14 (log Phi enters log L only: DESIGN.md R32)
+//   log Phi = log1p(-Q) = -2 atanh(Q/(2-Q))        -- degree-6 polynomial in z = (Q/(2-Q))^2
+//            <= 1/9; absolute error <= 1.8e-12 (log Phi enters log L only: DESIGN.md R32)
 //   phi/(sigma Phi) = E' / Phi                     -- shares E' with Q
 // The reciprocal and rsqrt seeds come from MUFU (rcp/rsqrt.approx) refined by one
 // cubic Newton step.  About 65 FP64 instructions per pair of math (+ ~8 for the

@@ -330,6 +330,7 @@ pass_kernel(PassArgs a) {
     if (a.prof && threadIdx.x == 0) a.prof[blockIdx.x * 4 + 0] = gtimer();
     A lik_w = A(0);
     A lacc[4] = {A(0), A(0), A(0), A(0)};   // fp64: running log L sums by lock-step position
+
 #ifndef MDS_Y_NO_EVICT_FIRST
     const uint64_t ypol = policy_evict_first();
 #endif

@@ -11,6 +11,11 @@ PassKernel pk() {
 }
 template <typename T, bool TR, int MODE>
 PassKernel pass_fn_d(int d) {
+#ifdef MDS_AB_D2ONLY
+    // A/B builds: only D = 2 is instantiated (fast compile; other d are not valid)
+    (void)d;
+    return pk<T, TR, MODE, 2>();
+#else
     switch (d) {
         case 1: return pk<T, TR, MODE, 1>();
         case 2: return pk<T, TR, MODE, 2>();
@@ -21,6 +26,7 @@ PassKernel pass_fn_d(int d) {
         case 7: return pk<T, TR, MODE, 7>();
         default: return pk<T, TR, MODE, 8>();
     }
+#endif
 }
 }  // namespace
 }  // namespace mdsk

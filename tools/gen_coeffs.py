@@ -178,7 +178,7 @@ def main():
     q64 = fit_q(13, kappa64)
     qr64 = fit_q_rational(6, 7)
     assert all(x > 0 for x in qr64[1]) and all(x > 0 for x in qr64[2]), "rational q: coefficient sign"
-    at64 = fit_atanh(7)
+    at64 = fit_atanh(6)
     exp32 = fit_exp(5)
     q32 = fit_q(6, kappa32, tmax=7)
     at32 = fit_atanh(3)
