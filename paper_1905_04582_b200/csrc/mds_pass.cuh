@@ -34,6 +34,7 @@
 #pragma once
 #include <cooperative_groups.h>
 #include <cstdint>
+#include <type_traits>
 #include "mds_math.cuh"
 #include "mds_tree_impl.cuh"
 
@@ -272,6 +273,8 @@ struct alignas(16) WarpStage {
     uint64_t bar0[4];                       // the kernel's first unit: one barrier per 4-column group
     alignas(16) double xcol[2][TB * D];     // bulk-copy destinations: 16-byte aligned
     alignas(16) T y[NSTAGE][UC * TB];
+    // fp32 pass: the tile's column x converted once per tile (not per pair)
+    alignas(16) std::conditional_t<sizeof(T) == 4, float[2][TB * D], float[1]> xcolf;
     int4 seg[MAXSEG_W];
     int spos[MAXSEG_W];                     // storage rows of the segments' row slabs
 };
@@ -453,6 +456,22 @@ pass_kernel(PassArgs a) {
                 const int c4b = max(sg.y - GPU * u, 0), c4e = min(sg.z - GPU * u, GPU);
                 const bool fu = first_pending;        // the staggered first unit (per-group barriers)
                 first_pending = false;
+                // fp32: this unit brought tile t's column x (first unit of the tile, or of the
+                // range): convert it to fp32 once, right after it has landed
+                const bool new_x = (u % UNITS_PER_TILE == 0) || u == ub;
+                auto cvt_xcol = [&]() {
+                    if constexpr (sizeof(T) == 4) {
+                        const int tb = (u / UNITS_PER_TILE) & 1;
+                        for (int e = lane; e < TB * D; e += 32) W.xcolf[tb][e] = (float)W.xcol[tb][e];
+                        __syncwarp();
+                    }
+                };
+                T gf0[D], gf1[D];                     // fp32: the unit's row sums (fp64 above the unit)
+                T lsu = T(0);
+                if constexpr (sizeof(T) == 4) {
+#pragma unroll
+                    for (int k = 0; k < D; ++k) gf0[k] = gf1[k] = T(0);
+                }
 #ifndef MDS_EXP_NO_TMA
                 if (!fu) {
                     if (a.prof && lane == 0 && !mbar_ready(&W.bar[cst], (phase >> cst) & 1)) ++not_ready;
@@ -464,6 +483,7 @@ pass_kernel(PassArgs a) {
                     phase ^= 1u << cst;
                     __syncwarp();                     // all lanes are done with the stage being refilled
                     if (iu < ue) issue_one();
+                    if (new_x) cvt_xcol();
                 }
 #endif
                 const int t = u / UNITS_PER_TILE, jb = (u % UNITS_PER_TILE) * UCOLS;
@@ -483,12 +503,15 @@ pass_kernel(PassArgs a) {
                         if (lane == 0)
                             for (int g = c4b + 1; g < c4e; ++g) issue_group(g, false);
                         if (iu < ue) issue_one();
+                        cvt_xcol();                   // the tile's x came with the first group
                     }
                 }
 #endif
                 const int jj0 = jb + 4 * c4;
                 const T* __restrict__ yst = W.y[cst] + 4 * c4 * TB;
-                const double* __restrict__ xc = W.xcol[t & 1] + jj0 * D;
+                const T* __restrict__ xc;
+                if constexpr (sizeof(T) == 4) xc = &W.xcolf[t & 1][jj0 * D];
+                else xc = W.xcol[t & 1] + jj0 * D;
                 T cv[4][D];
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {         // positions 2h, 2h+1: 4 pairs per lane in lock-step
@@ -548,15 +571,15 @@ pass_kernel(PassArgs a) {
                         if (WG) {
 #pragma unroll
                             for (int k = 0; k < D; ++k) {
-                                const T va0 = uu[0] * dd[0][k], vb0 = uu[1] * dd[1][k];
-                                const T va1 = uu[2] * dd[2][k], vb1 = uu[3] * dd[3][k];
-                                g0[k] -= A(va0 + va1);
-                                g1[k] -= A(vb0 + vb1);
-                                cv[2 * h][k] = va0 + vb0;
-                                cv[2 * h + 1][k] = va1 + vb1;
+                                gf0[k] = fmaf(-uu[0], dd[0][k], gf0[k]);
+                                gf0[k] = fmaf(-uu[2], dd[2][k], gf0[k]);
+                                gf1[k] = fmaf(-uu[1], dd[1][k], gf1[k]);
+                                gf1[k] = fmaf(-uu[3], dd[3][k], gf1[k]);
+                                cv[2 * h][k] = fmaf(uu[0], dd[0][k], uu[1] * dd[1][k]);
+                                cv[2 * h + 1][k] = fmaf(uu[2], dd[2][k], uu[3] * dd[3][k]);
                             }
                         }
-                        if (WL) lik_w += A(lsum);
+                        if (WL) lsu += lsum;
                     }
                 }
                 double* __restrict__ cslab = a.slabs + (size_t)cpos * TB * D + (size_t)jj0 * D;
@@ -576,6 +599,16 @@ pass_kernel(PassArgs a) {
                 (void)cslab;
 #endif
                 }   // 4-column groups
+                if constexpr (sizeof(T) == 4) {       // at most 16 columns x 2 terms in fp32 (reading R15)
+                    if (WG) {
+#pragma unroll
+                        for (int k = 0; k < D; ++k) {
+                            g0[k] += A(gf0[k]);
+                            g1[k] += A(gf1[k]);
+                        }
+                    }
+                    if (WL) lik_w += A(lsu);
+                }
                 cst = (cst + 1 == NSTAGE) ? 0 : cst + 1;
             }
             // the segment's row partial
