@@ -231,20 +231,25 @@ mds_status mds_sigma_mh_step(mds_ctx ctx, const mds_sigma_prior *prior, double s
  * and sigma otherwise as set ("changing the value of a
  * single x_i invalidates only N - 1 terms"):
  *   *delta = sum_{j != i, y_ij observed} [ ell(y_ij, ||x_new_i - x_j||) - ell(y_ij, ||x_i - x_j||) ]
- * with ell the Eq. 2 term.  O(N d), one CTA; the context is unchanged.
- * Synchronises.  Errors: MDS_E_INVALID_ARG (i outside [0, n), non-finite
- * x_new_i, NULL), MDS_E_STATE, MDS_E_UNSUPPORTED (sharded context), MDS_E_CUDA. */
+ * with ell the Eq. 2 term.  O(N d), one 8-CTA cluster; the context is
+ * unchanged.  Sharded contexts: each rank sums the pairs of its own tile-rows,
+ * one exchange of 1 double per rank, rank-ordered sum (identical on every
+ * rank; the call is collective).  Synchronises.  Errors: MDS_E_INVALID_ARG
+ * (i outside [0, n), non-finite x_new_i, NULL), MDS_E_STATE, MDS_E_COMM, MDS_E_CUDA. */
 mds_status mds_row_loglik_delta(mds_ctx ctx, int64_t i, const double *x_new_i, double *delta);
 
 /* k sequential single-location random-walk Metropolis updates (the sampler of
  * Bedford et al. the paper compares HMC against), all in one
- * device launch.  Update q: i = rows[q]; x' = x_i + step * z[q*d .. q*d+d-1];
+ * device launch (sharded contexts, collective: per update one propose kernel,
+ * this rank's share of Delta_i, one exchange of 1 double per rank and one
+ * decide kernel, stream-ordered, the same decision on every rank).
+ * Update q: i = rows[q]; x' = x_i + step * z[q*d .. q*d+d-1];
  * log r = Delta_i(x') - (|x'|^2 - |x_i|^2) / (2 prior_sd^2) (iid N(0, prior_sd^2)
  * prior, reading R20; prior_sd <= 0: flat); accept iff log(u[q]) < log r, then
  * x_i <- x'.  rows (int64), z (k x d) and u (k, in (0, 1]) are host arrays of
  * the caller's random numbers.  X moves in place; *accepted (may be NULL)
  * counts acceptances.  Synchronises.  Errors: MDS_E_INVALID_ARG, MDS_E_STATE,
- * MDS_E_UNSUPPORTED (sharded context), MDS_E_OOM, MDS_E_CUDA. */
+ * MDS_E_OOM, MDS_E_COMM, MDS_E_CUDA. */
 mds_status mds_rw_sweep(mds_ctx ctx, int64_t k, const int64_t *rows, const double *z, const double *u,
                         double step, double prior_sd, int64_t *accepted);
 

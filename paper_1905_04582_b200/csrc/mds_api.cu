@@ -1109,10 +1109,9 @@ mds_status mds_row_loglik_delta(mds_ctx c, int64_t i, const double* x_new_i, dou
     if (i < 0 || i >= c->n) return fail(c, MDS_E_INVALID_ARG, "row index out of range");
     for (int k = 0; k < c->d; ++k)
         if (!std::isfinite(x_new_i[k])) return fail(c, MDS_E_INVALID_ARG, "non-finite location");
-    if (c->world != 1) return fail(c, MDS_E_UNSUPPORTED, "single-location updates need an unsharded context");
     mds_status st = ready(c);
     if (st) return st;
-    if ((st = rw_scratch(c, 2 * sizeof(double) * 8))) return st;
+    if ((st = rw_scratch(c, 3 * sizeof(double) * 8))) return st;
     double* dx = static_cast<double*>(c->d_rwbuf);
     CK(cudaMemcpyAsync(dx, x_new_i, c->d * sizeof(double), cudaMemcpyHostToDevice, c->stream));
     RowArgs a = row_args(c);
@@ -1121,7 +1120,16 @@ mds_status mds_row_loglik_delta(mds_ctx c, int64_t i, const double* x_new_i, dou
     a.delta = dx + 8;
     a.K = 0;
     if ((st = launch_row(c, a))) return st;
-    CK(cudaMemcpyAsync(delta, dx + 8, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    const double* out = dx + 8;
+    if (!direct(c)) {
+        // sharded: this rank's share (the pairs of its tile-rows), then the
+        // rank-ordered sum of every rank's share
+        if ((st = exchange(c, dx + 8, c->d_gathered, 1, c->stream))) return st;
+        combine_kernel<<<1, 32, 0, c->stream>>>(c->d_gathered, c->world, 1, nullptr, dx + 16);
+        CK(cudaGetLastError());
+        out = dx + 16;
+    }
+    CK(cudaMemcpyAsync(delta, out, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
     return MDS_OK;
 }
@@ -1138,7 +1146,6 @@ mds_status mds_rw_sweep(mds_ctx c, int64_t k, const int64_t* rows, const double*
         for (int j = 0; j < c->d; ++j)
             if (!std::isfinite(z[q * c->d + j])) return fail(c, MDS_E_INVALID_ARG, "non-finite z");
     }
-    if (c->world != 1) return fail(c, MDS_E_UNSUPPORTED, "single-location updates need an unsharded context");
     mds_status st = ready(c);
     if (st) return st;
     if (k == 0) {
@@ -1146,24 +1153,48 @@ mds_status mds_rw_sweep(mds_ctx c, int64_t k, const int64_t* rows, const double*
         return MDS_OK;
     }
     const size_t zb = (size_t)k * c->d * sizeof(double), rb = (size_t)k * sizeof(int64_t), ub = (size_t)k * 8;
-    if ((st = rw_scratch(c, 64 + rb + zb + ub))) return st;
+    const size_t hdr = 256;   // accepted count (8 B), sharded: proposal (64 B) and partial delta (8 B)
+    if ((st = rw_scratch(c, hdr + rb + zb + ub))) return st;
     char* base = static_cast<char*>(c->d_rwbuf);
     unsigned long long* dacc = reinterpret_cast<unsigned long long*>(base);
-    int64_t* drows = reinterpret_cast<int64_t*>(base + 64);
-    double* dz = reinterpret_cast<double*>(base + 64 + rb);
-    double* du = reinterpret_cast<double*>(base + 64 + rb + zb);
+    double* dxnew = reinterpret_cast<double*>(base + 64);
+    double* dpart = reinterpret_cast<double*>(base + 128);
+    int64_t* drows = reinterpret_cast<int64_t*>(base + hdr);
+    double* dz = reinterpret_cast<double*>(base + hdr + rb);
+    double* du = reinterpret_cast<double*>(base + hdr + rb + zb);
     CK(cudaMemcpyAsync(drows, rows, rb, cudaMemcpyHostToDevice, c->stream));
     CK(cudaMemcpyAsync(dz, z, zb, cudaMemcpyHostToDevice, c->stream));
     CK(cudaMemcpyAsync(du, u, ub, cudaMemcpyHostToDevice, c->stream));
-    RowArgs a = row_args(c);
-    a.K = k;
-    a.rows = drows;
-    a.z = dz;
-    a.u = du;
-    a.step = step;
-    a.inv_tau2 = prior_sd > 0.0 ? 1.0 / (prior_sd * prior_sd) : 0.0;
-    a.accepted = dacc;
-    if ((st = launch_row(c, a))) return st;
+    const double inv_tau2 = prior_sd > 0.0 ? 1.0 / (prior_sd * prior_sd) : 0.0;
+    if (direct(c)) {
+        RowArgs a = row_args(c);
+        a.K = k;
+        a.rows = drows;
+        a.z = dz;
+        a.u = du;
+        a.step = step;
+        a.inv_tau2 = inv_tau2;
+        a.accepted = dacc;
+        if ((st = launch_row(c, a))) return st;
+    } else {
+        // sharded: every update needs all ranks' shares of Delta_i before its
+        // decision, so each one is propose -> row share -> exchange -> decide
+        // (stream-ordered; the decision and the move of x_i are identical on every rank)
+        CK(cudaMemsetAsync(dacc, 0, sizeof(unsigned long long), c->stream));
+        for (int64_t q = 0; q < k; ++q) {
+            rw_propose_launch(c->d_x, drows, dz, q, step, c->d, dxnew, c->stream);
+            RowArgs a = row_args(c);
+            a.K = 0;
+            a.i0 = rows[q];
+            a.xnew = dxnew;
+            a.delta = dpart;
+            if ((st = launch_row(c, a))) return st;
+            if ((st = exchange(c, dpart, c->d_gathered, 1, c->stream))) return st;
+            rw_decide_launch(c->d_gathered, c->world, 1, c->d_x, drows, du, q, dxnew, inv_tau2, c->d, dacc,
+                             c->stream);
+        }
+        CK(cudaGetLastError());
+    }
     unsigned long long na = 0;
     CK(cudaMemcpyAsync(&na, dacc, sizeof(na), cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));

@@ -6,9 +6,12 @@ namespace mdsk {
 namespace {
 
 // y_ab (a > b) in the tiled triangle: tile (a/B, b/B), column-major inside
+// (a sharded context stores only its own tile-rows: a pair of another rank's
+// tile-row reads as missing, so each rank forms its share of the row delta)
 template <typename T>
 __device__ __forceinline__ T y_pair(const T* __restrict__ Y, const int* __restrict__ row_local, int64_t a, int64_t b) {
     const int lt = __ldg(row_local + (a >> 6));
+    if (lt < 0) return T(NAN);
     return Y[((size_t)(lt + (b >> 6)) << 12) + ((b & 63) << 6) + (a & 63)];
 }
 
@@ -233,7 +236,52 @@ RowFn row_fn_d(int d) {
         default: return row_kernel<T, 8, TR>;
     }
 }
+// ---- sharded sweeps: one update = propose -> row partial (row_kernel, K = 0)
+// -> exchange of the partials -> decide, all stream-ordered (the decision needs
+// every rank's share of Delta_i, so a sweep cannot stay inside one launch)
+__global__ void rw_propose_kernel(const double* __restrict__ x, const int64_t* __restrict__ rows,
+                                  const double* __restrict__ z, int64_t q, double step, int d, double* xnew) {
+    const int k = threadIdx.x;
+    if (k < d) {
+        const int64_t i = rows[q];
+        xnew[k] = __fma_rn(step, z[q * d + k], x[i * d + k]);     // as row_kernel
+    }
+}
+
+// rank-ordered sum of the partial deltas, the iid-prior change and the decision
+// (the same expressions and order as row_kernel's), identical on every rank
+__global__ void rw_decide_kernel(const double* __restrict__ gathered, int world, int64_t stride, double* x,
+                                 const int64_t* __restrict__ rows, const double* __restrict__ u, int64_t q,
+                                 const double* __restrict__ xnew, double inv_tau2, int d,
+                                 unsigned long long* accepted) {
+    if (threadIdx.x != 0) return;
+    double dl = 0.0;
+    for (int r = 0; r < world; ++r) dl += gathered[(size_t)r * stride];
+    const int64_t i = rows[q];
+    double pn = 0.0, po = 0.0;
+    for (int k = 0; k < d; ++k) {
+        pn = fma(xnew[k], xnew[k], pn);
+        po = fma(x[i * d + k], x[i * d + k], po);
+    }
+    const double lr = dl - 0.5 * (pn - po) * inv_tau2;
+    if (isfinite(lr) && log(u[q]) < lr) {
+        for (int k = 0; k < d; ++k) x[i * d + k] = xnew[k];
+        ++*accepted;
+    }
+}
+
 }  // namespace
+
+void rw_propose_launch(const double* x, const int64_t* rows, const double* z, int64_t q, double step, int d,
+                       double* xnew, cudaStream_t s) {
+    rw_propose_kernel<<<1, 32, 0, s>>>(x, rows, z, q, step, d, xnew);
+}
+
+void rw_decide_launch(const double* gathered, int world, int64_t stride, double* x, const int64_t* rows,
+                      const double* u, int64_t q, const double* xnew, double inv_tau2, int d,
+                      unsigned long long* accepted, cudaStream_t s) {
+    rw_decide_kernel<<<1, 32, 0, s>>>(gathered, world, stride, x, rows, u, q, xnew, inv_tau2, d, accepted);
+}
 
 RowFn row_fn(int prec_is_f64, int trunc, int d) {
     if (prec_is_f64) return trunc ? row_fn_d<double, true>(d) : row_fn_d<double, false>(d);

@@ -18,6 +18,7 @@
 // in L2).
 #pragma once
 #include <cstdint>
+#include <cuda_runtime.h>
 #include "mds_math.cuh"
 
 namespace mdsk {
@@ -47,5 +48,12 @@ constexpr int ROW_THREADS = 512;    // per CTA
 constexpr int ROW_CLUSTER = 8;      // CTAs (SMs) per row: one thread-block cluster
 // row_kernel<T, D, TRUNC> for (precision, truncation, d); defined in mds_row.cu
 RowFn row_fn(int prec_is_f64, int trunc, int d);
+// sharded sweeps (mds_row.cu): proposal x_i + step z_q, and the decision from the
+// gathered partial deltas gathered[r * stride], r < world (rank order)
+void rw_propose_launch(const double* x, const int64_t* rows, const double* z, int64_t q, double step, int d,
+                       double* xnew, cudaStream_t s);
+void rw_decide_launch(const double* gathered, int world, int64_t stride, double* x, const int64_t* rows,
+                      const double* u, int64_t q, const double* xnew, double inv_tau2, int d,
+                      unsigned long long* accepted, cudaStream_t s);
 
 }  // namespace mdsk

@@ -10,8 +10,9 @@ several processes on one GPU.
    trajectories agree to rounding).
 2. Two PROCESSES sharing the one GPU, each a rank of a world-2 sharded
    context, exchanging through a host-staged gloo all-gather registered with
-   mds_set_allgather: evaluation, HMC trajectory and the likelihood-only
-   (sigma) pass match the oracle and are bitwise identical across ranks.
+   mds_set_allgather: evaluation, HMC trajectory, the likelihood-only
+   (sigma) pass and the single-location updates match the oracle and are
+   bitwise identical across ranks.
 """
 import os
 import socket
@@ -100,6 +101,34 @@ def test_world1_communicator_tree_prior_trajectory(mds):
     assert out["H1"] - out["H0"] == pytest.approx(ref["H1"] - ref["H0"], rel=1e-6, abs=1e-8)
 
 
+def test_world1_communicator_single_location_updates(mds):
+    """Sharded single-location updates: the row delta as this
+    rank's share + exchange + rank-ordered sum, and the random-walk sweep as
+    propose -> share -> exchange -> decide per update, through the NCCL path."""
+    n, d = 500, 2
+    w = workload.Workload(n, d, p_missing=0.05, seed=43)
+    y, x = w.y_packed(), w.x0
+    rng = np.random.default_rng(3)
+    k = 120
+    rows = rng.integers(0, n, size=k)
+    z = rng.normal(size=(k, d))
+    u = 1.0 - rng.random(k)
+    ref_x, ref_acc = oracle.rw_sweep(y, x, w.sigma, rows, z, u, 0.05, prior_sd=10.0)
+    with mds.MDS(n, d, rank=0, world=1, nccl_unique_id=mds.mds_nccl_unique_id()) as c:
+        c.set_dissimilarities_packed(y)
+        c.set_locations(x)
+        c.set_sigma(w.sigma)
+        for i in (0, 77, 499):
+            xn = x[i] + 0.1
+            got = c.row_loglik_delta(i, xn)
+            ref = oracle.row_delta(y, x, i, xn, w.sigma, 1)
+            assert got == pytest.approx(ref, rel=1e-10, abs=1e-9)
+        acc = c.rw_sweep(rows, z, u, 0.05, prior_sd=10.0)
+        xs = c.get_locations()
+    assert acc == ref_acc and 0 < acc < k
+    np.testing.assert_allclose(xs, ref_x, rtol=0, atol=1e-12)
+
+
 def _free_port():
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
@@ -130,8 +159,13 @@ def _rank_proc(rank, world, port, q):
         l2 = c.log_likelihood_at_sigma(1.1 * w.sigma)
         p0 = w.normals(3, (w.n, w.d))
         tr = c.hmc_trajectory(p0, 0.002, 5, prior_sd=10.0)
+        rd = c.row_loglik_delta(100, w.x0[100] + 0.1)
+        rng = np.random.default_rng(5)
+        rows = rng.integers(0, w.n, size=40)
+        acc = c.rw_sweep(rows, rng.normal(size=(40, w.d)), 1.0 - rng.random(40), 0.05, prior_sd=10.0)
+        xs = c.get_locations()
         c.close()
-        q.put((rank, ll, g, l2, tr["x"], tr["H0"], tr["H1"]))
+        q.put((rank, ll, g, l2, tr["x"], tr["H0"], tr["H1"], rd, acc, xs))
     except Exception as e:
         q.put((rank, repr(e)))
     finally:
@@ -150,8 +184,8 @@ def test_two_processes_share_the_gpu_hoststaged_exchange(mds):
     res = sorted([q.get(timeout=300) for _ in procs], key=lambda r: r[0])
     for p in procs:
         p.join(timeout=60)
-    assert all(len(r) == 7 for r in res), res
-    (_, ll0, g0, l20, x0, h00, h10), (_, ll1, g1, l21, x1, h01, h11) = res
+    assert all(len(r) == 10 for r in res), res
+    (_, ll0, g0, l20, x0, h00, h10, rd0, a0, xs0), (_, ll1, g1, l21, x1, h01, h11, rd1, a1, xs1) = res
     # bitwise identical on both ranks
     assert ll0 == ll1 and np.array_equal(g0, g1) and l20 == l21
     assert np.array_equal(x0, x1) and h00 == h01 and h10 == h11
@@ -162,3 +196,12 @@ def test_two_processes_share_the_gpu_hoststaged_exchange(mds):
     ref = oracle.leapfrog(y, w.x0, w.normals(3, (w.n, w.d)), w.sigma, 0.002, 5, 1, prior_sd=10.0)
     np.testing.assert_allclose(x0, ref["x"], rtol=1e-9, atol=1e-12)
     assert h00 == pytest.approx(ref["H0"], rel=1e-10) and h10 == pytest.approx(ref["H1"], rel=1e-10)
+    # single-location updates across the two ranks' shares
+    assert rd0 == rd1 and a0 == a1 and np.array_equal(xs0, xs1)
+    assert rd0 == pytest.approx(oracle.row_delta(y, w.x0, 100, w.x0[100] + 0.1, w.sigma, 1), rel=1e-10, abs=1e-9)
+    rng = np.random.default_rng(5)
+    rows = rng.integers(0, w.n, size=40)
+    rx, racc = oracle.rw_sweep(y, w.x0, w.sigma, rows, rng.normal(size=(40, w.d)), 1.0 - rng.random(40), 0.05,
+                               prior_sd=10.0)
+    assert a0 == racc
+    np.testing.assert_allclose(xs0, rx, rtol=0, atol=1e-12)
