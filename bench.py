@@ -428,30 +428,44 @@ def time_steps(R, ctx, w, steps, warmup, flush_buf, graph=False, clocks=None):
     return step_ms, kern_ms, clk
 
 
-def roofline_of(prec, d, pairs_per_launch, kern_ms, clk_mhz, traffic):
-    """ALU roofline of the pass kernel: FP64 (fp32: FP32+issue)
-    lane-instructions per pair x pairs per launch / launch time vs 148 x 64 lanes x clock."""
+def roofline_of(prec, d, pairs_per_launch, kern_ms, clk_mhz, traffic, cfg=None):
+    """Roofline of the pass kernel.  fp64: ALU-bound on the FP64
+    pipe -- FP64 lane-instructions per pair (static SASS count of the loop) x pairs per
+    launch / launch time vs 148 x 64 lanes x clock.  fp32: issue-bound -- issued
+    lane-instructions per pair (ncu's dynamic count of the kernel when captured, else the
+    static loop count) vs 148 SM x 4 schedulers x 32 lanes x clock."""
     sc = sass_counts(prec, d)
     if sc is None or not kern_ms:
         return None
-    lanes = 64 if prec == "f64" else 128
+    nc = profile_json("ncu_summary.json").get("%s_%s" % (cfg, prec)) if cfg else None
+    if prec == "f64":
+        lanes, bound, ipp = 64, "alu", sc["fp64_per_pair"]
+        unit, src = "T fp64-lane-op/s", "148 SM x 64 FP64 lanes/clk x 1.965 GHz max SM clock (B200_PROFILING.md)"
+    else:
+        lanes, bound = 128, "issue"
+        ipp = nc["issued_inst_per_pair_dynamic"] if nc and "issued_inst_per_pair_dynamic" in nc \
+            else sc["issued_per_pair"]
+        unit = "T issued lane-instr/s"
+        src = ("148 SM x 4 schedulers x 1 warp-instruction/clk x 32 lanes x 1.965 GHz (B200_PROFILING.md); "
+               "instructions per pair: %s" % ("ncu dynamic count (profiles/ncu_summary.json)"
+                                              if nc else "static loop count (profiles/sass_counts.json)"))
     peak = 148 * lanes * SM_MAX_GHZ * 1e9
-    ipp = sc["fp64_per_pair"] if prec == "f64" else sc["fp32_per_pair"]
     achieved = ipp * pairs_per_launch / (kern_ms * 1e-3)
     hbm, hbm_src = hbm_peak()
     bpp = 8.0 if prec == "f64" else 4.0
-    rf = {"bound": "alu", "achieved": achieved / 1e12, "peak": peak / 1e12,
-          "unit": "T %s-lane-op/s" % ("fp64" if prec == "f64" else "fp32"), "frac": achieved / peak,
+    rf = {"bound": bound, "achieved": achieved / 1e12, "peak": peak / 1e12,
+          "unit": unit, "frac": achieved / peak,
           "traffic": traffic,
           "kernel": "pass_kernel<%s,D=%d,T=1,LEAPFROG>" % (prec, d),
           "ops_per_pair": ipp, "issued_per_pair": sc.get("issued_per_pair"),
           "pass_kernel_ms": kern_ms,
-          "peak_source": "148 SM x %d %s lanes/clk x 1.965 GHz max SM clock (B200_PROFILING.md)" % (
-              lanes, "FP64" if prec == "f64" else "FP32"),
+          "peak_source": src,
           "hbm_gbs": bpp * pairs_per_launch / (kern_ms * 1e-3) / 1e9,
           "hbm_frac": bpp * pairs_per_launch / (kern_ms * 1e-3) / (hbm * 1e9), "hbm_peak_source": hbm_src}
     if clk_mhz:
         rf["frac_at_measured_clock"] = achieved / (148 * lanes * clk_mhz * 1e6)
+    if prec == "f32":
+        rf["fp32_lane_frac"] = sc["fp32_per_pair"] * pairs_per_launch / (kern_ms * 1e-3) / peak
     if prec == "f64":
         # SURVEY 8(d)(2): pair-evals/s against R_ALU with the FIXED libdevice reference
         # I64_ref = 160 FP64 instructions per pair (independent of this kernel's count)
@@ -538,7 +552,7 @@ def run_ours(args):
         del ce, fb
         kms = float(sm.mean())
         rf = roofline_of(prec, we.d, we.n_pairs, kms, clk.get("sm_mhz") if clk else None,
-                         profile_json("traffic.json").get("%s_%s" % (cfg, prec)))
+                         profile_json("traffic.json").get("%s_%s" % (cfg, prec)), cfg)
         extras[name] = {"workload": "%s: N=%d D=%d %s, %.0f%% missing" % (cfg, we.n, we.d, prec, 100 * we.p_missing),
                         "value": we.n_pairs / (kms * 1e-3), "unit": UNIT, "ms_per_step": kms, "steps": k,
                         "step_ms_p50": float(np.median(sm)),
@@ -546,6 +560,7 @@ def run_ours(args):
                         else "Y (%.1f GB) > L2, no flush" % (yb / 1e9),
                         "setup_s": su["setup_s"],
                         "roofline_frac": rf["frac"] if rf else None,
+                        "roofline_bound": rf["bound"] if rf else None,
                         "frac_fixed_I64_ref": rf.get("frac_fixed_I64_ref") if rf else None}
 
     if rank != 0:
@@ -554,7 +569,8 @@ def run_ours(args):
         return
 
     traffic = profile_json("traffic.json").get("%s_%s" % (args.workload, args.precision))
-    roofline = roofline_of(args.precision, d, P_N / world, kern_ms, clk.get("sm_mhz") if clk else None, traffic)
+    roofline = roofline_of(args.precision, d, P_N / world, kern_ms, clk.get("sm_mhz") if clk else None, traffic,
+                           args.workload)
     if roofline is not None:
         roofline["pass_kernel_share_of_step"] = kern_ms / ms_per_step
         nc = profile_json("ncu_summary.json").get("%s_%s" % (args.workload, args.precision))

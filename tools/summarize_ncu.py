@@ -27,6 +27,8 @@ METRICS = {
     "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active": "fp64_pipe_active_pct",
     "sm__inst_executed_pipe_fp64.sum": "fp64_warp_inst",
     "sm__inst_executed_pipe_xu.sum.pct_of_peak_sustained_active": "xu_pipe_pct",
+    "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active": "fp32_fma_pipe_active_pct",
+    "sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active": "alu_pipe_active_pct",
     "smsp__issue_active.avg.pct_of_peak_sustained_active": "issue_active_pct",
     "smsp__inst_executed.sum": "warp_inst",
     "sm__cycles_elapsed.avg.per_second": "sm_clock",
