@@ -205,3 +205,41 @@ def test_two_processes_share_the_gpu_hoststaged_exchange(mds):
                                prior_sd=10.0)
     assert a0 == racc
     np.testing.assert_allclose(xs0, rx, rtol=0, atol=1e-12)
+
+
+def _cb_proc(q):
+    """The binding's torch.distributed exchange callback on an NCCL process group
+    (world 1: the all_gather_into_tensor path libmds calls through
+    mds_set_allgather), driven with device buffers on a side stream."""
+    import torch
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(_free_port())
+    try:
+        torch.cuda.set_device(0)
+        dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+        import paper_1905_04582_b200 as m
+        cb = m.allgather_callback(1)
+        st = torch.cuda.Stream()
+        send = torch.arange(1000, dtype=torch.float64, device="cuda")
+        recv = torch.zeros(1000, dtype=torch.float64, device="cuda")
+        torch.cuda.synchronize()
+        rc = cb(None, send.data_ptr(), recv.data_ptr(), 1000, st.cuda_stream)
+        st.synchronize()
+        q.put((rc, bool(torch.equal(send, recv))))
+    except Exception as e:
+        q.put((repr(e), False))
+    finally:
+        if dist.is_initialized():
+            dist.destroy_process_group()
+
+
+def test_torch_nccl_exchange_callback(mds):
+    import torch.multiprocessing as tmp
+    ctx = tmp.get_context("spawn")
+    q = ctx.Queue()
+    p = ctx.Process(target=_cb_proc, args=(q,))
+    p.start()
+    rc, ok = q.get(timeout=300)
+    p.join(timeout=60)
+    assert rc == 0 and ok, rc
