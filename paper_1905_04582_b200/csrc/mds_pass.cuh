@@ -328,8 +328,16 @@ pass_kernel(PassArgs a) {
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         fence_async_smem();
     }
-    build_exptab(exptab, a.P);
-    __syncthreads();
+    // The exp table (cg 2^(j/256), built per launch) is only needed once compute
+    // starts: pair CTAs build it after their first TMA copies are in flight (the
+    // first data lands ~2 us after issue); the tree CTA and the tree modes' pair
+    // CTAs (tips pass first) build it here.
+    const bool skip_a = blockIdx.x >= a.pair_ctas;
+    const bool early_tab = TREE || skip_a || a.vpw < 1;
+    if (early_tab) {
+        build_exptab(exptab, a.P);
+        __syncthreads();
+    }
     if (a.prof && threadIdx.x == 0) a.prof[blockIdx.x * 4 + 0] = gtimer();
     A lik_w = A(0);
     A lacc[4] = {A(0), A(0), A(0), A(0)};   // fp64: running log L sums by lock-step position
@@ -340,7 +348,6 @@ pass_kernel(PassArgs a) {
     // With a tree prior, the last CTA walks the tree (d log prior / dX at xeval,
     // PAPER.md:243-246) while the others run phase A; the grid barrier below
     // orders phase B's leapfrog update after both.
-    const bool skip_a = blockIdx.x >= a.pair_ctas;
     if (TREE && !skip_a) {
         // this CTA's slice of the tree walk's tips pass (a few tips per CTA), then check in
         const int per = (a.tree.n_items + a.pair_ctas - 1) / a.pair_ctas;
@@ -373,10 +380,11 @@ pass_kernel(PassArgs a) {
         W.spos[lane] = __ldg(a.slab_pos + ws0 + lane);
     }
     __syncwarp();
-    if (nsw > 0) {
+    {
         // segments are in 4-column groups (g); the warp works in UCOLS-column units
         // u = g / GPU, whose first/last may be partly outside the warp's range
-        const int ub = W.seg[0].y / GPU, ue = (W.seg[nsw - 1].z + GPU - 1) / GPU;
+        // (an empty range, nsw == 0, reads stale table entries that are never used)
+        const int ub = W.seg[0].y / GPU, ue = (W.seg[max(nsw, 1) - 1].z + GPU - 1) / GPU;
         const int m = (lane >> 3) & 3;           // this lane's column order: position p <-> column p ^ m
         // issue cursor: units are staged in order, NSTAGE - 1 ahead of compute; tile t's
         // column x goes to xcol[t & 1] (consecutive tiles alternate)
@@ -430,15 +438,21 @@ pass_kernel(PassArgs a) {
             if (with_x) bulk_g2s(W.xcol[t & 1], X + (size_t)(t - itb) * TB * D, XB, &W.bar0[g]);
         };
 #ifndef MDS_EXP_NO_TMA
-        if (first_pending) {
-            if (lane == 0) issue_group(fc4b, true);
-            ++iu;
-            ist = (ist + 1 == NSTAGE) ? 0 : ist + 1;
-        } else {
-            issue_one();
+        if (nsw > 0) {
+            if (first_pending) {
+                if (lane == 0) issue_group(fc4b, true);
+                ++iu;
+                ist = (ist + 1 == NSTAGE) ? 0 : ist + 1;
+            } else {
+                issue_one();
+            }
+            if (NSTAGE > 2 && iu < ue) issue_one();
         }
-        if (NSTAGE > 2 && iu < ue) issue_one();
 #endif
+        if (!early_tab && vv == 0) {          // (uniform: every warp runs range 0)
+            build_exptab(exptab, a.P);
+            __syncthreads();
+        }
 #pragma unroll 1
         for (int si = 0; si < nsw; ++si) {
             const int4 sg = W.seg[si];

@@ -203,7 +203,7 @@ def main():
         "constexpr double EXPT64_STEP_HI = %r;    // ln2/256, 32 significant bits" % float(hi),
         "constexpr double EXPT64_STEP_LO = %r;" % float(lo),
         "static __constant__ double EXPT64_C[] = {%s};" % fmt(expt64[1]),
-        "static __constant__ double EXPT64_TAB[256] = {%s};" % fmt(table),
+        "static __device__ const double EXPT64_TAB[256] = {%s};   // global: the per-launch table build reads it coalesced" % fmt(table),
         "// q(w) = erfcx(t/sqrt2)/2, w = (t-K)/(t+K); max |E(t)(q - p)| = %.2e" % float(q64[0]),
         "// (host copy Q64_CH: the kernels take these scaled by 1/cg per sigma, SigmaParams::qc)",
         "constexpr int Q64_DEG = %d;" % (len(q64[1]) - 1),
