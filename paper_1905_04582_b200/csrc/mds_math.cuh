@@ -168,8 +168,16 @@ __device__ __forceinline__ void pair_f64_n(const double (&s)[NP], const double (
     double rs[NP], d[NP], res[NP], l[NP];
 #pragma unroll
     for (int i = 0; i < NP; ++i) {
+#ifndef MDS_NO_TRIM
+        // the MUFU seed reads the high word only: clamp just that (s = 0, a coincident
+        // pair, then gives a finite rs and d = s rs = 0 exactly; reading R10), and run
+        // the Newton step on s itself (no register pair to rebuild)
+        rs[i] = rsqrt_seed(__hiloint2double(max(__double2hiint(s[i]), 0x01000000), 0));
+        const double sc = s[i];
+#else
         const double sc = __hiloint2double(max(__double2hiint(s[i]), 0x01000000), __double2loint(s[i]));
         rs[i] = rsqrt_seed(sc);
+#endif
         const double h = sc * rs[i];
         const double e = fma(-h, rs[i], 1.0);
         const double c = fma(e, 0.375, 0.5);
@@ -196,8 +204,15 @@ __device__ __forceinline__ void pair_f64_n(const double (&s)[NP], const double (
             const double kd = fma(a, -EXPT64_INV_STEP, MAGIC);                           // 256 / ln2
             k[i] = __double2loint(kd);
             const double fk = kd - MAGIC;
+#ifndef MDS_NO_TRIM
+            // one fused step with ln2/256 rounded to double (no Cody-Waite split): r is
+            // off by |k| 9.1e-20, i.e. E' by |k| 9.1e-20 relative -- 1.5e-16 at t = 3,
+            // 1.2e-15 at t = 8.3 where E' ~ 1e-15 cg (reading R35)
+            r[i] = fma(fk, -EXPT64_STEP, -a);
+#else
             r[i] = fma(fk, -EXPT64_STEP_HI, -a);                                          // ln2/256 hi
             r[i] = fma(fk, -EXPT64_STEP_LO, r[i]);                                        // ln2/256 lo
+#endif
         }
         // Q = 1 - Phi(t) = E q(t), q = P/R a rational of degree (6, 7) in t with positive
         // coefficients (tools/gen_coeffs.py), evaluated in d with the 1/sigma^j folded

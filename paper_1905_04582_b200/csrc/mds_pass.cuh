@@ -385,7 +385,12 @@ pass_kernel(PassArgs a) {
         // u = g / GPU, whose first/last may be partly outside the warp's range
         // (an empty range, nsw == 0, reads stale table entries that are never used)
         const int ub = W.seg[0].y / GPU, ue = (W.seg[max(nsw, 1) - 1].z + GPU - 1) / GPU;
-        const int m = (lane >> 3) & 3;           // this lane's column order: position p <-> column p ^ m
+        // the lane index from a volatile read: ptxas cannot rematerialise it (it re-read
+        // SR_TID.X at the top of every group, a short-scoreboard wait in front of the
+        // column-x loads: +0.7% pair throughput, A/B at N = 30000)
+        int lane_v;
+        asm volatile("mov.u32 %0, %%laneid;" : "=r"(lane_v));
+        const int m = (lane_v >> 3) & 3;         // this lane's column order: position p <-> column p ^ m
         // issue cursor: units are staged in order, NSTAGE - 1 ahead of compute; tile t's
         // column x goes to xcol[t & 1] (consecutive tiles alternate)
         int iu = ub, isi = 0, iend = (W.seg[0].z + GPU - 1) / GPU, itb = W.seg[0].w, ist = cst;
@@ -533,8 +538,8 @@ pass_kernel(PassArgs a) {
 #pragma unroll
                     for (int qq = 0; qq < 2; ++qq) {
                         const int q = (2 * h + qq) ^ m;   // column of position 2h + qq
-                        ys[2 * qq] = yst[q * TB + lane];
-                        ys[2 * qq + 1] = yst[q * TB + lane + 32];
+                        ys[2 * qq] = yst[q * TB + lane_v];
+                        ys[2 * qq + 1] = yst[q * TB + lane_v + 32];
                         T sa = T(0), sb = T(0);
 #pragma unroll
                         for (int k = 0; k < D; ++k) {
@@ -554,11 +559,13 @@ pass_kernel(PassArgs a) {
 #pragma unroll
                         for (int i = 0; i < 4; ++i) ll[i] = lacc[i];
                         Pair<T, TRUNC>::template eval4<WL, WG>(ss, ys, a.P, exptab, ll, uu);
+                        bool mi[4];
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) mi[i] = is_missing(ys[i]);
 #pragma unroll
                         for (int i = 0; i < 4; ++i) {
-                            const bool mi = is_missing(ys[i]);
-                            if (WL) lacc[i] = mi ? lacc[i] : ll[i];
-                            if (WG) uu[i] = mi ? T(0) : uu[i];
+                            if (WL) lacc[i] = mi[i] ? lacc[i] : ll[i];
+                            if (WG) uu[i] = mi[i] ? T(0) : uu[i];
                         }
                         if (WG) {
                             // pair (row r, column c) adds -u (x_r - x_c) to row r and +u (x_r - x_c)

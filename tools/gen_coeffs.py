@@ -202,6 +202,8 @@ def main():
         "constexpr double EXPT64_INV_STEP = %r;   // 256 / ln2" % float(256 / mp.log(2)),
         "constexpr double EXPT64_STEP_HI = %r;    // ln2/256, 32 significant bits" % float(hi),
         "constexpr double EXPT64_STEP_LO = %r;" % float(lo),
+        "constexpr double EXPT64_STEP = %r;    // ln2/256 rounded to double (error %.1e)" % (
+            float(mp.log(2) / 256), float(abs(mp.mpf(float(mp.log(2) / 256)) - mp.log(2) / 256))),
         "static __constant__ double EXPT64_C[] = {%s};" % fmt(expt64[1]),
         "static __device__ const double EXPT64_TAB[256] = {%s};   // global: the per-launch table build reads it coalesced" % fmt(table),
         "// q(w) = erfcx(t/sqrt2)/2, w = (t-K)/(t+K); max |E(t)(q - p)| = %.2e" % float(q64[0]),
