@@ -193,6 +193,57 @@ mds_status mds_set_allgather(mds_ctx ctx, mds_allgather_fn fn, void *user);
 mds_status mds_combine_partials_device(mds_ctx ctx, const double *gathered_dev, int32_t world,
                                        double *loglik_dev, double *grad_dev);
 
+/* ---- fused peer-memory exchange (SURVEY.md 8(e) "stage 2") ---------------- */
+/* The exchange of the paper's multi-device cost model c0/S + c1
+ * done by the pass kernel itself over NVLink peer memory instead of a separate
+ * collective: in phase B every CTA stores the fixed-order sums of its row blocks
+ * (this rank's partial gradient) straight into a receive slot of EVERY rank's
+ * window (remote stores through NVLink/NVSwitch), the last CTA adds this rank's
+ * log L partial and raises this rank's arrival flag on every peer
+ * (release, system scope); each CTA then waits for all ranks' flags (acquire)
+ * and combines its row blocks from the local window in rank order, fused with
+ * the leapfrog update.  One launch per step, no host or NCCL call, so sharded
+ * steps are graph-capturable; results are bitwise identical to the all-gather
+ * path (same rank-ordered sum).  Other sharded exchanges (likelihood-only
+ * passes, single-location updates) go through the same windows with a one-CTA
+ * push/flag/wait kernel.  Receive slots are double-buffered by exchange count,
+ * so a fast rank never overwrites a slot a slower rank is still reading.
+ *
+ * Requirements: every rank's pass kernel must be co-resident with its peers'
+ * (one process per GPU, or contexts sharing one GPU whose grids together fit
+ * it: mds_set_grid_limit); ranks issue the same sequence of sharded calls.  A
+ * rank that waits more than 60 s for a peer abandons the step and the context
+ * is poisoned with MDS_E_COMM at its next synchronising call.
+ *
+ * Window: ((2 world (n d + 1)) doubles + 256 bytes of flags), allocated by the
+ * first mds_p2p_window call, owned and freed by the context. */
+#define MDS_IPC_HANDLE_BYTES 64
+/* This context's window: *window_dev (may be NULL) receives its device address
+ * (for contexts of one process), ipc_handle_out (may be NULL) receives
+ * MDS_IPC_HANDLE_BYTES bytes of cudaIpcMemHandle_t for other processes.
+ * A world-1 context connected to its own window runs the same push -> flag ->
+ * wait -> combine sequence (plumbing check on one GPU). */
+mds_status mds_p2p_window(mds_ctx ctx, void **window_dev, void *ipc_handle_out);
+/* Connect the exchange: peer_window_dev[r] is rank r's window (r = 0..world-1,
+ * this rank's own included) as a device address this context's device can
+ * store to (the same process; peer access is enabled when the windows live on
+ * other devices).  From then on every sharded exchange of the context goes
+ * through peer memory.  Collective in effect: all ranks must connect before
+ * any of them evaluates. */
+mds_status mds_p2p_connect(mds_ctx ctx, void *const *peer_window_dev);
+/* The same from ipc_handles[world][MDS_IPC_HANDLE_BYTES] (rank order, e.g.
+ * all-gathered through torch.distributed): peers' handles are opened
+ * (cudaIpcOpenMemHandle, lazy peer access) and closed by mds_destroy. */
+mds_status mds_p2p_connect_ipc(mds_ctx ctx, const void *ipc_handles);
+/* *connected = 1 when the context exchanges through peer memory. */
+mds_status mds_p2p_connected(mds_ctx ctx, int32_t *connected);
+
+/* Cap the pass kernel's grid at `ctas` CTAs (0 = all SMs; the schedule is
+ * rebuilt).  Leaves SMs to other work, e.g. the other ranks of a world that
+ * shares one GPU through the peer-memory exchange.  Errors: MDS_E_INVALID_ARG
+ * (ctas < 0). */
+mds_status mds_set_grid_limit(mds_ctx ctx, int32_t ctas);
+
 /* ---- sigma side ------------------------------------ */
 
 /* log L (Eq. 2) at the context's X and Y for another sigma

@@ -238,6 +238,31 @@ class MDS:
         self._ag_cb = _abi.ALLGATHER_FN(allgather_callback(self.world, group, host_staged, owner=self))
         _abi.mds_set_allgather(self.ctx, self._ag_cb, None)
 
+    def p2p_window(self):
+        """(device address, IPC handle bytes) of this context's peer-memory exchange window."""
+        return _abi.mds_p2p_window(self.ctx)
+
+    def p2p_connect(self, windows):
+        """Same-process ranks: the world's window addresses in rank order."""
+        _abi.mds_p2p_connect(self.ctx, windows)
+
+    def use_p2p_exchange(self, group=None):
+        """Multi-process ranks (one per GPU): all-gather the windows' IPC handles
+        through torch.distributed and connect the fused peer-memory exchange
+        (mds_p2p_connect_ipc).  Collective over the group."""
+        import torch.distributed as dist
+        _, h = self.p2p_window()
+        hs = [None] * self.world
+        dist.all_gather_object(hs, h, group=group)
+        _abi.mds_p2p_connect_ipc(self.ctx, hs)
+        dist.barrier(group=group)
+
+    def p2p_connected(self) -> bool:
+        return _abi.mds_p2p_connected(self.ctx)
+
+    def set_grid_limit(self, ctas: int):
+        _abi.mds_set_grid_limit(self.ctx, ctas)
+
     def get_locations(self) -> np.ndarray:
         x = np.zeros((self.n, self.d))
         _abi.mds_get_locations(self.ctx, x)

@@ -29,6 +29,7 @@ EXPORTS = [
     "mds_observed_pairs", "mds_zero_distance_pairs", "mds_set_timing", "mds_last_timing",
     "mds_hmc_trajectory", "mds_hmc_run", "mds_leapfrog_device", "mds_get_locations", "mds_get_momentum",
     "mds_set_allgather", "mds_plan",
+    "mds_p2p_window", "mds_p2p_connect", "mds_p2p_connect_ipc", "mds_p2p_connected", "mds_set_grid_limit",
     "mds_log_likelihood_at_sigma", "mds_sigma_mh_step", "mds_mcmc_run", "mds_row_loglik_delta", "mds_rw_sweep",
     "mds_cv_set_heldout", "mds_cv_accumulate", "mds_cv_lpd", "mds_set_tree_prior", "mds_tree_prior",
     "mds_last_error", "mds_status_string", "mds_version", "mds_device_info", "mds_measure_fma_peaks", "mds_l2_flush", "mds_l2_flush_clean",
@@ -106,6 +107,11 @@ def _load():
         "mds_get_locations": [vp, dp],
         "mds_get_momentum": [vp, dp],
         "mds_set_allgather": [vp, ALLGATHER_FN, vp],
+        "mds_p2p_window": [vp, P(vp), vp],
+        "mds_p2p_connect": [vp, P(vp)],
+        "mds_p2p_connect_ipc": [vp, vp],
+        "mds_p2p_connected": [vp, P(i32)],
+        "mds_set_grid_limit": [vp, i32],
         "mds_plan": [i64, i32, i32, i32, i32, P(PlanInfo), vp],
         "mds_device_info": [P(i32), P(i32), P(i32)],
         "mds_measure_fma_peaks": [P(ctypes.c_double), P(ctypes.c_double)],
@@ -309,6 +315,39 @@ def mds_get_momentum(ctx, p):
 def mds_set_allgather(ctx, fn, user=None):
     """fn: an ALLGATHER_FN instance (keep a reference alive while ctx lives)."""
     _check(lib.mds_set_allgather(ctx, fn, user), ctx)
+
+
+MDS_IPC_HANDLE_BYTES = 64
+
+
+def mds_p2p_window(ctx):
+    """-> (window device address, cudaIpcMemHandle_t bytes) of this context's exchange window."""
+    addr = ctypes.c_void_p()
+    h = ctypes.create_string_buffer(MDS_IPC_HANDLE_BYTES)
+    _check(lib.mds_p2p_window(ctx, ctypes.byref(addr), h), ctx)
+    return addr.value, h.raw
+
+
+def mds_p2p_connect(ctx, windows):
+    """windows: the world's window device addresses (ints), rank order."""
+    arr = (ctypes.c_void_p * len(windows))(*[int(w) for w in windows])
+    _check(lib.mds_p2p_connect(ctx, arr), ctx)
+
+
+def mds_p2p_connect_ipc(ctx, handles):
+    """handles: the world's IPC handle bytes (MDS_IPC_HANDLE_BYTES each), rank order."""
+    buf = ctypes.create_string_buffer(b"".join(bytes(h) for h in handles))
+    _check(lib.mds_p2p_connect_ipc(ctx, buf), ctx)
+
+
+def mds_p2p_connected(ctx) -> bool:
+    v = ctypes.c_int32()
+    _check(lib.mds_p2p_connected(ctx, ctypes.byref(v)), ctx)
+    return bool(v.value)
+
+
+def mds_set_grid_limit(ctx, ctas):
+    _check(lib.mds_set_grid_limit(ctx, int(ctas)), ctx)
 
 
 def mds_plan(n, rank, world, ctas, warps_per_cta, owned_rows=None):

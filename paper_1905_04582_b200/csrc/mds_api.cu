@@ -8,6 +8,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <ctime>
 #include <climits>
 #include <string>
 #include <vector>
@@ -119,6 +120,19 @@ struct mds_ctx_s {
     void* ag_user = nullptr;
     double* d_partial = nullptr;     // n*d + 1
     double* d_gathered = nullptr;    // world x (n*d + 1)
+    // fused peer-memory exchange (mds_p2p_window / mds_p2p_connect): this rank's
+    // window, the world's window addresses, local counters, a host-mapped error word
+    char* d_win = nullptr;
+    size_t win_bytes = 0;
+    char** d_peer_win = nullptr;     // [world]
+    std::vector<void*> ipc_opened;   // peers' windows opened from IPC handles (closed on destroy)
+    unsigned long long* d_p2p_state = nullptr;   // [4]
+    int* h_p2p_err = nullptr;        // pinned, mapped: set by a kernel that timed out waiting for a peer
+    int* d_p2p_err = nullptr;
+    bool p2p = false;
+    unsigned long long p2p_timeout_ns = 60000000000ull;   // MDS_P2P_TIMEOUT_S overrides (tests)
+    int grid_limit = 0;              // mds_set_grid_limit (0 = all SMs)
+    unsigned* d_gbar = nullptr;      // [2] the pass kernel's software grid barrier
 
     // leapfrog / HMC state
     double* d_p = nullptr;
@@ -168,6 +182,7 @@ struct mds_ctx_s {
     double* d_logprior = nullptr;    // [2]: log prior there, saved copy
     unsigned int* d_tips_done = nullptr;   // pass kernel: pair CTAs that finished their tips slice
 
+    double* h_pbuf = nullptr;        // pinned momentum staging of the HMC driver (n*d, allocated once)
     double* h_xstage = nullptr;      // pinned staging of mds_set_locations (asynchronous upload)
     cudaEvent_t xstage_done = nullptr;
 
@@ -190,11 +205,28 @@ mds_status fail(mds_ctx c, mds_status s, const std::string& msg) {
     return s;
 }
 
+// MDS_TRACE=1: host-side progress lines (rank, wall clock) at the points below
+void trace(mds_ctx c, const char* what) {
+    static const bool on = std::getenv("MDS_TRACE") != nullptr;
+    if (!on) return;
+    timespec ts;
+    clock_gettime(CLOCK_REALTIME, &ts);
+    std::fprintf(stderr, "[mds trace r%d %.6f] %s\n", c ? c->rank : -1, (ts.tv_sec % 1000) + ts.tv_nsec * 1e-9, what);
+}
+
 #define CK(call)                                                                            \
     do {                                                                                    \
         cudaError_t e_ = (call);                                                            \
         if (e_ != cudaSuccess)                                                              \
             return fail(c, MDS_E_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+    } while (0)
+
+// stream synchronisation that also reports a peer-memory exchange which timed out
+#define CKS(stream)                                                                                       \
+    do {                                                                                                  \
+        CK(cudaStreamSynchronize(stream));                                                                \
+        if (c->h_p2p_err && *(volatile int*)c->h_p2p_err)                                                 \
+            return fail(c, MDS_E_COMM, "peer-memory exchange: a peer did not arrive in time (MDS_P2P_TIMEOUT_S, default 60 s)");       \
     } while (0)
 
 #define GUARD(c)                                       \
@@ -237,15 +269,21 @@ void free_all(mds_ctx c) {
                   c->d_bad, c->d_count, c->d_partial, c->d_gathered, c->d_p, c->d_gl, c->d_xnext, c->d_xsave,
                   c->d_glsave, c->d_liksave, c->d_H, c->d_H0, c->d_prof, c->d_rwbuf,
                   c->d_cv_ij, c->d_cv_y, c->d_cv_max, c->d_cv_sum, c->d_cv_out,
-                  c->d_tree_int, c->d_tree_dbl, c->d_gprior, c->d_logprior, c->d_tips_done};
+                  c->d_tree_int, c->d_tree_dbl, c->d_gprior, c->d_logprior, c->d_tips_done, c->d_gbar};
     for (void* p : ps)
         if (p) cudaFree(p);
     for (auto& e : c->evpool)
         if (e) cudaEventDestroy(e);
     if (c->h_xstage) cudaFreeHost(c->h_xstage);
+    if (c->h_pbuf) cudaFreeHost(c->h_pbuf);
     if (c->xstage_done) cudaEventDestroy(c->xstage_done);
     if (c->comm) nccl_api().CommDestroy(c->comm);
     c->comm = nullptr;
+    for (void* q : c->ipc_opened) cudaIpcCloseMemHandle(q);
+    c->ipc_opened.clear();
+    for (void* q : {(void*)c->d_win, (void*)c->d_peer_win, (void*)c->d_p2p_state})
+        if (q) cudaFree(q);
+    if (c->h_p2p_err) cudaFreeHost(c->h_p2p_err);
 }
 
 inline int64_t packed_off(int64_t i) { return i * (i - 1) / 2; }
@@ -277,6 +315,19 @@ cudaEvent_t next_event(mds_ctx c) {
     return c->evpool[c->ev_used++];
 }
 
+P2PArgs p2p_args(mds_ctx c) {
+    P2PArgs q{};
+    if (!c->p2p) return q;
+    q.win = c->d_peer_win;
+    q.state = c->d_p2p_state;
+    q.err = c->d_p2p_err;
+    q.rank = c->rank;
+    q.world = c->world;
+    q.m1 = c->n * c->d + 1;
+    q.timeout_ns = c->p2p_timeout_ns;
+    return q;
+}
+
 PassArgs base_args(mds_ctx c, const double* xeval) {
     PassArgs a{};
     a.y = c->d_y;
@@ -295,6 +346,9 @@ PassArgs base_args(mds_ctx c, const double* xeval) {
     a.pair_ctas = c->pair_ctas;
     a.P = c->P;
     a.prof = c->d_prof;
+    a.p2p = p2p_args(c);
+    a.p2p_lf = 0;
+    a.gbar = c->d_gbar;
     return a;
 }
 
@@ -311,8 +365,17 @@ mds_status launch_coop(mds_ctx c, PassKernel k, PassArgs& a, cudaStream_t s) {
     cfg.dynamicSmemBytes = k.smem;
     cfg.stream = s;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    // Contexts on the peer-memory exchange launch WITHOUT the cooperative attribute:
+    // with it, a launch blocks the host while another rank's cooperative pass kernel
+    // (same process, sharing the GPU) is running -- which waits for this very launch
+    // (measured: tools/p2p_dbg.py, 3 ranks).  The grid is still sized by the occupancy
+    // API (one CTA per SM), so all CTAs are resident; the kernel then syncs through
+    // its own grid barrier (1.5 us slower than grid.sync at C2, so only here).
+    cfg.numAttrs = c->p2p ? 0 : 1;
+    a.soft_sync = c->p2p ? 1 : 0;
+    trace(c, "pass launch");
     CK(cudaLaunchKernelEx(&cfg, k.fn, a));
+    trace(c, "pass launched");
     return MDS_OK;
 }
 
@@ -321,6 +384,11 @@ mds_status launch_coop(mds_ctx c, PassKernel k, PassArgs& a, cudaStream_t s) {
 // callback)
 mds_status exchange(mds_ctx c, const double* send, double* recv, int64_t count, cudaStream_t s) {
     NvtxRange nv("mds_exchange");
+    if (c->p2p) {       // peer-memory windows: one CTA pushes, flags, waits, gathers
+        p2p_allgather_kernel<<<1, 256, 0, s>>>(p2p_args(c), send, count, recv);
+        CK(cudaGetLastError());
+        return MDS_OK;
+    }
     if (c->comm) {
         const ncclResult_t r = nccl_api().AllGather(send, recv, (size_t)count, ncclFloat64, c->comm, s);
         if (r != ncclSuccess)
@@ -335,7 +403,7 @@ mds_status exchange(mds_ctx c, const double* send, double* recv, int64_t count, 
 
 // unsharded: one pass kernel does everything; sharded (or a world-1 context with
 // a communicator): local partial -> exchange -> rank-ordered combine
-inline bool direct(mds_ctx c) { return c->world == 1 && !c->comm; }
+inline bool direct(mds_ctx c) { return c->world == 1 && !c->comm && !c->p2p; }
 
 // A fused pass at xeval.  EVAL: (grad_out, lik_out) <- full result.  With a
 // leapfrog state (lf = true): the pass runs at xnext and applies the leapfrog
@@ -379,6 +447,17 @@ mds_status run_pass(mds_ctx c, const double* xeval, double* grad_out, double* li
         st = launch_coop(c, pass_fn_mode(mode, c->prec, c->trunc, c->d), a, s);
         if (st) return st;
         if (timed) CK(cudaEventRecord(next_event(c), s));
+    } else if (c->p2p) {
+        // fused peer-memory exchange: the pass pushes its partial into every rank's
+        // window, waits for all ranks and combines (+ leapfrog update) itself
+        a.grad = grad_out;
+        a.lik = lik_out;
+        a.p2p_lf = lf ? 1 : 0;
+        const int mode = (lf && c->tree) ? (want_lik ? MODE_EVAL_TREE : MODE_EVAL_NOLIK_TREE)
+                                         : (want_lik ? MODE_EVAL : MODE_EVAL_NOLIK);
+        st = launch_coop(c, pass_fn_mode(mode, c->prec, c->trunc, c->d), a, s);
+        if (st) return st;
+        if (timed) CK(cudaEventRecord(next_event(c), s));
     } else {
         // local partial; with a tree prior the pass kernel's last CTA walks the tree
         // at xeval during phase A (EVAL_TREE modes: d log prior / dX into gprior)
@@ -411,7 +490,7 @@ mds_status sigma_mh_impl(mds_ctx c, cudaStream_t s, const mds_sigma_prior* prior
 
 // a pass sequence can be captured in a CUDA graph unless the exchange runs on
 // the host (the mds_set_allgather callback of a sharded context)
-bool graph_capturable(mds_ctx c) { return c->world == 1 || c->comm; }
+bool graph_capturable(mds_ctx c) { return c->world == 1 || c->comm || c->p2p; }
 
 // log L only (MODE_LIK) at the context's X for the SigmaParams given, into the
 // device double lik_out; sharded: local partial -> exchange -> rank-ordered sum
@@ -420,7 +499,7 @@ mds_status run_lik_pass(mds_ctx c, const SigmaParams& P, double* lik_out, cudaSt
     PassArgs a = base_args(c, c->d_x);
     a.P = P;
     const PassKernel k = pass_fn_mode(MODE_LIK, c->prec, c->trunc, c->d);
-    if (direct(c)) {
+    if (direct(c) || c->p2p) {      // (peer-memory exchange fused into the pass)
         a.lik = lik_out;
         return launch_coop(c, k, a, s);
     }
@@ -434,12 +513,14 @@ mds_status run_lik_pass(mds_ctx c, const SigmaParams& P, double* lik_out, cudaSt
     return MDS_OK;
 }
 
+// (stream-ordered: cudaFree would wait for the whole device, e.g. for a peer rank's
+// pass kernel sharing this GPU through the peer-memory exchange)
 mds_status rw_scratch(mds_ctx c, size_t bytes) {
     if (c->rwbuf_bytes >= bytes) return MDS_OK;
-    if (c->d_rwbuf) cudaFree(c->d_rwbuf);
+    if (c->d_rwbuf) cudaFreeAsync(c->d_rwbuf, c->stream);
     c->d_rwbuf = nullptr;
     c->rwbuf_bytes = 0;
-    cudaError_t e = cudaMalloc(&c->d_rwbuf, bytes);
+    cudaError_t e = cudaMallocAsync(&c->d_rwbuf, bytes, c->stream);
     if (e != cudaSuccess) {
         cudaGetLastError();
         return fail(c, MDS_E_OOM, "cudaMalloc of sweep scratch failed");
@@ -479,6 +560,7 @@ RowArgs row_args(mds_ctx c) {
 // observed pairs stored by this context (cached until Y changes; one count kernel)
 mds_status count_obs(mds_ctx c) {
     if (c->n_obs >= 0) return MDS_OK;
+    trace(c, "count_obs");
     CK(cudaMemsetAsync(c->d_count, 0, sizeof(unsigned long long), c->stream));
     const size_t cnt = (size_t)c->ntl * TB * TB;
     if (cnt) {
@@ -490,8 +572,9 @@ mds_status count_obs(mds_ctx c) {
     }
     unsigned long long h = 0;
     CK(cudaMemcpyAsync(&h, c->d_count, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
-    CK(cudaStreamSynchronize(c->stream));
+    CKS(c->stream);
     c->n_obs = (int64_t)h;
+    trace(c, "count_obs done");
     return MDS_OK;
 }
 
@@ -636,6 +719,7 @@ mds_status build_schedule(mds_ctx c) {
     c->wpc = ks[0].wpc;
     const int64_t U = (int64_t)GROUPS_PER_TILE * c->ntl;
     int64_t G = (int64_t)sms * occ;
+    if (c->grid_limit > 0) G = std::min<int64_t>(G, c->grid_limit);
     G = std::max<int64_t>(std::min<int64_t>(G, (U + c->wpc - 1) / c->wpc), 1);
     // with a tree prior one more CTA walks the tree during phase A
     const int64_t Gp = G;
@@ -698,7 +782,7 @@ mds_status build_schedule(mds_ctx c) {
     }
     // the host vectors above die on return and the uploads are stream-ordered on
     // the context's stream (possibly a non-blocking one): complete them here
-    CK(cudaStreamSynchronize(c->stream));
+    CKS(c->stream);
     return MDS_OK;
 }
 
@@ -726,6 +810,8 @@ void report_phases(mds_ctx c) {
         std::snprintf(buf, sizeof buf, "min %.2f med %.2f max %.2f", v.front(), v[v.size() / 2], v.back());
         return std::string(buf);
     };
+    std::fprintf(stderr, "[mds phases] rank %d of %d: grid %d, first CTA start at globaltimer %llu ns, last end %llu\n",
+                 c->rank, c->world, c->grid, t0, t3);
     std::fprintf(stderr, "[mds phases us] span %.2f | A end: %s | sync wait: %s | B: %s\n", (t3 - t0) * 1e-3,
                  st(a).c_str(), st(w).c_str(), st(b).c_str());
     {   // phase B of the job CTAs: slab loads, CTA reduction, final (update + stores)
@@ -811,7 +897,7 @@ mds_status create_impl(int64_t n, int32_t d, int32_t precision, int32_t truncati
         (st = dalloc(c, &yb, ntl * TB * TB * c->elem)) || (st = dalloc(c, &c->d_x, m)) ||
         (st = dalloc(c, &c->d_grad, m)) || (st = dalloc(c, &c->d_lik, 4)) || (st = dalloc(c, &c->d_bad, 1)) ||
         (st = dalloc(c, &c->d_count, 1)) || (st = dalloc(c, &c->d_p, m)) || (st = dalloc(c, &c->d_gl, m)) ||
-        (st = dalloc(c, &c->d_xnext, m)))
+        (st = dalloc(c, &c->d_xnext, m)) || (st = dalloc(c, &c->d_gbar, 2)))
         goto fail_alloc;
     c->d_y = yb;
     if ((world > 1 || nccl_id) && ((st = dalloc(c, &c->d_partial, (size_t)n * d + 1)) ||
@@ -824,6 +910,7 @@ mds_status create_impl(int64_t n, int32_t d, int32_t precision, int32_t truncati
         for (double* p : {c->d_x, c->d_grad, c->d_p, c->d_gl, c->d_xnext})
             if (!e) e = cudaMemset(p, 0, m * sizeof(double));
         if (!e) e = cudaMemset(c->d_lik, 0, 4 * sizeof(double));
+        if (!e) e = cudaMemset(c->d_gbar, 0, 2 * sizeof(unsigned));
         if (!e) {
             const size_t cnt = ntl * TB * TB;
             if (precision == MDS_F64) fill_nan_kernel<double><<<1184, 256>>>((double*)c->d_y, cnt);
@@ -884,7 +971,7 @@ mds_status pack_rows_device(mds_ctx c, int64_t i0, int64_t i1, const double* src
     }
     int bad = 0;
     CK(cudaMemcpyAsync(&bad, c->d_bad, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
-    CK(cudaStreamSynchronize(c->stream));
+    CKS(c->stream);
     c->n_obs = -1;
     ++c->version;
     if (bad) {
@@ -909,11 +996,15 @@ mds_status pack_rows_device(mds_ctx c, int64_t i0, int64_t i1, const double* src
 
 mds_status ensure_stage(mds_ctx c, size_t elems) {
     if (elems <= c->stage_elems) return MDS_OK;
-    if (c->d_stage) cudaFree(c->d_stage);
+    // stream-ordered (the rows are packed on c->stream; cudaFree would wait for the device)
+    if (c->d_stage) cudaFreeAsync(c->d_stage, c->stream);
     c->d_stage = nullptr;
     c->stage_elems = 0;
-    mds_status st = dalloc(c, &c->d_stage, elems);
-    if (st) return st;
+    if (cudaMallocAsync((void**)&c->d_stage, elems * sizeof(double), c->stream) != cudaSuccess) {
+        cudaGetLastError();
+        c->d_stage = nullptr;
+        return fail(c, MDS_E_OOM, "cudaMallocAsync of " + std::to_string(elems * sizeof(double)) + " bytes failed");
+    }
     c->stage_elems = elems;
     return MDS_OK;
 }
@@ -993,7 +1084,7 @@ mds_status mds_set_stream(mds_ctx c, void* s) {
     GUARD(c);
     // work already queued on the old stream (e.g. an asynchronous X upload) must
     // not race with what the new stream runs next
-    if ((cudaStream_t)s != c->stream) CK(cudaStreamSynchronize(c->stream));
+    if ((cudaStream_t)s != c->stream) CKS(c->stream);
     c->stream = (cudaStream_t)s;
     return MDS_OK;
 }
@@ -1053,7 +1144,7 @@ mds_status mds_set_locations(mds_ctx c, const double* x) {
         for (int64_t q = 0; q < m; ++q)
             if (!std::isfinite(x[q])) return fail(c, MDS_E_INVALID_ARG, "locations must be finite");
         CK(cudaMemcpyAsync(c->d_x, x, m * sizeof(double), cudaMemcpyHostToDevice, c->stream));
-        CK(cudaStreamSynchronize(c->stream));
+        CKS(c->stream);
     } else {
         CK(cudaEventSynchronize(c->xstage_done));      // the previous upload has left the buffer
         bool ok = true;
@@ -1099,7 +1190,7 @@ mds_status mds_log_likelihood_at_sigma(mds_ctx c, double sigma, double* loglik) 
     st = run_lik_pass(c, sigma_params(sigma), c->d_lik + 2, c->stream);
     if (st) return st;
     CK(cudaMemcpyAsync(loglik, c->d_lik + 2, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-    CK(cudaStreamSynchronize(c->stream));
+    CKS(c->stream);
     return MDS_OK;
 }
 
@@ -1130,7 +1221,7 @@ mds_status mds_row_loglik_delta(mds_ctx c, int64_t i, const double* x_new_i, dou
         out = dx + 16;
     }
     CK(cudaMemcpyAsync(delta, out, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-    CK(cudaStreamSynchronize(c->stream));
+    CKS(c->stream);
     return MDS_OK;
 }
 
@@ -1197,7 +1288,7 @@ mds_status mds_rw_sweep(mds_ctx c, int64_t k, const int64_t* rows, const double*
     }
     unsigned long long na = 0;
     CK(cudaMemcpyAsync(&na, dacc, sizeof(na), cudaMemcpyDeviceToHost, c->stream));
-    CK(cudaStreamSynchronize(c->stream));
+    CKS(c->stream);
     if (accepted) *accepted = (int64_t)na;
     ++c->version;      // X moved (possibly)
     return MDS_OK;
@@ -1423,7 +1514,7 @@ mds_status mds_set_tree_prior(mds_ctx c, int64_t n_nodes, const int64_t* parent,
     }
     A.grad = c->d_gprior;
     A.logp = c->d_logprior;
-    CK(cudaStreamSynchronize(c->stream));   // the uploads above read host vectors that die on return
+    CKS(c->stream);   // the uploads above read host vectors that die on return
     const char* pe = std::getenv("MDS_PROFILE_TREE");
     if (pe && pe[0] == '1') {
         static unsigned long long* prof = nullptr;
@@ -1464,7 +1555,7 @@ mds_status mds_tree_prior(mds_ctx c, double* logp, double* grad) {
     if (grad)
         CK(cudaMemcpyAsync(grad, c->d_gprior, (size_t)c->n * c->d * sizeof(double), cudaMemcpyDeviceToHost,
                            c->stream));
-    CK(cudaStreamSynchronize(c->stream));
+    CKS(c->stream);
     report_tree_profile(c);
     c->lf_version = 0;     // d_gprior / d_logprior now belong to X, not to the leapfrog state
     return MDS_OK;
@@ -1497,7 +1588,7 @@ mds_status mds_cv_set_heldout(mds_ctx c, int64_t m, const int64_t* i, const int6
     if (m > 0) {
         CK(cudaMemcpyAsync(c->d_cv_ij, ij.data(), (size_t)m * sizeof(int2), cudaMemcpyHostToDevice, c->stream));
         CK(cudaMemcpyAsync(c->d_cv_y, y, (size_t)m * sizeof(double), cudaMemcpyHostToDevice, c->stream));
-        CK(cudaStreamSynchronize(c->stream));   // ij dies on return; y belongs to the caller
+        CKS(c->stream);   // ij dies on return; y belongs to the caller
     }
     c->cv_m = m;
     return MDS_OK;
@@ -1545,7 +1636,7 @@ mds_status mds_cv_lpd(mds_ctx c, double* lpd, int64_t* draws) {
     cv_finalize_launch(c->d_cv_max, c->d_cv_sum, c->cv_m, c->cv_draws, c->d_cv_out, c->stream);
     CK(cudaGetLastError());
     CK(cudaMemcpyAsync(lpd, c->d_cv_out, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-    CK(cudaStreamSynchronize(c->stream));
+    CKS(c->stream);
     return MDS_OK;
 }
 
@@ -1588,7 +1679,7 @@ mds_status sigma_mh_impl(mds_ctx c, cudaStream_t s, const mds_sigma_prior* prior
     if (cur_ll_dev) CK(cudaMemcpyAsync(&ll[0], cur_ll_dev, sizeof(double), cudaMemcpyDeviceToHost, s));
     else if (need_cur) CK(cudaMemcpyAsync(&ll[0], c->d_lik + 2, sizeof(double), cudaMemcpyDeviceToHost, s));
     CK(cudaMemcpyAsync(&ll[1], c->d_lik + 3, sizeof(double), cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
+    CKS(s);
     // log prior of phi: tau = 1/sigma^2 = e^-phi ~ Gamma(shape, rate), Jacobian |dtau/dphi| = tau
     auto lp = [&](double phi) { return -prior->shape * phi - prior->rate * std::exp(-phi); };
     const double lr = (ll[1] - ll[0]) + (lp(phi1) - lp(phi0));
@@ -1641,11 +1732,13 @@ extern "C" {
 
 mds_status mds_log_likelihood_and_gradient(mds_ctx c, double* loglik, double* grad) {
     GUARD(c);
+    trace(c, "log_likelihood_and_gradient");
     mds_status st = eval_internal(c);
     if (st) return st;
+    trace(c, "results copy");
     if (loglik) CK(cudaMemcpyAsync(loglik, c->d_lik, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
     if (grad) CK(cudaMemcpyAsync(grad, c->d_grad, c->n * c->d * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-    CK(cudaStreamSynchronize(c->stream));
+    CKS(c->stream);
     return MDS_OK;
 }
 
@@ -1693,7 +1786,7 @@ mds_status mds_get_locations(mds_ctx c, double* x) {
     if (!x) return fail(c, MDS_E_INVALID_ARG, "NULL output");
     if (!c->x_set) return fail(c, MDS_E_STATE, "locations not set");
     CK(cudaMemcpyAsync(x, c->d_x, c->n * c->d * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-    CK(cudaStreamSynchronize(c->stream));
+    CKS(c->stream);
     return MDS_OK;
 }
 
@@ -1701,7 +1794,7 @@ mds_status mds_get_momentum(mds_ctx c, double* p) {
     GUARD(c);
     if (!p) return fail(c, MDS_E_INVALID_ARG, "NULL output");
     CK(cudaMemcpyAsync(p, c->d_p, c->n * c->d * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-    CK(cudaStreamSynchronize(c->stream));
+    CKS(c->stream);
     return MDS_OK;
 }
 
@@ -1713,6 +1806,140 @@ mds_status mds_combine_partials_device(mds_ctx c, const double* gathered_dev, in
     combine_kernel<<<(unsigned)((len + 255) / 256), 256, 0, c->stream>>>(gathered_dev, world, len, grad_dev, loglik_dev);
     CK(cudaGetLastError());
     return MDS_OK;
+}
+
+// ---- fused peer-memory exchange (SURVEY 8(e) stage 2; include/mds.h)
+namespace {
+mds_status hmc_alloc(mds_ctx c);     // mds_hmc.inl
+// Load every kernel a sharded context may launch.  With CUDA's lazy module loading
+// the first launch of a kernel loads it, and loading waits for the device to go idle
+// (measured: tools/lock_probe.cu) -- while a rank's pass kernel waits in the
+// peer-memory exchange for a rank whose host thread is in exactly such a first
+// launch (ranks sharing one GPU in one process), that is a deadlock.
+void preload_kernels(mds_ctx c) {
+    cudaFuncAttributes fa;
+    const void* fs[] = {(const void*)prime_kernel, (const void*)redrift_kernel, (const void*)leapfrog_update_kernel,
+                        (const void*)hamiltonian_kernel, (const void*)combine_update_kernel,
+                        (const void*)combine_kernel, (const void*)p2p_allgather_kernel,
+                        (const void*)count_obs_kernel<double>, (const void*)count_obs_kernel<float>,
+                        (const void*)zero_pairs_kernel<double>, (const void*)zero_pairs_kernel<float>,
+                        (const void*)row_fn(c->prec == MDS_F64, c->trunc, c->d)};
+    for (const void* f : fs) cudaFuncGetAttributes(&fa, f);
+    for (int m = 0; m < N_MODES; ++m) cudaFuncGetAttributes(&fa, (const void*)pass_fn_mode(m, c->prec, c->trunc, c->d).fn);
+    rw_preload();
+    tree_preload(c->d);
+    cudaGetLastError();
+}
+}  // namespace
+
+mds_status mds_p2p_window(mds_ctx c, void** window_dev, void* ipc_handle_out) {
+    GUARD(c);
+    if (c->world > P2P_MAX_WORLD) return fail(c, MDS_E_UNSUPPORTED, "mds_p2p_window: world > 32");
+    if (!c->d_win) {
+        const size_t m1 = (size_t)(c->n * c->d + 1);
+        c->win_bytes = P2P_FLAG_BYTES + 2 * (size_t)c->world * m1 * sizeof(double);
+        mds_status st;
+        if ((st = dalloc(c, &c->d_win, c->win_bytes))) return st;
+        if ((st = dalloc(c, &c->d_p2p_state, 4))) return st;
+        if (!c->d_gathered && ((st = dalloc(c, &c->d_partial, m1)) || (st = dalloc(c, &c->d_gathered, m1 * c->world))))
+            return st;      // (a world-1 context: the small exchanges gather here)
+        CK(cudaMemsetAsync(c->d_win, 0, c->win_bytes, c->stream));
+        CK(cudaMemsetAsync(c->d_p2p_state, 0, 4 * sizeof(unsigned long long), c->stream));
+        CK(cudaHostAlloc((void**)&c->h_p2p_err, sizeof(int), cudaHostAllocMapped));
+        *c->h_p2p_err = 0;
+        CK(cudaHostGetDevicePointer((void**)&c->d_p2p_err, c->h_p2p_err, 0));
+        CKS(c->stream);
+    }
+    if (window_dev) *window_dev = c->d_win;
+    if (ipc_handle_out) {
+        cudaIpcMemHandle_t h;
+        CK(cudaIpcGetMemHandle(&h, c->d_win));
+        static_assert(sizeof(h) == MDS_IPC_HANDLE_BYTES, "cudaIpcMemHandle_t size");
+        std::memcpy(ipc_handle_out, &h, sizeof(h));
+    }
+    return MDS_OK;
+}
+
+mds_status mds_p2p_connect(mds_ctx c, void* const* peer_window_dev) {
+    GUARD(c);
+    if (!peer_window_dev) return fail(c, MDS_E_INVALID_ARG, "mds_p2p_connect: NULL");
+    if (!c->d_win) return fail(c, MDS_E_STATE, "mds_p2p_connect: call mds_p2p_window first");
+    if (peer_window_dev[c->rank] != c->d_win)
+        return fail(c, MDS_E_INVALID_ARG, "mds_p2p_connect: entry [rank] is not this context's window");
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    for (int r = 0; r < c->world; ++r) {
+        if (!peer_window_dev[r]) return fail(c, MDS_E_INVALID_ARG, "mds_p2p_connect: NULL window");
+        cudaPointerAttributes at{};
+        CK(cudaPointerGetAttributes(&at, peer_window_dev[r]));
+        if (at.type == cudaMemoryTypeDevice && at.device != dev) {      // a window on another GPU
+            int ok = 0;
+            CK(cudaDeviceCanAccessPeer(&ok, dev, at.device));
+            if (!ok) return fail(c, MDS_E_UNSUPPORTED, "mds_p2p_connect: no peer access to device " +
+                                                           std::to_string(at.device));
+            const cudaError_t e = cudaDeviceEnablePeerAccess(at.device, 0);
+            if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+            else CK(e);
+        }
+    }
+    if (!c->d_peer_win) {
+        mds_status st = dalloc(c, &c->d_peer_win, (size_t)c->world);
+        if (st) return st;
+    }
+    CK(cudaMemcpyAsync(c->d_peer_win, peer_window_dev, c->world * sizeof(char*), cudaMemcpyHostToDevice, c->stream));
+    CKS(c->stream);
+    // everything a sharded call allocates lazily, now: a first cudaMalloc can wait for
+    // the device too (ranks sharing one GPU: the same deadlock as lazy loading)
+    preload_kernels(c);
+    if (const char* e = std::getenv("MDS_P2P_TIMEOUT_S")) {
+        const double v = std::atof(e);
+        if (v > 0) c->p2p_timeout_ns = (unsigned long long)(v * 1e9);
+    }
+    mds_status st = rw_scratch(c, 3 * sizeof(double) * 8);
+    if (!st) st = hmc_alloc(c);
+    if (st) return st;
+    if (!c->h_pbuf && cudaMallocHost(&c->h_pbuf, (size_t)(c->n * c->d) * sizeof(double)) != cudaSuccess) {
+        cudaGetLastError();
+        c->h_pbuf = nullptr;
+    }
+    CKS(c->stream);
+    c->p2p = true;
+    return MDS_OK;
+}
+
+mds_status mds_p2p_connect_ipc(mds_ctx c, const void* ipc_handles) {
+    GUARD(c);
+    if (!ipc_handles) return fail(c, MDS_E_INVALID_ARG, "mds_p2p_connect_ipc: NULL");
+    if (!c->d_win) return fail(c, MDS_E_STATE, "mds_p2p_connect_ipc: call mds_p2p_window first");
+    std::vector<void*> w(c->world, nullptr);
+    for (int r = 0; r < c->world; ++r) {
+        if (r == c->rank) {
+            w[r] = c->d_win;
+            continue;
+        }
+        cudaIpcMemHandle_t h;
+        std::memcpy(&h, static_cast<const char*>(ipc_handles) + (size_t)r * MDS_IPC_HANDLE_BYTES, sizeof(h));
+        void* q = nullptr;
+        CK(cudaIpcOpenMemHandle(&q, h, cudaIpcMemLazyEnablePeerAccess));
+        c->ipc_opened.push_back(q);
+        w[r] = q;
+    }
+    return mds_p2p_connect(c, w.data());
+}
+
+mds_status mds_p2p_connected(mds_ctx c, int32_t* connected) {
+    GUARD(c);
+    if (!connected) return MDS_E_INVALID_ARG;
+    *connected = c->p2p ? 1 : 0;
+    return MDS_OK;
+}
+
+mds_status mds_set_grid_limit(mds_ctx c, int32_t ctas) {
+    GUARD(c);
+    if (ctas < 0) return fail(c, MDS_E_INVALID_ARG, "mds_set_grid_limit: ctas < 0");
+    CKS(c->stream);                      // the old schedule may still be in use
+    c->grid_limit = ctas;
+    return build_schedule(c);
 }
 
 mds_status mds_observed_pairs(mds_ctx c, int64_t* count) {
@@ -1741,7 +1968,7 @@ mds_status mds_zero_distance_pairs(mds_ctx c, int64_t* count) {
     }
     unsigned long long h = 0;
     CK(cudaMemcpyAsync(&h, c->d_count, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
-    CK(cudaStreamSynchronize(c->stream));
+    CKS(c->stream);
     *count = (int64_t)h;
     return MDS_OK;
 }

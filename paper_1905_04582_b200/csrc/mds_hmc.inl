@@ -122,7 +122,8 @@ struct HmcSession {
 
 void hmc_session_end(HmcSession& S) {
     if (S.exec) cudaGraphExecDestroy(S.exec);
-    if (S.pinned && S.pbuf) cudaFreeHost(S.pbuf);
+    // (the pinned momentum buffer belongs to the context: cudaFreeHost would wait for
+    // the whole device, e.g. for a peer rank's pass kernel sharing this GPU)
     if (S.e0) cudaEventDestroy(S.e0);
     if (S.e1) cudaEventDestroy(S.e1);
     if (S.owned && S.s) cudaStreamDestroy(S.s);
@@ -171,7 +172,9 @@ mds_status hmc_session_begin(mds_ctx c, const mds_hmc_config* cfg, HmcSession& S
     S.eps = cfg->step_size;
     S.it2 = inv_tau2_of(c, cfg);
     const size_t m = (size_t)(c->n * c->d);
-    if (cudaMallocHost(&S.pbuf, m * sizeof(double)) == cudaSuccess) {
+    if (!c->h_pbuf && cudaMallocHost(&c->h_pbuf, m * sizeof(double)) != cudaSuccess) c->h_pbuf = nullptr;
+    if (c->h_pbuf) {
+        S.pbuf = c->h_pbuf;
         S.pinned = true;
     } else {
         cudaGetLastError();
@@ -197,7 +200,7 @@ mds_status hmc_session_transition(mds_ctx c, HmcSession& S, uint64_t seed, uint6
     cudaStream_t s = S.s;
     const int64_t m = c->n * c->d;
     const size_t mbytes = (size_t)c->npad * c->d * sizeof(double);
-    CK(cudaStreamSynchronize(s));                  // pbuf is reused: the previous upload must be done
+    CKS(s);                  // pbuf is reused: the previous upload must be done
     for (int64_t q = 0; q < m; ++q) S.pbuf[q] = hmc_normal(seed, it, (uint64_t)q);
     CK(cudaMemcpyAsync(c->d_p, S.pbuf, m * sizeof(double), cudaMemcpyHostToDevice, s));
     CK(cudaMemcpyAsync(c->d_xsave, c->d_x, mbytes, cudaMemcpyDeviceToDevice, s));
@@ -216,7 +219,7 @@ mds_status hmc_session_transition(mds_ctx c, HmcSession& S, uint64_t seed, uint6
     double hh[2] = {0, 0};
     CK(cudaMemcpyAsync(&hh[0], c->d_H0, sizeof(double), cudaMemcpyDeviceToHost, s));
     CK(cudaMemcpyAsync(&hh[1], c->d_H, sizeof(double), cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
+    CKS(s);
     const double dH = hh[1] - hh[0];
     const double u = hmc_u01(hmc_mix(seed ^ hmc_mix(0xACCE97ull ^ hmc_mix(it))));
     const bool ok = std::isfinite(dH) && std::log(u) < -dH;
@@ -236,7 +239,7 @@ mds_status hmc_session_transition(mds_ctx c, HmcSession& S, uint64_t seed, uint6
 mds_status hmc_session_finish(mds_ctx c, HmcSession& S, double* x_out, double* final_ll) {
     CK(cudaMemcpyAsync(final_ll, c->d_lik, sizeof(double), cudaMemcpyDeviceToHost, S.s));
     if (x_out) CK(cudaMemcpyAsync(x_out, c->d_x, (size_t)(c->n * c->d) * sizeof(double), cudaMemcpyDeviceToHost, S.s));
-    CK(cudaStreamSynchronize(S.s));
+    CKS(S.s);
     return MDS_OK;
 }
 
@@ -274,7 +277,7 @@ mds_status mds_hmc_trajectory(mds_ctx c, const mds_hmc_config* cfg, const double
     if (x_out) CK(cudaMemcpyAsync(x_out, c->d_x, m * sizeof(double), cudaMemcpyDeviceToHost, s));
     if (p_out) CK(cudaMemcpyAsync(p_out, c->d_p, m * sizeof(double), cudaMemcpyDeviceToHost, s));
     CK(cudaMemcpyAsync(c->d_x, c->d_xsave, mbytes, cudaMemcpyDeviceToDevice, s));
-    CK(cudaStreamSynchronize(s));
+    CKS(s);
     c->eval_version = 0;   // internal results now belong to the proposal, not X
     c->lf_version = 0;
     if (H0) *H0 = h0;

@@ -206,6 +206,25 @@ __global__ void combine_update_kernel(const double* __restrict__ gathered, int w
     xnext[k] = drift(xv, pn, gn, eps, heps);
 }
 
+// The exchanges other than the fused pass (likelihood-only passes, single-location
+// updates) over the peer-memory windows: ONE CTA pushes send[0..count) into slot
+// [rank] of every rank's window, raises this rank's flag everywhere, waits for all
+// ranks' flags and copies the world slots into recv[world][count] (rank order) for
+// the rank-ordered combine kernels.  Same exchange count and flags as the fused pass.
+__global__ void p2p_allgather_kernel(P2PArgs q, const double* __restrict__ send, int64_t count,
+                                     double* __restrict__ recv) {
+    const unsigned long long ep = p2p_epoch(q);
+    for (int64_t e = threadIdx.x; e < count; e += blockDim.x) p2p_push(q, ep, e, send[e]);
+    __syncthreads();
+    if (threadIdx.x == 0) p2p_arrive_and_wait(q, ep, 1u);
+    __syncthreads();
+    const double* rv = p2p_recv(q, q.win[q.rank], ep);
+    for (int r = 0; r < q.world; ++r)
+        for (int64_t e = threadIdx.x; e < count; e += blockDim.x) recv[(size_t)r * count + e] = rv[(size_t)r * q.m1 + e];
+    __syncthreads();
+    if (threadIdx.x == 0) p2p_finish(q, ep, 1u);
+}
+
 // rank-ordered sum of gathered partials: out[e] = sum_r gathered[r][e]
 __global__ void combine_kernel(const double* __restrict__ gathered, int world, int64_t len,
                                double* __restrict__ grad_out, double* __restrict__ lik_out) {

@@ -151,6 +151,97 @@ __device__ __forceinline__ double drift(double x, double p, double gl, double ep
     return __fma_rn(eps, __fma_rn(heps, gl, p), x);
 }
 
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
+// ------------------------------------------------------------ peer-memory exchange
+// Window of every rank (device memory, mds_p2p_window): 32 arrival flags (uint64,
+// flag r = the number of exchanges rank r has pushed into this window), then
+// recv[2][world][m + 1] doubles (m = n d; slot parity = exchange count & 1).
+// state (local, not in the window): [0] exchanges done, [1] CTAs done pushing,
+// [2] CTAs done combining.  err: host-mapped word, set to 1 on a 60 s timeout.
+constexpr int P2P_MAX_WORLD = 32;
+constexpr size_t P2P_FLAG_BYTES = P2P_MAX_WORLD * sizeof(unsigned long long);
+struct P2PArgs {
+    char* const* win;               // [world] window base addresses (device array); NULL = no P2P
+    unsigned long long* state;      // local counters
+    int* err;                       // host-mapped error word
+    int rank, world;
+    int64_t m1;                     // slot length m + 1
+    unsigned long long timeout_ns;  // give up waiting for a peer after this long
+};
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ unsigned long long p2p_epoch(const P2PArgs& q) {
+    return *reinterpret_cast<volatile unsigned long long*>(q.state);
+}
+// receive area of window w for the exchange ep: [world][m1]
+__device__ __forceinline__ double* p2p_recv(const P2PArgs& q, char* w, unsigned long long ep) {
+    return reinterpret_cast<double*>(w + P2P_FLAG_BYTES) + (size_t)(ep & 1) * q.world * q.m1;
+}
+// value e of this rank's partial -> slot [rank][e] of every rank's window (remote stores)
+__device__ __forceinline__ void p2p_push(const P2PArgs& q, unsigned long long ep, int64_t e, double v) {
+    for (int r = 0; r < q.world; ++r) p2p_recv(q, q.win[r], ep)[(size_t)q.rank * q.m1 + e] = v;
+}
+// thread 0 of each of `ctas` CTAs, after the CTA's pushes: count the CTA in; the
+// last raises this rank's flag in every window; then wait for every rank's flag
+__device__ __forceinline__ void p2p_arrive_and_wait(const P2PArgs& q, unsigned long long ep, unsigned ctas) {
+    __threadfence_system();                                // this CTA's remote stores, system-wide
+    if (atomicAdd(&q.state[1], 1ull) == ctas - 1) {
+        q.state[1] = 0;                                    // (reset for the next exchange)
+        __threadfence_system();
+        for (int r = 0; r < q.world; ++r)
+            st_release_sys(reinterpret_cast<unsigned long long*>(q.win[r]) + q.rank, ep + 1);
+    }
+    const unsigned long long* fl = reinterpret_cast<const unsigned long long*>(q.win[q.rank]);
+    const unsigned long long t0 = gtimer();
+    for (int r = 0; r < q.world; ++r) {
+        while (ld_acquire_sys(fl + r) < ep + 1) {
+            if (gtimer() - t0 > q.timeout_ns) {           // a peer never arrived: give up, report
+                *reinterpret_cast<volatile int*>(q.err) = 1;
+                return;
+            }
+        }
+    }
+}
+// thread 0 of each CTA at the end of the combine: the last advances the exchange count
+__device__ __forceinline__ void p2p_finish(const P2PArgs& q, unsigned long long ep, unsigned ctas) {
+    if (atomicAdd(&q.state[2], 1ull) == ctas - 1) {
+        q.state[2] = 0;
+        q.state[0] = ep + 1;
+    }
+}
+
+// grid-wide barrier of a co-resident grid (thread 0 of each CTA between two
+// __syncthreads): the last arriving CTA resets the count and advances the generation
+__device__ __forceinline__ void grid_barrier(unsigned* b, unsigned ctas) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        volatile unsigned* gen = b + 1;
+        const unsigned g = *gen;
+        __threadfence();
+        if (atomicAdd(b, 1u) == ctas - 1) {
+            b[0] = 0;
+            __threadfence();
+            atomicExch(b + 1, g + 1);
+        } else {
+            while (*gen == g) {
+            }
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
 struct PassArgs {
     // inputs
     const void* y;               // local tiles [ntl][B][B]
@@ -185,13 +276,15 @@ struct PassArgs {
     SigmaParams P;
     double lik_const;            // added to log L: n_obs x P.k0 (fp64 pass), 0 (fp32 pass)
     unsigned long long* prof;    // optional [G][4] globaltimer stamps (start, end A, after sync, end)
+    // fused peer-memory exchange (sharded contexts after mds_p2p_connect; EVAL* / LIK modes):
+    // phase B pushes this rank's partial into every rank's window, then phase C combines
+    // the world partials in rank order into grad / lik (and, p2p_lf, the leapfrog update)
+    P2PArgs p2p;
+    int p2p_lf;
+    unsigned* gbar;              // [2] software grid barrier: arrivals, generation
+    int soft_sync;               // 1: launched without the cooperative attribute -> gbar, not grid.sync
 };
 
-__device__ __forceinline__ unsigned long long gtimer() {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-    return t;
-}
 
 constexpr int MAXSEG_W = 32;    // segments per warp (host checks)
 
@@ -339,6 +432,9 @@ pass_kernel(PassArgs a) {
         __syncthreads();
     }
     if (a.prof && threadIdx.x == 0) a.prof[blockIdx.x * 4 + 0] = gtimer();
+    // the exchange this pass is (all CTAs read it before any can advance it, at the end)
+    const bool p2p = !LF && a.p2p.win != nullptr;
+    const unsigned long long p2p_ep = p2p ? p2p_epoch(a.p2p) : 0ull;
     A lik_w = A(0);
     A lacc[4] = {A(0), A(0), A(0), A(0)};   // fp64: running log L sums by lock-step position
 
@@ -668,7 +764,8 @@ pass_kernel(PassArgs a) {
     const int chunks = (TB * D + CH - 1) / CH;
     const int jobs = a.nb * chunks;
     __threadfence();
-    cg::this_grid().sync();
+    if (a.soft_sync) grid_barrier(a.gbar, gridDim.x);   // plain launch (peer-memory exchange)
+    else cg::this_grid().sync();
     if (a.prof && threadIdx.x == 0) a.prof[blockIdx.x * 4 + 2] = gtimer();
 
     // ------------------------------------------------------------ phase B
@@ -751,7 +848,8 @@ pass_kernel(PassArgs a) {
                 const int64_t e = (int64_t)b * TB * D + e_in;
                 if (e < a.n * D) {
                     if (!LF) {
-                        a.grad[e] = g;
+                        if (p2p) p2p_push(a.p2p, p2p_ep, e, g);   // this rank's partial -> every rank's window
+                        else a.grad[e] = g;
                     } else {
                         // leapfrog: the pass ran at xnext = x + eps (p + eps/2 gl)
                         const double xe = pre_xe;
@@ -773,7 +871,11 @@ pass_kernel(PassArgs a) {
     // partial sums over the warp partials, then warps in order
     if (!WL) {
         // nobody reads log L of this pass: mark it as not computed
-        if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) *a.lik = __longlong_as_double(0x7ff8000000000000LL);
+        if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) {
+            const double nan = __longlong_as_double(0x7ff8000000000000LL);
+            if (p2p) p2p_push(a.p2p, p2p_ep, a.n * D, nan);
+            else *a.lik = nan;
+        }
     } else if (blockIdx.x == gridDim.x - 1) {
         const int GW = gridDim.x * WPC;
         // 4 partials per thread per round: the loads are in flight together
@@ -794,8 +896,50 @@ pass_kernel(PassArgs a) {
             for (int m = 16; m >= 1; m >>= 1) t += __shfl_xor_sync(0xffffffffu, t, m);
             // the per-pair constant -1/2 log(2 pi sigma^2) of the fp64 path, once:
             // n_obs (this context's observed pairs) x k0
-            if (threadIdx.x == 0) *a.lik = t + a.lik_const;
+            if (threadIdx.x == 0) {
+                if (p2p) p2p_push(a.p2p, p2p_ep, a.n * D, t + a.lik_const);
+                else *a.lik = t + a.lik_const;
+            }
         }
+    }
+    // ------------------------------------------------------------ exchange + phase C
+    // (fused peer-memory exchange, SURVEY 8(e) stage 2) every CTA's pushes are
+    // fenced system-wide and counted; the last CTA raises this rank's flag on every
+    // rank; all CTAs wait for every rank's flag, then combine in rank order
+    if (p2p) {
+        __syncthreads();
+        if (threadIdx.x == 0) p2p_arrive_and_wait(a.p2p, p2p_ep, gridDim.x);
+        __syncthreads();
+        const int64_t m = a.n * D;
+        const double* __restrict__ rv = p2p_recv(a.p2p, a.p2p.win[a.p2p.rank], p2p_ep);   // own window
+        auto combine_one = [&](int64_t e) {
+            double g = 0.0;                      // the rank-ordered sum of combine_kernel
+            for (int r = 0; r < a.p2p.world; ++r) g += rv[(size_t)r * (m + 1) + e];
+            if (e == m) {
+                if (a.lik) *a.lik = g;
+            } else if (!a.p2p_lf) {
+                if (a.grad) a.grad[e] = g;
+            } else {
+                // combine_update_kernel's leapfrog update (the pass ran at xnext)
+                const double xv = a.xeval[e];
+                const double ph = __fma_rn(a.heps, a.gl[e], a.p[e]);
+                const double gn = a.gprior ? g + a.gprior[e] : g - xv * a.inv_tau2;
+                const double pn = __fma_rn(a.heps, gn, ph);
+                a.grad[e] = g;
+                a.x[e] = xv;
+                a.p[e] = pn;
+                a.gl[e] = gn;
+                a.xnext[e] = drift(xv, pn, gn, a.eps, a.heps);
+            }
+        };
+        if (WG) {
+            const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+            for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e <= m; e += stride) combine_one(e);
+        } else if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) {
+            combine_one(m);                      // likelihood-only pass: log L alone
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) p2p_finish(a.p2p, p2p_ep, gridDim.x);
     }
     if (a.prof) {
         __syncthreads();

@@ -283,6 +283,12 @@ void rw_decide_launch(const double* gathered, int world, int64_t stride, double*
     rw_decide_kernel<<<1, 32, 0, s>>>(gathered, world, stride, x, rows, u, q, xnew, inv_tau2, d, accepted);
 }
 
+void rw_preload() {
+    cudaFuncAttributes fa;
+    cudaFuncGetAttributes(&fa, rw_propose_kernel);
+    cudaFuncGetAttributes(&fa, rw_decide_kernel);
+}
+
 RowFn row_fn(int prec_is_f64, int trunc, int d) {
     if (prec_is_f64) return trunc ? row_fn_d<double, true>(d) : row_fn_d<double, false>(d);
     return trunc ? row_fn_d<float, true>(d) : row_fn_d<float, false>(d);

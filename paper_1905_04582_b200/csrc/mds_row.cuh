@@ -48,6 +48,9 @@ constexpr int ROW_THREADS = 512;    // per CTA
 constexpr int ROW_CLUSTER = 8;      // CTAs (SMs) per row: one thread-block cluster
 // row_kernel<T, D, TRUNC> for (precision, truncation, d); defined in mds_row.cu
 RowFn row_fn(int prec_is_f64, int trunc, int d);
+// load the sweep's helper kernels now (CUDA lazy loading would otherwise load them at
+// first launch, which waits for the device: see preload_kernels in mds_api.cu)
+void rw_preload();
 // sharded sweeps (mds_row.cu): proposal x_i + step z_q, and the decision from the
 // gathered partial deltas gathered[r * stride], r < world (rank order)
 void rw_propose_launch(const double* x, const int64_t* rows, const double* z, int64_t q, double step, int d,

@@ -27,6 +27,20 @@ void launch(const TreeArgs& a, cudaStream_t s) {
 
 }  // namespace
 
+void tree_preload(int d) {
+    cudaFuncAttributes fa;
+    switch (d) {
+        case 1: cudaFuncGetAttributes(&fa, tree_prior_kernel<1>); break;
+        case 2: cudaFuncGetAttributes(&fa, tree_prior_kernel<2>); break;
+        case 3: cudaFuncGetAttributes(&fa, tree_prior_kernel<3>); break;
+        case 4: cudaFuncGetAttributes(&fa, tree_prior_kernel<4>); break;
+        case 5: cudaFuncGetAttributes(&fa, tree_prior_kernel<5>); break;
+        case 6: cudaFuncGetAttributes(&fa, tree_prior_kernel<6>); break;
+        case 7: cudaFuncGetAttributes(&fa, tree_prior_kernel<7>); break;
+        default: cudaFuncGetAttributes(&fa, tree_prior_kernel<8>); break;
+    }
+}
+
 void tree_prior_launch(const TreeArgs& a, int d, cudaStream_t s) {
     switch (d) {
         case 1: launch<1>(a, s); break;

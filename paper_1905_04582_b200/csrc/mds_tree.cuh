@@ -91,5 +91,6 @@ struct TreeArgs {
 
 constexpr size_t TREE_SMEM_MAX = 200 * 1024;
 void tree_prior_launch(const TreeArgs& a, int d, cudaStream_t s);
+void tree_preload(int d);   // load the standalone walk kernel now (see preload_kernels)
 
 }  // namespace mdsk
