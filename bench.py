@@ -19,9 +19,13 @@ C4 (configs[3], N = 30000, D = 6, 10% missing, fp64 and fp32) under "configs".
 --gpus N > 1 without torchrun's environment re-launches this script under
 torch.distributed.run (one rank per GPU, 127.0.0.1 rendezvous).  Each rank
 owns the tile-rows r mod N, generates and uploads only those rows, and owns an
-NCCL communicator inside libmds (unique id broadcast over torch.distributed);
-the exchange is ncclAllGather of n*d + 1 doubles on the context stream.
---exchange gloo-host instead registers a host-staged gloo all-gather (several
+NCCL communicator inside libmds (unique id broadcast over torch.distributed).
+The exchange (--exchange p2p, default) is the fused peer-memory exchange: the
+pass kernel stores its partial into every rank's window over NVLink (IPC
+handles all-gathered through torch.distributed), waits for the ranks' flags and
+combines, one launch per step; --exchange nccl uses ncclAllGather of n*d + 1
+doubles on the context stream instead (also the fallback if the windows cannot
+be connected).  --exchange gloo-host registers a host-staged gloo all-gather (several
 ranks sharing one GPU: a plumbing check, not a measurement).  --dry-run: plan
 only (CPU, gloo): every rank reports its share of the pairs.
 """
@@ -66,7 +70,7 @@ def parse():
     ap.add_argument("--e2e-seconds", type=float, default=2.0)
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--exchange", choices=["nccl", "torch", "gloo-host"], default="nccl",
+    ap.add_argument("--exchange", choices=["p2p", "nccl", "torch", "gloo-host"], default="p2p",
                     help="sharded exchange: libmds-owned NCCL communicator (default), torch.distributed NCCL "
                          "callback, or host-staged gloo callback (ranks sharing a GPU)")
     ap.add_argument("--flush", choices=["auto", "mds", "none"], default="auto",
@@ -319,9 +323,12 @@ class Rank:
         self.torch, self.dist = torch, dist
         self.rank, self.world, self.local = dist_env()
         self.args = args
-        torch.cuda.set_device(self.local if args.exchange != "gloo-host" else 0)
+        # more ranks than GPUs (one test box): ranks share GPU 0 over a gloo group
+        # (a plumbing run -- time-sliced, not a measurement); NCCL needs a GPU per rank
+        self.shared = args.exchange == "gloo-host" or (self.world > 1 and self.world > torch.cuda.device_count())
+        torch.cuda.set_device(self.local if not self.shared else 0)
         if self.world > 1:
-            if args.exchange == "gloo-host":
+            if self.shared:
                 dist.init_process_group("gloo")
             else:
                 dist.init_process_group("nccl", device_id=torch.device("cuda", self.local))
@@ -334,12 +341,12 @@ class Rank:
         if self.world == 1:
             return [float(v) for v in vals]
         t = self.torch.tensor([float(v) for v in vals], dtype=self.torch.float64,
-                              device="cpu" if self.args.exchange == "gloo-host" else "cuda")
+                              device="cpu" if self.shared else "cuda")
         self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
         return [float(v) for v in t.cpu()]
 
     def nccl_id(self):
-        if self.args.exchange != "nccl":
+        if self.args.exchange not in ("nccl", "p2p") or self.shared:
             return None
         import paper_1905_04582_b200 as mds
         if self.world == 1:
@@ -354,7 +361,15 @@ def build_ctx(R, mds, w, prec, stream):
     uploaded row chunk by row chunk (the full triangle never exists on one host)."""
     t0 = time.perf_counter()
     ctx = mds.MDS(w.n, w.d, prec, True, rank=R.rank, world=R.world, stream=stream, nccl_unique_id=R.nccl_id())
-    if R.world > 1 and not ctx.has_communicator():
+    if R.world > 1 and R.args.exchange == "p2p":
+        # the fused peer-memory exchange over the windows' IPC handles; the context's
+        # NCCL communicator stays as the fallback if the windows cannot be connected
+        try:
+            ctx.use_p2p_exchange()
+        except Exception as e:  # noqa: BLE001 (reported in the JSON line)
+            R.p2p_error = repr(e)
+        R.dist.barrier()
+    elif R.world > 1 and not ctx.has_communicator():
         ctx.use_torch_allgather(host_staged=R.args.exchange == "gloo-host")
     t_gen = 0.0
     for i0, i1 in owned_row_ranges(mds, w.n, R.rank, R.world, 512):
@@ -584,7 +599,11 @@ def run_ours(args):
         par = "single GPU"
     else:
         par = "tile-row shards x %d (rank r owns tile-rows I mod %d == r); exchange: %s" % (
-            world, world, {"nccl": "ncclAllGather of n*d+1 doubles per step by the libmds-owned communicator",
+            world, world, {"p2p": ("fused peer-memory exchange: the pass kernel stores its partial into every "
+                                   "rank's window over NVLink and combines after the flags (one launch per step)"
+                                   if not getattr(R, "p2p_error", None) else
+                                   "ncclAllGather (peer-memory windows failed: %s)" % R.p2p_error),
+                           "nccl": "ncclAllGather of n*d+1 doubles per step by the libmds-owned communicator",
                            "torch": "torch.distributed all_gather_into_tensor (NCCL) callback",
                            "gloo-host": "host-staged gloo all-gather callback (ranks share one GPU)"}[args.exchange])
     out = {
