@@ -57,6 +57,21 @@ def run(n=130, d=2, prec="f64"):
             c.hmc_trajectory(p0, 0.002, 3, prior_sd=5.0)     # EVAL_NOLIK/EVAL + combine_update
             c.set_tree_prior(parent, t)
             c.hmc_trajectory(p0, 0.002, 3)                   # EVAL_NOLIK_TREE / EVAL_TREE
+        # fused peer-memory exchange at world 1 (own window): push, flags, wait,
+        # combine + leapfrog update in the pass kernel (plain launch, own grid barrier),
+        # and the one-CTA peer all-gather of the small exchanges
+        with mds.MDS(n, d, prec) as c:
+            a, _ = c.p2p_window()
+            c.p2p_connect([a])
+            c.set_dissimilarities_packed(y)
+            c.set_locations(w.x0)
+            c.set_sigma(w.sigma)
+            c.log_likelihood_and_gradient()
+            c.log_likelihood_at_sigma(1.1 * w.sigma)
+            c.row_loglik_delta(5, w.x0[5] + 0.1)
+            c.hmc_trajectory(p0, 0.002, 3, prior_sd=5.0)
+            c.set_tree_prior(parent, t)
+            c.hmc_trajectory(p0, 0.002, 3)
 
 
 if __name__ == "__main__":
