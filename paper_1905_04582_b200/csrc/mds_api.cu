@@ -132,6 +132,7 @@ struct mds_ctx_s {
     bool p2p = false;
     unsigned long long p2p_timeout_ns = 60000000000ull;   // MDS_P2P_TIMEOUT_S overrides (tests)
     int grid_limit = 0;              // mds_set_grid_limit (0 = all SMs)
+    bool pdl_ok = std::getenv("MDS_NO_PDL") == nullptr;   // programmatic dependent launch of leapfrog steps
     unsigned* d_gbar = nullptr;      // [2] the pass kernel's software grid barrier
 
     // leapfrog / HMC state
@@ -352,28 +353,52 @@ PassArgs base_args(mds_ctx c, const double* xeval) {
     return a;
 }
 
-mds_status launch_coop(mds_ctx c, PassKernel k, PassArgs& a, cudaStream_t s) {
+mds_status launch_coop(mds_ctx c, PassKernel k, PassArgs& a, cudaStream_t s, bool pdl = false) {
     // the fp64 pass leaves the per-pair constant of Eq. 2 out of its sums (n_obs is
     // counted by ready() whenever Y changed)
     a.lik_const = c->prec == MDS_F64 ? (double)c->n_obs * a.P.k0 : 0.0;
     cudaLaunchConfig_t cfg{};
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeCooperative;
-    attr[0].val.cooperative = 1;
-    cfg.gridDim = dim3((unsigned)c->grid);
-    cfg.blockDim = dim3(32 * k.wpc);
-    cfg.dynamicSmemBytes = k.smem;
-    cfg.stream = s;
-    cfg.attrs = attr;
+    cudaLaunchAttribute attr[2];
+    int na = 0;
     // Contexts on the peer-memory exchange launch WITHOUT the cooperative attribute:
     // with it, a launch blocks the host while another rank's cooperative pass kernel
     // (same process, sharing the GPU) is running -- which waits for this very launch
     // (measured: tools/p2p_dbg.py, 3 ranks).  The grid is still sized by the occupancy
     // API (one CTA per SM), so all CTAs are resident; the kernel then syncs through
     // its own grid barrier (1.5 us slower than grid.sync at C2, so only here).
-    cfg.numAttrs = c->p2p ? 0 : 1;
+    if (!c->p2p) {
+        attr[na].id = cudaLaunchAttributeCooperative;
+        attr[na].val.cooperative = 1;
+        ++na;
+    }
     a.soft_sync = c->p2p ? 1 : 0;
+    // pdl: programmatic dependent launch after the previous leapfrog step's pass on
+    // this stream (its prologue -- barriers, exp table, the first y copies -- overlaps
+    // that grid's phase B; the kernel waits in pdl_wait before touching its results)
+    const bool use_pdl = pdl && c->pdl_ok;
+    if (use_pdl) {
+        attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[na].val.programmaticStreamSerializationAllowed = 1;
+        ++na;
+    }
+    cfg.gridDim = dim3((unsigned)c->grid);
+    cfg.blockDim = dim3(32 * k.wpc);
+    cfg.dynamicSmemBytes = k.smem;
+    cfg.stream = s;
+    cfg.attrs = attr;
+    cfg.numAttrs = na;
     trace(c, "pass launch");
+    if (use_pdl) {
+        const cudaError_t e = cudaLaunchKernelEx(&cfg, k.fn, a);
+        if (e == cudaSuccess) {
+            trace(c, "pass launched");
+            return MDS_OK;
+        }
+        // not supported with this launch configuration: plain stream order from now on
+        cudaGetLastError();
+        c->pdl_ok = false;
+        cfg.numAttrs = na - 1;
+    }
     CK(cudaLaunchKernelEx(&cfg, k.fn, a));
     trace(c, "pass launched");
     return MDS_OK;
@@ -412,7 +437,7 @@ inline bool direct(mds_ctx c) { return c->world == 1 && !c->comm && !c->p2p; }
 // the local partial, the exchange callback and the rank-ordered combine.  In
 // timing mode three events bracket the pass kernel and the post-kernel work.
 mds_status run_pass(mds_ctx c, const double* xeval, double* grad_out, double* lik_out, bool lf, double eps,
-                    double inv_tau2, cudaStream_t s, bool timed, bool want_lik = true) {
+                    double inv_tau2, cudaStream_t s, bool timed, bool want_lik = true, bool pdl = false) {
     NvtxRange nv(lf ? "mds_leapfrog_step" : "mds_pass");
     timed = timed && c->timing;
     const int64_t nd = c->n * c->d;
@@ -444,7 +469,7 @@ mds_status run_pass(mds_ctx c, const double* xeval, double* grad_out, double* li
         const int mode = lf ? (c->tree ? (want_lik ? MODE_LEAPFROG_TREE : MODE_LEAPFROG_NOLIK_TREE)
                                        : (want_lik ? MODE_LEAPFROG : MODE_LEAPFROG_NOLIK))
                             : (want_lik ? MODE_EVAL : MODE_EVAL_NOLIK);
-        st = launch_coop(c, pass_fn_mode(mode, c->prec, c->trunc, c->d), a, s);
+        st = launch_coop(c, pass_fn_mode(mode, c->prec, c->trunc, c->d), a, s, pdl && !timed);
         if (st) return st;
         if (timed) CK(cudaEventRecord(next_event(c), s));
     } else if (c->p2p) {
@@ -455,7 +480,7 @@ mds_status run_pass(mds_ctx c, const double* xeval, double* grad_out, double* li
         a.p2p_lf = lf ? 1 : 0;
         const int mode = (lf && c->tree) ? (want_lik ? MODE_EVAL_TREE : MODE_EVAL_NOLIK_TREE)
                                          : (want_lik ? MODE_EVAL : MODE_EVAL_NOLIK);
-        st = launch_coop(c, pass_fn_mode(mode, c->prec, c->trunc, c->d), a, s);
+        st = launch_coop(c, pass_fn_mode(mode, c->prec, c->trunc, c->d), a, s, pdl && !timed);
         if (st) return st;
         if (timed) CK(cudaEventRecord(next_event(c), s));
     } else {

@@ -82,7 +82,9 @@ mds_status hmc_redrift(mds_ctx c, double eps, cudaStream_t s) {
 // gradient-only pass: nobody reads their log L)
 mds_status hmc_enqueue_steps(mds_ctx c, int L, double eps, double inv_tau2, cudaStream_t s, bool timed) {
     for (int step = 0; step < L; ++step) {
-        mds_status st = run_pass(c, c->d_xnext, c->d_grad, c->d_lik, true, eps, inv_tau2, s, timed, step == L - 1);
+        // steps after the first: programmatic dependent launch on the previous step's pass
+        mds_status st = run_pass(c, c->d_xnext, c->d_grad, c->d_lik, true, eps, inv_tau2, s, timed, step == L - 1,
+                                 step > 0);
         if (st) return st;
     }
     return MDS_OK;

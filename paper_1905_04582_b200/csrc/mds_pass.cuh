@@ -334,6 +334,10 @@ __device__ __forceinline__ bool mbar_ready(uint64_t* b, uint32_t parity) {
     return ok != 0;
 }
 __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+// programmatic dependent launch: wait for the preceding grid of the stream (a no-op
+// when the launch was not programmatic), and let the next grid be scheduled
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
 // per-warp staging area (dynamic shared memory).  One TMA bulk copy per unit
 // brings its UCOLS tile columns of y (NSTAGE-deep ring); x of the tile's 64
@@ -430,11 +434,10 @@ pass_kernel(PassArgs a) {
     if (early_tab) {
         build_exptab(exptab, a.P);
         __syncthreads();
+        pdl_wait();      // (everything below may read the previous step's results)
     }
     if (a.prof && threadIdx.x == 0) a.prof[blockIdx.x * 4 + 0] = gtimer();
-    // the exchange this pass is (all CTAs read it before any can advance it, at the end)
     const bool p2p = !LF && a.p2p.win != nullptr;
-    const unsigned long long p2p_ep = p2p ? p2p_epoch(a.p2p) : 0ull;
     A lik_w = A(0);
     A lacc[4] = {A(0), A(0), A(0), A(0)};   // fp64: running log L sums by lock-step position
 
@@ -526,10 +529,12 @@ pass_kernel(PassArgs a) {
 #endif
         const int fc4b = max(W.seg[0].y - GPU * ub, 0), fc4e = min(W.seg[0].z - GPU * ub, GPU);
         const int fst = ist;                     // the first unit's stage
-        auto issue_group = [&](int g, bool with_x) {
+        // xmode: 0 = y only, 1 = y and the tile's x, 2 = y now, x later (counted now)
+        auto issue_group = [&](int g, int xmode) {
+            const bool with_x = xmode == 1;
             const int t = ub / UNITS_PER_TILE, jj0 = (ub % UNITS_PER_TILE) * UCOLS;
             constexpr uint32_t GB = 4 * TB * sizeof(T);
-            mbar_arrive_tx(&W.bar0[g], GB + (with_x ? XB : 0));
+            mbar_arrive_tx(&W.bar0[g], GB + (xmode ? XB : 0));
 #ifndef MDS_Y_NO_EVICT_FIRST
             bulk_g2s_hint(W.y[fst] + 4 * g * TB, Y + (size_t)t * TB * TB + (size_t)(jj0 + 4 * g) * TB, GB,
                           &W.bar0[g], ypol);
@@ -539,9 +544,12 @@ pass_kernel(PassArgs a) {
             if (with_x) bulk_g2s(W.xcol[t & 1], X + (size_t)(t - itb) * TB * D, XB, &W.bar0[g]);
         };
 #ifndef MDS_EXP_NO_TMA
+        // the first group's x (the previous step's drift) is issued after pdl_wait below;
+        // its y (constant) goes out now, overlapping the previous grid's tail
+        const bool defer_x = first_pending && !early_tab && vv == 0;
         if (nsw > 0) {
             if (first_pending) {
-                if (lane == 0) issue_group(fc4b, true);
+                if (lane == 0) issue_group(fc4b, defer_x ? 2 : 1);
                 ++iu;
                 ist = (ist + 1 == NSTAGE) ? 0 : ist + 1;
             } else {
@@ -553,6 +561,10 @@ pass_kernel(PassArgs a) {
         if (!early_tab && vv == 0) {          // (uniform: every warp runs range 0)
             build_exptab(exptab, a.P);
             __syncthreads();
+            pdl_wait();
+            if (defer_x && nsw > 0 && lane == 0)
+                bulk_g2s(W.xcol[(ub / UNITS_PER_TILE) & 1], X + (size_t)(ub / UNITS_PER_TILE - W.seg[0].w) * TB * D,
+                         XB, &W.bar0[fc4b]);
         }
 #pragma unroll 1
         for (int si = 0; si < nsw; ++si) {
@@ -603,7 +615,7 @@ pass_kernel(PassArgs a) {
 #endif
                 const int t = u / UNITS_PER_TILE, jb = (u % UNITS_PER_TILE) * UCOLS;
                 const int cpos = __ldg(a.slab_pos + a.nseg + t);    // used after the groups' math
-#pragma unroll 1
+#pragma unroll 1      // (unroll 2 measured: 168 regs + spills, 219 -> 154 G pair-evals/s)
                 for (int c4 = c4b; c4 < c4e; ++c4) {       // 4-column reduce groups of the unit
 #ifndef MDS_EXP_NO_TMA
                 if (fu) {
@@ -616,7 +628,7 @@ pass_kernel(PassArgs a) {
                         __syncwarp();
                         // the first group has landed: fetch the rest of the unit and the next unit
                         if (lane == 0)
-                            for (int g = c4b + 1; g < c4e; ++g) issue_group(g, false);
+                            for (int g = c4b + 1; g < c4e; ++g) issue_group(g, 0);
                         if (iu < ue) issue_one();
                         cvt_xcol();                   // the tile's x came with the first group
                     }
@@ -766,6 +778,10 @@ pass_kernel(PassArgs a) {
     __threadfence();
     if (a.soft_sync) grid_barrier(a.gbar, gridDim.x);   // plain launch (peer-memory exchange)
     else cg::this_grid().sync();
+    pdl_launch_dependents();     // the next leapfrog step's grid may be scheduled (it waits in pdl_wait)
+    // the exchange this pass is: read after pdl_wait (the previous pass advances it at
+    // its very end) and before any CTA can advance it (at the end of this one)
+    const unsigned long long p2p_ep = p2p ? p2p_epoch(a.p2p) : 0ull;
     if (a.prof && threadIdx.x == 0) a.prof[blockIdx.x * 4 + 2] = gtimer();
 
     // ------------------------------------------------------------ phase B
