@@ -229,12 +229,18 @@ mds_status mds_p2p_window(mds_ctx ctx, void **window_dev, void *ipc_handle_out);
  * store to (the same process; peer access is enabled when the windows live on
  * other devices).  From then on every sharded exchange of the context goes
  * through peer memory.  Collective in effect: all ranks must connect before
- * any of them evaluates. */
+ * any of them evaluates.  Ends with a handshake (one peer all-gather of the rank
+ * ids, at most 30 s): MDS_E_COMM if it fails, the context then stays on its other
+ * exchange. */
 mds_status mds_p2p_connect(mds_ctx ctx, void *const *peer_window_dev);
 /* The same from ipc_handles[world][MDS_IPC_HANDLE_BYTES] (rank order, e.g.
  * all-gathered through torch.distributed): peers' handles are opened
  * (cudaIpcOpenMemHandle, lazy peer access) and closed by mds_destroy. */
 mds_status mds_p2p_connect_ipc(mds_ctx ctx, const void *ipc_handles);
+/* Leave the peer-memory exchange (the context's NCCL communicator or callback,
+ * if any, is used again).  All ranks must do the same, e.g. when one rank's
+ * mds_p2p_connect failed. */
+mds_status mds_p2p_disconnect(mds_ctx ctx);
 /* *connected = 1 when the context exchanges through peer memory. */
 mds_status mds_p2p_connected(mds_ctx ctx, int32_t *connected);
 

@@ -254,8 +254,17 @@ class MDS:
         _, h = self.p2p_window()
         hs = [None] * self.world
         dist.all_gather_object(hs, h, group=group)
-        _abi.mds_p2p_connect_ipc(self.ctx, hs)
-        dist.barrier(group=group)
+        err = None
+        try:
+            _abi.mds_p2p_connect_ipc(self.ctx, hs)
+        except MDSError as e:           # (its handshake failed: the context stays on its other exchange)
+            err = e
+        oks = [None] * self.world
+        dist.all_gather_object(oks, err is None, group=group)
+        if not all(oks):                # every rank leaves together, or none would match
+            if err is None:
+                _abi.mds_p2p_disconnect(self.ctx)
+            raise err or MDSError(5, "peer-memory exchange: another rank's handshake failed")
 
     def p2p_connected(self) -> bool:
         return _abi.mds_p2p_connected(self.ctx)

@@ -29,7 +29,8 @@ EXPORTS = [
     "mds_observed_pairs", "mds_zero_distance_pairs", "mds_set_timing", "mds_last_timing",
     "mds_hmc_trajectory", "mds_hmc_run", "mds_leapfrog_device", "mds_get_locations", "mds_get_momentum",
     "mds_set_allgather", "mds_plan",
-    "mds_p2p_window", "mds_p2p_connect", "mds_p2p_connect_ipc", "mds_p2p_connected", "mds_set_grid_limit",
+    "mds_p2p_window", "mds_p2p_connect", "mds_p2p_connect_ipc", "mds_p2p_disconnect", "mds_p2p_connected",
+    "mds_set_grid_limit",
     "mds_log_likelihood_at_sigma", "mds_sigma_mh_step", "mds_mcmc_run", "mds_row_loglik_delta", "mds_rw_sweep",
     "mds_cv_set_heldout", "mds_cv_accumulate", "mds_cv_lpd", "mds_set_tree_prior", "mds_tree_prior",
     "mds_last_error", "mds_status_string", "mds_version", "mds_device_info", "mds_measure_fma_peaks", "mds_l2_flush", "mds_l2_flush_clean",
@@ -111,6 +112,7 @@ def _load():
         "mds_p2p_connect": [vp, P(vp)],
         "mds_p2p_connect_ipc": [vp, vp],
         "mds_p2p_connected": [vp, P(i32)],
+        "mds_p2p_disconnect": [vp],
         "mds_set_grid_limit": [vp, i32],
         "mds_plan": [i64, i32, i32, i32, i32, P(PlanInfo), vp],
         "mds_device_info": [P(i32), P(i32), P(i32)],
@@ -338,6 +340,10 @@ def mds_p2p_connect_ipc(ctx, handles):
     """handles: the world's IPC handle bytes (MDS_IPC_HANDLE_BYTES each), rank order."""
     buf = ctypes.create_string_buffer(b"".join(bytes(h) for h in handles))
     _check(lib.mds_p2p_connect_ipc(ctx, buf), ctx)
+
+
+def mds_p2p_disconnect(ctx):
+    _check(lib.mds_p2p_disconnect(ctx), ctx)
 
 
 def mds_p2p_connected(ctx) -> bool:

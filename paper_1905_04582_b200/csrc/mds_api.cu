@@ -1873,6 +1873,20 @@ mds_status mds_p2p_window(mds_ctx c, void** window_dev, void* ipc_handle_out) {
         CK(cudaHostAlloc((void**)&c->h_p2p_err, sizeof(int), cudaHostAllocMapped));
         *c->h_p2p_err = 0;
         CK(cudaHostGetDevicePointer((void**)&c->d_p2p_err, c->h_p2p_err, 0));
+        // everything a sharded call would load or allocate lazily, now, before any rank
+        // can be waiting in an exchange: a kernel's first launch (lazy module loading)
+        // and a first cudaMalloc can wait for the whole device (ranks sharing one GPU
+        // would deadlock; profiles/r02/p2p_probes.md)
+        preload_kernels(c);
+        if (const char* e = std::getenv("MDS_P2P_TIMEOUT_S")) {
+            const double v = std::atof(e);
+            if (v > 0) c->p2p_timeout_ns = (unsigned long long)(v * 1e9);
+        }
+        if ((st = rw_scratch(c, 3 * sizeof(double) * 8)) || (st = hmc_alloc(c))) return st;
+        if (!c->h_pbuf && cudaMallocHost(&c->h_pbuf, (size_t)(c->n * c->d) * sizeof(double)) != cudaSuccess) {
+            cudaGetLastError();
+            c->h_pbuf = nullptr;
+        }
         CKS(c->stream);
     }
     if (window_dev) *window_dev = c->d_win;
@@ -1913,22 +1927,40 @@ mds_status mds_p2p_connect(mds_ctx c, void* const* peer_window_dev) {
     }
     CK(cudaMemcpyAsync(c->d_peer_win, peer_window_dev, c->world * sizeof(char*), cudaMemcpyHostToDevice, c->stream));
     CKS(c->stream);
-    // everything a sharded call allocates lazily, now: a first cudaMalloc can wait for
-    // the device too (ranks sharing one GPU: the same deadlock as lazy loading)
-    preload_kernels(c);
-    if (const char* e = std::getenv("MDS_P2P_TIMEOUT_S")) {
-        const double v = std::atof(e);
-        if (v > 0) c->p2p_timeout_ns = (unsigned long long)(v * 1e9);
-    }
-    mds_status st = rw_scratch(c, 3 * sizeof(double) * 8);
-    if (!st) st = hmc_alloc(c);
-    if (st) return st;
-    if (!c->h_pbuf && cudaMallocHost(&c->h_pbuf, (size_t)(c->n * c->d) * sizeof(double)) != cudaSuccess) {
-        cudaGetLastError();
-        c->h_pbuf = nullptr;
-    }
-    CKS(c->stream);
     c->p2p = true;
+    // handshake: one peer all-gather of (rank + 1) through the windows, checked on the
+    // host, with a 30 s wait at most -- a broken path (IPC mapping, peer access) fails
+    // here with MDS_E_COMM instead of inside a pass
+    {
+        const unsigned long long keep = c->p2p_timeout_ns;
+        c->p2p_timeout_ns = std::min<unsigned long long>(keep, 30000000000ull);
+        double* send = c->d_partial;
+        double* recv = c->d_gathered;
+        const double me = (double)(c->rank + 1);
+        CK(cudaMemcpyAsync(send, &me, sizeof(double), cudaMemcpyHostToDevice, c->stream));
+        p2p_allgather_kernel<<<1, 32, 0, c->stream>>>(p2p_args(c), send, 1, recv);
+        CK(cudaGetLastError());
+        std::vector<double> got(c->world, 0.0);
+        CK(cudaMemcpyAsync(got.data(), recv, c->world * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+        const cudaError_t e = cudaStreamSynchronize(c->stream);
+        c->p2p_timeout_ns = keep;
+        bool ok = e == cudaSuccess && !*(volatile int*)c->h_p2p_err;
+        for (int r = 0; ok && r < c->world; ++r) ok = got[r] == (double)(r + 1);
+        if (!ok) {
+            c->p2p = false;
+            *c->h_p2p_err = 0;
+            if (e != cudaSuccess) return fail(c, MDS_E_CUDA, std::string("peer handshake: ") + cudaGetErrorString(e));
+            return fail(c, MDS_E_COMM, "peer-memory handshake failed (a peer did not answer, or its window is not "
+                                       "this rank's view of it); the context keeps its other exchange");
+        }
+    }
+    return MDS_OK;
+}
+
+mds_status mds_p2p_disconnect(mds_ctx c) {
+    GUARD(c);
+    CKS(c->stream);
+    c->p2p = false;
     return MDS_OK;
 }
 
