@@ -1749,6 +1749,7 @@ SigmaParams sigma_params(double sigma) {
     P.half_inv_sigma2_f = (float)P.half_inv_sigma2;
     P.k0_f = (float)P.k0;
     P.cg_f = (float)P.cg;
+    P.ex2_slope_f = (float)(-1.4426950408889634 * P.half_inv_sigma2);
     return P;
 }
 }  // namespace
@@ -1882,7 +1883,9 @@ mds_status mds_p2p_window(mds_ctx c, void** window_dev, void* ipc_handle_out) {
             const double v = std::atof(e);
             if (v > 0) c->p2p_timeout_ns = (unsigned long long)(v * 1e9);
         }
-        if ((st = rw_scratch(c, 3 * sizeof(double) * 8)) || (st = hmc_alloc(c))) return st;
+        if ((st = rw_scratch(c, 3 * sizeof(double) * 8)) || (st = hmc_alloc(c)) ||
+            (st = dalloc(c, &c->d_peer_win, (size_t)c->world)))
+            return st;
         if (!c->h_pbuf && cudaMallocHost(&c->h_pbuf, (size_t)(c->n * c->d) * sizeof(double)) != cudaSuccess) {
             cudaGetLastError();
             c->h_pbuf = nullptr;
@@ -1921,10 +1924,7 @@ mds_status mds_p2p_connect(mds_ctx c, void* const* peer_window_dev) {
             else CK(e);
         }
     }
-    if (!c->d_peer_win) {
-        mds_status st = dalloc(c, &c->d_peer_win, (size_t)c->world);
-        if (st) return st;
-    }
+    if (!c->d_peer_win) return fail(c, MDS_E_STATE, "mds_p2p_connect: call mds_p2p_window first");
     CK(cudaMemcpyAsync(c->d_peer_win, peer_window_dev, c->world * sizeof(char*), cudaMemcpyHostToDevice, c->stream));
     CKS(c->stream);
     c->p2p = true;
@@ -1944,14 +1944,20 @@ mds_status mds_p2p_connect(mds_ctx c, void* const* peer_window_dev) {
         CK(cudaMemcpyAsync(got.data(), recv, c->world * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
         const cudaError_t e = cudaStreamSynchronize(c->stream);
         c->p2p_timeout_ns = keep;
-        bool ok = e == cudaSuccess && !*(volatile int*)c->h_p2p_err;
-        for (int r = 0; ok && r < c->world; ++r) ok = got[r] == (double)(r + 1);
+        const bool timed_out = *(volatile int*)c->h_p2p_err != 0;
+        bool ok = e == cudaSuccess && !timed_out;
+        std::string seen;
+        for (int r = 0; r < c->world; ++r) {
+            ok = ok && got[r] == (double)(r + 1);
+            seen += (r ? " " : "") + std::to_string(got[r]);
+        }
         if (!ok) {
             c->p2p = false;
             *c->h_p2p_err = 0;
             if (e != cudaSuccess) return fail(c, MDS_E_CUDA, std::string("peer handshake: ") + cudaGetErrorString(e));
-            return fail(c, MDS_E_COMM, "peer-memory handshake failed (a peer did not answer, or its window is not "
-                                       "this rank's view of it); the context keeps its other exchange");
+            return fail(c, MDS_E_COMM, std::string("peer-memory handshake failed (") +
+                                           (timed_out ? "a peer did not answer in time" : "wrong values") +
+                                           "; rank slots read: " + seen + "); the context keeps its other exchange");
         }
     }
     return MDS_OK;

@@ -14,7 +14,11 @@ PassKernel pass_fn_d(int d) {
 #ifdef MDS_AB_D2ONLY
     // A/B builds: only D = 2 is instantiated (fast compile; other d are not valid)
     (void)d;
+#ifdef MDS_AB_D6
+    return pk<T, TR, MODE, 6>();
+#else
     return pk<T, TR, MODE, 2>();
+#endif
 #else
     switch (d) {
         case 1: return pk<T, TR, MODE, 1>();
