@@ -173,7 +173,12 @@ def sass_counts(prec: str, d: int, mode: int = 2) -> dict | None:
     try:
         tab = json.load(open(path))
         key = "%s_d%d_t1" % (prec, d) if mode == 2 else "%s_d%d_t1_m%d" % (prec, d, mode)
-        return tab[key]
+        # fp64: the rotation-mode loop (every unit but a warp range's first and last) is the
+        # one that runs; the libmds.so loop's static count also holds the group mode's code
+        r = dict(tab[key + "_rot"]) if key + "_rot" in tab else dict(tab[key])
+        r["count_source"] = ("static SASS count of the rotation-mode loop (MDS_ROT_ALWAYS build, "
+                             "tools/count_sass.py)" if key + "_rot" in tab else "static SASS count of the loop")
+        return r
     except Exception:
         return None
 
@@ -473,6 +478,7 @@ def roofline_of(prec, d, pairs_per_launch, kern_ms, clk_mhz, traffic, cfg=None):
           "traffic": traffic,
           "kernel": "pass_kernel<%s,D=%d,T=1,LEAPFROG>" % (prec, d),
           "ops_per_pair": ipp, "issued_per_pair": sc.get("issued_per_pair"),
+          "ops_source": sc.get("count_source"),
           "pass_kernel_ms": kern_ms,
           "peak_source": src,
           "hbm_gbs": bpp * pairs_per_launch / (kern_ms * 1e-3) / 1e9,

@@ -615,45 +615,34 @@ pass_kernel(PassArgs a) {
 #endif
                 const int t = u / UNITS_PER_TILE, jb = (u % UNITS_PER_TILE) * UCOLS;
                 const int cpos = __ldg(a.slab_pos + a.nseg + t);    // used after the groups' math
-#pragma unroll 1      // (unroll 2 measured: 168 regs + spills, 219 -> 154 G pair-evals/s)
-                for (int c4 = c4b; c4 < c4e; ++c4) {       // 4-column reduce groups of the unit
-#ifndef MDS_EXP_NO_TMA
-                if (fu) {
-                    mbar_wait(&W.bar0[c4], 0);
-                    if (c4 == c4b) {
-                        if (a.prof && threadIdx.x == 0) {
-                            a.prof[gridDim.x * 6 + blockIdx.x] = gtimer();
-                            not_ready |= 0x80000000u;
-                        }
-                        __syncwarp();
-                        // the first group has landed: fetch the rest of the unit and the next unit
-                        if (lane == 0)
-                            for (int g = c4b + 1; g < c4e; ++g) issue_group(g, 0);
-                        if (iu < ue) issue_one();
-                        cvt_xcol();                   // the tile's x came with the first group
-                    }
-                }
-#endif
-                const int jj0 = jb + 4 * c4;
-                const T* __restrict__ yst = W.y[cst] + 4 * c4 * TB;
-                const T* __restrict__ xc;
-                if constexpr (sizeof(T) == 4) xc = &W.xcolf[t & 1][jj0 * D];
-                else xc = W.xcol[t & 1] + jj0 * D;
-                T cv[4][D];
-#pragma unroll
-                for (int h = 0; h < 2; ++h) {         // positions 2h, 2h+1: 4 pairs per lane in lock-step
+                // One lock-step block: 4 pairs per lane -- rows lane and lane+32 against the
+                // columns qa and qb of yb/xb (per-lane column indices) -- with the Eq. 2 terms
+                // into the running sums, the row sums by fused multiply-adds, and the column
+                // side into ca/cb: fresh 2-row sums (group path) or accumulated (ACC).
+                auto block4 = [&](const T* __restrict__ yb, const T* __restrict__ xb, int qa, int qb,
+                                  T (&ca)[D], T (&cb)[D], auto acc_tag) {
+                    constexpr bool ACC = decltype(acc_tag)::value;
                     T ys[4], ss[4], dd[4][D];
 #pragma unroll
                     for (int qq = 0; qq < 2; ++qq) {
-                        const int q = (2 * h + qq) ^ m;   // column of position 2h + qq
-                        ys[2 * qq] = yst[q * TB + lane_v];
-                        ys[2 * qq + 1] = yst[q * TB + lane_v + 32];
+                        const int q = qq ? qb : qa;
+                        ys[2 * qq] = yb[q * TB + lane_v];
+                        ys[2 * qq + 1] = yb[q * TB + lane_v + 32];
+                        T xj[D];
+                        if constexpr (D == 2 && sizeof(T) == 8 && ACC) {
+                            // per-lane columns: one 16-byte load (conflict-free per quarter warp)
+                            const double2 v = *reinterpret_cast<const double2*>(xb + q * 2);
+                            xj[0] = v.x;
+                            xj[1] = v.y;
+                        } else {
+#pragma unroll
+                            for (int k = 0; k < D; ++k) xj[k] = (T)xb[q * D + k];
+                        }
                         T sa = T(0), sb = T(0);
 #pragma unroll
                         for (int k = 0; k < D; ++k) {
-                            const T xjk = (T)xc[q * D + k];
-                            dd[2 * qq][k] = xi0[k] - xjk;
-                            dd[2 * qq + 1][k] = xi1[k] - xjk;
+                            dd[2 * qq][k] = xi0[k] - xj[k];
+                            dd[2 * qq + 1][k] = xi1[k] - xj[k];
                             sa = fma(dd[2 * qq][k], dd[2 * qq][k], sa);
                             sb = fma(dd[2 * qq + 1][k], dd[2 * qq + 1][k], sb);
                         }
@@ -677,15 +666,13 @@ pass_kernel(PassArgs a) {
                         }
                         if (WG) {
                             // pair (row r, column c) adds -u (x_r - x_c) to row r and +u (x_r - x_c)
-                            // to column c: rows by fused multiply-adds, columns as one product + one fma
+                            // to column c: rows by fused multiply-adds
 #pragma unroll
                             for (int k = 0; k < D; ++k) {
                                 g0[k] = fma(-uu[0], dd[0][k], g0[k]);
                                 g0[k] = fma(-uu[2], dd[2][k], g0[k]);
                                 g1[k] = fma(-uu[1], dd[1][k], g1[k]);
                                 g1[k] = fma(-uu[3], dd[3][k], g1[k]);
-                                cv[2 * h][k] = fma(uu[0], dd[0][k], uu[1] * dd[1][k]);
-                                cv[2 * h + 1][k] = fma(uu[2], dd[2][k], uu[3] * dd[3][k]);
                             }
                         }
                     } else {
@@ -704,30 +691,129 @@ pass_kernel(PassArgs a) {
                                 gf0[k] = fmaf(-uu[2], dd[2][k], gf0[k]);
                                 gf1[k] = fmaf(-uu[1], dd[1][k], gf1[k]);
                                 gf1[k] = fmaf(-uu[3], dd[3][k], gf1[k]);
-                                cv[2 * h][k] = fmaf(uu[0], dd[0][k], uu[1] * dd[1][k]);
-                                cv[2 * h + 1][k] = fmaf(uu[2], dd[2][k], uu[3] * dd[3][k]);
                             }
                         }
                         if (WL) lsu += lsum;
                     }
-                }
-                double* __restrict__ cslab = a.slabs + (size_t)cpos * TB * D + (size_t)jj0 * D;
-#ifndef MDS_EXP_NO_COLRED
+                    if (WG) {
 #pragma unroll
-                for (int k = 0; k < (WG ? D : 0); ++k) {
-                    const T cs = reduce_scatter4_perm(cv[0][k], cv[1][k], cv[2][k], cv[3][k]);
-#ifndef MDS_EXP_NO_CSTORE
-                    if ((lane & 7) == 0) cslab[m * D + k] = A(cs);
+                        for (int k = 0; k < D; ++k) {
+                            if constexpr (ACC) {
+                                ca[k] = fma(uu[1], dd[1][k], fma(uu[0], dd[0][k], ca[k]));
+                                cb[k] = fma(uu[3], dd[3][k], fma(uu[2], dd[2][k], cb[k]));
+                            } else {
+                                ca[k] = fma(uu[0], dd[0][k], uu[1] * dd[1][k]);
+                                cb[k] = fma(uu[2], dd[2][k], uu[3] * dd[3][k]);
+                            }
+                        }
+                    }
+                };
+                // Two ways through a unit, one copy of the pair math (ptxas keeps the
+                // coefficients in uniform registers only with one copy):
+                //  * group mode (a warp range's first and last unit, and the staggered first
+                //    unit): per 4-column group, a 2-row sum per column and a select-free
+                //    reduce-scatter over the 32 lanes (the column order p ^ m, see m);
+                //  * rotation mode (every other unit): rotating column accumulators.  Lanes
+                //    form groups of UCOLS; at step s lane L takes column (L + s) mod UCOLS of
+                //    the unit (rows L and L+32), four steps per trip (two lock-step blocks),
+                //    each step of the trip with its own accumulator; at the end of the trip
+                //    all four move 4 lanes down the lane group, so each follows its column
+                //    across the group.  A column's sum is then one fused multiply-add per
+                //    pair plus, once per unit, 3 + log2(32 / UCOLS) adds, instead of a 2-row
+                //    sum and a reduce-scatter (6 adds per 8 pairs) per 4 columns.
+                // Fixed order either way: deterministic.
+                // (fp64 only: the fp32 pass at D = 6 spills with the four D-sized accumulators
+                // at 128 registers -- N = 30000 A/B 322.9 -> 287.8 G pair-evals/s; fp64 D = 2:
+                // 217.0 -> 223.3 G, N = 5392: 181.8 -> 186.5 G)
+#if defined(MDS_ROT_ALWAYS)
+                constexpr bool rot = sizeof(T) == 8;   // (count_sass.py: the rotation-mode loop alone)
+#elif !defined(MDS_NO_ROT)
+                const bool rot = sizeof(T) == 8 &&
+                                 __all_sync(0xffffffffu, !fu && c4b == 0 && c4e == GPU);   // (a vote: warp-uniform to ptxas)
 #else
-                    lik_w += A(cs);
+                constexpr bool rot = false;
 #endif
-                }
-#else
+                const int lr = lane_v & (UCOLS - 1);
+                const T* __restrict__ yu = W.y[cst];
+                const T* __restrict__ xu;
+                if constexpr (sizeof(T) == 4) xu = &W.xcolf[t & 1][jb * D];
+                else xu = W.xcol[t & 1] + jb * D;
+                T cv[4][D];
 #pragma unroll
-                for (int k = 0; k < D; ++k) lik_w += A(cv[0][k] + cv[1][k] + cv[2][k] + cv[3][k]);
-                (void)cslab;
+                for (int p = 0; p < 4; ++p)
+#pragma unroll
+                    for (int k = 0; k < D; ++k) cv[p][k] = T(0);
+                const int it_b = rot ? 0 : c4b, it_e = rot ? GPU : c4e;
+#pragma unroll 1      // (unroll 2 measured: 168 regs + spills, 219 -> 154 G pair-evals/s)
+                for (int c4 = it_b; c4 < it_e; ++c4) {     // 8 pairs per lane: a 4-column group / 4 steps
+#ifndef MDS_EXP_NO_TMA
+                if (fu) {
+                    mbar_wait(&W.bar0[c4], 0);
+                    if (c4 == c4b) {
+                        if (a.prof && threadIdx.x == 0) {
+                            a.prof[gridDim.x * 6 + blockIdx.x] = gtimer();
+                            not_ready |= 0x80000000u;
+                        }
+                        __syncwarp();
+                        // the first group has landed: fetch the rest of the unit and the next unit
+                        if (lane == 0)
+                            for (int g = c4b + 1; g < c4e; ++g) issue_group(g, 0);
+                        if (iu < ue) issue_one();
+                        cvt_xcol();                   // the tile's x came with the first group
+                    }
+                }
 #endif
-                }   // 4-column groups
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {         // positions 2h, 2h+1: 4 pairs per lane in lock-step
+                    int qa, qb;
+                    if (rot) {
+                        qa = (lr + 4 * c4 + 2 * h) & (UCOLS - 1);
+                        qb = (lr + 4 * c4 + 2 * h + 1) & (UCOLS - 1);
+                    } else {
+                        qa = 4 * c4 + ((2 * h) ^ m);
+                        qb = 4 * c4 + ((2 * h + 1) ^ m);
+                    }
+                    block4(yu, xu, qa, qb, cv[2 * h], cv[2 * h + 1], std::true_type());
+                }
+                // (the exchanges sit at the end of the trip, after both blocks' math: a
+                // shuffle between the blocks made ptxas keep the polynomial coefficients in
+                // vector registers instead of uniform ones -- 168 registers and spills)
+                if (rot) {
+                    // every accumulator moves 4 lanes down its lane group (step s's accumulator
+                    // follows its column: lane L + 4 takes it over at step s + 4)
+#pragma unroll
+                    for (int p = 0; p < 4; ++p)
+#pragma unroll
+                        for (int k = 0; k < (WG ? D : 0); ++k)
+                            cv[p][k] = __shfl_sync(0xffffffffu, cv[p][k], lane_v + 4, UCOLS);
+                } else {
+                    double* __restrict__ cslab = a.slabs + (size_t)cpos * TB * D + (size_t)(jb + 4 * c4) * D;
+#pragma unroll
+                    for (int k = 0; k < (WG ? D : 0); ++k) {
+                        const T cs = reduce_scatter4_perm(cv[0][k], cv[1][k], cv[2][k], cv[3][k]);
+                        if ((lane & 7) == 0) cslab[m * D + k] = A(cs);
+                    }
+#pragma unroll
+                    for (int p = 0; p < 4; ++p)
+#pragma unroll
+                        for (int k = 0; k < D; ++k) cv[p][k] = T(0);
+                }
+                }   // 4-column groups / steps
+                if (rot) {
+                    // after the last trip's move, accumulator p of lane L holds (its share of)
+                    // column L + p mod UCOLS: lane L sums column L from lanes L, L-1, L-2, L-3,
+                    // then over the lane groups
+                    double* __restrict__ cslab = a.slabs + (size_t)cpos * TB * D + (size_t)jb * D;
+#pragma unroll
+                    for (int k = 0; k < (WG ? D : 0); ++k) {
+                        T cs = cv[0][k];
+#pragma unroll
+                        for (int p = 1; p < 4; ++p) cs += __shfl_sync(0xffffffffu, cv[p][k], lane_v + UCOLS - p, UCOLS);
+#pragma unroll
+                        for (int o = UCOLS; o < 32; o <<= 1) cs += shfl_xor(cs, o);
+                        if (lane_v < UCOLS) cslab[lr * D + k] = A(cs);
+                    }
+                }
                 if constexpr (sizeof(T) == 4) {       // at most 16 columns x 2 terms in fp32 (reading R15)
                     if (WG) {
 #pragma unroll

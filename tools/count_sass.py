@@ -17,14 +17,27 @@ LIB = os.path.join(ROOT, "paper_1905_04582_b200", "libmds.so")
 OUT = os.path.join(ROOT, "profiles", "sass_counts.json")
 
 FP64 = {"DFMA", "DMUL", "DADD", "DSETP", "DMNMX"}
+CSRC = os.path.join(ROOT, "paper_1905_04582_b200", "csrc")
 FP32 = {"FFMA", "FMUL", "FADD", "FSETP", "FMNMX", "FSEL"}
+
+
+def rotation_only_sass():
+    """fp64 LEAPFROG pass kernels (mode 2) built with MDS_ROT_ALWAYS: the loop of the
+    rotation mode alone, which runs every unit but a warp range's first and last (the
+    libmds.so loop also holds the group mode's reduce-scatter, executed at those two)."""
+    obj = "/tmp/mds_count_rot_m2_f64.o"
+    subprocess.check_call(["nvcc", "-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a",
+                           "-I", os.path.join(ROOT, "include"), "-DMDS_ROT_ALWAYS", "-c", "-o", obj,
+                           os.path.join(CSRC, "pass_m2_f64.cu")])
+    return subprocess.check_output(["cuobjdump", "-sass", obj], text=True)
 
 
 def main():
     sass = subprocess.check_output(["cuobjdump", "-sass", LIB], text=True)
-    funcs = re.split(r"\n\s+Function : ", sass)
+    funcs = [("", f) for f in re.split(r"\n\s+Function : ", sass)[1:]]
+    funcs += [("_rot", f) for f in re.split(r"\n\s+Function : ", rotation_only_sass())[1:]]
     res = {}
-    for f in funcs[1:]:
+    for tag, f in funcs:
         name = f.split("\n", 1)[0].strip()
         m = re.match(r"_ZN4mdsk11pass_kernelI([fd])Li(\d)ELb([01])ELi(\d)EEEvNS_8PassArgsE", name)
         if not m:
@@ -61,7 +74,7 @@ def main():
         nmufu = sum(o == "MUFU" for o in ops)
         # key: <prec>_d<D>_t<T> for the leapfrog pass (mode 2, the bench kernel),
         # + "_m<mode>" for the other modes (mds_pass.cuh "Mode")
-        key = "%s_d%d_t%d" % (prec, d, t) + ("" if mode == 2 else "_m%d" % mode)
+        key = "%s_d%d_t%d" % (prec, d, t) + ("" if mode == 2 else "_m%d" % mode) + tag
         res[key] = {
             "kernel": name, "loop_instructions": len(ops),
             "pairs_per_trip": npairs,
