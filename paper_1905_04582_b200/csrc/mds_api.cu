@@ -183,7 +183,7 @@ struct mds_ctx_s {
     double* d_logprior = nullptr;    // [2]: log prior there, saved copy
     unsigned int* d_tips_done = nullptr;   // pass kernel: pair CTAs that finished their tips slice
 
-    double* h_pbuf = nullptr;        // pinned momentum staging of the HMC driver (n*d, allocated once)
+    double* h_pbuf = nullptr;        // pinned momentum staging of the HMC driver (2 x n*d + H0, H1; allocated once)
     double* h_xstage = nullptr;      // pinned staging of mds_set_locations (asynchronous upload)
     cudaEvent_t xstage_done = nullptr;
 
@@ -1886,7 +1886,7 @@ mds_status mds_p2p_window(mds_ctx c, void** window_dev, void* ipc_handle_out) {
         if ((st = rw_scratch(c, 3 * sizeof(double) * 8)) || (st = hmc_alloc(c)) ||
             (st = dalloc(c, &c->d_peer_win, (size_t)c->world)))
             return st;
-        if (!c->h_pbuf && cudaMallocHost(&c->h_pbuf, (size_t)(c->n * c->d) * sizeof(double)) != cudaSuccess) {
+        if (!c->h_pbuf && cudaMallocHost(&c->h_pbuf, (2 * (size_t)(c->n * c->d) + 2) * sizeof(double)) != cudaSuccess) {
             cudaGetLastError();
             c->h_pbuf = nullptr;
         }

@@ -107,8 +107,9 @@ struct HmcSession {
     cudaStream_t s = nullptr;
     bool owned = false;                 // stream created here (the context had the legacy stream)
     cudaGraphExec_t exec = nullptr;
-    double* pbuf = nullptr;             // pinned momentum staging (or the vector below)
+    double* pbuf = nullptr;             // pinned momentum staging, two halves of n*d (or the vector below)
     bool pinned = false;
+    int64_t ready_it = -1;              // transition whose momenta already sit in pbuf[ready_it & 1]
     std::vector<double> pvec;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     int L = 1;
@@ -137,6 +138,7 @@ void hmc_session_end(HmcSession& S) {
 mds_status hmc_session_capture(mds_ctx c, HmcSession& S) {
     NvtxRange nv("mds_hmc_capture");
     if (!graph_capturable(c)) return MDS_OK;      // host-callback exchange: direct launches
+    if (std::getenv("MDS_NO_HMC_GRAPH")) return MDS_OK;   // (A/B: direct launches)
     cudaGraph_t graph = nullptr;
     CK(cudaStreamBeginCapture(S.s, cudaStreamCaptureModeThreadLocal));
     mds_status st = hmc_enqueue_steps(c, S.L, S.eps, S.it2, S.s, false);
@@ -174,13 +176,15 @@ mds_status hmc_session_begin(mds_ctx c, const mds_hmc_config* cfg, HmcSession& S
     S.eps = cfg->step_size;
     S.it2 = inv_tau2_of(c, cfg);
     const size_t m = (size_t)(c->n * c->d);
-    if (!c->h_pbuf && cudaMallocHost(&c->h_pbuf, m * sizeof(double)) != cudaSuccess) c->h_pbuf = nullptr;
+    // two momentum halves + H0, H1 (pinned: the D2H copies of the energies must not
+    // block the host, which draws the next transition's momenta meanwhile)
+    if (!c->h_pbuf && cudaMallocHost(&c->h_pbuf, (2 * m + 2) * sizeof(double)) != cudaSuccess) c->h_pbuf = nullptr;
     if (c->h_pbuf) {
         S.pbuf = c->h_pbuf;
         S.pinned = true;
     } else {
         cudaGetLastError();
-        S.pvec.assign(m, 0.0);
+        S.pvec.assign(2 * m + 2, 0.0);
         S.pbuf = S.pvec.data();
     }
     CK(cudaEventCreate(&S.e0));
@@ -196,15 +200,22 @@ mds_status hmc_session_mark(mds_ctx c, HmcSession& S, cudaEvent_t e) {
     return MDS_OK;
 }
 
-// one HMC transition with momentum stream (seed, it): Metropolis accept on dH
-mds_status hmc_session_transition(mds_ctx c, HmcSession& S, uint64_t seed, uint64_t it) {
+void hmc_fill_momenta(double* pb, int64_t m, uint64_t seed, uint64_t it) {
+    for (int64_t q = 0; q < m; ++q) pb[q] = hmc_normal(seed, it, (uint64_t)q);
+}
+
+// one HMC transition with momentum stream (seed, it): Metropolis accept on dH.
+// more: another transition (it + 1, same seed) follows -- its momenta are drawn on
+// the host while this one runs on the device (double-buffered staging: half it & 1
+// was last uploaded by transition it - 2, complete at transition it - 1's sync)
+mds_status hmc_session_transition(mds_ctx c, HmcSession& S, uint64_t seed, uint64_t it, bool more) {
     NvtxRange nv("mds_hmc_transition");
     cudaStream_t s = S.s;
     const int64_t m = c->n * c->d;
     const size_t mbytes = (size_t)c->npad * c->d * sizeof(double);
-    CKS(s);                  // pbuf is reused: the previous upload must be done
-    for (int64_t q = 0; q < m; ++q) S.pbuf[q] = hmc_normal(seed, it, (uint64_t)q);
-    CK(cudaMemcpyAsync(c->d_p, S.pbuf, m * sizeof(double), cudaMemcpyHostToDevice, s));
+    double* pb = S.pbuf + (size_t)(it & 1) * m;
+    if (S.ready_it != (int64_t)it) hmc_fill_momenta(pb, m, seed, it);
+    CK(cudaMemcpyAsync(c->d_p, pb, m * sizeof(double), cudaMemcpyHostToDevice, s));
     CK(cudaMemcpyAsync(c->d_xsave, c->d_x, mbytes, cudaMemcpyDeviceToDevice, s));
     CK(cudaMemcpyAsync(c->d_glsave, c->d_gl, m * sizeof(double), cudaMemcpyDeviceToDevice, s));
     CK(cudaMemcpyAsync(c->d_liksave, c->d_lik, sizeof(double), cudaMemcpyDeviceToDevice, s));
@@ -218,9 +229,14 @@ mds_status hmc_session_transition(mds_ctx c, HmcSession& S, uint64_t seed, uint6
         return st;
     }
     if ((st = hmc_energy(c, c->d_H, S.it2, s))) return st;
-    double hh[2] = {0, 0};
+    double* hh = S.pbuf + 2 * (size_t)m;       // pinned: asynchronous
     CK(cudaMemcpyAsync(&hh[0], c->d_H0, sizeof(double), cudaMemcpyDeviceToHost, s));
     CK(cudaMemcpyAsync(&hh[1], c->d_H, sizeof(double), cudaMemcpyDeviceToHost, s));
+    S.ready_it = -1;
+    if (more) {
+        hmc_fill_momenta(S.pbuf + (size_t)((it + 1) & 1) * m, m, seed, it + 1);
+        S.ready_it = (int64_t)it + 1;
+    }
     CKS(s);
     const double dH = hh[1] - hh[0];
     const double u = hmc_u01(hmc_mix(seed ^ hmc_mix(0xACCE97ull ^ hmc_mix(it))));
@@ -326,7 +342,8 @@ mds_status mds_hmc_run(mds_ctx c, const mds_hmc_config* cfg, double* x_inout, md
     st = hmc_session_begin(c, cfg, S);
     if (!st) st = hmc_session_prime(c, S);
     if (!st) st = hmc_session_mark(c, S, S.e0);
-    for (int it = 0; it < cfg->n_iter && !st; ++it) st = hmc_session_transition(c, S, cfg->seed, (uint64_t)it);
+    for (int it = 0; it < cfg->n_iter && !st; ++it)
+        st = hmc_session_transition(c, S, cfg->seed, (uint64_t)it, it + 1 < cfg->n_iter);
     if (!st) st = hmc_session_mark(c, S, S.e1);
     double final_ll = 0.0;
     if (!st) st = hmc_session_finish(c, S, x_inout, &final_ll);
@@ -380,7 +397,7 @@ extern "C" mds_status mds_mcmc_run(mds_ctx c, const mds_hmc_config* cfg, const m
     int64_t acc_s = 0;
     const uint64_t xseed = hmc_mix(cfg->seed ^ 0x3C3Cull);
     for (int it = 0; it < cfg->n_iter && !st; ++it) {
-        if ((st = hmc_session_transition(c, S, xseed, (uint64_t)it))) break;
+        if ((st = hmc_session_transition(c, S, xseed, (uint64_t)it, it + 1 < cfg->n_iter))) break;
         const double z = hmc_normal(cfg->seed ^ 0x5167A5ull, (uint64_t)it, 0);
         const double u = hmc_u01(hmc_mix(cfg->seed ^ hmc_mix(0x5167A6ull ^ hmc_mix((uint64_t)it))));
         int32_t a = 0;
