@@ -872,6 +872,8 @@ void report_phases(mds_ctx c) {
     if (pe && pe[0] == '2') {      // every CTA's phase-A end, in CTA order
         std::fprintf(stderr, "[mds phases] A end by cta:");
         for (int g = 0; g < c->grid; ++g) std::fprintf(stderr, " %.1f", a[g]);
+        std::fprintf(stderr, "\n[mds phases] sm by cta:");
+        for (int g = 0; g < c->grid; ++g) std::fprintf(stderr, " %llu", h[(size_t)c->grid * 5 + g]);
         std::fprintf(stderr, "\n");
     }
 }
