@@ -64,7 +64,7 @@ def parse():
     ap.add_argument("--workload", default="C5")
     ap.add_argument("--precision", default="f64", choices=["f64", "f32"])
     ap.add_argument("--extra", default="auto",
-                    help="extra configs at N = 1 (comma list of C2, C4, C4f32; 'none'); auto = all at N = 1")
+                    help="extra configs at N = 1 (comma list of C2, C3, C4, C4f32; 'none'); auto = all at N = 1")
     ap.add_argument("--step-size", type=float, default=2e-5)
     ap.add_argument("--prior-sd", type=float, default=10.0)
     ap.add_argument("--e2e-seconds", type=float, default=2.0)
@@ -389,6 +389,32 @@ def build_ctx(R, mds, w, prec, stream):
     return ctx, {"setup_s": time.perf_counter() - t0, "generate_s": t_gen}
 
 
+# C3's step size: the 50-transition pilot of tools/run_configs.py (acceptance 0.65-0.85)
+# settles at 2.352e-3 on this workload (acceptance 0.67 over the 1000 transitions)
+C3_STEP_SIZE = 2.352e-3
+
+
+def run_c3_chain(R, mds, workload, stream):
+    """BASELINE configs[2]: the C2 data as a full HMC chain, 1000 transitions x 20
+    leapfrog steps through the library's own driver (mds_hmc_run: one CUDA graph of
+    the 20 fused passes per transition, momenta drawn on the host, one host sync per
+    transition for the accept/reject).  Device time between the chain's first and last
+    event (mds_hmc_run's own)."""
+    w = workload.config("C3")
+    ce, su = build_ctx(R, mds, w, "f64", stream)
+    ce.hmc_run(5, 20, C3_STEP_SIZE, 10.0, seed=1905045922, x0=w.x0.copy())       # warm-up (graph, buffers)
+    n_iter, L = 1000, 20
+    _, st = ce.hmc_run(n_iter, L, C3_STEP_SIZE, 10.0, seed=1905045922 + 100, x0=w.x0.copy())
+    ce.close()
+    P = w.n * (w.n - 1) // 2
+    return {"workload": "C3: N=%d D=%d f64, HMC chain of %d transitions x %d leapfrog steps (prior sd 10, "
+                        "step %.4g)" % (w.n, w.d, n_iter, L, C3_STEP_SIZE),
+            "value": P * st["grad_evals"] / st["seconds"], "unit": UNIT, "chain_seconds": st["seconds"],
+            "us_per_leapfrog_step": st["seconds"] * 1e6 / (n_iter * L), "grad_evals": st["grad_evals"],
+            "acceptance": st["accepted"] / n_iter, "l2": "no flush: the chain runs back to back (Y, 120 MB tiled, stays largely in the 126 MB L2)",
+            "setup_s": su["setup_s"]}
+
+
 def time_steps(R, ctx, w, steps, warmup, flush_buf, graph=False, clocks=None):
     """W untimed warm-up leapfrog steps, then K timed ones, each bracketed by CUDA
     events on the context's stream; barrier + synchronize on both sides; optional
@@ -558,9 +584,12 @@ def run_ours(args):
 
     # ---- extra configs at N = 1 (the paper's size and BASELINE's "1/2/4/8" config)
     extras = {}
-    want = [] if world > 1 else (["C2", "C4", "C4f32"] if args.extra == "auto" else
+    want = [] if world > 1 else (["C2", "C3", "C4", "C4f32"] if args.extra == "auto" else
                                  [e for e in args.extra.split(",") if e and e != "none"])
     for name in want:
+        if name == "C3":
+            extras[name] = run_c3_chain(R, mds, workload, stream)
+            continue
         cfg = name.replace("f32", "")
         prec = "f32" if name.endswith("f32") else "f64"
         we = workload.config(cfg)
