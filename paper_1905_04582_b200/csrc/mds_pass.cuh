@@ -344,6 +344,12 @@ __device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepc
 // columns is copied once per tile into xcol[t & 1].  x of the segment's 64
 // rows is read straight into registers at the segment start.
 constexpr int NSTAGE = 2;        // y stages per warp (the next unit is in flight)
+// largest D whose fp64 pass uses the rotating column accumulators (see the unit loop)
+#ifndef MDS_ROT_DMAX
+constexpr int ROT_DMAX = 4;
+#else
+constexpr int ROT_DMAX = MDS_ROT_DMAX;
+#endif
 
 // Warps per CTA and tile columns per unit (one bulk copy each; a multiple of
 // the 4-column reduce group).  ONE CTA per SM with as many warps as the register
@@ -722,13 +728,16 @@ pass_kernel(PassArgs a) {
                 //    pair plus, once per unit, 3 + log2(32 / UCOLS) adds, instead of a 2-row
                 //    sum and a reduce-scatter (6 adds per 8 pairs) per 4 columns.
                 // Fixed order either way: deterministic.
-                // (fp64 only: the fp32 pass at D = 6 spills with the four D-sized accumulators
-                // at 128 registers -- N = 30000 A/B 322.9 -> 287.8 G pair-evals/s; fp64 D = 2:
-                // 217.0 -> 223.3 G, N = 5392: 181.8 -> 186.5 G)
+                // (fp64 with 16-column units at D <= ROT_DMAX only -- N = 30000 A/B, G pair-evals/s:
+                // fp64 D = 2: 217.0 -> 223.3 (N = 5392: 181.8 -> 186.5), D = 4: 173.0 -> 177.6;
+                // but D = 3 (8-column units, two trips per unit): 191.9 -> 186.0, D = 6 (8 warps,
+                // 254 registers): 155.5 -> 154.0, and the fp32 pass at D = 6 spills with the
+                // four D-sized accumulators at 128 registers: 322.9 -> 287.8)
+                constexpr bool ROT_OK = sizeof(T) == 8 && UCOLS == 16 && D <= ROT_DMAX;
 #if defined(MDS_ROT_ALWAYS)
-                constexpr bool rot = sizeof(T) == 8;   // (count_sass.py: the rotation-mode loop alone)
+                constexpr bool rot = ROT_OK;   // (count_sass.py: the rotation-mode loop alone)
 #elif !defined(MDS_NO_ROT)
-                const bool rot = sizeof(T) == 8 &&
+                const bool rot = ROT_OK &&
                                  __all_sync(0xffffffffu, !fu && c4b == 0 && c4e == GPU);   // (a vote: warp-uniform to ptxas)
 #else
                 constexpr bool rot = false;

@@ -14,8 +14,10 @@ PassKernel pass_fn_d(int d) {
 #ifdef MDS_AB_D2ONLY
     // A/B builds: only D = 2 is instantiated (fast compile; other d are not valid)
     (void)d;
-#ifdef MDS_AB_D6
+#if defined(MDS_AB_D6)
     return pk<T, TR, MODE, 6>();
+#elif defined(MDS_AB_DV)
+    return pk<T, TR, MODE, MDS_AB_DV>();
 #else
     return pk<T, TR, MODE, 2>();
 #endif
