@@ -216,13 +216,14 @@ mds_status hmc_session_transition(mds_ctx c, HmcSession& S, uint64_t seed, uint6
     double* pb = S.pbuf + (size_t)(it & 1) * m;
     if (S.ready_it != (int64_t)it) hmc_fill_momenta(pb, m, seed, it);
     CK(cudaMemcpyAsync(c->d_p, pb, m * sizeof(double), cudaMemcpyHostToDevice, s));
-    CK(cudaMemcpyAsync(c->d_xsave, c->d_x, mbytes, cudaMemcpyDeviceToDevice, s));
-    CK(cudaMemcpyAsync(c->d_glsave, c->d_gl, m * sizeof(double), cudaMemcpyDeviceToDevice, s));
-    CK(cudaMemcpyAsync(c->d_liksave, c->d_lik, sizeof(double), cudaMemcpyDeviceToDevice, s));
-    if (c->tree) CK(cudaMemcpyAsync(c->d_logprior + 1, c->d_logprior, sizeof(double), cudaMemcpyDeviceToDevice, s));
-    mds_status st = hmc_redrift(c, S.eps, s);     // xnext for the new momentum
-    if (st) return st;
-    if ((st = hmc_energy(c, c->d_H0, S.it2, s))) return st;
+    // save for a rejection, xnext for the new momentum, H0: one launch
+    const int64_t mpad = (int64_t)(mbytes / sizeof(double));
+    transition_begin_kernel<<<1, 1024, 0, s>>>(c->d_x, c->d_p, c->d_gl, c->d_xsave, c->d_glsave, c->d_xnext, m, mpad,
+                                               S.eps, 0.5 * S.eps, c->d_lik, c->d_liksave,
+                                               c->tree ? c->d_logprior : nullptr, S.it2, c->d_H0);
+    CK(cudaGetLastError());
+    c->lf_eps = S.eps;
+    mds_status st = MDS_OK;
     if (S.exec) {
         CK(cudaGraphLaunch(S.exec, s));
     } else if ((st = hmc_enqueue_steps(c, S.L, S.eps, S.it2, s, false))) {
@@ -245,10 +246,11 @@ mds_status hmc_session_transition(mds_ctx c, HmcSession& S, uint64_t seed, uint6
     if (ok) {
         ++S.accepted;
     } else {
-        CK(cudaMemcpyAsync(c->d_x, c->d_xsave, mbytes, cudaMemcpyDeviceToDevice, s));
-        CK(cudaMemcpyAsync(c->d_gl, c->d_glsave, m * sizeof(double), cudaMemcpyDeviceToDevice, s));
-        CK(cudaMemcpyAsync(c->d_lik, c->d_liksave, sizeof(double), cudaMemcpyDeviceToDevice, s));
-        if (c->tree) CK(cudaMemcpyAsync(c->d_logprior, c->d_logprior + 1, sizeof(double), cudaMemcpyDeviceToDevice, s));
+        const int64_t mpad = (int64_t)(mbytes / sizeof(double));
+        transition_restore_kernel<<<(unsigned)((mpad + 255) / 256), 256, 0, s>>>(
+            c->d_x, c->d_xsave, c->d_gl, c->d_glsave, m, mpad, c->d_lik, c->d_liksave,
+            c->tree ? c->d_logprior : nullptr);
+        CK(cudaGetLastError());
     }
     return MDS_OK;
 }

@@ -178,6 +178,62 @@ __global__ void hamiltonian_kernel(const double* __restrict__ x, const double* _
     }
 }
 
+// Start of an HMC transition, one block of 1024 threads: save x (mpad entries, padding
+// included), gl, log L (and the log prior) for a rejection, xnext = drift(x, p, gl) for
+// the new momentum, and H0 -- the three save copies, redrift_kernel and
+// hamiltonian_kernel in one launch; the H0 reduction has hamiltonian_kernel's order
+// (same per-thread partition, same tree), so H0 is bitwise the same.
+__global__ void __launch_bounds__(1024) transition_begin_kernel(
+    const double* __restrict__ x, const double* __restrict__ p, const double* __restrict__ gl,
+    double* __restrict__ xsave, double* __restrict__ glsave, double* __restrict__ xnext, int64_t m, int64_t mpad,
+    double eps, double heps, const double* __restrict__ loglik, double* __restrict__ liksave,
+    double* __restrict__ logprior, double inv_tau2, double* __restrict__ out) {
+    __shared__ double sp[1024], sk[1024];
+    double a = 0.0, kin = 0.0;
+    for (int64_t k = threadIdx.x; k < m; k += blockDim.x) {
+        const double xv = x[k], pv = p[k], gv = gl[k];
+        xsave[k] = xv;
+        glsave[k] = gv;
+        xnext[k] = drift(xv, pv, gv, eps, heps);
+        a += xv * xv;
+        kin += pv * pv;
+    }
+    for (int64_t k = m + threadIdx.x; k < mpad; k += blockDim.x) xsave[k] = x[k];
+    sp[threadIdx.x] = a;
+    sk[threadIdx.x] = kin;
+    __syncthreads();
+    for (int s = blockDim.x / 2; s >= 1; s >>= 1) {
+        if (threadIdx.x < s) {
+            sp[threadIdx.x] += sp[threadIdx.x + s];
+            sk[threadIdx.x] += sk[threadIdx.x + s];
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        liksave[0] = loglik[0];
+        if (logprior) logprior[1] = logprior[0];
+        const double prior = logprior ? logprior[0] : -0.5 * sp[0] * inv_tau2;
+        const double K = 0.5 * sk[0];
+        out[0] = -(loglik[0] + prior) + K;
+        out[1] = loglik[0];
+        out[2] = K;
+    }
+}
+
+// a rejected HMC transition: x, gl, log L (and the log prior) back to the saved state
+__global__ void transition_restore_kernel(double* __restrict__ x, const double* __restrict__ xsave,
+                                          double* __restrict__ gl, const double* __restrict__ glsave, int64_t m,
+                                          int64_t mpad, double* __restrict__ loglik,
+                                          const double* __restrict__ liksave, double* __restrict__ logprior) {
+    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k < mpad) x[k] = xsave[k];
+    if (k < m) gl[k] = glsave[k];
+    if (k == 0) {
+        loglik[0] = liksave[0];
+        if (logprior) logprior[0] = logprior[1];
+    }
+}
+
 // Sharded leapfrog step after the exchange: the rank-ordered sum of the gathered
 // partials (gathered[r][0..m) = gradient partials, gathered[r][m] = log L partial)
 // fused with the leapfrog update of leapfrog_update_kernel.  Bitwise identical on
