@@ -354,6 +354,59 @@ def test_hmc_run_c1_chain(mds):
     assert ll == pytest.approx(st["final_loglik"], rel=1e-12)
 
 
+# The HMC driver's momenta and accept draws come from a counter-based generator
+# (splitmix64 finaliser + Box-Muller, PAPER.md:321-336 leaves the generator open):
+# the same generator written out here, independently of libmds, so that an
+# oracle-driven chain can be replayed transition by transition.
+_M64 = (1 << 64) - 1
+
+
+def _mix(z):
+    z = (z + 0x9E3779B97F4A7C15) & _M64
+    z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & _M64
+    z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & _M64
+    return z ^ (z >> 31)
+
+
+def _u01(h):
+    return (float(h >> 11) + 1.0) * (1.0 / 9007199254740992.0)
+
+
+def _normal(seed, it, q):
+    h1 = _mix(seed ^ _mix(it ^ _mix(2 * q)))
+    h2 = _mix(seed ^ _mix(it ^ _mix(2 * q + 1)))
+    return math.sqrt(-2.0 * math.log(_u01(h1))) * math.cos(6.283185307179586 * _u01(h2))
+
+
+def test_hmc_run_matches_oracle_chain(mds):
+    """mds_hmc_run (momenta staged on the host while the previous transition runs,
+    fused save / redrift / H0 and restore launches, one graph per trajectory) against
+    the same chain driven by the oracle's leapfrog: every transition's Metropolis
+    decision, the acceptance count and the final X."""
+    w = workload.config("C1")
+    y = w.y_packed()
+    # eps 0.08: 8 of 15 accepted, every decision at least 0.06 away from its threshold
+    n, d, seed, n_iter, L, eps, tau = w.n, w.d, 4242, 15, 10, 0.08, 10.0
+    x = w.x0.copy()
+    acc = 0
+    for it in range(n_iter):
+        p0 = np.array([_normal(seed, it, q) for q in range(n * d)]).reshape(n, d)
+        ref = oracle.leapfrog(y, x, p0, w.sigma, eps, L, 1, prior_sd=tau)
+        dh = ref["H1"] - ref["H0"]
+        u = _u01(_mix(seed ^ _mix(0xACCE97 ^ _mix(it))))
+        if math.isfinite(dh) and math.log(u) < -dh:
+            x = ref["x"]
+            acc += 1
+    assert 0 < acc < n_iter          # both branches (accept and restore) were taken
+    with mds.MDS(n, d) as c:
+        c.set_dissimilarities_packed(y)
+        c.set_sigma(w.sigma)
+        xg, st = c.hmc_run(n_iter, L, eps, tau, seed=seed, x0=w.x0)
+    assert st["accepted"] == acc
+    np.testing.assert_allclose(xg, x, rtol=1e-9, atol=1e-12)
+    assert st["final_loglik"] == pytest.approx(oracle.loglik_grad(y, x, w.sigma, 1)["loglik"], rel=1e-10)
+
+
 def test_virtual_ranges_and_wide_d(mds):
     """Warp ranges split into several segment tables (forced small with
     MDS_DEBUG_MAXSEG), and the widest D in both precisions."""
