@@ -752,7 +752,47 @@ pass_kernel(PassArgs a) {
                 for (int p = 0; p < 4; ++p)
 #pragma unroll
                     for (int k = 0; k < D; ++k) cv[p][k] = T(0);
-                const int it_b = rot ? 0 : c4b, it_e = rot ? GPU : c4e;
+                // fp32 whole units: the rotation with two accumulators (even / odd steps) moved
+                // 2 lanes after every block -- with four, the fp32 pass spills at D = 6 (the
+                // coefficients are few in fp32, so a shuffle between the blocks costs nothing
+                // there).  Lane L ends with column (L - 2) mod UCOLS.
+                bool unit_done = false;
+#ifndef MDS_NO_F32_ROT
+                if constexpr (sizeof(T) == 4) {
+                    if (WG && __all_sync(0xffffffffu, !fu && c4b == 0 && c4e == GPU)) {
+                        T ce[D], co[D];
+#pragma unroll
+                        for (int k = 0; k < D; ++k) ce[k] = co[k] = T(0);
+#pragma unroll 1
+                        for (int s4 = 0; s4 < UCOLS; s4 += 4) {
+#pragma unroll
+                            for (int h = 0; h < 2; ++h) {
+                                const int k0 = s4 + 2 * h;
+                                block4(yu, xu, (lr + k0) & (UCOLS - 1), (lr + k0 + 1) & (UCOLS - 1), ce, co,
+                                       std::true_type());
+                                if (k0 + 2 < UCOLS) {
+#pragma unroll
+                                    for (int k = 0; k < D; ++k) {
+                                        ce[k] = __shfl_sync(0xffffffffu, ce[k], lane_v + 2, UCOLS);
+                                        co[k] = __shfl_sync(0xffffffffu, co[k], lane_v + 2, UCOLS);
+                                    }
+                                }
+                            }
+                        }
+                        double* __restrict__ cslab = a.slabs + (size_t)cpos * TB * D + (size_t)jb * D;
+                        const int cc = (lr + UCOLS - 2) & (UCOLS - 1);
+#pragma unroll
+                        for (int k = 0; k < D; ++k) {
+                            T cs = ce[k] + __shfl_sync(0xffffffffu, co[k], lane_v + UCOLS - 1, UCOLS);
+#pragma unroll
+                            for (int o = UCOLS; o < 32; o <<= 1) cs += shfl_xor(cs, o);
+                            if (lane_v < UCOLS) cslab[cc * D + k] = A(cs);
+                        }
+                        unit_done = true;
+                    }
+                }
+#endif
+                const int it_b = rot ? 0 : c4b, it_e = unit_done ? c4b : (rot ? GPU : c4e);
 #pragma unroll 1      // (unroll 2 measured: 168 regs + spills, 219 -> 154 G pair-evals/s)
                 for (int c4 = it_b; c4 < it_e; ++c4) {     // 8 pairs per lane: a 4-column group / 4 steps
 #ifndef MDS_EXP_NO_TMA
