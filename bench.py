@@ -173,10 +173,10 @@ def sass_counts(prec: str, d: int, mode: int = 2) -> dict | None:
     try:
         tab = json.load(open(path))
         key = "%s_d%d_t1" % (prec, d) if mode == 2 else "%s_d%d_t1_m%d" % (prec, d, mode)
-        # fp64: the rotation-mode loop (every unit but a warp range's first and last) is the
-        # one that runs; the libmds.so loop's static count also holds the group mode's code
+        # the rotation loop (every whole unit) is the one that runs; a warp range's partial
+        # first / last unit goes through the group-mode loop
         r = dict(tab[key + "_rot"]) if key + "_rot" in tab else dict(tab[key])
-        r["count_source"] = ("static SASS count of the rotation-mode loop (MDS_ROT_ALWAYS build, "
+        r["count_source"] = ("static SASS count of the rotation loop (MDS_ROT_COUNT build, "
                              "tools/count_sass.py)" if key + "_rot" in tab else "static SASS count of the loop")
         return r
     except Exception:

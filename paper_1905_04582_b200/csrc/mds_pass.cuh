@@ -344,12 +344,6 @@ __device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepc
 // columns is copied once per tile into xcol[t & 1].  x of the segment's 64
 // rows is read straight into registers at the segment start.
 constexpr int NSTAGE = 2;        // y stages per warp (the next unit is in flight)
-// largest D whose fp64 pass uses the rotating column accumulators (see the unit loop)
-#ifndef MDS_ROT_DMAX
-constexpr int ROT_DMAX = 4;
-#else
-constexpr int ROT_DMAX = MDS_ROT_DMAX;
-#endif
 
 // Warps per CTA and tile columns per unit (one bulk copy each; a multiple of
 // the 4-column reduce group).  ONE CTA per SM with as many warps as the register
@@ -624,10 +618,9 @@ pass_kernel(PassArgs a) {
                 // One lock-step block: 4 pairs per lane -- rows lane and lane+32 against the
                 // columns qa and qb of yb/xb (per-lane column indices) -- with the Eq. 2 terms
                 // into the running sums, the row sums by fused multiply-adds, and the column
-                // side into ca/cb: fresh 2-row sums (group path) or accumulated (ACC).
+                // side added to the accumulators ca (column qa) and cb (column qb).
                 auto block4 = [&](const T* __restrict__ yb, const T* __restrict__ xb, int qa, int qb,
-                                  T (&ca)[D], T (&cb)[D], auto acc_tag) {
-                    constexpr bool ACC = decltype(acc_tag)::value;
+                                  T (&ca)[D], T (&cb)[D]) {
                     T ys[4], ss[4], dd[4][D];
 #pragma unroll
                     for (int qq = 0; qq < 2; ++qq) {
@@ -635,7 +628,7 @@ pass_kernel(PassArgs a) {
                         ys[2 * qq] = yb[q * TB + lane_v];
                         ys[2 * qq + 1] = yb[q * TB + lane_v + 32];
                         T xj[D];
-                        if constexpr (D == 2 && sizeof(T) == 8 && ACC) {
+                        if constexpr (D == 2 && sizeof(T) == 8) {
                             // per-lane columns: one 16-byte load (conflict-free per quarter warp)
                             const double2 v = *reinterpret_cast<const double2*>(xb + q * 2);
                             xj[0] = v.x;
@@ -704,95 +697,77 @@ pass_kernel(PassArgs a) {
                     if (WG) {
 #pragma unroll
                         for (int k = 0; k < D; ++k) {
-                            if constexpr (ACC) {
-                                ca[k] = fma(uu[1], dd[1][k], fma(uu[0], dd[0][k], ca[k]));
-                                cb[k] = fma(uu[3], dd[3][k], fma(uu[2], dd[2][k], cb[k]));
-                            } else {
-                                ca[k] = fma(uu[0], dd[0][k], uu[1] * dd[1][k]);
-                                cb[k] = fma(uu[2], dd[2][k], uu[3] * dd[3][k]);
-                            }
+                            ca[k] = fma(uu[1], dd[1][k], fma(uu[0], dd[0][k], ca[k]));
+                            cb[k] = fma(uu[3], dd[3][k], fma(uu[2], dd[2][k], cb[k]));
                         }
                     }
                 };
-                // Two ways through a unit, one copy of the pair math (ptxas keeps the
-                // coefficients in uniform registers only with one copy):
-                //  * group mode (a warp range's first and last unit, and the staggered first
-                //    unit): per 4-column group, a 2-row sum per column and a select-free
-                //    reduce-scatter over the 32 lanes (the column order p ^ m, see m);
-                //  * rotation mode (every other unit): rotating column accumulators.  Lanes
-                //    form groups of UCOLS; at step s lane L takes column (L + s) mod UCOLS of
-                //    the unit (rows L and L+32), four steps per trip (two lock-step blocks),
-                //    each step of the trip with its own accumulator; at the end of the trip
-                //    all four move 4 lanes down the lane group, so each follows its column
-                //    across the group.  A column's sum is then one fused multiply-add per
-                //    pair plus, once per unit, 3 + log2(32 / UCOLS) adds, instead of a 2-row
-                //    sum and a reduce-scatter (6 adds per 8 pairs) per 4 columns.
-                // Fixed order either way: deterministic.
-                // (fp64 with 16-column units at D <= ROT_DMAX only -- N = 30000 A/B, G pair-evals/s:
-                // fp64 D = 2: 217.0 -> 223.3 (N = 5392: 181.8 -> 186.5), D = 4: 173.0 -> 177.6;
-                // but D = 3 (8-column units, two trips per unit): 191.9 -> 186.0, D = 6 (8 warps,
-                // 254 registers): 155.5 -> 154.0, and the fp32 pass at D = 6 spills with the
-                // four D-sized accumulators at 128 registers: 322.9 -> 287.8)
-                constexpr bool ROT_OK = sizeof(T) == 8 && UCOLS == 16 && D <= ROT_DMAX;
-#if defined(MDS_ROT_ALWAYS)
-                constexpr bool rot = ROT_OK;   // (count_sass.py: the rotation-mode loop alone)
-#elif !defined(MDS_NO_ROT)
-                const bool rot = ROT_OK &&
-                                 __all_sync(0xffffffffu, !fu && c4b == 0 && c4e == GPU);   // (a vote: warp-uniform to ptxas)
-#else
-                constexpr bool rot = false;
-#endif
+                // Two ways through a unit:
+                //  * rotation (every whole unit but the warp's staggered first one): rotating
+                //    column accumulators.  Lanes form groups of UCOLS; at step s lane L takes
+                //    column (L + s) mod UCOLS of the unit (rows L and L+32), two steps per
+                //    lock-step block, one accumulator for the even and one for the odd
+                //    steps; after every block both move 2 lanes down the lane group, so each
+                //    follows its column across the group.  A column's sum is then one fused
+                //    multiply-add per pair plus, once per unit, 1 + log2(32 / UCOLS) adds,
+                //    instead of a 2-row sum and a reduce-scatter (6 adds per 8 pairs) per 4
+                //    columns.  Lane L ends with column (L - 2) mod UCOLS.
+                //  * group mode (a warp range's partial first / last unit, the staggered first
+                //    unit): per 4-column group a 2-row sum per column and a select-free
+                //    reduce-scatter over the 32 lanes (the column order p ^ m, see m).
+                // Fixed order either way: deterministic.  (N = 30000 A/B, G pair-evals/s,
+                // group mode only -> rotation: fp64 D = 2 217.0 -> 227.4, D = 3 191.6 -> 200.7,
+                // D = 4 173.0 -> 189.4, D = 6 155.4 -> 171.3; fp32 D = 2 508.2 -> 526.4, D = 6
+                // 322.4 -> 344.0.  Four accumulators moved 4 lanes at the end of each 4-step
+                // trip were slower: fp64 D = 2 223.4, D = 4 178.0, D = 3 186.0, D = 6 154.0,
+                // and spilled the fp32 pass.)
                 const int lr = lane_v & (UCOLS - 1);
                 const T* __restrict__ yu = W.y[cst];
                 const T* __restrict__ xu;
                 if constexpr (sizeof(T) == 4) xu = &W.xcolf[t & 1][jb * D];
                 else xu = W.xcol[t & 1] + jb * D;
-                T cv[4][D];
+                bool unit_done = false;
+#ifndef MDS_NO_ROT
+                if (WG && __all_sync(0xffffffffu, !fu && c4b == 0 && c4e == GPU)) {   // (a vote: warp-uniform)
+                    T ce[D], co[D];
+#pragma unroll
+                    for (int k = 0; k < D; ++k) ce[k] = co[k] = T(0);
+#pragma unroll 1
+                    for (int s4 = 0; s4 < UCOLS; s4 += 4) {
+#pragma unroll
+                        for (int h = 0; h < 2; ++h) {
+                            const int k0 = s4 + 2 * h;
+                            block4(yu, xu, (lr + k0) & (UCOLS - 1), (lr + k0 + 1) & (UCOLS - 1), ce, co);
+                            if (k0 + 2 < UCOLS) {
+#pragma unroll
+                                for (int k = 0; k < D; ++k) {
+                                    ce[k] = __shfl_sync(0xffffffffu, ce[k], lane_v + 2, UCOLS);
+                                    co[k] = __shfl_sync(0xffffffffu, co[k], lane_v + 2, UCOLS);
+                                }
+                            }
+                        }
+                    }
+                    double* __restrict__ cslab = a.slabs + (size_t)cpos * TB * D + (size_t)jb * D;
+                    const int cc = (lr + UCOLS - 2) & (UCOLS - 1);
+#pragma unroll
+                    for (int k = 0; k < D; ++k) {
+                        T cs = ce[k] + __shfl_sync(0xffffffffu, co[k], lane_v + UCOLS - 1, UCOLS);
+#pragma unroll
+                        for (int o = UCOLS; o < 32; o <<= 1) cs += shfl_xor(cs, o);
+                        if (lane_v < UCOLS) cslab[cc * D + k] = A(cs);
+                    }
+                    unit_done = true;
+                }
+#endif
+#ifdef MDS_ROT_COUNT
+                unit_done = true;     // (count_sass.py: a build whose only pair loop is the rotation's)
+#endif
+                const int it_b = c4b, it_e = unit_done ? c4b : c4e;
+                T cv[4][D];           // group mode: the 4 columns' 2-row sums (accumulated from zero)
 #pragma unroll
                 for (int p = 0; p < 4; ++p)
 #pragma unroll
                     for (int k = 0; k < D; ++k) cv[p][k] = T(0);
-                // fp32 whole units: the rotation with two accumulators (even / odd steps) moved
-                // 2 lanes after every block -- with four, the fp32 pass spills at D = 6 (the
-                // coefficients are few in fp32, so a shuffle between the blocks costs nothing
-                // there).  Lane L ends with column (L - 2) mod UCOLS.
-                bool unit_done = false;
-#ifndef MDS_NO_F32_ROT
-                if constexpr (sizeof(T) == 4) {
-                    if (WG && __all_sync(0xffffffffu, !fu && c4b == 0 && c4e == GPU)) {
-                        T ce[D], co[D];
-#pragma unroll
-                        for (int k = 0; k < D; ++k) ce[k] = co[k] = T(0);
-#pragma unroll 1
-                        for (int s4 = 0; s4 < UCOLS; s4 += 4) {
-#pragma unroll
-                            for (int h = 0; h < 2; ++h) {
-                                const int k0 = s4 + 2 * h;
-                                block4(yu, xu, (lr + k0) & (UCOLS - 1), (lr + k0 + 1) & (UCOLS - 1), ce, co,
-                                       std::true_type());
-                                if (k0 + 2 < UCOLS) {
-#pragma unroll
-                                    for (int k = 0; k < D; ++k) {
-                                        ce[k] = __shfl_sync(0xffffffffu, ce[k], lane_v + 2, UCOLS);
-                                        co[k] = __shfl_sync(0xffffffffu, co[k], lane_v + 2, UCOLS);
-                                    }
-                                }
-                            }
-                        }
-                        double* __restrict__ cslab = a.slabs + (size_t)cpos * TB * D + (size_t)jb * D;
-                        const int cc = (lr + UCOLS - 2) & (UCOLS - 1);
-#pragma unroll
-                        for (int k = 0; k < D; ++k) {
-                            T cs = ce[k] + __shfl_sync(0xffffffffu, co[k], lane_v + UCOLS - 1, UCOLS);
-#pragma unroll
-                            for (int o = UCOLS; o < 32; o <<= 1) cs += shfl_xor(cs, o);
-                            if (lane_v < UCOLS) cslab[cc * D + k] = A(cs);
-                        }
-                        unit_done = true;
-                    }
-                }
-#endif
-                const int it_b = rot ? 0 : c4b, it_e = unit_done ? c4b : (rot ? GPU : c4e);
 #pragma unroll 1      // (unroll 2 measured: 168 regs + spills, 219 -> 154 G pair-evals/s)
                 for (int c4 = it_b; c4 < it_e; ++c4) {     // 8 pairs per lane: a 4-column group / 4 steps
 #ifndef MDS_EXP_NO_TMA
@@ -814,28 +789,9 @@ pass_kernel(PassArgs a) {
 #endif
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {         // positions 2h, 2h+1: 4 pairs per lane in lock-step
-                    int qa, qb;
-                    if (rot) {
-                        qa = (lr + 4 * c4 + 2 * h) & (UCOLS - 1);
-                        qb = (lr + 4 * c4 + 2 * h + 1) & (UCOLS - 1);
-                    } else {
-                        qa = 4 * c4 + ((2 * h) ^ m);
-                        qb = 4 * c4 + ((2 * h + 1) ^ m);
-                    }
-                    block4(yu, xu, qa, qb, cv[2 * h], cv[2 * h + 1], std::true_type());
+                    block4(yu, xu, 4 * c4 + ((2 * h) ^ m), 4 * c4 + ((2 * h + 1) ^ m), cv[2 * h], cv[2 * h + 1]);
                 }
-                // (the exchanges sit at the end of the trip, after both blocks' math: a
-                // shuffle between the blocks made ptxas keep the polynomial coefficients in
-                // vector registers instead of uniform ones -- 168 registers and spills)
-                if (rot) {
-                    // every accumulator moves 4 lanes down its lane group (step s's accumulator
-                    // follows its column: lane L + 4 takes it over at step s + 4)
-#pragma unroll
-                    for (int p = 0; p < 4; ++p)
-#pragma unroll
-                        for (int k = 0; k < (WG ? D : 0); ++k)
-                            cv[p][k] = __shfl_sync(0xffffffffu, cv[p][k], lane_v + 4, UCOLS);
-                } else {
+                {
                     double* __restrict__ cslab = a.slabs + (size_t)cpos * TB * D + (size_t)(jb + 4 * c4) * D;
 #pragma unroll
                     for (int k = 0; k < (WG ? D : 0); ++k) {
@@ -848,21 +804,6 @@ pass_kernel(PassArgs a) {
                         for (int k = 0; k < D; ++k) cv[p][k] = T(0);
                 }
                 }   // 4-column groups / steps
-                if (rot) {
-                    // after the last trip's move, accumulator p of lane L holds (its share of)
-                    // column L + p mod UCOLS: lane L sums column L from lanes L, L-1, L-2, L-3,
-                    // then over the lane groups
-                    double* __restrict__ cslab = a.slabs + (size_t)cpos * TB * D + (size_t)jb * D;
-#pragma unroll
-                    for (int k = 0; k < (WG ? D : 0); ++k) {
-                        T cs = cv[0][k];
-#pragma unroll
-                        for (int p = 1; p < 4; ++p) cs += __shfl_sync(0xffffffffu, cv[p][k], lane_v + UCOLS - p, UCOLS);
-#pragma unroll
-                        for (int o = UCOLS; o < 32; o <<= 1) cs += shfl_xor(cs, o);
-                        if (lane_v < UCOLS) cslab[lr * D + k] = A(cs);
-                    }
-                }
                 if constexpr (sizeof(T) == 4) {       // at most 16 columns x 2 terms in fp32 (reading R15)
                     if (WG) {
 #pragma unroll

@@ -22,14 +22,18 @@ FP32 = {"FFMA", "FMUL", "FADD", "FSETP", "FMNMX", "FSEL"}
 
 
 def rotation_only_sass():
-    """fp64 LEAPFROG pass kernels (mode 2) built with MDS_ROT_ALWAYS: the loop of the
-    rotation mode alone, which runs every unit but a warp range's first and last (the
-    libmds.so loop also holds the group mode's reduce-scatter, executed at those two)."""
-    obj = "/tmp/mds_count_rot_m2_f64.o"
-    subprocess.check_call(["nvcc", "-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a",
-                           "-I", os.path.join(ROOT, "include"), "-DMDS_ROT_ALWAYS", "-c", "-o", obj,
-                           os.path.join(CSRC, "pass_m2_f64.cu")])
-    return subprocess.check_output(["cuobjdump", "-sass", obj], text=True)
+    """LEAPFROG pass kernels (mode 2) built with MDS_ROT_COUNT, whose only pair loop is
+    the rotation's (it runs every whole unit; the group-mode loop of a warp range's
+    partial first / last unit is compiled out there).  The libmds.so kernels hold
+    both loops; the static count picks the smaller one."""
+    out = []
+    for prec in ("f64", "f32"):
+        obj = "/tmp/mds_count_rot_m2_%s.o" % prec
+        subprocess.check_call(["nvcc", "-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a",
+                               "-I", os.path.join(ROOT, "include"), "-DMDS_ROT_COUNT", "-c", "-o", obj,
+                               os.path.join(CSRC, "pass_m2_%s.cu" % prec)])
+        out.append(subprocess.check_output(["cuobjdump", "-sass", obj], text=True))
+    return "\n".join(out)
 
 
 def main():
