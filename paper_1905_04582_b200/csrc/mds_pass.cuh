@@ -716,7 +716,7 @@ pass_kernel(PassArgs a) {
                 //    unit): per 4-column group a 2-row sum per column and a select-free
                 //    reduce-scatter over the 32 lanes (the column order p ^ m, see m).
                 // Fixed order either way: deterministic.  (N = 30000 A/B, G pair-evals/s,
-                // group mode only -> rotation: fp64 D = 2 217.0 -> 227.4, D = 3 191.6 -> 200.7,
+                // group mode only -> rotation: fp64 D = 2 216.8 -> 227.0, D = 3 191.6 -> 200.7,
                 // D = 4 173.0 -> 189.4, D = 6 155.4 -> 171.3; fp32 D = 2 508.2 -> 526.4, D = 6
                 // 322.4 -> 344.0.  Four accumulators moved 4 lanes at the end of each 4-step
                 // trip were slower: fp64 D = 2 223.4, D = 4 178.0, D = 3 186.0, D = 6 154.0,
