@@ -732,10 +732,14 @@ pass_kernel(PassArgs a) {
                     T ce[D], co[D];
 #pragma unroll
                     for (int k = 0; k < D; ++k) ce[k] = co[k] = T(0);
-                    // fp32: the unit's trips unrolled (N = 30000 D = 6 A/B 343.9 -> 353.9 G); fp64's
-                    // larger blocks do not fit the instruction cache unrolled (D = 2 227.2 -> 156.2 G,
-                    // D = 6 171.6 -> 80.6 G)
-                    constexpr int ROT_UNROLL = sizeof(T) == 4 ? UCOLS / 4 : 1;
+                    // trips unrolled: fp32 all of the unit's (N = 30000 D = 6 A/B 343.9 -> 353.9 G),
+                    // fp64 two (D = 2 227.2 -> 229.9 G, D = 6 171.6 -> 175.6 G); fp64's four trips
+                    // unrolled do not fit the instruction cache (D = 2 156.2 G, D = 6 80.6 G)
+#ifndef MDS_F64_ROT_UNROLL
+                    constexpr int ROT_UNROLL = sizeof(T) == 4 ? UCOLS / 4 : 2;
+#else
+                    constexpr int ROT_UNROLL = sizeof(T) == 4 ? UCOLS / 4 : MDS_F64_ROT_UNROLL;
+#endif
 #pragma unroll (ROT_UNROLL)
                     for (int s4 = 0; s4 < UCOLS; s4 += 4) {
 #pragma unroll
