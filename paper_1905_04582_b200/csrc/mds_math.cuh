@@ -93,49 +93,6 @@ __device__ __forceinline__ T horner(const T* c, T x) {
     return p;
 }
 
-// p(x) = E(x^2) + x O(x^2): two independent Horner chains of half the depth
-// (one extra multiply and one extra fma); shortens the FP64 dependency chain
-template <int DEG>
-__device__ __forceinline__ double horner_eo(const double* c, double x) {
-    const double x2 = x * x;
-    constexpr int DE = DEG / 2;                 // even part degree (in x^2)
-    constexpr int DO = (DEG - 1) / 2;           // odd part degree (in x^2)
-    double pe = c[2 * DE], po = c[2 * DO + 1];
-#pragma unroll
-    for (int k = DE - 1; k >= 0; --k) {
-        pe = fma(pe, x2, c[2 * k]);
-        if (k <= DO - 1) po = fma(po, x2, c[2 * k + 1]);
-    }
-    return fma(po, x, pe);
-}
-
-// p(x) = [A(x^4) + x B(x^4)] + x^2 [C(x^4) + x D(x^4)]: four independent
-// Horner chains of quarter depth.  Measured on B200 (tools/fp64_probe.cu): a
-// warp whose consecutive DFMAs are dependent caps the FP64 pipe at ~65% of
-// peak however many warps are resident; 4 independent chains reach ~91%.
-template <int DEG>
-__device__ __forceinline__ double horner4(const double* c, double x) {
-    const double x2 = x * x;
-    const double x4 = x2 * x2;
-    double ch[4];
-#pragma unroll
-    for (int m = 0; m < 4; ++m) {
-        const int top = (DEG - m) / 4;            // highest k with 4k + m <= DEG
-        ch[m] = (m <= DEG) ? c[4 * top + m] : 0.0;
-    }
-#pragma unroll
-    for (int k = DEG / 4; k >= 0; --k) {
-#pragma unroll
-        for (int m = 0; m < 4; ++m) {
-            const int top = (DEG - m) / 4;
-            if (m <= DEG && k < top) ch[m] = fma(ch[m], x4, c[4 * k + m]);
-        }
-    }
-    const double lo = fma(ch[1], x, ch[0]);
-    const double hi = fma(ch[3], x, ch[2]);
-    return fma(hi, x2, lo);
-}
-
 // the per-launch exp table of pair_f64_n: cg 2^(j/256), j < EXPT64_N (call with
 // every thread of the block, then __syncthreads)
 __device__ __forceinline__ void build_exptab(double* tab, const SigmaParams& P) {

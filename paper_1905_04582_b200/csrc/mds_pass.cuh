@@ -97,24 +97,6 @@ template <bool TRUNC> struct Pair<float, TRUNC> {
 template <typename T>
 __device__ __forceinline__ T shfl_xor(T v, int m) { return __shfl_xor_sync(0xffffffffu, v, m); }
 
-// Sum of 4 per-lane values a0..a3 over the 32 lanes; lane L ends with the total
-// of column c = (L >> 3) & 3 (all 8 lanes of that group hold it).  Fixed order.
-template <typename T>
-__device__ __forceinline__ T reduce_scatter4(T a0, T a1, T a2, T a3, int lane) {
-    const bool b4 = lane & 16, b3 = lane & 8;
-    T k0 = b4 ? a2 : a0, k1 = b4 ? a3 : a1;
-    T s0 = b4 ? a0 : a2, s1 = b4 ? a1 : a3;
-    k0 += shfl_xor(s0, 16);
-    k1 += shfl_xor(s1, 16);
-    T k = b3 ? k1 : k0;
-    T sd = b3 ? k0 : k1;
-    k += shfl_xor(sd, 8);
-    k += shfl_xor(k, 4);
-    k += shfl_xor(k, 2);
-    k += shfl_xor(k, 1);
-    return k;
-}
-
 // Sum over the 32 lanes of 4 per-lane column values stored in the per-lane
 // order v[p] = column p ^ m, m = (L >> 3) & 3 (see the unit loop): every
 // exchange then sends a fixed register, so no selects are needed.  Lane L ends
@@ -124,21 +106,6 @@ __device__ __forceinline__ T reduce_scatter4_perm(T v0, T v1, T v2, T v3) {
     T k0 = v0 + shfl_xor(v2, 16);     // partner L^16 holds my columns 0,1 at its positions 2,3
     T k1 = v1 + shfl_xor(v3, 16);
     T k = k0 + shfl_xor(k1, 8);       // partner L^8 holds my column 0 at its position 1
-    k += shfl_xor(k, 4);
-    k += shfl_xor(k, 2);
-    k += shfl_xor(k, 1);
-    return k;
-}
-
-// Sum of 2 per-lane values over the 32 lanes; lane L ends with the total of
-// column (L >> 4) & 1.  Fixed order.
-template <typename T>
-__device__ __forceinline__ T reduce_scatter2(T a0, T a1, int lane) {
-    const bool b4 = lane & 16;
-    T k = b4 ? a1 : a0;
-    const T sd = b4 ? a0 : a1;
-    k += shfl_xor(sd, 16);
-    k += shfl_xor(k, 8);
     k += shfl_xor(k, 4);
     k += shfl_xor(k, 2);
     k += shfl_xor(k, 1);
