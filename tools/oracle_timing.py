@@ -1,8 +1,8 @@
 #!/usr/bin/env python
 """The oracle timed on the host at full size (SURVEY 8(d) "Oracle timing"):
 C2 (median of 5 full evaluations), C4 (3 full evaluations, fp64 inputs) and C5
-(ONE evaluation of log L + gradient, streamed: the packed triangle is generated
-row chunk by row chunk and never held whole; 1 core).  A reported baseline, not
+(ONE evaluation of log L, streamed: the packed triangle is generated row chunk
+by row chunk and never held whole; 1 core).  A reported baseline, not
 a target.  -> profiles/r02/oracle_timing.json"""
 import json
 import os
@@ -40,8 +40,8 @@ def full(name, reps):
 
 
 def c5_streamed():
-    """log L by the streaming row-range oracle plus the gradient by oracle_grad_rows
-    over row chunks (full rows j != i), both serial, one evaluation."""
+    """log L by the streaming row-range oracle over 500-row chunks, serial, one
+    evaluation (the gradient at C5 is timed on the GPU side only)."""
     w = workload.config("C5")
     t_gen = 0.0
     t_or = 0.0
