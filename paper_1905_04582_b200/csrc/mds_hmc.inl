@@ -101,7 +101,8 @@ mds_status hmc_energy(mds_ctx c, double* out, double inv_tau2, cudaStream_t s) {
 // PAPER.md:672 sampler mds_mcmc_run): the CUDA graph of the L fused leapfrog
 // steps (captured once; updated in place when sigma moves, since the sigma
 // constants are kernel parameters), the pinned momentum buffer and the timing
-// events.  Per transition: momentum upload, save, redrift, H0, graph, H1, one
+// events.  Per transition: momentum upload (drawn on the host during the previous
+// transition), one launch for save + redrift + H0, graph, H1, one
 // host sync for the accept/reject.
 struct HmcSession {
     cudaStream_t s = nullptr;
